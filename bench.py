@@ -1,0 +1,518 @@
+#!/usr/bin/env python
+"""bench.py -- AdaServe hot path (select -> tree-verify attention -> accept+commit)
+on B200.  Prints ONE JSON line (rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (KV-head sharding, NCCL all-gather)
+
+Metric (BASELINE.json): verified tree tokens/sec (sum_i K_i per step / step time)
+and the attention kernel's HBM GB/s as a fraction of the measured HBM peak.
+A step = one pass of the whole hot path over one batch: as_select_trees ->
+as_tree_verify_attn (one layer) -> as_accept_tokens (walk + KV commit), plus at
+N>1 the all-gather of accept records.  Inputs are resident in HBM; the
+per-request prefix length is restored before each step (a 256-byte D2D copy)
+so every step verifies the same workload.
+
+The only place outside tests/ that touches oracle/ is the `cpu_baseline` leg
+and `--impl reference`, which time the CPU oracle as it stands on this host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+# --------------------------------------------------------------------------- configs (BASELINE.json)
+CONFIGS = {
+    "c1": dict(desc="1 request, 8-node speculation tree, 1 layer, 4 heads x head_dim 64, 128-token KV prefix, fp32",
+               n_req=1, d=3, w=3, sigma=(1.0, 4.0), A="c1", n_max=7, budget=8, L=128, n_q=4, n_kv=4, head_dim=64,
+               page_size=16, dtype="f32"),
+    "c2": dict(desc="Llama-3-8B shapes (32 q / 8 kv heads, d=128), 64 requests, 32-node trees, 2k-token paged KV, "
+                    "bf16", n_req=64, d=8, w=8, sigma=(1.0, 4.0), A=9.0, n_max=31, budget=2048, L=2048, n_q=32,
+               n_kv=8, head_dim=128, page_size=64, dtype="bf16"),
+    "c3": dict(desc="mixed-SLO batch: 256 requests, per-request trees 4-64 under a 4096-token global budget, "
+                    "Llama-3-8B shapes, 2k KV (assumed)", n_req=256, d=8, w=8, sigma=(1.0, 8.0), A="mix", n_max=63,
+               budget=4096, L=2048, n_q=32, n_kv=8, head_dim=128, page_size=64, dtype="bf16"),
+    "c4": dict(desc="Llama-3-70B shapes (64 q / 8 kv heads), 128 requests, 64-node trees, 2k KV (assumed)",
+               n_req=128, d=8, w=8, sigma=(1.0, 4.0), A=9.0, n_max=63, budget=8192, L=2048, n_q=64, n_kv=8,
+               head_dim=128, page_size=64, dtype="bf16"),
+    "c5": dict(desc="long-context stress: 32 requests, 32k-token KV prefixes, 64-node trees, Llama-3-8B shapes",
+               n_req=32, d=8, w=8, sigma=(1.0, 4.0), A=9.0, n_max=63, budget=2048, L=32768, n_q=32, n_kv=8,
+               head_dim=128, page_size=64, dtype="bf16"),
+}
+CONFIG_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}
+METRIC = "verified tree tokens/sec and attn HBM GB/s (% roofline) at 1/2/4/8 B200"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# --------------------------------------------------------------------------- workload
+def make_workload(cfg_name, device="cuda", seed_salt=0, rank=0, world=1, engine="ours"):
+    """Synthetic inputs with the shapes of BASELINE config `cfg_name`.
+    KV-head sharding: this rank holds kv heads [rank*n_kv/world, (rank+1)*n_kv/world).
+    engine="ours" builds the CUDA-path buffers; engine="oracle" (the --impl
+    reference arm, CPU only) builds host tensors and never touches the library."""
+    c = dict(CONFIGS[cfg_name])
+    rng = synth.rng_for(CONFIG_INDEX[cfg_name], seed_salt)
+    n = c["n_req"]
+    F = synth.beam_forest(rng, n, c["d"], c["w"], *c["sigma"])
+    if c["A"] == "mix":
+        A = synth.slo_mix(rng, n)
+    elif c["A"] == "c1":
+        A = np.array([0.5])
+    else:
+        A = np.full(n, float(c["A"]))
+    assert c["n_kv"] % world == 0, "KV-head sharding needs n_kv % world == 0"
+    n_kv = c["n_kv"] // world
+    G = c["n_q"] // c["n_kv"]
+    n_q = n_kv * G
+    D = c["head_dim"]
+    ps = c["page_size"]
+    kv_len = np.full(n, c["L"], np.int32)
+    table, n_pages = synth.paged_kv(rng, kv_len, ps, extra_slots=c["d"] + 1)
+    R = c["budget"]  # tree rows allocated = budget (upper bound of sum K_i)
+    dt = torch.float32 if c["dtype"] == "f32" else torch.bfloat16
+    gen = torch.Generator(device=device).manual_seed(synth.SEED_BASE + 17 * CONFIG_INDEX[cfg_name] + 1000 * seed_salt
+                                                     + 7919 * rank)
+    kv_bytes = 2 * n_pages * n_kv * ps * D * (4 if dt == torch.float32 else 2)
+    n_pools = 1 if kv_bytes >= 3 * L2_BYTES else int(math.ceil(3 * L2_BYTES / kv_bytes))
+    if cfg_name == "c1":
+        n_pools = 1
+
+    def rnd(*shape):
+        return torch.randn(*shape, generator=gen, device=device, dtype=torch.float32).to(dt)
+
+    pools = [(rnd(n_pages, n_kv, ps, D), rnd(n_pages, n_kv, ps, D)) for _ in range(n_pools)]
+    W = dict(cfg=cfg_name, c=c, host=F, A=A, n=n, n_q=n_q, n_kv=n_kv, D=D, page_size=ps, R=R, dtype=dt,
+             sm_scale=float(np.float32(1.0 / math.sqrt(D))), rank=rank, world=world, n_pools=n_pools,
+             kv_bytes=kv_bytes, pools=pools, pool_idx=0, device=device, kv_len_host=kv_len, table_host=table,
+             n_pages=n_pages)
+    W["cand_offsets"] = torch.from_numpy(F["cand_offsets"]).to(device)
+    W["cand_parent"] = torch.from_numpy(F["cand_parent"]).to(device)
+    W["cand_prob"] = torch.from_numpy(F["cand_prob"]).to(device)
+    W["cand_token"] = torch.from_numpy(F["cand_token"]).to(device)
+    W["slo_deficit"] = torch.from_numpy(np.ascontiguousarray(A, np.float64)).to(device)
+    W["page_table"] = torch.from_numpy(table).to(device)
+    W["kv_len0"] = torch.from_numpy(kv_len).to(device)
+    W["kv_len"] = W["kv_len0"].clone()
+    W["q"] = rnd(R, n_q, D)
+    W["k_tree"] = rnd(R, n_kv, D)
+    W["v_tree"] = rnd(R, n_kv, D)
+    W["out"] = torch.empty_like(W["q"])
+    W["sample_requests"] = sorted(set([0, n // 3, n - 1]))
+    W["max_path"] = c["d"] + 1
+    if engine == "oracle":
+        import oracle  # reference arm only
+        sel = oracle.select_literal(F["cand_offsets"], F["cand_parent"], F["cand_prob"], A, c["d"], c["n_max"],
+                                    c["budget"])
+        _set_targets(W, sel["tree_offsets"], sel["tree_src"])
+        return W
+    import paper_2501_12162_b200 as ada
+    W["ada"] = ada
+    N = int(F["cand_offsets"][-1])
+    W["ws_select"] = ada.Workspace(ada.select_workspace_size(n, N), device)
+    W["ws_attn"] = ada.Workspace(ada.attn_workspace_size(1, n, R, n_q, D, c["L"]), device)
+    W["ws_accept"] = ada.Workspace(ada.accept_workspace_size(R), device)
+    dev = torch.device(device)
+    W["sel"] = dict(tree_offsets=torch.empty(n + 1, dtype=torch.int32, device=dev),
+                    tree_parent=torch.zeros(R, dtype=torch.int32, device=dev),
+                    tree_src=torch.zeros(R, dtype=torch.int32, device=dev),
+                    tree_depth=torch.zeros(R, dtype=torch.int32, device=dev),
+                    tree_token=torch.zeros(R, dtype=torch.int32, device=dev),
+                    slo_count=torch.empty(n, dtype=torch.int32, device=dev))
+    W["acc"] = dict(accept_len=torch.empty(n, dtype=torch.int32, device=dev),
+                    accept_path=torch.empty((n, W["max_path"]), dtype=torch.int32, device=dev),
+                    bonus_token=torch.empty(n, dtype=torch.int32, device=dev))
+    # Per-node target samples (the target model's output at every tree node): the
+    # trees are a deterministic function of the forest, so they are fixed once from
+    # the first (GPU) selection and gathered on the host (synthetic target model).
+    run_select(W)
+    _set_targets(W, W["sel"]["tree_offsets"].cpu().numpy(), W["sel"]["tree_src"].cpu().numpy())
+    return W
+
+
+def _set_targets(W, to, src):
+    F, n, R = W["host"], W["n"], W["R"]
+    used = int(to[-1])
+    req = np.repeat(np.arange(n), np.diff(to))
+    tgt = np.zeros(R, np.int32)
+    tgt[:used] = F["cand_target"][F["cand_offsets"][req] + src[:used]]
+    W["target_tokens"] = torch.from_numpy(tgt).to(W["device"])
+    W["tree_sizes"] = np.diff(to)
+    W["tree_tokens_total"] = used
+
+
+def run_select(W):
+    ada = W["ada"]
+    ada.select_trees(W["cand_offsets"], W["cand_parent"], W["cand_prob"], W["slo_deficit"], W["c"]["d"],
+                     W["c"]["n_max"], W["c"]["budget"], cand_token=W["cand_token"], out=W["sel"],
+                     workspace=W["ws_select"])
+
+
+def run_attention(W):
+    ada = W["ada"]
+    kc, vc = W["pools"][W["pool_idx"]]
+    out, _ = ada.tree_verify_attn(W["q"], W["k_tree"], W["v_tree"], kc, vc, W["page_table"], W["kv_len"],
+                                  W["sel"]["tree_offsets"], W["sel"]["tree_parent"], W["sm_scale"], out=W["out"],
+                                  workspace=W["ws_attn"])
+    return out
+
+
+def run_accept(W, phase=None, req_range=None):
+    ada = W["ada"]
+    kc, vc = W["pools"][W["pool_idx"]]
+    ada.accept_tokens(ada.AS_ACCEPT_FUSED if phase is None else phase, W["sel"]["tree_offsets"],
+                      W["sel"]["tree_parent"], W["sel"]["tree_token"], target_tokens=W["target_tokens"],
+                      max_path=W["max_path"], k_tree=W["k_tree"], v_tree=W["v_tree"], k_cache=kc, v_cache=vc,
+                      page_table=W["page_table"], kv_len=W["kv_len"], req_range=req_range,
+                      accept_len=W["acc"]["accept_len"], accept_path=W["acc"]["accept_path"],
+                      bonus_token=W["acc"]["bonus_token"], n_tree_rows=W["R"], workspace=W["ws_accept"])
+
+
+def attn_algorithmic_bytes(W):
+    """Per launch: K and V of every (request, kv head) prefix + tree (read once),
+    Q read and O written once."""
+    eb = 4 if W["dtype"] == torch.float32 else 2
+    D = W["D"]
+    L = W["kv_len_host"].astype(np.int64)
+    K = W["tree_sizes"].astype(np.int64)
+    kv = int(np.sum(2 * D * eb * (L + K))) * W["n_kv"]
+    qo = int(np.sum(K)) * W["n_q"] * D * eb * 2
+    return kv + qo
+
+
+def attn_flops(W):
+    D = W["D"]
+    L = W["kv_len_host"].astype(np.int64)
+    K = W["tree_sizes"].astype(np.int64)
+    return int(np.sum(4 * D * K * L)) * W["n_q"]
+
+
+class Step:
+    """One hot-path step on the current stream; records per-kernel events."""
+
+    def __init__(self, W, dist_ctx=None):
+        self.W = W
+        self.dist = dist_ctx
+        self.ev = None
+
+    def __call__(self, record=False):
+        W = self.W
+        W["pool_idx"] = (W["pool_idx"] + 1) % W["n_pools"]
+        W["kv_len"].copy_(W["kv_len0"], non_blocking=True)
+        if record:
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record()
+        run_select(W)
+        if record:
+            e[1].record()
+        run_attention(W)
+        if record:
+            e[2].record()
+        if self.dist is None:
+            run_accept(W)
+        else:
+            self.dist.accept_and_commit(W)
+        if record:
+            e[3].record()
+            self.ev = e
+        return self.ev
+
+
+def _clock_sampler_start():
+    try:
+        return subprocess.Popen(
+            ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+             "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+            text=True)
+    except Exception:
+        return None
+
+
+def _clock_sampler_stop(p, dev_index):
+    if p is None:
+        return None
+    time.sleep(0.25)
+    p.terminate()
+    try:
+        out = p.communicate(timeout=5)[0]
+    except Exception:
+        return None
+    sm, mx, reasons = [], [], set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in out.strip().splitlines():
+        f = [x.strip() for x in line.split(",")]
+        if len(f) < 9 or f[0] != str(dev_index):
+            continue
+        try:
+            sm.append(float(f[1]))
+            mx.append(float(f[2]))
+        except ValueError:
+            continue
+        for nm, v in zip(names, f[5:9]):
+            if v.lower() == "active":
+                reasons.add(nm)
+    if not sm:
+        return None
+    return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+def _traffic_from_profiles(cfg):
+    p = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(cfg)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- CPU oracle legs
+def cpu_oracle_sample(W, n_sample_req, threads):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload:
+    full select (Alg. 2 literal), attention for `n_sample_req` requests, and the
+    walk + commit for those requests.  Returns (tokens, seconds, description)."""
+    import oracle  # test/baseline infrastructure only
+    F = W["host"]
+    c = W["c"]
+    t0 = time.perf_counter()
+    sel = oracle.select_literal(F["cand_offsets"], F["cand_parent"], F["cand_prob"], W["A"], c["d"], c["n_max"],
+                                c["budget"])
+    t_sel = time.perf_counter() - t0
+    n = W["n"]
+    reqs = list(range(min(n_sample_req, n)))
+    to = sel["tree_offsets"]
+    rows = np.concatenate([np.arange(to[i], to[i + 1]) for i in reqs])
+    sizes = np.array([to[i + 1] - to[i] for i in reqs])
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    pt = W["table_host"][reqs]
+    used = np.unique(pt[pt >= 0])
+    remap = -np.ones(W["n_pages"], np.int64)
+    remap[used] = np.arange(len(used))
+    pt2 = np.where(pt >= 0, remap[np.maximum(pt, 0)], -1).astype(np.int32)
+    idx = torch.from_numpy(used).to(W["device"])
+    kc, vc = W["pools"][0]
+    hk = kc.index_select(0, idx).float().cpu().numpy()
+    hv = vc.index_select(0, idx).float().cpu().numpy()
+    rows_t = torch.from_numpy(rows).to(W["device"])
+    q = W["q"].index_select(0, rows_t).float().cpu().numpy()
+    kt = W["k_tree"].index_select(0, rows_t).float().cpu().numpy()
+    vt = W["v_tree"].index_select(0, rows_t).float().cpu().numpy()
+    kl = W["kv_len_host"][reqs].copy()
+    t0 = time.perf_counter()
+    oracle.tree_attn(q, kt, vt, hk, hv, pt2, kl, offs, sel["tree_parent"][rows], np.float32(W["sm_scale"]),
+                     n_threads=threads, want_lse=False)
+    t_attn = time.perf_counter() - t0
+    toks = np.asarray(F["cand_token"])
+    req_of = np.repeat(np.arange(len(reqs)), sizes)
+    tt = toks[F["cand_offsets"][np.array(reqs)][req_of] + sel["tree_src"][rows]]
+    tg = W["target_tokens"].cpu().numpy()[rows]
+    t0 = time.perf_counter()
+    acc = oracle.accept_walk(offs, sel["tree_parent"][rows], tt, target_tokens=tg, max_path=W["max_path"])
+    oracle.commit(offs, acc["accept_len"], acc["accept_path"], kt, vt, hk, hv, pt2, kl)
+    t_acc = time.perf_counter() - t0
+    frac = len(reqs) / n
+    secs = t_sel * frac + t_attn + t_acc
+    desc = (f"oracle (C, fp64) on {len(reqs)}/{n} requests of {W['cfg']}: attention + walk/commit for those "
+            f"requests, Alg. 2 select on the full batch pro-rated ({t_sel:.3f}s x {frac:.3f}); {threads} threads")
+    return int(sizes.sum()), secs, desc
+
+
+# --------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e / cpu legs)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return main_reference(args, rank, world)
+    torch.cuda.set_device(local_rank)
+    dist_ctx = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        from paper_2501_12162_b200.dist import ShardedAccept
+        dist_ctx = ShardedAccept(rank, world)
+    W = make_workload(args.config, "cuda", rank=rank, world=world)
+    step = Step(W, dist_ctx)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler = None if args.profile else _clock_sampler_start()
+    if sampler is not None:
+        time.sleep(0.3)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    evs = []
+    start.record()
+    for _ in range(args.steps):
+        evs.append(step(record=True))
+    end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = _clock_sampler_stop(sampler, local_rank)
+    total_ms = start.elapsed_time(end)
+    t_sel = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    t_attn = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+    t_acc = float(np.mean([e[2].elapsed_time(e[3]) for e in evs]))
+    if world > 1:
+        t = torch.tensor([total_ms, t_attn], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms, t_attn_max = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    tokens = int(W["tree_tokens_total"])
+    value = tokens / (ms_per_step / 1e3)
+
+    peaks, peak_kind = _peaks()
+    abytes = attn_algorithmic_bytes(W)
+    aflops = attn_flops(W)
+    achieved_gbs = abytes / (t_attn / 1e3) / 1e9
+    hbm_peak = float(peaks["hbm_gbs"])
+    roofline = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved_gbs / hbm_peak, 4), "traffic": _traffic_from_profiles(args.config),
+                "kernel": "tree_attn_tc_kernel" if W["dtype"] == torch.bfloat16 else "tree_attn_simt_kernel",
+                "algorithmic_bytes_per_launch": abytes, "attn_ms": round(t_attn, 4),
+                "tensor_tflops": round(aflops / (t_attn / 1e3) / 1e12, 1),
+                "tensor_frac_sustained": round(aflops / (t_attn / 1e3) / 1e12 / float(peaks.get(
+                    "bf16_tflops_sustained", 1400.0)), 4), "peak_source": peak_kind}
+
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        e2e = measure_e2e(W, step, args.steps, world)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        threads = os.cpu_count() or 1
+        n_s = {"c1": 1, "c2": 6, "c3": 24, "c4": 3, "c5": 1}[args.config]
+        toks, secs, desc = cpu_oracle_sample(W, n_s, threads)
+        cpu = {"value": round(toks / secs, 2), "unit": "tree tokens/s", "cores": threads, "kind": "oracle",
+               "sample": desc, "seconds": round(secs, 3)}
+    launches_per_step = 3
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "verified tree tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16" if W["dtype"] == torch.bfloat16 else "f32", "data": "synthetic (seeded; no datasets)",
+            "config": {"workload": f"{args.config}: {W['c']['desc']}", "n_req": W["n"],
+                       "tree_tokens": tokens, "kv_len": W["c"]["L"], "q_heads": W["c"]["n_q"],
+                       "kv_heads": W["c"]["n_kv"], "head_dim": W["D"], "page_size": W["page_size"],
+                       "budget": W["c"]["budget"], "parallelism": f"kv-head sharding x{world}" if world > 1
+                       else "1 GPU", "l2": ("inputs larger than L2: KV %.0f MiB/GPU" % (W["kv_bytes"] / 2**20))
+                       if W["n_pools"] == 1 else f"{W['n_pools']} rotating KV pools (> 3x L2)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+            "breakdown_ms": {"select": round(t_sel, 4), "attention": round(t_attn, 4), "accept_commit": round(t_acc, 4)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def measure_e2e(W, step, steps, world):
+    """Same metric through the public API with HOST inputs: each step copies its
+    inputs (candidate forest, A, q/k_tree/v_tree, per-node targets) from pinned
+    host memory and reads the accept records back."""
+    names = ["cand_offsets", "cand_parent", "cand_prob", "cand_token", "slo_deficit", "q", "k_tree", "v_tree",
+             "target_tokens"]
+    host = {k: W[k].cpu().pin_memory() for k in names}
+    outs = ["accept_len", "accept_path", "bonus_token"]
+    host_out = {k: torch.empty_like(W["acc"][k], device="cpu").pin_memory() for k in outs}
+    h2d = sum(host[k].numel() * host[k].element_size() for k in names)
+    d2h = sum(host_out[k].numel() * host_out[k].element_size() for k in outs)
+    for _ in range(2):
+        for k in names:
+            W[k].copy_(host[k], non_blocking=True)
+        step()
+        for k in outs:
+            host_out[k].copy_(W["acc"][k], non_blocking=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        for k in names:
+            W[k].copy_(host[k], non_blocking=True)
+        step()
+        for k in outs:
+            host_out[k].copy_(W["acc"][k], non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t[0])
+    v = W["tree_tokens_total"] / (ms / steps / 1e3)
+    return {"value": round(v, 1), "unit": "verified tree tokens/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms / steps, 4)}
+
+
+def main_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands (this tier's reference arm)."""
+    if rank != 0:
+        return
+    W = make_workload(args.config, "cpu", engine="oracle")
+    threads = os.cpu_count() or 1
+    n_s = {"c1": 1, "c2": 2, "c3": 8, "c4": 1, "c5": 1}[args.config]
+    for _ in range(args.warmup):
+        cpu_oracle_sample(W, n_s, threads)
+    tot_tok, tot_s = 0, 0.0
+    desc = ""
+    for _ in range(args.steps):
+        toks, secs, desc = cpu_oracle_sample(W, n_s, threads)
+        tot_tok += toks
+        tot_s += secs
+    value = tot_tok / tot_s
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": "verified tree tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * tot_s / args.steps, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; no datasets)",
+            "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}"},
+            "cpu_baseline": {"value": round(value, 2), "unit": "verified tree tokens/s", "cores": threads,
+                             "kind": "oracle", "sample": desc},
+            "e2e": {"value": round(value, 2), "unit": "verified tree tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

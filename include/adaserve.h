@@ -1,0 +1,232 @@
+/*
+ * adaserve.h -- C ABI of the B200-native AdaServe hot path (libadaserve.so).
+ *
+ * The three calls are the data-parallel hot path of one speculate-select-verify
+ * iteration of AdaServe (arXiv 2501.12162, "SLO-Customized LLM Serving with
+ * Fine-Grained Speculative Decoding").  Citations "P:Lnnn" are lines of the
+ * paper's LaTeX source; "Rnn" are the readings listed in DESIGN.md
+ * where the paper is silent or ambiguous.
+ *
+ *   as_select_trees      Alg. 2 SLO-customized + throughput-optimized selection
+ *                         on the GPU.
+ *   as_tree_verify_attn  Step 4 verification attention:
+ *                        every tree node attends to its request's paged KV
+ *                        prefix plus its tree ancestors.
+ *   as_accept_tokens     "uses these logits to identify the verified tokens"
+ *                        (P:L860): greedy/stochastic acceptance walk and the
+ *                        KV commit of the accepted path.
+ *
+ * Conventions (all calls):
+ *  - Every pointer argument is a DEVICE pointer unless stated otherwise; all
+ *    arrays are dense, row-major, naturally aligned; tensors of bf16/fp32
+ *    elements additionally need 16-byte aligned base pointers and row strides.
+ *  - Calls are asynchronous and ordered on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream).  The library never allocates or frees
+ *    device memory and never synchronises the host (except as_check_device_error).
+ *  - Scratch memory is caller-owned `workspace` of at least as_*_workspace_size()
+ *    bytes, 256-byte aligned, ZERO-FILLED ONCE before its first use (the library
+ *    leaves it reusable after every call).  One workspace must not be used by two
+ *    calls that may run concurrently.
+ *  - Host-checkable errors return a status and launch nothing.  Data-dependent
+ *    precondition violations (listed per call) are detected on the device: the
+ *    kernel records a sticky {code, request} pair in the workspace header and
+ *    still finishes with defined-but-unspecified outputs; read it with
+ *    as_check_device_error().  Launch failures return AS_ERR_CUDA.  No C++
+ *    exception crosses this ABI.  Thread-safe and re-entrant.
+ */
+#ifndef ADASERVE_H_
+#define ADASERVE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    AS_OK = 0,
+    AS_ERR_INVALID_ARG = 1,      /* null pointer, negative size, inconsistent shape  */
+    AS_ERR_BUDGET_TOO_SMALL = 2, /* budget < n_req (R10)                             */
+    AS_ERR_UNSUPPORTED = 3,      /* head_dim / page_size / dtype / GQA ratio        */
+    AS_ERR_WORKSPACE = 4,        /* workspace too small or misaligned                */
+    AS_ERR_CUDA = 5              /* a CUDA runtime/driver call failed               */
+} as_status;
+
+typedef enum { AS_F32 = 0, AS_BF16 = 1 } as_dtype;
+
+/* Device-side precondition codes (workspace header, see as_check_device_error). */
+enum {
+    AS_DEV_OK = 0,
+    AS_DEV_BAD_PARENT = 1,     /* parent not in [0, j) for node j > 0 (not topological)   */
+    AS_DEV_BAD_PROB = 2,       /* f-hat NaN, <= 0, or > f-hat(parent)                     */
+    AS_DEV_TOO_MANY_CAND = 3,  /* a request has more than AS_MAX_CAND non-root candidates */
+    AS_DEV_TREE_TOO_BIG = 4,   /* a tree exceeds AS_MAX_TREE nodes in attention          */
+    AS_DEV_ROWS_OVERFLOW = 5,  /* tree_offsets[n_req] > n_tree_rows                       */
+    AS_DEV_PAGE_OVERFLOW = 6,  /* a KV slot falls outside the request's page-table row    */
+    AS_DEV_NAN_LOGIT = 7,      /* NaN in target_logits                                    */
+    AS_DEV_PATH_TOO_LONG = 8,  /* accepted path longer than max_path (truncated)          */
+    AS_DEV_BAD_PAGE = 9        /* page id outside [0, num_pages)                          */
+};
+
+#define AS_MAX_TREE 128 /* nodes per tree (incl. root) accepted by as_tree_verify_attn */
+#define AS_MAX_CAND 256 /* non-root candidates per request accepted by as_select_trees */
+
+/* ------------------------------------------------------------------------- */
+/* Select: Alg. 2                                                */
+/* ------------------------------------------------------------------------- */
+/*
+ * Builds each request's draft token tree from its candidate tree (the beam of
+ * Step 1) under the global budget B (Eq. 1) and the
+ * per-request SLO threshold A_cap(r) = min(A(r), d+1):
+ *   roots are charged first (B0 = B - n, R1);
+ *   SLO stage: requests in descending A (ties: lower id, R5) take their best
+ *     remaining candidates (f-hat desc, then lower local index, R8) while
+ *     1.0 + sum f-hat (fp64, R3/R9) < A_cap, at most n_max each (R6), and while
+ *     budget remains (R2);
+ *   throughput stage: the remaining budget goes to the global best candidates
+ *     (f-hat desc, request asc, index asc, R8).
+ * The result is bit-identical to the sequential algorithm (the oracle).
+ *
+ * Inputs (device):
+ *   cand_offsets [n_req+1]  CSR offsets; request i owns candidates
+ *                           [cand_offsets[i], cand_offsets[i+1]); local index 0
+ *                           is the root; 1 <= C_i, C_i - 1 <= AS_MAX_CAND.
+ *   cand_parent  [N]        local parent; parent of root = 0; 0 <= parent[j] < j.
+ *   cand_prob    [N] f32    f-hat = product of draft conditionals on the path
+ *                           (P:L691-694); root 1.0; 0 < f[j] <= f[parent[j]].
+ *   cand_token   [N] i32    draft token id per candidate, or NULL.
+ *   slo_deficit  [n_req] f64  A(r_i) = (l_i + t_spec)/t_TPOT_i - o_i, finite.
+ * Scalars (host): n_req >= 0; n_cand_total = cand_offsets[n_req] (host copy,
+ *   used only to size/check the workspace); depth_d >= 0 (R11); n_max >= 0;
+ *   budget >= n_req.
+ * Outputs (device):
+ *   tree_offsets [n_req+1]  tree_offsets[n_req] = nodes used <= budget.
+ *   tree_parent  [budget]   compact local parent (root -> 0), topological.
+ *   tree_src     [budget]   local candidate index, ascending within a tree.
+ *   tree_depth   [budget]   or NULL.
+ *   tree_token   [budget]   cand_token[src] or NULL (requires cand_token).
+ *   slo_count    [n_req]    non-root nodes taken in the SLO stage, or NULL.
+ *   Entries beyond tree_offsets[n_req] are left untouched.
+ * Device preconditions: AS_DEV_BAD_PARENT, AS_DEV_BAD_PROB, AS_DEV_TOO_MANY_CAND.
+ */
+size_t as_select_workspace_size(int32_t n_req, int32_t n_cand_total);
+as_status as_select_trees(int32_t n_req, int32_t n_cand_total, const int32_t* cand_offsets,
+                          const int32_t* cand_parent, const float* cand_prob,
+                          const int32_t* cand_token, const double* slo_deficit, int32_t depth_d,
+                          int32_t n_max, int32_t budget, int32_t* tree_offsets,
+                          int32_t* tree_parent, int32_t* tree_src, int32_t* tree_depth,
+                          int32_t* tree_token, int32_t* slo_count, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------- */
+/* Verify: tree-masked attention over the paged KV cache */
+/* ------------------------------------------------------------------------- */
+/*
+ * For request i, tree node j (global row r = tree_offsets[i] + j) and query
+ * head h (kv head h / (n_q_heads / n_kv_heads)):
+ *   out[r, h] = softmax_k(sm_scale * q[r,h] . key_k) value_k
+ * over the keys k = committed prefix positions t < kv_len[i] (key/value at page
+ * page_table[i][t / page_size], slot t % page_size of k_cache / v_cache) and the
+ * tree nodes u that are ancestors of j or j itself (k_tree/v_tree rows
+ * tree_offsets[i] + u) (R15, R16).  A chain tree is exactly causal decoding.
+ * lse[r, h] = natural log of sum_k exp(sm_scale q.key_k) (optional).
+ *
+ * dtype AS_BF16: q, k_tree, v_tree, caches, out are bf16; tcgen05 tensor-core
+ *   path (fp32 accumulation in TMEM, fp32 softmax, P rounded to bf16).
+ * dtype AS_F32: all fp32; CUDA-core path (the 1e-5 parity configuration).
+ * Layouts:
+ *   q, out        [n_tree_rows, n_q_heads, head_dim]
+ *   k_tree,v_tree [n_tree_rows, n_kv_heads, head_dim]   (RoPE already applied)
+ *   k_cache,v_cache [num_pages, n_kv_heads, page_size, head_dim]
+ *   page_table    [n_req, max_pages_per_req] i32
+ *   kv_len        [n_req] i32, 0 <= kv_len[i] <= max_pages_per_req * page_size
+ *   tree_offsets  [n_req+1], tree_parent [n_tree_rows] (compact local parents,
+ *                 as produced by as_select_trees); rows >= tree_offsets[n_req]
+ *                 of out/lse are not written.
+ *   lse           [n_tree_rows, n_q_heads] f32, or NULL.
+ * Supported: head_dim in {64, 128}; page_size in {16, 32, 64, 128};
+ *   n_q_heads % n_kv_heads == 0; for AS_BF16 the group size n_q/n_kv must be
+ *   a power of two <= 16.  Heads are the caller's LOCAL heads (KV-head sharding).
+ * Device preconditions: AS_DEV_TREE_TOO_BIG, AS_DEV_BAD_PARENT,
+ *   AS_DEV_ROWS_OVERFLOW, AS_DEV_BAD_PAGE.
+ */
+size_t as_attn_workspace_size(as_dtype dtype, int32_t n_req, int32_t n_tree_rows,
+                              int32_t n_q_heads, int32_t head_dim, int32_t max_kv_len);
+as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows,
+                              int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
+                              const void* q, const void* k_tree, const void* v_tree,
+                              const void* k_cache, const void* v_cache, int32_t num_pages,
+                              int32_t page_size, const int32_t* page_table,
+                              int32_t max_pages_per_req, const int32_t* kv_len,
+                              const int32_t* tree_offsets, const int32_t* tree_parent,
+                              float sm_scale, void* out, float* lse, void* workspace,
+                              size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------- */
+/* Accept: acceptance walk + KV commit                               */
+/* ------------------------------------------------------------------------- */
+/*
+ * Walk (R13/R14): for each request in [req_begin, req_end): v = root; repeat
+ *   t* = target token at v (target_tokens[row] if target_tokens != NULL, else
+ *   the argmax of target_logits[row, :] with the lowest index winning ties);
+ *   move to the lowest-index child c of v with tree_tokens[c] == t*, else stop.
+ *   accept_len[i] = nodes on the path including the root; accept_path[i][k] =
+ *   local index of the k-th path node (-1 padded to max_path); bonus_token[i] = t*
+ *   at the last accepted node.  With target_tokens holding per-node samples of
+ *   the target distribution this is the lossless stochastic walk for which
+ *   E[accept_len] = sum_v f(v) (Thm. 1).
+ * Commit (R14/R16): rows accept_path[i][0..len) of k_tree/v_tree are copied
+ *   into cache slots [kv_len[i], kv_len[i] + len) through the page table, then
+ *   kv_len[i] += len.  COMMIT covers ALL requests [0, n_req) (for KV-head
+ *   sharding every rank commits every request's path for its own heads).
+ * Phases: AS_ACCEPT_FUSED = walk [begin,end) + commit of the same requests;
+ *   AS_ACCEPT_WALK_ONLY = walk only; AS_ACCEPT_COMMIT_ONLY = commit from
+ *   accept_len/accept_path given as inputs (e.g. after an all-gather).
+ * Inputs: tree_offsets [n_req+1], tree_parent/tree_tokens [n_tree_rows];
+ *   target_tokens [n_tree_rows] or NULL; target_logits [n_tree_rows, vocab] of
+ *   logits_dtype or NULL (one of the two is required for the walk);
+ *   k_tree/v_tree [n_tree_rows, n_kv_heads, head_dim] of kv_dtype;
+ *   caches [num_pages, n_kv_heads, page_size, head_dim]; page_table
+ *   [n_req, max_pages_per_req]; kv_len [n_req] (in/out).
+ * For WALK_ONLY the KV arguments may be NULL.
+ * Device preconditions: AS_DEV_NAN_LOGIT, AS_DEV_PATH_TOO_LONG,
+ *   AS_DEV_PAGE_OVERFLOW, AS_DEV_BAD_PAGE.
+ */
+typedef enum { AS_ACCEPT_FUSED = 0, AS_ACCEPT_WALK_ONLY = 1, AS_ACCEPT_COMMIT_ONLY = 2 } as_accept_phase;
+
+size_t as_accept_workspace_size(int32_t n_tree_rows);
+as_status as_accept_tokens(as_accept_phase phase, int32_t n_req, int32_t req_begin,
+                           int32_t req_end, int32_t n_tree_rows, const int32_t* tree_offsets,
+                           const int32_t* tree_parent, const int32_t* tree_tokens,
+                           const int32_t* target_tokens, const void* target_logits,
+                           as_dtype logits_dtype, int32_t vocab, int32_t max_path,
+                           int32_t* accept_len, int32_t* accept_path, int32_t* bonus_token,
+                           const void* k_tree, const void* v_tree, as_dtype kv_dtype,
+                           int32_t n_kv_heads, int32_t head_dim, void* k_cache, void* v_cache,
+                           int32_t num_pages, int32_t page_size, const int32_t* page_table,
+                           int32_t max_pages_per_req, int32_t* kv_len, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------- */
+/* Utilities                                                                 */
+/* ------------------------------------------------------------------------- */
+const char* as_status_string(as_status s);
+const char* as_version(void);
+/* Synchronises `stream`, then copies the workspace header's sticky device error
+ * {code, request} to the HOST pointers (either may be NULL).  Tests/debug only. */
+as_status as_check_device_error(const void* workspace, int32_t* code, int32_t* request,
+                                void* stream);
+/* Zero-fills a workspace (async on stream); equivalent to cudaMemsetAsync(ws, 0, bytes). */
+as_status as_reset_workspace(void* workspace, size_t workspace_bytes, void* stream);
+/* Self-test of the tcgen05/TMA building blocks used by the bf16 attention:
+ * D[M=128, N] = A[128, K] . B[N, K]^T with bf16 A/B (device, K-major rows) and
+ * fp32 D (device), N in {64,128}, K in {64,128}; b_mn_major != 0 treats B as
+ * [K, N] (N contiguous), as the PV product does with V.  Debug/tests only. */
+as_status as_selftest_umma(const void* a, const void* b, float* d, int32_t n, int32_t k,
+                           int32_t b_mn_major, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADASERVE_H_ */

@@ -1,0 +1,236 @@
+"""B200-native AdaServe hot path: select -> tree-verify attention -> accept.
+
+Thin Python binding over ``libadaserve.so`` (C ABI declared in
+``include/adaserve.h``).  This module only marshals torch tensors (device
+memory, the current CUDA stream) into the C calls; every step of the path runs
+in the library's CUDA kernels.  There is no CPU fallback: if the library is
+missing or a tensor is not on a CUDA device, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+__all__ = ["lib", "select_trees", "tree_verify_attn", "accept_tokens", "Workspace", "check_device_error",
+           "selftest_umma", "AS_ACCEPT_FUSED", "AS_ACCEPT_WALK_ONLY", "AS_ACCEPT_COMMIT_ONLY", "AdaServeError",
+           "select_workspace_size", "attn_workspace_size", "accept_workspace_size", "DEVICE_ERRORS"]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libadaserve.so")
+
+AS_F32, AS_BF16 = 0, 1
+AS_ACCEPT_FUSED, AS_ACCEPT_WALK_ONLY, AS_ACCEPT_COMMIT_ONLY = 0, 1, 2
+DEVICE_ERRORS = {0: "ok", 1: "bad parent", 2: "bad f-hat", 3: "too many candidates", 4: "tree too big",
+                 5: "rows overflow", 6: "page overflow", 7: "NaN logit", 8: "path too long", 9: "bad page"}
+
+_c_i32, _c_sz, _vp, _f32 = ctypes.c_int32, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_float
+_lib = None
+
+
+class AdaServeError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load libadaserve.so (built in-tree by ``build.py``); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise AdaServeError(f"{LIB_PATH} not built: run `python -m paper_2501_12162_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        L.as_status_string.restype = ctypes.c_char_p
+        L.as_version.restype = ctypes.c_char_p
+        for name in ("as_select_workspace_size", "as_attn_workspace_size", "as_accept_workspace_size"):
+            getattr(L, name).restype = _c_sz
+        L.as_select_workspace_size.argtypes = [_c_i32, _c_i32]
+        L.as_attn_workspace_size.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32]
+        L.as_accept_workspace_size.argtypes = [_c_i32]
+        L.as_select_trees.argtypes = [_c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32,
+                                      _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_sz, _vp]
+        L.as_tree_verify_attn.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp,
+                                          _c_i32, _c_i32, _vp, _c_i32, _vp, _vp, _vp, _f32, _vp, _vp, _vp, _c_sz,
+                                          _vp]
+        L.as_accept_tokens.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_i32,
+                                       _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _vp,
+                                       _c_i32, _c_i32, _vp, _c_i32, _vp, _vp, _c_sz, _vp]
+        L.as_check_device_error.argtypes = [_vp, _vp, _vp, _vp]
+        L.as_reset_workspace.argtypes = [_vp, _c_sz, _vp]
+        L.as_selftest_umma.argtypes = [_vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _vp]
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise AdaServeError(f"{what}: {lib().as_status_string(status).decode()} (status {status})")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise AdaServeError("tensors must live on a CUDA device (no CPU fallback)")
+    if not t.is_contiguous():
+        raise AdaServeError("tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dt(t):
+    if t.dtype == torch.bfloat16:
+        return AS_BF16
+    if t.dtype == torch.float32:
+        return AS_F32
+    raise AdaServeError(f"unsupported dtype {t.dtype}")
+
+
+def _need(t, dtype, name):
+    if t.dtype != dtype:
+        raise AdaServeError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def select_workspace_size(n_req, n_cand_total):
+    return int(lib().as_select_workspace_size(n_req, n_cand_total))
+
+
+def attn_workspace_size(dtype, n_req, n_tree_rows, n_q, head_dim, max_kv_len):
+    return int(lib().as_attn_workspace_size(dtype, n_req, n_tree_rows, n_q, head_dim, max_kv_len))
+
+
+def accept_workspace_size(n_tree_rows):
+    return int(lib().as_accept_workspace_size(n_tree_rows))
+
+
+class Workspace:
+    """A zero-initialised device scratch buffer (the C ABI's `workspace`)."""
+
+    def __init__(self, nbytes: int, device=None):
+        self.nbytes = max(256, int(nbytes))
+        self.buf = torch.zeros(self.nbytes + 256, dtype=torch.uint8, device=device or "cuda")
+        off = (-self.buf.data_ptr()) % 256
+        self.view = self.buf[off:off + self.nbytes]
+
+    @property
+    def ptr(self):
+        return ctypes.c_void_p(self.view.data_ptr())
+
+    def ensure(self, nbytes):
+        if nbytes > self.nbytes:
+            self.__init__(nbytes, self.buf.device)
+        return self
+
+
+def check_device_error(ws: Workspace):
+    code, req = ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(lib().as_check_device_error(ws.ptr, ctypes.byref(code), ctypes.byref(req), _stream()), "check")
+    return code.value, req.value
+
+
+# ---------------------------------------------------------------------------
+def select_trees(cand_offsets, cand_parent, cand_prob, slo_deficit, depth_d, n_max, budget, cand_token=None,
+                 n_cand_total=None, out=None, workspace=None):
+    """as_select_trees (Alg. 2).  Inputs are device tensors:
+    cand_offsets/cand_parent int32, cand_prob float32, slo_deficit float64,
+    cand_token int32 or None.  Returns dict of device int32 tensors
+    (tree_offsets [n+1], tree_parent/tree_src/tree_depth/tree_token [budget],
+    slo_count [n]).  `n_cand_total` is the host-known size of cand_prob."""
+    n = cand_offsets.numel() - 1
+    _need(cand_offsets, torch.int32, "cand_offsets")
+    _need(cand_parent, torch.int32, "cand_parent")
+    _need(cand_prob, torch.float32, "cand_prob")
+    _need(slo_deficit, torch.float64, "slo_deficit")
+    N = cand_prob.numel() if n_cand_total is None else int(n_cand_total)
+    dev = cand_prob.device
+    if out is None:
+        cap = max(int(budget), 1)
+        out = dict(tree_offsets=torch.empty(n + 1, dtype=torch.int32, device=dev),
+                   tree_parent=torch.empty(cap, dtype=torch.int32, device=dev),
+                   tree_src=torch.empty(cap, dtype=torch.int32, device=dev),
+                   tree_depth=torch.empty(cap, dtype=torch.int32, device=dev),
+                   tree_token=torch.empty(cap, dtype=torch.int32, device=dev) if cand_token is not None else None,
+                   slo_count=torch.empty(max(n, 1), dtype=torch.int32, device=dev))
+    ws = workspace if workspace is not None else Workspace(select_workspace_size(n, N), dev)
+    ws.ensure(select_workspace_size(n, N))
+    st = lib().as_select_trees(n, N, _ptr(cand_offsets), _ptr(cand_parent), _ptr(cand_prob), _ptr(cand_token),
+                               _ptr(slo_deficit), depth_d, n_max, int(budget), _ptr(out["tree_offsets"]),
+                               _ptr(out["tree_parent"]), _ptr(out["tree_src"]), _ptr(out.get("tree_depth")),
+                               _ptr(out.get("tree_token")), _ptr(out.get("slo_count")), ws.ptr, ws.nbytes,
+                               _stream())
+    _check(st, "as_select_trees")
+    out["workspace"] = ws
+    return out
+
+
+def tree_verify_attn(q, k_tree, v_tree, k_cache, v_cache, page_table, kv_len, tree_offsets, tree_parent, sm_scale,
+                     want_lse=False, out=None, lse=None, workspace=None):
+    """as_tree_verify_attn.  q [R, n_q, d], k_tree/v_tree [R, n_kv, d],
+    caches [pages, n_kv, page_size, d] (bf16 -> tcgen05 path, fp32 -> SIMT path),
+    page_table [n, max_pages] int32, kv_len [n] int32.  Returns (out, lse)."""
+    R, n_q, d = q.shape
+    n_kv = k_tree.shape[1]
+    n = tree_offsets.numel() - 1
+    dt = _dt(q)
+    for t, name in ((k_tree, "k_tree"), (v_tree, "v_tree"), (k_cache, "k_cache"), (v_cache, "v_cache")):
+        _need(t, q.dtype, name)
+    _need(page_table, torch.int32, "page_table")
+    _need(kv_len, torch.int32, "kv_len")
+    if out is None:
+        out = torch.empty_like(q)
+    if want_lse and lse is None:
+        lse = torch.empty((R, n_q), dtype=torch.float32, device=q.device)
+    ws = workspace if workspace is not None else Workspace(attn_workspace_size(dt, n, R, n_q, d, 0), q.device)
+    st = lib().as_tree_verify_attn(dt, n, R, n_q, n_kv, d, _ptr(q), _ptr(k_tree), _ptr(v_tree), _ptr(k_cache),
+                                   _ptr(v_cache), k_cache.shape[0], k_cache.shape[2], _ptr(page_table),
+                                   page_table.shape[1] if page_table.dim() == 2 else 0, _ptr(kv_len),
+                                   _ptr(tree_offsets), _ptr(tree_parent), float(sm_scale), _ptr(out),
+                                   _ptr(lse if want_lse else None), ws.ptr, ws.nbytes, _stream())
+    _check(st, "as_tree_verify_attn")
+    return out, (lse if want_lse else None)
+
+
+def accept_tokens(phase, tree_offsets, tree_parent=None, tree_tokens=None, target_tokens=None, target_logits=None,
+                  max_path=16, k_tree=None, v_tree=None, k_cache=None, v_cache=None, page_table=None, kv_len=None,
+                  req_range=None, accept_len=None, accept_path=None, bonus_token=None, n_tree_rows=None,
+                  workspace=None):
+    """as_accept_tokens (walk + commit).  Returns dict(accept_len,
+    accept_path, bonus_token); the caches and kv_len are updated in place
+    for FUSED / COMMIT_ONLY."""
+    n = tree_offsets.numel() - 1
+    dev = tree_offsets.device
+    b, e = (0, n) if req_range is None else req_range
+    R = int(n_tree_rows if n_tree_rows is not None else
+            (tree_parent.numel() if tree_parent is not None else (k_tree.shape[0] if k_tree is not None else 0)))
+    if accept_len is None:
+        accept_len = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    if accept_path is None:
+        accept_path = torch.empty((max(n, 1), max_path), dtype=torch.int32, device=dev)
+    if bonus_token is None:
+        bonus_token = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    ws = workspace if workspace is not None else Workspace(accept_workspace_size(R), dev)
+    ws.ensure(accept_workspace_size(R))
+    kv_dt = _dt(k_tree) if k_tree is not None else AS_BF16
+    lg_dt = _dt(target_logits) if target_logits is not None else AS_F32
+    vocab = target_logits.shape[1] if target_logits is not None else 0
+    n_kv = k_tree.shape[1] if k_tree is not None else 0
+    d = k_tree.shape[2] if k_tree is not None else 0
+    st = lib().as_accept_tokens(phase, n, b, e, R, _ptr(tree_offsets), _ptr(tree_parent), _ptr(tree_tokens),
+                                _ptr(target_tokens), _ptr(target_logits), lg_dt, vocab, max_path, _ptr(accept_len),
+                                _ptr(accept_path), _ptr(bonus_token), _ptr(k_tree), _ptr(v_tree), kv_dt, n_kv, d,
+                                _ptr(k_cache), _ptr(v_cache), k_cache.shape[0] if k_cache is not None else 0,
+                                k_cache.shape[2] if k_cache is not None else 0, _ptr(page_table),
+                                page_table.shape[1] if page_table is not None else 0, _ptr(kv_len), ws.ptr, ws.nbytes,
+                                _stream())
+    _check(st, "as_accept_tokens")
+    return dict(accept_len=accept_len, accept_path=accept_path, bonus_token=bonus_token, workspace=ws)
+
+
+def selftest_umma(a, b, n, k, b_mn_major):
+    """Debug: D = A . B^T (or A . B for MN-major B) through tcgen05 (see adaserve.h)."""
+    d = torch.empty((128, n), dtype=torch.float32, device=a.device)
+    _check(lib().as_selftest_umma(_ptr(a), _ptr(b), _ptr(d), n, k, int(b_mn_major), _stream()), "selftest")
+    return d

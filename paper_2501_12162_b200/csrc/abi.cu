@@ -1,0 +1,280 @@
+// abi.cu -- the extern "C" boundary of libadaserve.so (see include/adaserve.h).
+// Host-side argument checking, workspace carving, TMA tensor-map encoding and
+// kernel launches.  No exception crosses this file's functions.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
+
+#include "params.cuh"
+
+
+using namespace as;
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// bf16 tensor map, SWIZZLE_128B, zero OOB fill.  dims/box innermost first;
+// strides_bytes has rank-1 entries (dims 1..rank-1).
+bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+              const uint32_t* box) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bd[5], es[5];
+    for (int r = 0; r < rank; ++r) {
+        gd[r] = dims[r];
+        bd[r] = box[r];
+        es[r] = 1;
+    }
+    for (int r = 0; r < rank - 1; ++r) gs[r] = strides_bytes[r];
+    CUresult res = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank, const_cast<void*>(base), gd, gs, bd, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return res == CUDA_SUCCESS;
+}
+
+int sm_count() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    static int cache[64] = {0};
+    if (dev < 64 && cache[dev]) return cache[dev];
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (dev < 64) cache[dev] = n;
+    return n;
+}
+
+inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool al256(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 255u) == 0; }
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+const char* as_version(void) { return "adaserve-b200 0.1 (sm_100a)"; }
+
+const char* as_status_string(as_status s) {
+    switch (s) {
+        case AS_OK: return "ok";
+        case AS_ERR_INVALID_ARG: return "invalid argument";
+        case AS_ERR_BUDGET_TOO_SMALL: return "budget smaller than the number of requests";
+        case AS_ERR_UNSUPPORTED: return "unsupported shape or dtype";
+        case AS_ERR_WORKSPACE: return "workspace too small or misaligned";
+        case AS_ERR_CUDA: return "CUDA error";
+    }
+    return "unknown status";
+}
+
+as_status as_check_device_error(const void* workspace, int32_t* code, int32_t* request, void* stream) {
+    if (!workspace) return AS_ERR_INVALID_ARG;
+    int32_t h[2] = {0, 0};
+    if (cudaStreamSynchronize(S(stream)) != cudaSuccess) return AS_ERR_CUDA;
+    if (cudaMemcpy(h, workspace, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return AS_ERR_CUDA;
+    if (code) *code = h[0];
+    if (request) *request = h[1];
+    return AS_OK;
+}
+
+as_status as_reset_workspace(void* workspace, size_t workspace_bytes, void* stream) {
+    if (!workspace) return AS_ERR_INVALID_ARG;
+    return cudaMemsetAsync(workspace, 0, workspace_bytes, S(stream)) == cudaSuccess ? AS_OK : AS_ERR_CUDA;
+}
+
+// ----------------------------------------------------------------- select
+size_t as_select_workspace_size(int32_t n_req, int32_t n_cand_total) {
+    if (n_req < 0 || n_cand_total < 0) return 0;
+    return select_ws_bytes(n_req, n_cand_total);
+}
+
+as_status as_select_trees(int32_t n_req, int32_t n_cand_total, const int32_t* cand_offsets, const int32_t* cand_parent,
+                          const float* cand_prob, const int32_t* cand_token, const double* slo_deficit,
+                          int32_t depth_d, int32_t n_max, int32_t budget, int32_t* tree_offsets, int32_t* tree_parent,
+                          int32_t* tree_src, int32_t* tree_depth, int32_t* tree_token, int32_t* slo_count,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+    if (n_req < 0 || n_cand_total < n_req || depth_d < 0 || n_max < 0 || !tree_offsets) return AS_ERR_INVALID_ARG;
+    if (budget < n_req) return AS_ERR_BUDGET_TOO_SMALL;
+    if (n_req > 4096) return AS_ERR_UNSUPPORTED;
+    if (n_req == 0) {
+        return cudaMemsetAsync(tree_offsets, 0, sizeof(int32_t), S(stream)) == cudaSuccess ? AS_OK : AS_ERR_CUDA;
+    }
+    if (!cand_offsets || !cand_parent || !cand_prob || !slo_deficit || !tree_parent || !tree_src)
+        return AS_ERR_INVALID_ARG;
+    if (tree_token && !cand_token) return AS_ERR_INVALID_ARG;
+    if (!workspace || !al256(workspace) || workspace_bytes < select_ws_bytes(n_req, n_cand_total))
+        return AS_ERR_WORKSPACE;
+    int rc = launch_select(n_req, n_cand_total, cand_offsets, cand_parent, cand_prob, cand_token, slo_deficit, depth_d,
+                           n_max, budget, tree_offsets, tree_parent, tree_src, tree_depth, tree_token, slo_count,
+                           workspace, S(stream));
+    return rc == 0 ? AS_OK : AS_ERR_CUDA;
+}
+
+// ----------------------------------------------------------------- attention
+size_t as_attn_workspace_size(as_dtype dtype, int32_t n_req, int32_t n_tree_rows, int32_t n_q_heads,
+                              int32_t head_dim, int32_t max_kv_len) {
+    (void)dtype; (void)n_req; (void)n_tree_rows; (void)n_q_heads; (void)head_dim; (void)max_kv_len;
+    return kWsHeaderBytes;
+}
+
+as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows, int32_t n_q_heads,
+                              int32_t n_kv_heads, int32_t head_dim, const void* q, const void* k_tree,
+                              const void* v_tree, const void* k_cache, const void* v_cache, int32_t num_pages,
+                              int32_t page_size, const int32_t* page_table, int32_t max_pages_per_req,
+                              const int32_t* kv_len, const int32_t* tree_offsets, const int32_t* tree_parent,
+                              float sm_scale, void* out, float* lse, void* workspace, size_t workspace_bytes,
+                              void* stream) {
+    if (n_req < 0 || n_tree_rows < 0 || n_q_heads <= 0 || n_kv_heads <= 0 || num_pages < 0 || max_pages_per_req < 0)
+        return AS_ERR_INVALID_ARG;
+    if (n_q_heads % n_kv_heads != 0) return AS_ERR_UNSUPPORTED;
+    if (head_dim != 64 && head_dim != 128) return AS_ERR_UNSUPPORTED;
+    if (page_size != 16 && page_size != 32 && page_size != 64 && page_size != 128) return AS_ERR_UNSUPPORTED;
+    if (dtype != AS_F32 && dtype != AS_BF16) return AS_ERR_UNSUPPORTED;
+    if (!workspace || !al256(workspace) || workspace_bytes < kWsHeaderBytes) return AS_ERR_WORKSPACE;
+    if (n_req == 0 || n_tree_rows == 0) return AS_OK;
+    if (!q || !k_tree || !v_tree || !out || !kv_len || !tree_offsets || !tree_parent) return AS_ERR_INVALID_ARG;
+    if (num_pages > 0 && max_pages_per_req > 0 && (!k_cache || !v_cache || !page_table)) return AS_ERR_INVALID_ARG;
+    const int G = n_q_heads / n_kv_heads;
+    if (dtype == AS_F32) {
+        SimtParams p;
+        p.n_req = n_req; p.n_tree_rows = n_tree_rows; p.n_q = n_q_heads; p.n_kv = n_kv_heads; p.G = G;
+        p.q = (const float*)q; p.k_tree = (const float*)k_tree; p.v_tree = (const float*)v_tree;
+        p.k_cache = (const float*)k_cache; p.v_cache = (const float*)v_cache;
+        p.num_pages = num_pages; p.page_size = page_size; p.page_table = page_table; p.max_pages = max_pages_per_req;
+        p.kv_len = kv_len; p.tree_offsets = tree_offsets; p.tree_parent = tree_parent; p.sm_scale = sm_scale;
+        p.out = (float*)out; p.lse = lse; p.ws = workspace;
+        return launch_attn_simt(p, head_dim, S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
+    }
+    // bf16 tcgen05 path
+    if ((G & (G - 1)) != 0 || G > 16) return AS_ERR_UNSUPPORTED;
+    if (!al16(q) || !al16(k_tree) || !al16(v_tree) || !al16(out) || (k_cache && !al16(k_cache)) ||
+        (v_cache && !al16(v_cache)))
+        return AS_ERR_INVALID_ARG;
+    const uint64_t D = (uint64_t)head_dim;
+    CUtensorMap maps[5];
+    {
+        uint64_t dims[3] = {D, (uint64_t)n_q_heads, (uint64_t)n_tree_rows};
+        uint64_t str[2] = {D * 2, (uint64_t)n_q_heads * D * 2};
+        uint32_t box[3] = {64, (uint32_t)G, (uint32_t)(128 / G)};
+        if (!make_map(&maps[0], q, 3, dims, str, box)) return AS_ERR_CUDA;
+    }
+    const int box_rows = page_size < 64 ? page_size : 64;
+    {
+        const uint64_t np = (uint64_t)(num_pages > 0 ? num_pages : 1);
+        uint64_t dims[4] = {D, (uint64_t)page_size, (uint64_t)n_kv_heads, np};
+        uint64_t str[3] = {D * 2, (uint64_t)page_size * D * 2, (uint64_t)n_kv_heads * page_size * D * 2};
+        uint32_t box[4] = {64, (uint32_t)box_rows, 1, 1};
+        const void* kc = k_cache ? k_cache : k_tree;  // never dereferenced when there are no pages
+        const void* vc = v_cache ? v_cache : v_tree;
+        if (!make_map(&maps[1], kc, 4, dims, str, box)) return AS_ERR_CUDA;
+        if (!make_map(&maps[2], vc, 4, dims, str, box)) return AS_ERR_CUDA;
+    }
+    {
+        uint64_t dims[3] = {D, (uint64_t)n_kv_heads, (uint64_t)n_tree_rows};
+        uint64_t str[2] = {D * 2, (uint64_t)n_kv_heads * D * 2};
+        uint32_t box[3] = {64, 1, 64};
+        if (!make_map(&maps[3], k_tree, 3, dims, str, box)) return AS_ERR_CUDA;
+        if (!make_map(&maps[4], v_tree, 3, dims, str, box)) return AS_ERR_CUDA;
+    }
+    TcParams p;
+    p.n_req = n_req; p.n_tree_rows = n_tree_rows; p.n_q = n_q_heads; p.n_kv = n_kv_heads; p.G = G;
+    p.page_size = page_size; p.box_rows = box_rows; p.max_pages = max_pages_per_req; p.num_pages = num_pages;
+    p.page_table = page_table; p.kv_len = kv_len; p.tree_offsets = tree_offsets; p.tree_parent = tree_parent;
+    p.scale_log2 = sm_scale * 1.4426950408889634f;
+    p.out = (__nv_bfloat16*)out; p.lse = lse; p.ws = workspace;
+    const int mt_max = (AS_MAX_TREE * G + 127) / 128;
+    p.n_units = mt_max * n_req * n_kv_heads;
+    return launch_attn_tc(maps, p, head_dim, sm_count(), S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
+}
+
+// ----------------------------------------------------------------- accept
+size_t as_accept_workspace_size(int32_t n_tree_rows) {
+    return kWsHeaderBytes + align_up((size_t)(n_tree_rows > 0 ? n_tree_rows : 1) * 4, 256);
+}
+
+as_status as_accept_tokens(as_accept_phase phase, int32_t n_req, int32_t req_begin, int32_t req_end,
+                           int32_t n_tree_rows, const int32_t* tree_offsets, const int32_t* tree_parent,
+                           const int32_t* tree_tokens, const int32_t* target_tokens, const void* target_logits,
+                           as_dtype logits_dtype, int32_t vocab, int32_t max_path, int32_t* accept_len,
+                           int32_t* accept_path, int32_t* bonus_token, const void* k_tree, const void* v_tree,
+                           as_dtype kv_dtype, int32_t n_kv_heads, int32_t head_dim, void* k_cache, void* v_cache,
+                           int32_t num_pages, int32_t page_size, const int32_t* page_table, int32_t max_pages_per_req,
+                           int32_t* kv_len, void* workspace, size_t workspace_bytes, void* stream) {
+    if (phase != AS_ACCEPT_FUSED && phase != AS_ACCEPT_WALK_ONLY && phase != AS_ACCEPT_COMMIT_ONLY)
+        return AS_ERR_INVALID_ARG;
+    if (n_req < 0 || req_begin < 0 || req_end < req_begin || req_end > n_req || n_tree_rows < 0) return AS_ERR_INVALID_ARG;
+    if (max_path < 1 || max_path > 64) return AS_ERR_UNSUPPORTED;
+    if (!workspace || !al256(workspace) || workspace_bytes < as_accept_workspace_size(n_tree_rows))
+        return AS_ERR_WORKSPACE;
+    if (!tree_offsets || !accept_len || !accept_path) return AS_ERR_INVALID_ARG;
+    const bool walk = phase != AS_ACCEPT_COMMIT_ONLY;
+    const bool commit = phase != AS_ACCEPT_WALK_ONLY;
+    if (walk) {
+        if (!tree_parent || !tree_tokens || !bonus_token) return AS_ERR_INVALID_ARG;
+        if (!target_tokens && !target_logits) return AS_ERR_INVALID_ARG;
+        if (!target_tokens && (vocab <= 0 || (logits_dtype != AS_F32 && logits_dtype != AS_BF16)))
+            return AS_ERR_INVALID_ARG;
+    }
+    if (commit) {
+        if (!k_tree || !v_tree || !k_cache || !v_cache || !page_table || !kv_len) return AS_ERR_INVALID_ARG;
+        if (kv_dtype != AS_F32 && kv_dtype != AS_BF16) return AS_ERR_UNSUPPORTED;
+        if (head_dim <= 0 || n_kv_heads <= 0 || page_size <= 0) return AS_ERR_INVALID_ARG;
+        const int eb = kv_dtype == AS_BF16 ? 2 : 4;
+        if ((head_dim * eb) % 16 != 0) return AS_ERR_UNSUPPORTED;
+        if (!al16(k_tree) || !al16(v_tree) || !al16(k_cache) || !al16(v_cache)) return AS_ERR_INVALID_ARG;
+    }
+    AcceptParams p;
+    p.n_req = n_req; p.req_begin = req_begin; p.req_end = req_end; p.n_tree_rows = n_tree_rows;
+    p.tree_offsets = tree_offsets; p.tree_parent = tree_parent; p.tree_tokens = tree_tokens;
+    p.target_tokens = target_tokens; p.max_path = max_path;
+    p.accept_len = accept_len; p.accept_path = accept_path; p.bonus_token = bonus_token;
+    p.k_tree = (const unsigned char*)k_tree; p.v_tree = (const unsigned char*)v_tree;
+    p.elem_bytes = kv_dtype == AS_BF16 ? 2 : 4; p.n_kv = n_kv_heads; p.head_dim = head_dim;
+    p.k_cache = (unsigned char*)k_cache; p.v_cache = (unsigned char*)v_cache;
+    p.num_pages = num_pages; p.page_size = page_size; p.page_table = page_table; p.max_pages = max_pages_per_req;
+    p.kv_len = kv_len; p.ws = workspace;
+    p.do_walk = walk ? 1 : 0;
+    p.do_commit = commit ? 1 : 0;
+    int32_t* argmax_buf = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(workspace) + kWsHeaderBytes);
+    return launch_accept(p, target_logits, logits_dtype == AS_BF16, vocab, argmax_buf, S(stream)) == 0 ? AS_OK
+                                                                                                      : AS_ERR_CUDA;
+}
+
+// ----------------------------------------------------------------- selftest
+as_status as_selftest_umma(const void* a, const void* b, float* d, int32_t n, int32_t k, int32_t b_mn_major,
+                           void* stream) {
+    if (!a || !b || !d) return AS_ERR_INVALID_ARG;
+    if ((n != 64 && n != 128) || (k != 64 && k != 128)) return AS_ERR_UNSUPPORTED;
+    CUtensorMap ma, mb;
+    {
+        uint64_t dims[2] = {(uint64_t)k, 128};
+        uint64_t str[1] = {(uint64_t)k * 2};
+        uint32_t box[2] = {64, 128};
+        if (!make_map(&ma, a, 2, dims, str, box)) return AS_ERR_CUDA;
+    }
+    if (!b_mn_major) {
+        uint64_t dims[2] = {(uint64_t)k, (uint64_t)n};
+        uint64_t str[1] = {(uint64_t)k * 2};
+        uint32_t box[2] = {64, (uint32_t)n};
+        if (!make_map(&mb, b, 2, dims, str, box)) return AS_ERR_CUDA;
+    } else {
+        uint64_t dims[2] = {(uint64_t)n, (uint64_t)k};
+        uint64_t str[1] = {(uint64_t)n * 2};
+        uint32_t box[2] = {64, (uint32_t)k};
+        if (!make_map(&mb, b, 2, dims, str, box)) return AS_ERR_CUDA;
+    }
+    return launch_umma_selftest(&ma, &mb, d, n, k, b_mn_major ? 1 : 0, S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
+}
+
+}  // extern "C"

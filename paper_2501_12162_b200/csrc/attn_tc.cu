@@ -1,0 +1,469 @@
+// attn_tc.cu -- K2: as_tree_verify_attn for dtype AS_BF16 on sm_100a.
+//
+// Step 4 verification: every tree node of request i attends to
+// the request's committed prefix (paged KV cache, D6/P:L935) and to its tree
+// ancestors-or-self (R15).  Per (request i, kv head g) the G query heads of
+// all K_i nodes form Q rows r = node*G + hh, so one kv head's keys are read
+// from HBM once for all G*K_i rows (c2: 4*32 = 128 rows = one UMMA M tile).
+//
+// Structure (persistent, one 192-thread CTA per SM, static unit schedule):
+//   warp 0      TMA producer: Q tile (3-D map, box 64 x G x 128/G, SW128) and
+//               K/V tiles of 64 keys, one 4-D box per page fragment
+//               [d 64 x page rows x 1 head x 1 page] through the page table,
+//               or from k_tree/v_tree (3-D map) for the tree tile(s);
+//               4-stage K and V rings, mbarrier complete_tx.
+//   warp 1      TMEM owner + single-thread tcgen05.mma issuer:
+//               S_t = Q K_t^T  (M=128, N=64, K=d; both K-major SW128) into one of
+//               two TMEM S buffers; O += P_t V_t (M=128, N=d, K=64; P K-major,
+//               V MN-major SW128) into the TMEM O accumulator.  QK_{t+1} is
+//               issued before PV_t so softmax(t+1) overlaps PV_t.
+//   warps 2-5   softmax + epilogue, one TMEM lane (= Q row) per thread:
+//               tcgen05.ld S -> mask (prefix length / ancestor bitmask) ->
+//               online softmax in the log2 domain with lazy O rescaling
+//               (only when the running max grows by > 8, i.e. 256x) ->
+//               P (bf16) written to shared memory in the SW128 K-major layout
+//               -> fence.proxy.async -> PV.  Epilogue: tcgen05.ld O, * 1/l,
+//               bf16 store, optional natural-log LSE.
+// Units: (q-tile mt, request i, kv head g), mt slowest so that the non-empty
+// units are spread round-robin over the SMs.
+#include "params.cuh"
+#include "tc_ptx.cuh"
+
+namespace as {
+
+constexpr int kBM = 128;          // query rows per tile (UMMA M)
+constexpr int kBN = 64;           // keys per tile
+constexpr int kStages = 4;        // K and V ring depth
+constexpr int kThreads = 192;     // 6 warps
+constexpr int kTmemCols = 256;    // S0 [0,64) S1 [64,128) O [128, 128+D)
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThresh = 8.0f;  // log2 units
+
+
+template <int D>
+struct TcSmem {
+    static constexpr int NCH = D / 64;                        // 128-byte swizzle chunks along d
+    static constexpr int Q_BYTES = NCH * kBM * 128;           // 16 KB per chunk
+    static constexpr int KV_BYTES = NCH * kBN * 128;          // 8 KB per chunk
+    static constexpr int P_BYTES = kBM * kBN * 2;             // 16 KB
+    static constexpr int OFF_Q = 0;
+    static constexpr int OFF_K = OFF_Q + Q_BYTES;
+    static constexpr int OFF_V = OFF_K + kStages * KV_BYTES;
+    static constexpr int OFF_P = OFF_V + kStages * KV_BYTES;
+    static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+    static constexpr int N_BAR = 2 + 4 * kStages + 8 + 2;
+    static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
+    static constexpr int BYTES = OFF_TMEM + 16;
+    static constexpr int ALLOC = BYTES + 1024;  // alignment slack
+};
+
+struct Unit {
+    int i, g, mt, off, K, L, nt, n_prefix;
+};
+
+__device__ __forceinline__ bool decode_unit(const TcParams& p, int w, Unit& u) {
+    const int per_mt = p.n_req * p.n_kv;
+    u.mt = w / per_mt;
+    const int rem = w - u.mt * per_mt;
+    u.i = rem / p.n_kv;
+    u.g = rem - u.i * p.n_kv;
+    u.off = __ldg(p.tree_offsets + u.i);
+    u.K = __ldg(p.tree_offsets + u.i + 1) - u.off;
+    if (u.K <= 0 || u.K > AS_MAX_TREE || u.off + u.K > p.n_tree_rows) return false;
+    if (u.K * p.G <= u.mt * kBM) return false;
+    u.L = __ldg(p.kv_len + u.i);
+    if (u.L < 0) u.L = 0;
+    if (u.L > p.max_pages * p.page_size) u.L = p.max_pages * p.page_size;
+    u.n_prefix = (u.L + kBN - 1) / kBN;
+    u.nt = u.n_prefix + (u.K + kBN - 1) / kBN;
+    return true;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
+                        const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kt,
+                        const __grid_constant__ CUtensorMap tm_vt, const TcParams p) {
+    using S = TcSmem<D>;
+    constexpr int NCH = S::NCH;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
+    uint64_t* q_full = bars + 0;
+    uint64_t* q_empty = bars + 1;
+    uint64_t* k_full = bars + 2;
+    uint64_t* k_empty = k_full + kStages;
+    uint64_t* v_full = k_empty + kStages;
+    uint64_t* v_empty = v_full + kStages;
+    uint64_t* s_full = v_empty + kStages;  // [2]
+    uint64_t* s_empty = s_full + 2;        // [2]
+    uint64_t* p_full = s_empty + 2;        // [2]
+    uint64_t* p_empty = p_full + 2;        // [2]
+    uint64_t* o_full = p_empty + 2;
+    uint64_t* o_empty = o_full + 1;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + S::OFF_TMEM);
+
+    const int warp = warp_id();
+    const int lane = lane_id();
+
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(q_full, 1);
+        ptx::mbar_init(q_empty, 1);
+        for (int s = 0; s < kStages; ++s) {
+            ptx::mbar_init(k_full + s, 1);
+            ptx::mbar_init(k_empty + s, 1);
+            ptx::mbar_init(v_full + s, 1);
+            ptx::mbar_init(v_empty + s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(s_full + b, 1);
+            ptx::mbar_init(s_empty + b, 4);
+            ptx::mbar_init(p_full + b, 4);
+            ptx::mbar_init(p_empty + b, 1);
+        }
+        ptx::mbar_init(o_full, 1);
+        ptx::mbar_init(o_empty, 4);
+        ptx::fence_mbar_init();
+        ptx::tma_prefetch(&tm_q);
+        ptx::tma_prefetch(&tm_kc);
+        ptx::tma_prefetch(&tm_vc);
+        ptx::tma_prefetch(&tm_kt);
+        ptx::tma_prefetch(&tm_vt);
+    }
+    if (warp == 1) ptx::tmem_alloc(tmem_holder, kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_holder;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            uint32_t kv_it = 0, unit_it = 0;
+            const uint64_t pol = ptx::policy_evict_first();
+            for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
+                Unit u;
+                if (!decode_unit(p, w, u)) {
+                    if (u.K > AS_MAX_TREE && u.mt == 0 && u.g == 0) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, u.i);
+                    continue;
+                }
+                if (u.mt == 0 && u.g == 0 && __ldg(p.kv_len + u.i) > p.max_pages * p.page_size)
+                    set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, u.i);
+                ptx::mbar_wait(q_empty, (unit_it & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(q_full, S::Q_BYTES);
+                const int node0 = u.off + u.mt * (kBM / p.G);
+#pragma unroll
+                for (int c = 0; c < NCH; ++c)
+                    ptx::tma_load_3d(smem + S::OFF_Q + c * kBM * 128, &tm_q, q_full, c * 64, u.g * p.G, node0);
+                for (int t = 0; t < u.nt; ++t, ++kv_it) {
+                    const int st = kv_it % kStages;
+                    const uint32_t ph = (kv_it / kStages) & 1;
+                    unsigned char* kdst = smem + S::OFF_K + st * S::KV_BYTES;
+                    unsigned char* vdst = smem + S::OFF_V + st * S::KV_BYTES;
+                    if (t < u.n_prefix) {
+                        const int key0 = t * kBN;
+                        const int valid = min(kBN, u.L - key0);
+                        const int nbox = (valid + p.box_rows - 1) / p.box_rows;
+                        const uint32_t bytes = (uint32_t)(nbox * NCH * p.box_rows * 128);
+                        ptx::mbar_wait(k_empty + st, ph ^ 1);
+                        ptx::mbar_arrive_expect_tx(k_full + st, bytes);
+                        for (int b = 0; b < nbox; ++b) {
+                            const int kp = key0 + b * p.box_rows;
+                            const int page = __ldg(p.page_table + (size_t)u.i * p.max_pages + kp / p.page_size);
+                            const int slot = kp % p.page_size;
+                            // out-of-range pages read as zeros (TMA bounds check); flag them
+                            if (page < 0 || page >= p.num_pages) set_dev_error(p.ws, AS_DEV_BAD_PAGE, u.i);
+#pragma unroll
+                            for (int c = 0; c < NCH; ++c)
+                                ptx::tma_load_4d_hint(kdst + c * kBN * 128 + b * p.box_rows * 128, &tm_kc, k_full + st,
+                                                      c * 64, slot, u.g, page, pol);
+                        }
+                        ptx::mbar_wait(v_empty + st, ph ^ 1);
+                        ptx::mbar_arrive_expect_tx(v_full + st, bytes);
+                        for (int b = 0; b < nbox; ++b) {
+                            const int kp = key0 + b * p.box_rows;
+                            const int page = __ldg(p.page_table + (size_t)u.i * p.max_pages + kp / p.page_size);
+                            const int slot = kp % p.page_size;
+#pragma unroll
+                            for (int c = 0; c < NCH; ++c)
+                                ptx::tma_load_4d_hint(vdst + c * kBN * 128 + b * p.box_rows * 128, &tm_vc, v_full + st,
+                                                      c * 64, slot, u.g, page, pol);
+                        }
+                    } else {
+                        const int row0 = u.off + (t - u.n_prefix) * kBN;
+                        const uint32_t bytes = (uint32_t)(NCH * kBN * 128);
+                        ptx::mbar_wait(k_empty + st, ph ^ 1);
+                        ptx::mbar_arrive_expect_tx(k_full + st, bytes);
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c)
+                            ptx::tma_load_3d(kdst + c * kBN * 128, &tm_kt, k_full + st, c * 64, u.g, row0);
+                        ptx::mbar_wait(v_empty + st, ph ^ 1);
+                        ptx::mbar_arrive_expect_tx(v_full + st, bytes);
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c)
+                            ptx::tma_load_3d(vdst + c * kBN * 128, &tm_vt, v_full + st, c * 64, u.g, row0);
+                    }
+                }
+                ++unit_it;
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(kBM, kBN, 0);
+        constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(kBM, D, 1);
+        const uint32_t q_base = ptx::smem_u32(smem + S::OFF_Q);
+        const uint32_t k_base = ptx::smem_u32(smem + S::OFF_K);
+        const uint32_t v_base = ptx::smem_u32(smem + S::OFF_V);
+        const uint32_t p_base = ptx::smem_u32(smem + S::OFF_P);
+        const uint32_t tm_o = tmem + 128;
+        uint32_t k_it = 0, v_it = 0, s_it = 0, unit_it = 0;
+        for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
+            Unit u;
+            if (!decode_unit(p, w, u)) continue;
+            ptx::mbar_wait(q_full, unit_it & 1);
+            const uint32_t s_first = s_it;
+            auto do_pv = [&](int tp) {
+                const uint32_t sidx = s_first + tp;
+                const int st = v_it % kStages;
+                const uint32_t ph = (v_it / kStages) & 1;
+                const int pb = sidx & 1;
+                ptx::mbar_wait(v_full + st, ph);
+                // zero V rows past the prefix end (stale/uninitialised smem or cache
+                // slots >= L may hold NaN; P is 0 there but 0 * NaN = NaN)
+                if (tp < u.n_prefix) {
+                    const int valid = min(kBN, u.L - tp * kBN);
+                    if (valid < kBN) {
+                        unsigned char* vs = smem + S::OFF_V + st * S::KV_BYTES;
+                        const int nvec = (kBN - valid) * 8;  // 16-byte vectors per chunk
+                        for (int c = 0; c < NCH; ++c)
+                            for (int x = lane; x < nvec; x += 32)
+                                reinterpret_cast<uint4*>(vs + c * kBN * 128 + valid * 128)[x] = make_uint4(0, 0, 0, 0);
+                        ptx::fence_proxy_async_smem();
+                    }
+                }
+                ptx::mbar_wait(p_full + pb, (sidx >> 1) & 1);
+                if (tp == 0) ptx::mbar_wait(o_empty, (unit_it & 1) ^ 1);
+                ptx::tc_fence_after();
+                __syncwarp();
+                if (lane == 0) {
+#pragma unroll
+                    for (int kk = 0; kk < kBN / 16; ++kk) {
+                        const uint64_t a = ptx::sw128_desc(p_base + pb * S::P_BYTES + kk * 32, 0, 1024);
+                        const uint64_t b =
+                            ptx::sw128_desc(v_base + st * S::KV_BYTES + kk * 16 * 128, kBN * 128, 1024);
+                        ptx::mma_bf16_ss(tm_o, a, b, idesc_pv, (tp > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    ptx::mma_commit(v_empty + st);
+                    ptx::mma_commit(p_empty + pb);
+                }
+                __syncwarp();
+                ++v_it;
+            };
+            for (int t = 0; t < u.nt; ++t) {
+                const int st = k_it % kStages;
+                const uint32_t ph = (k_it / kStages) & 1;
+                const int sb = s_it & 1;
+                ptx::mbar_wait(k_full + st, ph);
+                ptx::mbar_wait(s_empty + sb, ((s_it >> 1) & 1) ^ 1);
+                ptx::tc_fence_after();
+                if (lane == 0) {
+#pragma unroll
+                    for (int ks = 0; ks < D / 16; ++ks) {
+                        const int c = ks >> 2, kk = ks & 3;
+                        const uint64_t a = ptx::sw128_desc(q_base + c * kBM * 128 + kk * 32, 0, 1024);
+                        const uint64_t b = ptx::sw128_desc(k_base + st * S::KV_BYTES + c * kBN * 128 + kk * 32, 0, 1024);
+                        ptx::mma_bf16_ss(tmem + sb * kBN, a, b, idesc_qk, ks > 0 ? 1u : 0u);
+                    }
+                    ptx::mma_commit(k_empty + st);
+                    ptx::mma_commit(s_full + sb);
+                    if (t == u.nt - 1) ptx::mma_commit(q_empty);
+                }
+                __syncwarp();
+                ++k_it;
+                ++s_it;
+                if (t > 0) do_pv(t - 1);
+            }
+            do_pv(u.nt - 1);
+            if (lane == 0) ptx::mma_commit(o_full);
+            __syncwarp();
+            ++unit_it;
+        }
+    } else {
+        // ===================== softmax + epilogue (warps 2..5) =====================
+        const int quad = warp & 3;       // TMEM lane quadrant this warp may access
+        const int r = quad * 32 + lane;  // Q row in the tile == TMEM lane
+        const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+        unsigned char* p_smem = smem + S::OFF_P;
+        uint32_t s_it = 0, unit_it = 0;
+        for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
+            Unit u;
+            if (!decode_unit(p, w, u)) continue;
+            const int G = p.G;
+            const int rr = u.mt * kBM + r;
+            const bool row_ok = rr < u.K * G;
+            const int node = rr / G;
+            const int hh = rr - node * G;
+            // ancestor-or-self bitmask of this row's node (R15)
+            uint64_t anc0 = 0, anc1 = 0;
+            if (row_ok) {
+                int v = node, steps = 0;
+                for (;;) {
+                    if (v < 64) anc0 |= 1ull << v; else anc1 |= 1ull << (v - 64);
+                    if (v == 0) break;
+                    const int pv = __ldg(p.tree_parent + u.off + v);
+                    if (pv < 0 || pv >= v || ++steps > u.K) {
+                        set_dev_error(p.ws, AS_DEV_BAD_PARENT, u.i);
+                        break;
+                    }
+                    v = pv;
+                }
+            }
+            float m_ref = -INFINITY, l_sum = 0.f;
+            for (int t = 0; t < u.nt; ++t, ++s_it) {
+                const int sb = s_it & 1;
+                ptx::mbar_wait(s_full + sb, (s_it >> 1) & 1);
+                ptx::tc_fence_after();
+                uint32_t sr[kBN];
+                ptx::tmem_ld32(tmem + lane_addr + sb * kBN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+                ptx::tmem_ld32(tmem + lane_addr + sb * kBN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+                ptx::tmem_ld_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(s_empty + sb);
+                float x[kBN];
+                float tmax = -INFINITY;
+                if (t < u.n_prefix) {
+                    const int valid = u.L - t * kBN;
+#pragma unroll
+                    for (int c = 0; c < kBN; ++c) {
+                        x[c] = (c < valid) ? __uint_as_float(sr[c]) * p.scale_log2 : -INFINITY;
+                        tmax = fmaxf(tmax, x[c]);
+                    }
+                } else {
+                    const uint64_t bits = (t - u.n_prefix) == 0 ? anc0 : anc1;
+#pragma unroll
+                    for (int c = 0; c < kBN; ++c) {
+                        x[c] = ((bits >> c) & 1ull) ? __uint_as_float(sr[c]) * p.scale_log2 : -INFINITY;
+                        tmax = fmaxf(tmax, x[c]);
+                    }
+                }
+                const float m_new = fmaxf(m_ref, tmax);
+                if (t == 0) {
+                    m_ref = m_new;
+                } else {
+                    const bool need = m_new > m_ref + kRescaleThresh;
+                    if (__any_sync(0xffffffffu, need)) {
+                        // PV_{t-1} must have landed in O before we rescale it
+                        const uint32_t prev = s_it - 1;
+                        ptx::mbar_wait(p_empty + (prev & 1), (prev >> 1) & 1);
+                        ptx::tc_fence_after();
+                        const float sc = need ? ptx::ex2(m_ref - m_new) : 1.f;
+#pragma unroll
+                        for (int c0 = 0; c0 < D; c0 += 32) {
+                            uint32_t o[32];
+                            ptx::tmem_ld32(tmem + lane_addr + 128 + c0, o);
+                            ptx::tmem_ld_wait();
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * sc);
+                            ptx::tmem_st32(tmem + lane_addr + 128 + c0, o);
+                        }
+                        ptx::tmem_st_wait();
+                        ptx::tc_fence_before();
+                        if (need) {
+                            l_sum *= sc;
+                            m_ref = m_new;
+                        }
+                    }
+                }
+                const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+                // P buffer sb is free once PV_{t-2} completed
+                ptx::mbar_wait(p_empty + sb, ((s_it >> 1) & 1) ^ 1);
+                float rsum = 0.f;
+                uint32_t pk[kBN / 2];
+#pragma unroll
+                for (int c = 0; c < kBN; c += 2) {
+                    const float p0 = ptx::ex2(x[c] - m_use);
+                    const float p1 = ptx::ex2(x[c + 1] - m_use);
+                    rsum += p0 + p1;
+                    __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                    pk[c >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+                }
+                l_sum += rsum;
+                unsigned char* prow = p_smem + sb * S::P_BYTES + r * 128;
+#pragma unroll
+                for (int ch = 0; ch < 8; ++ch) {
+                    const int phys = ch ^ (r & 7);
+                    *reinterpret_cast<uint4*>(prow + phys * 16) =
+                        make_uint4(pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(p_full + sb);
+            }
+            // epilogue
+            ptx::mbar_wait(o_full, unit_it & 1);
+            ptx::tc_fence_after();
+            const float inv = 1.f / l_sum;
+            const size_t orow = (size_t)(u.off + node) * p.n_q + (size_t)u.g * G + hh;
+#pragma unroll
+            for (int c0 = 0; c0 < D; c0 += 32) {
+                uint32_t o[32];
+                ptx::tmem_ld32(tmem + lane_addr + 128 + c0, o);
+                ptx::tmem_ld_wait();
+                if (row_ok) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(o[2 * j]) * inv,
+                                                                  __uint_as_float(o[2 * j + 1]) * inv);
+                        pk[j] = *reinterpret_cast<uint32_t*>(&h2);
+                    }
+                    uint4* dst = reinterpret_cast<uint4*>(p.out + orow * D + c0);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+                }
+            }
+            if (row_ok && p.lse) {
+                const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+                p.lse[orow] = (m_use + __log2f(l_sum)) * 0.6931471805599453f;
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(o_empty);
+            ++unit_it;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, kTmemCols);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+int tc_smem_bytes(int head_dim) {
+    return head_dim == 64 ? TcSmem<64>::ALLOC : TcSmem<128>::ALLOC;
+}
+
+int launch_attn_tc(const CUtensorMap* maps, const TcParams& p, int head_dim, int n_sms, cudaStream_t stream) {
+    const int smem = tc_smem_bytes(head_dim);
+    int grid = p.n_units < n_sms ? p.n_units : n_sms;
+    if (grid <= 0) return 0;
+    if (head_dim == 128) {
+        if (cudaFuncSetAttribute(tree_attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
+            return -1;
+        tree_attn_tc_kernel<128><<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
+    } else {
+        if (cudaFuncSetAttribute(tree_attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
+            return -1;
+        tree_attn_tc_kernel<64><<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace as

@@ -1,0 +1,74 @@
+// params.cuh -- launch parameter blocks shared by abi.cu and the kernels.
+#pragma once
+#include <cuda.h>
+#include "common.cuh"
+
+namespace as {
+
+struct AcceptParams {
+    int n_req, req_begin, req_end, n_tree_rows;
+    const int32_t* tree_offsets;
+    const int32_t* tree_parent;
+    const int32_t* tree_tokens;
+    const int32_t* target_tokens;
+    int max_path;
+    int32_t* accept_len;
+    int32_t* accept_path;
+    int32_t* bonus_token;
+    const unsigned char* k_tree;
+    const unsigned char* v_tree;
+    int elem_bytes, n_kv, head_dim;
+    unsigned char* k_cache;
+    unsigned char* v_cache;
+    int num_pages, page_size;
+    const int32_t* page_table;
+    int max_pages;
+    int32_t* kv_len;
+    void* ws;
+    int do_walk, do_commit;
+};
+
+struct SimtParams {
+    int n_req, n_tree_rows, n_q, n_kv, G;
+    const float* q;
+    const float* k_tree;
+    const float* v_tree;
+    const float* k_cache;
+    const float* v_cache;
+    int num_pages, page_size;
+    const int32_t* page_table;
+    int max_pages;
+    const int32_t* kv_len;
+    const int32_t* tree_offsets;
+    const int32_t* tree_parent;
+    float sm_scale;
+    float* out;
+    float* lse;
+    void* ws;
+};
+
+struct TcParams {
+    int n_req, n_tree_rows, n_q, n_kv, G;
+    int page_size, box_rows, max_pages, num_pages;
+    const int32_t* page_table;
+    const int32_t* kv_len;
+    const int32_t* tree_offsets;
+    const int32_t* tree_parent;
+    float scale_log2;
+    __nv_bfloat16* out;
+    float* lse;
+    void* ws;
+    int n_units;
+};
+
+size_t select_ws_bytes(int n_req, int n_cand_total);
+int launch_select(int, int, const int32_t*, const int32_t*, const float*, const int32_t*, const double*, int, int,
+                  int, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, void*, cudaStream_t);
+int launch_accept(const AcceptParams& p, const void* target_logits, int logits_bf16, int vocab, int32_t* argmax_buf,
+                  cudaStream_t stream);
+int launch_attn_simt(const SimtParams& p, int head_dim, cudaStream_t stream);
+int launch_attn_tc(const CUtensorMap* maps, const TcParams& p, int head_dim, int n_sms, cudaStream_t stream);
+int launch_umma_selftest(const CUtensorMap* ma, const CUtensorMap* mb, float* d, int N, int K, int b_mn,
+                         cudaStream_t stream);
+
+}  // namespace as

@@ -1,0 +1,81 @@
+// selftest.cu -- as_selftest_umma: one-CTA tcgen05 GEMM that exercises the
+// exact building blocks of the bf16 attention kernel (TMA SW128 tiles, K-major
+// and MN-major UMMA shared-memory descriptors, the kind::f16 instruction
+// descriptor, TMEM alloc / commit / 32x32b loads).  Debug and tests only.
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace as {
+
+__global__ void __launch_bounds__(128, 1)
+    umma_selftest_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                         float* d, int N, int K, int b_mn) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* sa = smem;                  // (K/64) chunks of [128 x 64]
+    unsigned char* sb = smem + 2 * 128 * 128;  // K-major: (K/64) chunks of [N x 64]; MN-major: (N/64) chunks of [K x 64]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 4 * 128 * 128);
+    uint32_t* holder = reinterpret_cast<uint32_t*>(bar + 2);
+    const int warp = warp_id(), lane = lane_id();
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(bar, 1);
+        ptx::mbar_init(bar + 1, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) ptx::tmem_alloc(holder, 256);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *holder;
+    if (threadIdx.x == 0) {
+        const int kch = K / 64;
+        const uint32_t bytes = (uint32_t)(kch * 128 * 128 + K * N * 2);
+        ptx::mbar_arrive_expect_tx(bar, bytes);
+        for (int c = 0; c < kch; ++c) ptx::tma_load_2d(sa + c * 128 * 128, &tm_a, bar, c * 64, 0);
+        if (!b_mn) {
+            for (int c = 0; c < kch; ++c) ptx::tma_load_2d(sb + c * N * 128, &tm_b, bar, c * 64, 0);
+        } else {
+            for (int c = 0; c < N / 64; ++c) ptx::tma_load_2d(sb + c * K * 128, &tm_b, bar, c * 64, 0);
+        }
+        ptx::mbar_wait(bar, 0);
+        ptx::tc_fence_after();
+        const uint32_t idesc = ptx::idesc_bf16_f32(128, N, b_mn);
+        const uint32_t a0 = ptx::smem_u32(sa), b0 = ptx::smem_u32(sb);
+        for (int ks = 0; ks < K / 16; ++ks) {
+            const int c = ks >> 2, kk = ks & 3;
+            const uint64_t ad = ptx::sw128_desc(a0 + c * 128 * 128 + kk * 32, 0, 1024);
+            uint64_t bd;
+            if (!b_mn) bd = ptx::sw128_desc(b0 + c * N * 128 + kk * 32, 0, 1024);
+            else bd = ptx::sw128_desc(b0 + ks * 16 * 128, K * 128, 1024);
+            ptx::mma_bf16_ss(tmem, ad, bd, idesc, ks > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(bar + 1);
+    }
+    __syncwarp();
+    ptx::mbar_wait(bar + 1, 0);
+    ptx::tc_fence_after();
+    const int row = warp * 32 + lane;
+    for (int c0 = 0; c0 < N; c0 += 32) {
+        uint32_t r[32];
+        ptx::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, r);
+        ptx::tmem_ld_wait();
+        for (int j = 0; j < 32; ++j) d[(size_t)row * N + c0 + j] = __uint_as_float(r[j]);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 256);
+    }
+}
+
+int launch_umma_selftest(const CUtensorMap* ma, const CUtensorMap* mb, float* d, int N, int K, int b_mn,
+                         cudaStream_t stream) {
+    const int smem = 4 * 128 * 128 + 64 + 1024;
+    if (cudaFuncSetAttribute(umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return -1;
+    umma_selftest_kernel<<<1, 128, smem, stream>>>(*ma, *mb, d, N, K, b_mn);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace as

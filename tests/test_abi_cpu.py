@@ -1,0 +1,82 @@
+"""The C-ABI library loads on a CPU-only box, exports every symbol the header
+declares, and rejects host-checkable bad arguments without launching."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "adaserve.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2501_12162_b200 import build as b
+    b.build()
+    import paper_2501_12162_b200 as pk
+    return pk.lib()
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(as_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(L):
+    names = _declared()
+    assert "as_select_trees" in names and "as_tree_verify_attn" in names and "as_accept_tokens" in names
+    for n in names:
+        assert hasattr(L, n), n
+    nm = os.popen(f"nm -D {os.path.join(ROOT, 'paper_2501_12162_b200', 'libadaserve.so')}").read()
+    for n in names:
+        assert re.search(rf"\bT {n}\b", nm), n
+
+
+def test_status_strings_and_sizes(L):
+    assert L.as_status_string(0).decode() == "ok"
+    assert "budget" in L.as_status_string(2).decode()
+    assert L.as_version().decode().startswith("adaserve-b200")
+    assert L.as_select_workspace_size(256, 16640) >= 16640 * 8
+    assert L.as_accept_workspace_size(4096) >= 4096 * 4
+    assert L.as_attn_workspace_size(1, 64, 2048, 32, 128, 2048) >= 256
+
+
+def test_host_checks_return_without_launch(L):
+    vp = ctypes.c_void_p
+    dummy = vp(4096)
+    # budget < n_req -> AS_ERR_BUDGET_TOO_SMALL (R10)
+    st = L.as_select_trees(4, 8, dummy, dummy, dummy, None, dummy, 3, 3, 3, dummy, dummy, dummy, None, None, None,
+                           dummy, 1 << 20, None)
+    assert st == 2
+    # unsupported head_dim -> AS_ERR_UNSUPPORTED
+    st = L.as_tree_verify_attn(1, 1, 8, 4, 4, 96, dummy, dummy, dummy, dummy, dummy, 4, 16, dummy, 4, dummy,
+                               dummy, dummy, ctypes.c_float(0.1), dummy, None, vp(256 * 64), 256, None)
+    assert st == 3
+    # n_q % n_kv != 0
+    st = L.as_tree_verify_attn(1, 1, 8, 6, 4, 128, dummy, dummy, dummy, dummy, dummy, 4, 16, dummy, 4, dummy,
+                               dummy, dummy, ctypes.c_float(0.1), dummy, None, vp(256 * 64), 256, None)
+    assert st == 3
+    # misaligned workspace
+    st = L.as_tree_verify_attn(1, 1, 8, 4, 4, 128, dummy, dummy, dummy, dummy, dummy, 4, 16, dummy, 4, dummy,
+                               dummy, dummy, ctypes.c_float(0.1), dummy, None, vp(256 * 64 + 4), 256, None)
+    assert st == 4
+    # accept: bad phase / max_path
+    st = L.as_accept_tokens(7, 1, 0, 1, 4, dummy, dummy, dummy, dummy, None, 0, 0, 8, dummy, dummy, dummy,
+                            None, None, 1, 0, 0, None, None, 0, 0, None, 0, None, vp(1 << 16), 1 << 12, None)
+    assert st == 1
+    st = L.as_accept_tokens(1, 1, 0, 1, 4, dummy, dummy, dummy, dummy, None, 0, 0, 65, dummy, dummy, dummy,
+                            None, None, 1, 0, 0, None, None, 0, 0, None, 0, None, vp(1 << 16), 1 << 12, None)
+    assert st == 3
+
+
+def test_product_path_does_not_import_oracle():
+    """The product package never imports / links anything under oracle/."""
+    pkg = os.path.join(ROOT, "paper_2501_12162_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src and "liboracle" not in src, f
+                assert "adaserve_ref" not in src, f

@@ -1,0 +1,329 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element on the same seeded inputs.  Select and accept are bit-exact; attention
+max-abs error <= 2e-2 (bf16 inputs) or <= 1e-5 (fp32), per BASELINE north_star.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.helpers import bf16_bits, dev, oracle_attn, workload_to_device
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 2e-2
+F32_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def ada():
+    import paper_2501_12162_b200 as ada
+    ada.lib()
+    return ada
+
+
+# --------------------------------------------------------------------------- tcgen05 building blocks
+@pytest.mark.parametrize("n,k,mn", [(64, 128, 0), (128, 128, 0), (64, 64, 0), (128, 64, 1), (64, 64, 1),
+                                    (128, 128, 1)])
+def test_umma_selftest(ada, n, k, mn):
+    g = torch.Generator(device="cpu").manual_seed(n * 7 + k + mn)
+    a = torch.randn(128, k, generator=g).to(torch.bfloat16)
+    b = torch.randn((k, n) if mn else (n, k), generator=g).to(torch.bfloat16)
+    d = ada.selftest_umma(a.cuda(), b.cuda(), n, k, mn).cpu()
+    ref = a.double() @ (b.double() if mn else b.double().T)
+    torch.cuda.synchronize()
+    assert torch.allclose(d.double(), ref, atol=1e-3, rtol=1e-4), (d - ref).abs().max()
+
+
+# --------------------------------------------------------------------------- select
+def _gpu_select(ada, F, A, d, n_max, B):
+    co, cp, cf = F["cand_offsets"], F["cand_parent"], F["cand_prob"]
+    tok = F.get("cand_token")
+    out = ada.select_trees(dev(co), dev(cp), dev(cf), dev(np.asarray(A, np.float64)), d, n_max, B,
+                           cand_token=None if tok is None else dev(tok))
+    code, req = ada.check_device_error(out["workspace"])
+    assert code == 0, (code, req)
+    return {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in out.items()}
+
+
+def _assert_select_equal(F, A, d, n_max, B, got):
+    ref = oracle.select_literal(F["cand_offsets"], F["cand_parent"], F["cand_prob"], A, d, n_max, B)
+    n = len(F["cand_offsets"]) - 1
+    used = int(ref["tree_offsets"][-1])
+    np.testing.assert_array_equal(got["tree_offsets"][: n + 1], ref["tree_offsets"])
+    np.testing.assert_array_equal(got["tree_src"][:used], ref["tree_src"])
+    np.testing.assert_array_equal(got["tree_parent"][:used], ref["tree_parent"])
+    np.testing.assert_array_equal(got["tree_depth"][:used], ref["tree_depth"])
+    np.testing.assert_array_equal(got["slo_count"][:n], ref["slo_count"])
+    if F.get("cand_token") is not None:
+        to = ref["tree_offsets"]
+        req = np.repeat(np.arange(n), np.diff(to))
+        want = F["cand_token"][F["cand_offsets"][req] + ref["tree_src"]]
+        np.testing.assert_array_equal(got["tree_token"][:used], want)
+    return ref
+
+
+def test_select_fig4(ada):
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fig4.json")))
+    offs = [0]
+    par, prob = [], []
+    for r in g["requests"]:
+        par += r["parent"]
+        prob += r["prob"]
+        offs.append(offs[-1] + len(r["parent"]))
+    F = dict(cand_offsets=np.array(offs, np.int32), cand_parent=np.array(par, np.int32),
+             cand_prob=np.array(prob, np.float32))
+    got = _gpu_select(ada, F, g["slo_deficit"], g["depth_d"], g["n_max"], g["budget"])
+    ref = _assert_select_equal(F, g["slo_deficit"], g["depth_d"], g["n_max"], g["budget"], got)
+    assert got["slo_count"][:2].tolist() == g["expected"]["slo_count"]
+    assert int(ref["tree_offsets"][-1]) == g["expected"]["used"]
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c1slo", "c2", "c3", "c4", "c5"])
+def test_select_configs(ada, cfg):
+    rng = synth.rng_for(hash(cfg) % 97)
+    if cfg.startswith("c1"):
+        F = synth.beam_forest(rng, 1, 3, 3)
+        A, n_max, B, d = ([0.5], 7, 8, 3) if cfg == "c1" else ([2.5], 7, 8, 3)
+    elif cfg == "c2":
+        F = synth.beam_forest(rng, 64, 8, 8, 1.0, 4.0)
+        A, n_max, B, d = np.full(64, 9.0), 31, 2048, 8
+    elif cfg == "c3":
+        F = synth.beam_forest(rng, 256, 8, 8, 1.0, 8.0)
+        A, n_max, B, d = synth.slo_mix(rng, 256), 63, 4096, 8
+    elif cfg == "c4":
+        F = synth.beam_forest(rng, 128, 8, 8, 1.0, 4.0)
+        A, n_max, B, d = np.full(128, 9.0), 63, 8192, 8
+    else:
+        F = synth.beam_forest(rng, 32, 8, 8, 1.0, 4.0)
+        A, n_max, B, d = np.full(32, 9.0), 63, 2048, 8
+    got = _gpu_select(ada, F, A, d, n_max, B)
+    ref = _assert_select_equal(F, A, d, n_max, B, got)
+    if cfg == "c2":
+        assert (np.diff(ref["tree_offsets"]) == 32).all()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_select_fuzz(ada, seed):
+    rng = np.random.default_rng(100 + seed)
+    for it in range(40):
+        n = int(rng.integers(1, [8, 40, 300, 1200, 64, 2][seed]))
+        maxn = int([12, 40, 80, 6, 257, 257][seed])
+        F = synth.random_forest(rng, n, maxn, tie_prob=float(rng.choice([0.0, 0.5])))
+        N = int(F["cand_offsets"][-1])
+        F["cand_token"] = rng.integers(0, 128256, N).astype(np.int32)
+        A = rng.uniform(-1, 7, n)
+        if rng.random() < 0.5:
+            A[rng.integers(0, n, max(1, n // 3))] = A[0]
+        d = int(rng.integers(1, 9))
+        n_max = int(rng.integers(0, 70))
+        B = int(rng.integers(n, N + 5))
+        got = _gpu_select(ada, F, A, d, n_max, B)
+        _assert_select_equal(F, A, d, n_max, B, got)
+
+
+# --------------------------------------------------------------------------- accept
+def _accept_inputs(rng, n, maxK, vocab=50, dtype=np.float32, n_kv=2, d=64, ps=16, L_max=70):
+    sizes = rng.integers(1, maxK + 1, n)
+    to = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    R = int(to[-1])
+    par = np.concatenate([synth.random_tree_parents(rng, int(k), shape=rng.choice(["random", "chain", "star"]))
+                          for k in sizes]).astype(np.int32)
+    toks = np.zeros(R, np.int32)
+    for i in range(n):
+        for p in range(int(sizes[i])):
+            kids = [c for c in range(1, int(sizes[i])) if par[to[i] + c] == p]
+            vals = rng.permutation(vocab)[: len(kids)]
+            if rng.random() < 0.2 and len(kids) > 1:
+                vals[1] = vals[0]  # duplicate sibling token: lowest index must win
+            for c, v in zip(kids, vals):
+                toks[to[i] + c] = v
+    tgt = rng.integers(0, vocab, R).astype(np.int32)
+    for i in range(n):  # make walks go deep: 75% of nodes target one of their children
+        for p in range(int(sizes[i])):
+            kids = [c for c in range(1, int(sizes[i])) if par[to[i] + c] == p]
+            if kids and rng.random() < 0.75:
+                tgt[to[i] + p] = toks[to[i] + kids[int(rng.integers(0, len(kids)))]]
+    kv_len = rng.integers(0, L_max, n).astype(np.int32)
+    table, n_pages = synth.paged_kv(rng, kv_len, ps, extra_slots=maxK + 2)
+    shape_t, shape_c = (R, n_kv, d), (n_pages, n_kv, ps, d)
+    if dtype == np.float32:
+        kt, vt = rng.standard_normal(shape_t).astype(np.float32), rng.standard_normal(shape_t).astype(np.float32)
+        kc, vc = rng.standard_normal(shape_c).astype(np.float32), rng.standard_normal(shape_c).astype(np.float32)
+    else:
+        kt = synth.bf16_round(rng.standard_normal(shape_t).astype(np.float32))
+        vt = synth.bf16_round(rng.standard_normal(shape_t).astype(np.float32))
+        kc = synth.bf16_round(rng.standard_normal(shape_c).astype(np.float32))
+        vc = synth.bf16_round(rng.standard_normal(shape_c).astype(np.float32))
+    return dict(to=to, par=par, toks=toks, tgt=tgt, kv_len=kv_len, table=table, kt=kt, vt=vt, kc=kc, vc=vc)
+
+
+@pytest.mark.parametrize("kv_dtype", [torch.float32, torch.bfloat16])
+def test_accept_fused_tokens(ada, kv_dtype):
+    rng = np.random.default_rng(11)
+    for it in range(6):
+        n = int(rng.integers(1, 200))
+        X = _accept_inputs(rng, n, int(rng.integers(1, 65)), dtype=np.float32 if kv_dtype == torch.float32 else "bf16")
+        max_path = 64
+        ref = oracle.accept_walk(X["to"], X["par"], X["toks"], target_tokens=X["tgt"], max_path=max_path)
+        kc_g, vc_g, kl_g = dev(X["kc"], kv_dtype), dev(X["vc"], kv_dtype), dev(X["kv_len"])
+        res = ada.accept_tokens(ada.AS_ACCEPT_FUSED, dev(X["to"]), dev(X["par"]), dev(X["toks"]),
+                                target_tokens=dev(X["tgt"]), max_path=max_path, k_tree=dev(X["kt"], kv_dtype),
+                                v_tree=dev(X["vt"], kv_dtype), k_cache=kc_g, v_cache=vc_g, page_table=dev(X["table"]),
+                                kv_len=kl_g)
+        assert ada.check_device_error(res["workspace"])[0] == 0
+        np.testing.assert_array_equal(res["accept_len"].cpu().numpy()[:n], ref["accept_len"])
+        np.testing.assert_array_equal(res["accept_path"].cpu().numpy()[:n], ref["accept_path"])
+        np.testing.assert_array_equal(res["bonus_token"].cpu().numpy()[:n], ref["bonus_token"])
+        # commit, byte-exact (oracle on the same byte patterns)
+        if kv_dtype == torch.bfloat16:
+            to_bits = lambda a: bf16_bits(torch.from_numpy(a).to(torch.bfloat16))
+            kc, vc, kt, vt = (to_bits(X[k]) for k in ("kc", "vc", "kt", "vt"))
+            got_k, got_v = bf16_bits(kc_g), bf16_bits(vc_g)
+        else:
+            kc, vc, kt, vt = (X[k].copy() for k in ("kc", "vc", "kt", "vt"))
+            got_k, got_v = kc_g.cpu().numpy(), vc_g.cpu().numpy()
+        kl = X["kv_len"].copy()
+        assert oracle.commit(X["to"], ref["accept_len"], ref["accept_path"], kt, vt, kc, vc, X["table"], kl) == 0
+        np.testing.assert_array_equal(kl_g.cpu().numpy(), kl)
+        np.testing.assert_array_equal(got_k.view(np.uint8), kc.view(np.uint8))
+        np.testing.assert_array_equal(got_v.view(np.uint8), vc.view(np.uint8))
+
+
+@pytest.mark.parametrize("ldt", [torch.float32, torch.bfloat16])
+def test_accept_logits_greedy(ada, ldt):
+    rng = np.random.default_rng(12)
+    n = 37
+    X = _accept_inputs(rng, n, 20, vocab=3000)
+    R = int(X["to"][-1])
+    vocab = 3001  # odd: exercises the unaligned tail path
+    logits = rng.standard_normal((R, vocab)).astype(np.float32)
+    logits[np.arange(R), X["tgt"]] = 9.0
+    tie = rng.random(R) < 0.3  # exact ties: the lower index must win
+    alt = rng.integers(0, vocab, R)
+    logits[tie, alt[tie]] = 9.0
+    if ldt == torch.bfloat16:
+        logits = synth.bf16_round(logits)
+    ref = oracle.accept_walk(X["to"], X["par"], X["toks"], target_logits=logits, max_path=32)
+    res = ada.accept_tokens(ada.AS_ACCEPT_WALK_ONLY, dev(X["to"]), dev(X["par"]), dev(X["toks"]),
+                            target_logits=dev(logits, ldt), max_path=32)
+    assert ada.check_device_error(res["workspace"])[0] == 0
+    np.testing.assert_array_equal(res["accept_len"].cpu().numpy()[:n], ref["accept_len"])
+    np.testing.assert_array_equal(res["accept_path"].cpu().numpy()[:n], ref["accept_path"])
+    np.testing.assert_array_equal(res["bonus_token"].cpu().numpy()[:n], ref["bonus_token"])
+
+
+def test_accept_sharded_walk_then_commit_equals_fused(ada):
+    """WALK_ONLY over request shards + COMMIT_ONLY over all == FUSED (the
+    multi-GPU protocol with the all-gather replaced by local copies)."""
+    rng = np.random.default_rng(13)
+    n = 50
+    X = _accept_inputs(rng, n, 30, dtype="bf16")
+    args = dict(k_tree=dev(X["kt"], torch.bfloat16), v_tree=dev(X["vt"], torch.bfloat16),
+                page_table=dev(X["table"]))
+    kc1, vc1, kl1 = dev(X["kc"], torch.bfloat16), dev(X["vc"], torch.bfloat16), dev(X["kv_len"])
+    fused = ada.accept_tokens(ada.AS_ACCEPT_FUSED, dev(X["to"]), dev(X["par"]), dev(X["toks"]),
+                              target_tokens=dev(X["tgt"]), max_path=24, k_cache=kc1, v_cache=vc1, kv_len=kl1, **args)
+    al = torch.full((n,), -5, dtype=torch.int32, device="cuda")
+    ap = torch.full((n, 24), -5, dtype=torch.int32, device="cuda")
+    bt = torch.full((n,), -5, dtype=torch.int32, device="cuda")
+    for b, e in [(0, 17), (17, 34), (34, 50)]:
+        ada.accept_tokens(ada.AS_ACCEPT_WALK_ONLY, dev(X["to"]), dev(X["par"]), dev(X["toks"]),
+                          target_tokens=dev(X["tgt"]), max_path=24, req_range=(b, e), accept_len=al,
+                          accept_path=ap, bonus_token=bt)
+    kc2, vc2, kl2 = dev(X["kc"], torch.bfloat16), dev(X["vc"], torch.bfloat16), dev(X["kv_len"])
+    ada.accept_tokens(ada.AS_ACCEPT_COMMIT_ONLY, dev(X["to"]), max_path=24, accept_len=al, accept_path=ap,
+                      k_cache=kc2, v_cache=vc2, kv_len=kl2, n_tree_rows=int(X["to"][-1]), **args)
+    assert torch.equal(al, fused["accept_len"]) and torch.equal(ap, fused["accept_path"])
+    assert torch.equal(bt, fused["bonus_token"])
+    assert torch.equal(kl1, kl2) and torch.equal(kc1, kc2) and torch.equal(vc1, vc2)
+
+
+# --------------------------------------------------------------------------- attention
+ATTN_CASES = [
+    # (sizes, kv_lens, n_q, n_kv, d, page_size, shape, q_scale)
+    ([8], [128], 4, 4, 64, 16, "random", 1.0),                     # BASELINE config 1
+    ([8], [128], 4, 2, 64, 16, "random", 1.0),                     # c1 GQA variant
+    ([1, 1, 2], [0, 1, 63], 4, 4, 64, 16, "random", 1.0),          # L=0, root-only
+    ([5, 17, 33], [64, 65, 127], 8, 2, 128, 32, "chain", 1.0),     # tile boundaries, chains
+    ([40, 7], [300, 129], 8, 1, 128, 128, "star", 1.0),            # G=8, star, page 128
+    ([64, 3, 128], [200, 5, 77], 4, 1, 128, 64, "random", 4.0),    # multi m-tile, K=128, peaky
+    ([128], [96], 16, 1, 128, 16, "chain", 1.0),                   # G=16, 16 m-tiles, deep chain
+    ([9, 31, 2, 64, 15], [1000, 33, 0, 511, 2049], 32, 8, 128, 64, "random", 1.0),  # Llama-3-8B heads
+]
+
+
+def _attn_case(case, bf16, seed):
+    sizes, kv_lens, n_q, n_kv, d, ps, shape, qs = case
+    rng = np.random.default_rng(seed)
+    return synth.tree_workload(rng, sizes, kv_lens, n_q, n_kv, d, ps, shape=shape, bf16=bf16, q_scale=qs)
+
+
+@pytest.mark.parametrize("ci", range(len(ATTN_CASES)))
+def test_attn_fp32(ada, ci):
+    w = _attn_case(ATTN_CASES[ci], False, 300 + ci)
+    scale = np.float32(1.0 / np.sqrt(w["q"].shape[2]))
+    ref, ref_lse = oracle_attn(w, scale)
+    g = workload_to_device(w, torch.float32)
+    ws = ada.Workspace(256)
+    out, lse = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"], g["page_table"],
+                                    g["kv_len"], g["tree_offsets"], g["tree_parent"], scale, want_lse=True,
+                                    workspace=ws)
+    assert ada.check_device_error(ws)[0] == 0
+    err = np.abs(out.cpu().numpy() - ref).max()
+    assert err <= F32_TOL, err
+    assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-4
+
+
+@pytest.mark.parametrize("ci", range(1, len(ATTN_CASES)))
+def test_attn_bf16(ada, ci):
+    w = _attn_case(ATTN_CASES[ci], True, 400 + ci)
+    scale = np.float32(1.0 / np.sqrt(w["q"].shape[2]))
+    ref, ref_lse = oracle_attn(w, scale)
+    g = workload_to_device(w, torch.bfloat16)
+    ws = ada.Workspace(256)
+    out, lse = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"], g["page_table"],
+                                    g["kv_len"], g["tree_offsets"], g["tree_parent"], scale, want_lse=True,
+                                    workspace=ws)
+    assert ada.check_device_error(ws)[0] == 0
+    err = np.abs(out.float().cpu().numpy() - ref).max()
+    assert err <= BF16_TOL, err
+    assert np.abs(lse.cpu().numpy() - ref_lse).max() <= BF16_TOL
+
+
+def test_attn_bf16_nan_in_unused_cache_slots(ada):
+    """Cache slots past kv_len may hold garbage (NaN): outputs must not see them."""
+    w = _attn_case(([6, 9], [70, 33], 8, 2, 128, 64, "random", 1.0), True, 77)
+    scale = np.float32(1.0 / np.sqrt(128))
+    ref, _ = oracle_attn(w, scale)
+    ps = 64
+    for i, L in enumerate(w["kv_len"]):
+        for t in range(int(L), w["page_table"].shape[1] * ps):
+            pg = w["page_table"][i, t // ps]
+            if pg >= 0:
+                w["k_cache"][pg, :, t % ps] = np.nan
+                w["v_cache"][pg, :, t % ps] = np.nan
+    g = workload_to_device(w, torch.bfloat16)
+    out, _ = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"], g["page_table"],
+                                  g["kv_len"], g["tree_offsets"], g["tree_parent"], scale)
+    o = out.float().cpu().numpy()
+    assert np.isfinite(o).all()
+    assert np.abs(o - ref).max() <= BF16_TOL
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c4", "c5"])
+def test_attn_bf16_full_size_sampled(ada, cfg):
+    """BASELINE full sizes, the launch bench.py times; oracle on sampled requests."""
+    import bench
+    W = bench.make_workload(cfg, device="cuda", seed_salt=5)
+    out = bench.run_attention(W)
+    torch.cuda.synchronize()
+    w = bench.workload_host_copy(W, requests=W["sample_requests"])
+    scale = np.float32(W["sm_scale"])
+    rows, ref, _ = oracle_attn(w, scale, requests=list(range(len(W["sample_requests"]))))
+    got = out[torch.from_numpy(w["global_rows"]).cuda()].float().cpu().numpy()
+    assert np.abs(got - ref).max() <= BF16_TOL
