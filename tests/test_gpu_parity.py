@@ -315,15 +315,37 @@ def test_attn_bf16_nan_in_unused_cache_slots(ada):
     assert np.abs(o - ref).max() <= BF16_TOL
 
 
-@pytest.mark.parametrize("cfg", ["c2", "c4", "c5"])
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
 def test_attn_bf16_full_size_sampled(ada, cfg):
-    """BASELINE full sizes, the launch bench.py times; oracle on sampled requests."""
+    """BASELINE full sizes in the launch bench.py times; the oracle checks sampled
+    requests (all their heads).  The oracle's trees come from the oracle's own
+    select on the same forest (asserted bit-identical to the GPU's)."""
     import bench
     W = bench.make_workload(cfg, device="cuda", seed_salt=5)
+    bench.run_select(W)
     out = bench.run_attention(W)
     torch.cuda.synchronize()
-    w = bench.workload_host_copy(W, requests=W["sample_requests"])
-    scale = np.float32(W["sm_scale"])
-    rows, ref, _ = oracle_attn(w, scale, requests=list(range(len(W["sample_requests"]))))
-    got = out[torch.from_numpy(w["global_rows"]).cuda()].float().cpu().numpy()
+    F, c = W["host"], W["c"]
+    ref_sel = oracle.select_literal(F["cand_offsets"], F["cand_parent"], F["cand_prob"], W["A"], c["d"], c["n_max"],
+                                    c["budget"])
+    used = int(ref_sel["tree_offsets"][-1])
+    np.testing.assert_array_equal(W["sel"]["tree_offsets"].cpu().numpy(), ref_sel["tree_offsets"])
+    np.testing.assert_array_equal(W["sel"]["tree_parent"].cpu().numpy()[:used], ref_sel["tree_parent"])
+    reqs = W["sample_requests"]
+    to = ref_sel["tree_offsets"]
+    kc, vc = W["pools"][W["pool_idx"]]
+    w = dict(q=W["q"].float().cpu().numpy(), k_tree=W["k_tree"].float().cpu().numpy(),
+             v_tree=W["v_tree"].float().cpu().numpy(), tree_offsets=to,
+             tree_parent=np.concatenate([ref_sel["tree_parent"], np.zeros(W["R"] - used, np.int32)]),
+             page_table=W["table_host"], kv_len=W["kv_len_host"])
+    pt = W["table_host"][reqs]
+    pages = np.unique(pt[pt >= 0])
+    idx = torch.from_numpy(pages).cuda()
+    kfull = np.zeros((W["n_pages"],) + tuple(kc.shape[1:]), np.float32)
+    vfull = np.zeros_like(kfull)
+    kfull[pages] = kc.index_select(0, idx).float().cpu().numpy()
+    vfull[pages] = vc.index_select(0, idx).float().cpu().numpy()
+    w["k_cache"], w["v_cache"] = kfull, vfull
+    rows, ref, _ = oracle_attn(w, np.float32(W["sm_scale"]), requests=reqs)
+    got = out[torch.from_numpy(rows).cuda()].float().cpu().numpy()
     assert np.abs(got - ref).max() <= BF16_TOL
