@@ -207,35 +207,61 @@ def attn_flops(W):
     return int(np.sum(4 * D * K * L)) * W["n_q"]
 
 
+_cudart = None
+
+
+def _record(ev, external):
+    """Record `ev` on the current stream.  Inside CUDA-graph capture the event
+    must become an event-record NODE (cudaEventRecordExternal) to be timeable."""
+    global _cudart
+    if not external:
+        ev.record()
+        return
+    import ctypes
+    if _cudart is None:
+        _cudart = ctypes.CDLL("libcudart.so.12")
+        _cudart.cudaEventRecordWithFlags.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint]
+    rc = _cudart.cudaEventRecordWithFlags(ctypes.c_void_p(ev.cuda_event),
+                                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream), 1)
+    if rc != 0:
+        raise RuntimeError(f"cudaEventRecordWithFlags failed: {rc}")
+
+
+def make_events(n):
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    for e in evs:  # materialise the CUDA events outside any capture
+        e.record()
+    torch.cuda.synchronize()
+    return evs
+
+
 class Step:
-    """One hot-path step on the current stream; records per-kernel events."""
+    """One hot-path step on the current stream; optionally records 4 events
+    (before select, before attention, before accept, after accept)."""
 
     def __init__(self, W, dist_ctx=None):
         self.W = W
         self.dist = dist_ctx
-        self.ev = None
 
-    def __call__(self, record=False):
+    def __call__(self, events=None, external=False):
         W = self.W
         W["pool_idx"] = (W["pool_idx"] + 1) % W["n_pools"]
         W["kv_len"].copy_(W["kv_len0"], non_blocking=True)
-        if record:
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-            e[0].record()
+        if events:
+            _record(events[0], external)
         run_select(W)
-        if record:
-            e[1].record()
+        if events:
+            _record(events[1], external)
         run_attention(W)
-        if record:
-            e[2].record()
+        if events:
+            _record(events[2], external)
         if self.dist is None:
             run_accept(W)
         else:
             self.dist.accept_and_commit(W)
-        if record:
-            e[3].record()
-            self.ev = e
-        return self.ev
+        if events:
+            _record(events[3], external)
+        return events
 
 
 def _clock_sampler_start():
@@ -372,21 +398,21 @@ def main():
     for _ in range(2):  # eager warm-up (attribute setup, NCCL communicator)
         step()
     torch.cuda.synchronize()
+    all_ev = make_events(4 * args.steps + 2)
+    start, end = all_ev[-2], all_ev[-1]
+    evs = [all_ev[4 * k:4 * k + 4] for k in range(args.steps)]
     if use_graph:
         # The whole hot path of a step is replayed from CUDA graphs:
-        # one graph of K unrolled steps with CUDA events around every kernel call.
+        # one graph of K unrolled steps with event-record nodes around every call.
         g_warm = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_warm):
             step()
         g_timed = torch.cuda.CUDAGraph()
-        evs = []
         with torch.cuda.graph(g_timed):
-            start = torch.cuda.Event(enable_timing=True)
-            end = torch.cuda.Event(enable_timing=True)
-            start.record()
-            for _ in range(args.steps):
-                evs.append(step(record=True))
-            end.record()
+            _record(start, True)
+            for k in range(args.steps):
+                step(evs[k], external=True)
+            _record(end, True)
         for _ in range(args.warmup):
             g_warm.replay()
     else:
@@ -402,12 +428,9 @@ def main():
     if use_graph:
         g_timed.replay()
     else:
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
-        evs = []
         start.record()
-        for _ in range(args.steps):
-            evs.append(step(record=True))
+        for k in range(args.steps):
+            step(evs[k])
         end.record()
     torch.cuda.synchronize()
     if world > 1:

@@ -34,9 +34,9 @@ namespace as {
 constexpr int kBM = 128;          // query rows per tile (UMMA M)
 constexpr int kBN = 64;           // keys per tile
 constexpr int kStages = 4;        // K and V ring depth
-constexpr int kThreads = 192;     // 6 warps
-constexpr int kTmemCols = 256;    // S0 [0,64) S1 [64,128) O [128, 128+D)
-constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kThreads = 320;     // 10 warps: TMA, MMA, 2 x 4 softmax
+constexpr int kTmemCols = 512;    // S0 [0,64) S1 [64,128) O0 [128,128+D) O1 [128+D, 128+2D)
+constexpr int kOcol = 128;
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
 
@@ -50,7 +50,8 @@ struct TcSmem {
     static constexpr int OFF_K = OFF_Q + Q_BYTES;
     static constexpr int OFF_V = OFF_K + kStages * KV_BYTES;
     static constexpr int OFF_P = OFF_V + kStages * KV_BYTES;
-    static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+    static constexpr int OFF_ML = OFF_P + 2 * P_BYTES;        // [2][2][2][128] f32 merge scratch
+    static constexpr int OFF_BAR = OFF_ML + 2 * 2 * 2 * 128 * 4;
     static constexpr int N_BAR = 2 + 4 * kStages + 8 + 2;
     static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
     static constexpr int BYTES = OFF_TMEM + 16;
@@ -117,12 +118,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(s_full + b, 1);
-            ptx::mbar_init(s_empty + b, 4);
+            ptx::mbar_init(s_empty + b, 4);  // the 4 warps of softmax warpgroup b
             ptx::mbar_init(p_full + b, 4);
             ptx::mbar_init(p_empty + b, 1);
         }
         ptx::mbar_init(o_full, 1);
-        ptx::mbar_init(o_empty, 4);
+        ptx::mbar_init(o_empty, 8);
         ptx::fence_mbar_init();
         ptx::tma_prefetch(&tm_q);
         ptx::tma_prefetch(&tm_kc);
@@ -209,29 +210,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
+        // Softmax warpgroup w (0/1) owns the tiles t = w (mod 2) of every unit, with
+        // its own TMEM S buffer S[w], smem P buffer P[w] and TMEM accumulator O[w].
+        // Issue order per unit: QK0 QK1 | PV0 QK2 | PV1 QK3 | ... so that S_{t+2}
+        // is computed while warpgroup w^1 runs the softmax of tile t+1.
         constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(kBM, kBN, 0);
         constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(kBM, D, 1);
         const uint32_t q_base = ptx::smem_u32(smem + S::OFF_Q);
         const uint32_t k_base = ptx::smem_u32(smem + S::OFF_K);
         const uint32_t v_base = ptx::smem_u32(smem + S::OFF_V);
         const uint32_t p_base = ptx::smem_u32(smem + S::OFF_P);
-        const uint32_t tm_o = tmem + 128;
-        uint32_t k_it = 0, v_it = 0, s_it = 0, unit_it = 0;
+        uint32_t k_it = 0, v_it = 0, unit_it = 0;
+        uint32_t s_ph = 0, p_ph = 0;  // bit wg = phase parity of S[wg] / P[wg] uses
         for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
             Unit u;
             if (!decode_unit(p, w, u)) continue;
             ptx::mbar_wait(q_full, unit_it & 1);
-            const uint32_t s_first = s_it;
-            auto do_pv = [&](int tp) {
-                const uint32_t sidx = s_first + tp;
+            auto do_qk = [&](int t) {
+                const int wg = t & 1;
+                const int st = k_it % kStages;
+                ptx::mbar_wait(k_full + st, (k_it / kStages) & 1);
+                ptx::mbar_wait(s_empty + wg, ((s_ph >> wg) & 1) ^ 1);
+                ptx::tc_fence_after();
+                if (lane == 0) {
+#pragma unroll
+                    for (int ks = 0; ks < D / 16; ++ks) {
+                        const int c = ks >> 2, kk = ks & 3;
+                        const uint64_t a = ptx::sw128_desc(q_base + c * kBM * 128 + kk * 32, 0, 1024);
+                        const uint64_t b = ptx::sw128_desc(k_base + st * S::KV_BYTES + c * kBN * 128 + kk * 32, 0, 1024);
+                        ptx::mma_bf16_ss(tmem + wg * kBN, a, b, idesc_qk, ks > 0 ? 1u : 0u);
+                    }
+                    ptx::mma_commit(k_empty + st);
+                    ptx::mma_commit(s_full + wg);
+                    if (t == u.nt - 1) ptx::mma_commit(q_empty);
+                }
+                __syncwarp();
+                ++k_it;
+                s_ph ^= 1u << wg;
+            };
+            auto do_pv = [&](int t) {
+                const int wg = t & 1;
                 const int st = v_it % kStages;
-                const uint32_t ph = (v_it / kStages) & 1;
-                const int pb = sidx & 1;
-                ptx::mbar_wait(v_full + st, ph);
+                ptx::mbar_wait(v_full + st, (v_it / kStages) & 1);
                 // zero V rows past the prefix end (stale/uninitialised smem or cache
                 // slots >= L may hold NaN; P is 0 there but 0 * NaN = NaN)
-                if (tp < u.n_prefix) {
-                    const int valid = min(kBN, u.L - tp * kBN);
+                if (t < u.n_prefix) {
+                    const int valid = min(kBN, u.L - t * kBN);
                     if (valid < kBN) {
                         unsigned char* vs = smem + S::OFF_V + st * S::KV_BYTES;
                         const int nvec = (kBN - valid) * 8;  // 16-byte vectors per chunk
@@ -241,60 +265,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::fence_proxy_async_smem();
                     }
                 }
-                ptx::mbar_wait(p_full + pb, (sidx >> 1) & 1);
-                if (tp == 0) ptx::mbar_wait(o_empty, (unit_it & 1) ^ 1);
+                ptx::mbar_wait(p_full + wg, (p_ph >> wg) & 1);
+                if (t == 0) ptx::mbar_wait(o_empty, (unit_it & 1) ^ 1);  // both O buffers drained
                 ptx::tc_fence_after();
                 __syncwarp();
                 if (lane == 0) {
 #pragma unroll
                     for (int kk = 0; kk < kBN / 16; ++kk) {
-                        const uint64_t a = ptx::sw128_desc(p_base + pb * S::P_BYTES + kk * 32, 0, 1024);
-                        const uint64_t b =
-                            ptx::sw128_desc(v_base + st * S::KV_BYTES + kk * 16 * 128, kBN * 128, 1024);
-                        ptx::mma_bf16_ss(tm_o, a, b, idesc_pv, (tp > 0 || kk > 0) ? 1u : 0u);
+                        const uint64_t a = ptx::sw128_desc(p_base + wg * S::P_BYTES + kk * 32, 0, 1024);
+                        const uint64_t b = ptx::sw128_desc(v_base + st * S::KV_BYTES + kk * 16 * 128, kBN * 128, 1024);
+                        ptx::mma_bf16_ss(tmem + kOcol + wg * D, a, b, idesc_pv, (t >= 2 || kk > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(v_empty + st);
-                    ptx::mma_commit(p_empty + pb);
+                    ptx::mma_commit(p_empty + wg);
                 }
                 __syncwarp();
                 ++v_it;
+                p_ph ^= 1u << wg;
             };
+            do_qk(0);
+            if (u.nt > 1) do_qk(1);
             for (int t = 0; t < u.nt; ++t) {
-                const int st = k_it % kStages;
-                const uint32_t ph = (k_it / kStages) & 1;
-                const int sb = s_it & 1;
-                ptx::mbar_wait(k_full + st, ph);
-                ptx::mbar_wait(s_empty + sb, ((s_it >> 1) & 1) ^ 1);
-                ptx::tc_fence_after();
-                if (lane == 0) {
-#pragma unroll
-                    for (int ks = 0; ks < D / 16; ++ks) {
-                        const int c = ks >> 2, kk = ks & 3;
-                        const uint64_t a = ptx::sw128_desc(q_base + c * kBM * 128 + kk * 32, 0, 1024);
-                        const uint64_t b = ptx::sw128_desc(k_base + st * S::KV_BYTES + c * kBN * 128 + kk * 32, 0, 1024);
-                        ptx::mma_bf16_ss(tmem + sb * kBN, a, b, idesc_qk, ks > 0 ? 1u : 0u);
-                    }
-                    ptx::mma_commit(k_empty + st);
-                    ptx::mma_commit(s_full + sb);
-                    if (t == u.nt - 1) ptx::mma_commit(q_empty);
-                }
-                __syncwarp();
-                ++k_it;
-                ++s_it;
-                if (t > 0) do_pv(t - 1);
+                do_pv(t);
+                if (t + 2 < u.nt) do_qk(t + 2);
             }
-            do_pv(u.nt - 1);
             if (lane == 0) ptx::mma_commit(o_full);
             __syncwarp();
             ++unit_it;
         }
     } else {
-        // ===================== softmax + epilogue (warps 2..5) =====================
+        // ===================== softmax + epilogue (warps 2..9) =====================
+        const int wg = (warp - 2) >> 2;  // warpgroup: tiles t = wg (mod 2)
         const int quad = warp & 3;       // TMEM lane quadrant this warp may access
         const int r = quad * 32 + lane;  // Q row in the tile == TMEM lane
         const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-        unsigned char* p_smem = smem + S::OFF_P;
-        uint32_t s_it = 0, unit_it = 0;
+        const uint32_t s_addr = tmem + lane_addr + wg * kBN;
+        const uint32_t o_addr = tmem + lane_addr + kOcol + wg * D;
+        unsigned char* p_row = smem + S::OFF_P + wg * S::P_BYTES + r * 128;
+        float* ml = reinterpret_cast<float*>(smem + S::OFF_ML);  // [2 units][2 wg][2 (m,l)][128]
+        const float sl2 = p.scale_log2;
+        uint32_t s_cnt = 0, unit_it = 0;
         for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
             Unit u;
             if (!decode_unit(p, w, u)) continue;
@@ -319,53 +329,53 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             float m_ref = -INFINITY, l_sum = 0.f;
-            for (int t = 0; t < u.nt; ++t, ++s_it) {
-                const int sb = s_it & 1;
-                ptx::mbar_wait(s_full + sb, (s_it >> 1) & 1);
+            for (int t = wg; t < u.nt; t += 2, ++s_cnt) {
+                const uint32_t par = s_cnt & 1;
+                ptx::mbar_wait(s_full + wg, par);
                 ptx::tc_fence_after();
                 uint32_t sr[kBN];
-                ptx::tmem_ld32(tmem + lane_addr + sb * kBN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-                ptx::tmem_ld32(tmem + lane_addr + sb * kBN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+                ptx::tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+                ptx::tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
                 ptx::tmem_ld_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(s_empty + sb);
-                float x[kBN];
-                float tmax = -INFINITY;
+                if (lane == 0) ptx::mbar_arrive(s_empty + wg);
+                float* x = reinterpret_cast<float*>(sr);
                 if (t < u.n_prefix) {
                     const int valid = u.L - t * kBN;
+                    if (valid < kBN) {
 #pragma unroll
-                    for (int c = 0; c < kBN; ++c) {
-                        x[c] = (c < valid) ? __uint_as_float(sr[c]) * p.scale_log2 : -INFINITY;
-                        tmax = fmaxf(tmax, x[c]);
+                        for (int c = 0; c < kBN; ++c) x[c] = (c < valid) ? x[c] : -INFINITY;
                     }
                 } else {
                     const uint64_t bits = (t - u.n_prefix) == 0 ? anc0 : anc1;
 #pragma unroll
-                    for (int c = 0; c < kBN; ++c) {
-                        x[c] = ((bits >> c) & 1ull) ? __uint_as_float(sr[c]) * p.scale_log2 : -INFINITY;
-                        tmax = fmaxf(tmax, x[c]);
-                    }
+                    for (int c = 0; c < kBN; ++c) x[c] = ((bits >> c) & 1ull) ? x[c] : -INFINITY;
                 }
+                // tree max of the raw scores (sm_scale > 0 commutes with max)
+                float mx[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) mx[j] = fmaxf(fmaxf(x[j], x[j + 8]), fmaxf(x[j + 16], x[j + 24]));
+#pragma unroll
+                for (int j = 0; j < 8; ++j) mx[j] = fmaxf(mx[j], fmaxf(fmaxf(x[j + 32], x[j + 40]), fmaxf(x[j + 48], x[j + 56])));
+                const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
                 const float m_new = fmaxf(m_ref, tmax);
-                if (t == 0) {
-                    m_ref = m_new;
-                } else {
+                // P buffer wg is free (and O[wg] stable) once PV of this warpgroup's previous tile completed
+                ptx::mbar_wait(p_empty + wg, par ^ 1);
+                if (t >= 2) {
                     const bool need = m_new > m_ref + kRescaleThresh;
                     if (__any_sync(0xffffffffu, need)) {
-                        // PV_{t-1} must have landed in O before we rescale it
-                        const uint32_t prev = s_it - 1;
-                        ptx::mbar_wait(p_empty + (prev & 1), (prev >> 1) & 1);
                         ptx::tc_fence_after();
                         const float sc = need ? ptx::ex2(m_ref - m_new) : 1.f;
 #pragma unroll
                         for (int c0 = 0; c0 < D; c0 += 32) {
                             uint32_t o[32];
-                            ptx::tmem_ld32(tmem + lane_addr + 128 + c0, o);
+                            ptx::tmem_ld32(o_addr + c0, o);
                             ptx::tmem_ld_wait();
 #pragma unroll
                             for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * sc);
-                            ptx::tmem_st32(tmem + lane_addr + 128 + c0, o);
+                            ptx::tmem_st32(o_addr + c0, o);
                         }
                         ptx::tmem_st_wait();
                         ptx::tc_fence_before();
@@ -374,48 +384,64 @@ __global__ void __launch_bounds__(kThreads, 1)
                             m_ref = m_new;
                         }
                     }
+                } else {
+                    m_ref = m_new;
                 }
-                const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-                // P buffer sb is free once PV_{t-2} completed
-                ptx::mbar_wait(p_empty + sb, ((s_it >> 1) & 1) ^ 1);
-                float rsum = 0.f;
+                const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
+                float rs[4] = {0.f, 0.f, 0.f, 0.f};
                 uint32_t pk[kBN / 2];
 #pragma unroll
                 for (int c = 0; c < kBN; c += 2) {
-                    const float p0 = ptx::ex2(x[c] - m_use);
-                    const float p1 = ptx::ex2(x[c + 1] - m_use);
-                    rsum += p0 + p1;
+                    const float p0 = ptx::ex2(fmaf(x[c], sl2, neg_m));
+                    const float p1 = ptx::ex2(fmaf(x[c + 1], sl2, neg_m));
+                    rs[(c >> 1) & 3] += p0 + p1;
                     __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                     pk[c >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                 }
-                l_sum += rsum;
-                unsigned char* prow = p_smem + sb * S::P_BYTES + r * 128;
+                l_sum += (rs[0] + rs[1]) + (rs[2] + rs[3]);
 #pragma unroll
                 for (int ch = 0; ch < 8; ++ch) {
                     const int phys = ch ^ (r & 7);
-                    *reinterpret_cast<uint4*>(prow + phys * 16) =
+                    *reinterpret_cast<uint4*>(p_row + phys * 16) =
                         make_uint4(pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
                 }
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(p_full + sb);
+                if (lane == 0) ptx::mbar_arrive(p_full + wg);
             }
-            // epilogue
+            // ---- epilogue: merge the two warpgroups' partial softmax states ----
+            float* mlu = ml + (unit_it & 1) * 512;
+            mlu[wg * 256 + r] = m_ref;
+            mlu[wg * 256 + 128 + r] = l_sum;
             ptx::mbar_wait(o_full, unit_it & 1);
             ptx::tc_fence_after();
-            const float inv = 1.f / l_sum;
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            const float m0 = mlu[r], l0 = mlu[128 + r], m1 = mlu[256 + r], l1 = mlu[384 + r];
+            const float mm = fmaxf(m0, m1);
+            const float a0 = (m0 == -INFINITY) ? 0.f : ptx::ex2(m0 - mm);
+            const float a1 = (m1 == -INFINITY) ? 0.f : ptx::ex2(m1 - mm);
+            const float lt = l0 * a0 + l1 * a1;
+            const float inv = 1.f / lt;
+            const float f0 = a0 * inv, f1 = a1 * inv;
             const size_t orow = (size_t)(u.off + node) * p.n_q + (size_t)u.g * G + hh;
+            const uint32_t o0_addr = tmem + lane_addr + kOcol;
+            const uint32_t o1_addr = o0_addr + D;
 #pragma unroll
-            for (int c0 = 0; c0 < D; c0 += 32) {
-                uint32_t o[32];
-                ptx::tmem_ld32(tmem + lane_addr + 128 + c0, o);
+            for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
+                uint32_t oa[32], ob[32];
+                ptx::tmem_ld32(o0_addr + c0, oa);
+                ptx::tmem_ld32(o1_addr + c0, ob);
                 ptx::tmem_ld_wait();
                 if (row_ok) {
                     uint32_t pk[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(o[2 * j]) * inv,
-                                                                  __uint_as_float(o[2 * j + 1]) * inv);
+                        float v0 = __uint_as_float(oa[2 * j]) * f0, v1 = __uint_as_float(oa[2 * j + 1]) * f0;
+                        if (f1 != 0.f) {  // warpgroup 1 may have had no tile (garbage O[1])
+                            v0 = fmaf(__uint_as_float(ob[2 * j]), f1, v0);
+                            v1 = fmaf(__uint_as_float(ob[2 * j + 1]), f1, v1);
+                        }
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(v0, v1);
                         pk[j] = *reinterpret_cast<uint32_t*>(&h2);
                     }
                     uint4* dst = reinterpret_cast<uint4*>(p.out + orow * D + c0);
@@ -423,10 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
                 }
             }
-            if (row_ok && p.lse) {
-                const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-                p.lse[orow] = (m_use + __log2f(l_sum)) * 0.6931471805599453f;
-            }
+            if (row_ok && p.lse && wg == 0) p.lse[orow] = (mm + __log2f(lt)) * 0.6931471805599453f;
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(o_empty);

@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
     int* rank_s = ord_s + n;                                              // [n]
     int* remap_all = rank_s + n;                                          // [32][kRemapWords]
     unsigned* bitmap_all = reinterpret_cast<unsigned*>(remap_all + kSelWarps * kRemapWords);  // [32][kBitmapWords]
+    int* parent_all = reinterpret_cast<int*>(bitmap_all + kSelWarps * kBitmapWords);          // [32][kRemapWords]
 
     for (int i = threadIdx.x; i < n; i += kSelThreads) A_s[i] = p.A[i];
     __syncthreads();
@@ -385,6 +386,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
     // (5) emit: warp per request.
     int* remap = remap_all + warp_id() * kRemapWords;
     unsigned* bits = bitmap_all + warp_id() * kBitmapWords;
+    int* cpar = parent_all + warp_id() * kRemapWords;
     for (int i = warp_id(); i < n; i += kSelWarps) {
         int off;
         const int nr = n_nonroot(p, i, &off);
@@ -392,6 +394,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
         const int tbase = ord_s[i];
         const int sbase = off - i;
         for (int w = lane; w < kBitmapWords; w += 32) bits[w] = 0u;
+        for (int c = lane; c <= nr; c += 32) cpar[c] = p.cand_parent[off + c];  // staged: depth walks stay on chip
         __syncwarp();
         for (int t = lane; t < take; t += 32) {
             uint32_t idx = 0xFFFFFFFFu - (uint32_t)(__ldcg(p.skey + sbase + t) & 0xFFFFFFFFull);
@@ -418,14 +421,14 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
             const bool sel = c <= nr && ((bits[c >> 5] >> (c & 31)) & 1u);
             if (sel) {
                 const int row = tbase + remap[c];
-                const int par = p.cand_parent[off + c];
+                const int par = cpar[c];
                 const bool ok = par >= 0 && par < c;
                 p.tree_src[row] = c;
                 p.tree_parent[row] = (ok && par > 0) ? remap[par] : 0;
                 if (p.tree_depth) {
                     int dep = 1, u = par, guard = 0;
                     while (u > 0 && guard < AS_MAX_CAND + 1) {
-                        int pu = p.cand_parent[off + u];
+                        int pu = cpar[u];
                         u = (pu >= 0 && pu < u) ? pu : 0;
                         ++dep;
                         ++guard;
@@ -445,7 +448,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
 
 size_t select_smem_bytes(int n) {
     return (size_t)n * sizeof(double) + 2 * (size_t)n * sizeof(int) +
-           (size_t)kSelWarps * kRemapWords * sizeof(int) + (size_t)kSelWarps * kBitmapWords * sizeof(unsigned);
+           2 * (size_t)kSelWarps * kRemapWords * sizeof(int) + (size_t)kSelWarps * kBitmapWords * sizeof(unsigned);
 }
 
 size_t select_ws_bytes(int n_req, int n_cand_total) {
