@@ -3,6 +3,7 @@
 // kernel launches.  No exception crosses this file's functions.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdlib>
 #include <mutex>
 
 #include "params.cuh"
@@ -195,6 +196,8 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     p.out = (__nv_bfloat16*)out; p.lse = lse; p.ws = workspace;
     const int mt_max = (AS_MAX_TREE * G + 127) / 128;
     p.n_units = mt_max * n_req * n_kv_heads;
+    const char* dbg = getenv("AS_ATTN_DEBUG_MODE");  // timing experiments only (wrong outputs)
+    p.debug_mode = dbg ? atoi(dbg) : 0;
     return launch_attn_tc(maps, p, head_dim, sm_count(), S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
 }
 

@@ -232,7 +232,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(k_full + st, (k_it / kStages) & 1);
                 ptx::mbar_wait(s_empty + wg, ((s_ph >> wg) & 1) ^ 1);
                 ptx::tc_fence_after();
-                if (lane == 0) {
+                if (p.debug_mode >= 2) {
+                    if (lane == 0) {
+                        ptx::mbar_arrive(k_empty + st);
+                        ptx::mbar_arrive(s_full + wg);
+                        if (t == u.nt - 1) ptx::mbar_arrive(q_empty);
+                    }
+                } else if (lane == 0) {
 #pragma unroll
                     for (int ks = 0; ks < D / 16; ++ks) {
                         const int c = ks >> 2, kk = ks & 3;
@@ -269,7 +275,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t == 0) ptx::mbar_wait(o_empty, (unit_it & 1) ^ 1);  // both O buffers drained
                 ptx::tc_fence_after();
                 __syncwarp();
-                if (lane == 0) {
+                if (p.debug_mode >= 2) {
+                    if (lane == 0) {
+                        ptx::mbar_arrive(v_empty + st);
+                        ptx::mbar_arrive(p_empty + wg);
+                    }
+                } else if (lane == 0) {
 #pragma unroll
                     for (int kk = 0; kk < kBN / 16; ++kk) {
                         const uint64_t a = ptx::sw128_desc(p_base + wg * S::P_BYTES + kk * 32, 0, 1024);
@@ -289,7 +300,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 do_pv(t);
                 if (t + 2 < u.nt) do_qk(t + 2);
             }
-            if (lane == 0) ptx::mma_commit(o_full);
+            if (lane == 0) {
+                if (p.debug_mode >= 2) ptx::mbar_arrive(o_full);
+                else ptx::mma_commit(o_full);
+            }
             __syncwarp();
             ++unit_it;
         }
@@ -340,6 +354,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(s_empty + wg);
+                if (p.debug_mode >= 1) {  // timing experiment: no softmax math
+                    ptx::mbar_wait(p_empty + wg, par ^ 1);
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(p_full + wg);
+                    continue;
+                }
                 float* x = reinterpret_cast<float*>(sr);
                 if (t < u.n_prefix) {
                     const int valid = u.L - t * kBN;

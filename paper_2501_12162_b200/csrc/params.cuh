@@ -59,6 +59,7 @@ struct TcParams {
     float* lse;
     void* ws;
     int n_units;
+    int debug_mode;  // 0 = normal; 1 = skip softmax math; 2 = also skip MMAs (timing experiments only)
 };
 
 size_t select_ws_bytes(int n_req, int n_cand_total);

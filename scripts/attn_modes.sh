@@ -1,0 +1,13 @@
+#!/bin/bash
+# Timing experiments for the bf16 attention kernel (debug modes produce wrong outputs).
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+for CFG in ${CFGS:-c2}; do
+for M in 0 1 2; do
+  AS_ATTN_DEBUG_MODE=$M timeout 200 python bench.py --config $CFG --steps 20 --warmup 5 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python -c "
+import json,sys
+d=json.loads(sys.stdin.read()); r=d['roofline']
+print('$CFG mode $M', 'attn_ms', r['attn_ms'], 'GB/s', r['achieved'], 'frac', r['frac'], 'breakdown', d['breakdown_ms'])"
+done
+done
