@@ -88,7 +88,8 @@ def make_workload(cfg_name, device="cuda", seed_salt=0, rank=0, world=1, engine=
     D = c["head_dim"]
     ps = c["page_size"]
     kv_len = np.full(n, c["L"], np.int32)
-    table, n_pages = synth.paged_kv(rng, kv_len, ps, extra_slots=c["d"] + 1)
+    table, n_pages = synth.paged_kv(rng, kv_len, ps, extra_slots=c["d"] + 1,
+                                    permute=os.environ.get("AS_BENCH_CONTIGUOUS_PAGES") != "1")
     R = c["budget"]  # tree rows allocated = budget (upper bound of sum K_i)
     dt = torch.float32 if c["dtype"] == "f32" else torch.bfloat16
     gen = torch.Generator(device=device).manual_seed(synth.SEED_BASE + 17 * CONFIG_INDEX[cfg_name] + 1000 * seed_salt

@@ -139,15 +139,64 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         // ===================== TMA producer =====================
+        // Two cursors over the flattened (unit, tile) sequence of this CTA: the
+        // load cursor fills the smem rings; the prefetch cursor runs kPrefetch
+        // tiles ahead issuing L2 prefetches (no smem), so DRAM + TLB latency is
+        // covered by L2 capacity instead of shared memory.
         if (lane == 0) {
             uint32_t kv_it = 0, unit_it = 0;
             const uint64_t pol = ptx::policy_evict_first();
+            auto next_unit = [&](int w, Unit& u) -> int {  // first non-empty unit at or after w
+                for (; w < p.n_units; w += gridDim.x) {
+                    if (decode_unit(p, w, u)) return w;
+                    if (u.K > AS_MAX_TREE && u.mt == 0 && u.g == 0) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, u.i);
+                }
+                return w;
+            };
+            auto prefetch_tile = [&](const Unit& u, int t) {
+                if (t == 0) {
+                    const int node0 = u.off + u.mt * (kBM / p.G);
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) ptx::tma_prefetch_3d(&tm_q, c * 64, u.g * p.G, node0);
+                }
+                if (t < u.n_prefix) {
+                    const int key0 = t * kBN;
+                    const int valid = min(kBN, u.L - key0);
+                    const int nbox = (valid + p.box_rows - 1) / p.box_rows;
+                    for (int b = 0; b < nbox; ++b) {
+                        const int kp = key0 + b * p.box_rows;
+                        const int page = __ldg(p.page_table + (size_t)u.i * p.max_pages + kp / p.page_size);
+                        const int slot = kp % p.page_size;
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c) {
+                            ptx::tma_prefetch_4d(&tm_kc, c * 64, slot, u.g, page);
+                            ptx::tma_prefetch_4d(&tm_vc, c * 64, slot, u.g, page);
+                        }
+                    }
+                } else {
+                    const int row0 = u.off + (t - u.n_prefix) * kBN;
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) {
+                        ptx::tma_prefetch_3d(&tm_kt, c * 64, u.g, row0);
+                        ptx::tma_prefetch_3d(&tm_vt, c * 64, u.g, row0);
+                    }
+                }
+            };
+            // prefetch cursor
+            Unit pu;
+            int pw = next_unit(blockIdx.x, pu), pt = 0;
+            auto pf_step = [&]() {
+                if (pw >= p.n_units) return;
+                prefetch_tile(pu, pt);
+                if (++pt >= pu.nt) {
+                    pt = 0;
+                    pw = next_unit(pw + gridDim.x, pu);
+                }
+            };
+            for (int k = 0; k < p.prefetch_tiles; ++k) pf_step();
             for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
                 Unit u;
-                if (!decode_unit(p, w, u)) {
-                    if (u.K > AS_MAX_TREE && u.mt == 0 && u.g == 0) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, u.i);
-                    continue;
-                }
+                if (!decode_unit(p, w, u)) continue;
                 if (u.mt == 0 && u.g == 0 && __ldg(p.kv_len + u.i) > p.max_pages * p.page_size)
                     set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, u.i);
                 ptx::mbar_wait(q_empty, (unit_it & 1) ^ 1);
@@ -157,6 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int c = 0; c < NCH; ++c)
                     ptx::tma_load_3d(smem + S::OFF_Q + c * kBM * 128, &tm_q, q_full, c * 64, u.g * p.G, node0);
                 for (int t = 0; t < u.nt; ++t, ++kv_it) {
+                    pf_step();
                     const int st = kv_it % kStages;
                     const uint32_t ph = (kv_it / kStages) & 1;
                     unsigned char* kdst = smem + S::OFF_K + st * S::KV_BYTES;

@@ -151,15 +151,16 @@ def random_tree_parents(rng, K, max_depth=None, shape="random"):
     return np.array(par, np.int32)
 
 
-def paged_kv(rng, kv_len, page_size, extra_slots=0, spare_pages=0):
+def paged_kv(rng, kv_len, page_size, extra_slots=0, spare_pages=0, permute=True):
     """Page table for requests with prefix lengths kv_len (plus extra_slots of
-    capacity for commits).  Pages are a random permutation of the pool."""
+    capacity for commits).  Pages are a random permutation of the pool
+    (permute=False: each request's pages are contiguous, for experiments)."""
     kv_len = np.asarray(kv_len, np.int64)
     n = len(kv_len)
     pages_per = (kv_len + extra_slots + page_size - 1) // page_size
     max_pages = int(max(1, pages_per.max() if n else 1))
     total = int(pages_per.sum()) + spare_pages
-    perm = rng.permutation(max(total, 1)).astype(np.int32)
+    perm = rng.permutation(max(total, 1)).astype(np.int32) if permute else np.arange(max(total, 1), dtype=np.int32)
     table = np.full((max(n, 1), max_pages), -1, np.int32)
     c = 0
     for i in range(n):
