@@ -198,8 +198,6 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     p.n_units = mt_max * n_req * n_kv_heads;
     const char* dbg = getenv("AS_ATTN_DEBUG_MODE");  // timing experiments only (wrong outputs)
     p.debug_mode = dbg ? atoi(dbg) : 0;
-    const char* pf = getenv("AS_ATTN_PREFETCH");  // tuning override
-    p.prefetch_tiles = pf ? atoi(pf) : 8;
     return launch_attn_tc(maps, p, head_dim, sm_count(), S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
 }
 

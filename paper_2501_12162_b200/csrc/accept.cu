@@ -102,34 +102,35 @@ __global__ void __launch_bounds__(512) argmax_rows_kernel(const T* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// Walk + commit: one warp per request.  The request's tree (parent, draft
-// token, target token) is staged in shared memory with coalesced loads, so each
-// walk step costs a few shared-memory round trips instead of dependent global
-// loads; the commit copies every (path node, kv head, 16-byte chunk) in one
-// flattened, 4-way unrolled sweep.
+// Walk + commit: one CTA per request.  The request's tree (parent, draft token,
+// target token) is staged in shared memory with coalesced loads; warp 0 walks
+// it (each step = a few shared-memory round trips and one ballot per 32 nodes);
+// then all 8 warps commit the path: every (path node, kv head, 16-byte chunk)
+// vector of K and V is copied in one flattened, unrolled sweep, so the copy
+// costs ~one memory round trip.
 // ---------------------------------------------------------------------------
-constexpr int kAccWarps = 8;
+constexpr int kAccThreads = 256;
 constexpr int kAccMaxNodes = 256;  // staged in smem; larger trees walk from global memory
 constexpr int kAccMaxPath = 64;
 
-struct AccWarpSmem {
+struct AccSmem {
     int parent[kAccMaxNodes];
     int token[kAccMaxNodes];
     int target[kAccMaxNodes];
-    long long dst[kAccMaxPath];   // byte offset of the cache row for path position k (-1: skip)
-    long long src[kAccMaxPath];   // byte offset of the k_tree/v_tree row of path node k
+    int path[kAccMaxPath];
+    long long dst[kAccMaxPath];  // byte offset of the cache row for path position k (-1: skip)
+    long long src[kAccMaxPath];  // byte offset of the k_tree/v_tree row of path node k
+    int len;
 };
 
-__device__ __forceinline__ void commit_request(const AcceptParams& p, AccWarpSmem& sm, int i, int len, int p0,
-                                               int p1) {
-    const int lane = lane_id();
+__device__ __forceinline__ void commit_request(const AcceptParams& p, AccSmem& sm, int i, int len) {
+    const int tid = threadIdx.x;
     const int off = p.tree_offsets[i];
     const int L = p.kv_len[i];
     const long long row_bytes = (long long)p.head_dim * p.elem_bytes;
     const int vpr = (int)(row_bytes / 16);
-    // per path position: source row (node) and destination row (page, slot)
-    for (int k = lane; k < kAccMaxPath; k += 32) {
-        const int pk = (k < 32) ? p0 : p1;
+    if (tid < kAccMaxPath) {
+        const int k = tid;
         long long d = -1, s = 0;
         if (k < len) {
             const int slot = L + k;
@@ -142,24 +143,24 @@ __device__ __forceinline__ void commit_request(const AcceptParams& p, AccWarpSme
                     set_dev_error(p.ws, AS_DEV_BAD_PAGE, i);
                 } else {
                     d = ((long long)page * p.n_kv * p.page_size + slot % p.page_size) * row_bytes;
-                    s = (long long)(off + pk) * p.n_kv * row_bytes;
+                    s = (long long)(off + sm.path[k]) * p.n_kv * row_bytes;
                 }
             }
         }
         sm.dst[k] = d;
         sm.src[k] = s;
     }
-    __syncwarp();
+    __syncthreads();
     const int per_k = p.n_kv * vpr;
     const int total = len * per_k;
-    const long long head_src = row_bytes;                        // k_tree: [node][h][d]
     const long long head_dst = (long long)p.page_size * row_bytes;  // cache: [page][h][slot][d]
-    for (int v0 = lane; v0 < total; v0 += 4 * 32) {
-        uint4 kv[4], vv[4];
-        long long dd[4];
+    constexpr int U = 4;
+    for (int v0 = tid; v0 < total; v0 += U * kAccThreads) {
+        uint4 kv[U], vv[U];
+        long long dd[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int v = v0 + u * 32;
+        for (int u = 0; u < U; ++u) {
+            const int v = v0 + u * kAccThreads;
             dd[u] = -1;
             if (v < total) {
                 const int k = v / per_k;
@@ -167,7 +168,7 @@ __device__ __forceinline__ void commit_request(const AcceptParams& p, AccWarpSme
                 const int h = rem / vpr, c = rem - h * vpr;
                 const long long d = sm.dst[k];
                 if (d >= 0) {
-                    const long long so = sm.src[k] + h * head_src + c * 16;
+                    const long long so = sm.src[k] + h * row_bytes + c * 16;
                     kv[u] = *reinterpret_cast<const uint4*>(p.k_tree + so);
                     vv[u] = *reinterpret_cast<const uint4*>(p.v_tree + so);
                     dd[u] = d + h * head_dst + c * 16;
@@ -175,88 +176,89 @@ __device__ __forceinline__ void commit_request(const AcceptParams& p, AccWarpSme
             }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
             if (dd[u] >= 0) {
                 *reinterpret_cast<uint4*>(p.k_cache + dd[u]) = kv[u];
                 *reinterpret_cast<uint4*>(p.v_cache + dd[u]) = vv[u];
             }
         }
     }
-    __syncwarp();
-    if (lane == 0) p.kv_len[i] = L + len;
+    if (tid == 0) p.kv_len[i] = L + len;
 }
 
-__global__ void __launch_bounds__(kAccWarps * 32) walk_commit_kernel(AcceptParams p) {
-    __shared__ AccWarpSmem smem_all[kAccWarps];
-    AccWarpSmem& sm = smem_all[warp_id()];
+__global__ void __launch_bounds__(kAccThreads) walk_commit_kernel(AcceptParams p) {
+    __shared__ AccSmem sm;
+    const int tid = threadIdx.x;
     const int lane = lane_id();
-    const int wid = blockIdx.x * kAccWarps + warp_id();
     if (p.do_walk) {
-        const int i = p.req_begin + wid;
+        const int i = p.req_begin + blockIdx.x;
         if (i >= p.req_end) return;
         const int off = p.tree_offsets[i];
         const int K = p.tree_offsets[i + 1] - off;
-        int32_t* path = p.accept_path + (size_t)i * p.max_path;
         if (off + K > p.n_tree_rows) {
-            if (lane == 0) set_dev_error(p.ws, AS_DEV_ROWS_OVERFLOW, i);
+            if (tid == 0) set_dev_error(p.ws, AS_DEV_ROWS_OVERFLOW, i);
             return;
         }
         const bool staged = K <= kAccMaxNodes;
         if (staged) {
-            for (int c = lane; c < K; c += 32) {
+            for (int c = tid; c < K; c += kAccThreads) {
                 sm.parent[c] = p.tree_parent[off + c];
                 sm.token[c] = p.tree_tokens[off + c];
                 sm.target[c] = p.target_tokens[off + c];
             }
-            __syncwarp();
         }
-        const int* par = staged ? sm.parent : p.tree_parent + off;
-        const int* tok = staged ? sm.token : p.tree_tokens + off;
-        const int* tgt = staged ? sm.target : p.target_tokens + off;
-        int len = 0, tstar = -1;
-        int p0 = -1, p1 = -1;  // path in registers: lane k -> path[k], path[32+k]
-        if (K > 0) {
-            int v = 0;
-            len = 1;
-            if (lane == 0) p0 = 0;
-            for (;;) {
-                tstar = tgt[v];
-                int next = -1;
-                for (int c0 = v + 1; c0 < K; c0 += 32) {  // children follow their parent
-                    const int c = c0 + lane;
-                    const bool m = c < K && par[c] == v && tok[c] == tstar;
-                    const unsigned b = __ballot_sync(0xffffffffu, m);
-                    if (b) { next = c0 + __ffs(b) - 1; break; }
+        __syncthreads();
+        if (warp_id() == 0) {
+            const int* par = staged ? sm.parent : p.tree_parent + off;
+            const int* tok = staged ? sm.token : p.tree_tokens + off;
+            const int* tgt = staged ? sm.target : p.target_tokens + off;
+            int len = 0, tstar = -1;
+            if (K > 0) {
+                int v = 0;
+                len = 1;
+                if (lane == 0) sm.path[0] = 0;
+                for (;;) {
+                    tstar = tgt[v];
+                    int next = -1;
+                    for (int c0 = v + 1; c0 < K; c0 += 32) {  // children follow their parent
+                        const int c = c0 + lane;
+                        const bool m = c < K && par[c] == v && tok[c] == tstar;
+                        const unsigned b = __ballot_sync(0xffffffffu, m);
+                        if (b) { next = c0 + __ffs(b) - 1; break; }
+                    }
+                    if (next < 0) break;
+                    if (len >= p.max_path || len >= kAccMaxPath) {
+                        if (lane == 0) set_dev_error(p.ws, AS_DEV_PATH_TOO_LONG, i);
+                        break;
+                    }
+                    if (lane == 0) sm.path[len] = next;
+                    ++len;
+                    v = next;
                 }
-                if (next < 0) break;
-                if (len >= p.max_path || len >= kAccMaxPath) {
-                    if (lane == 0) set_dev_error(p.ws, AS_DEV_PATH_TOO_LONG, i);
-                    break;
-                }
-                if (len < 32) { if (lane == len) p0 = next; }
-                else { if (lane == len - 32) p1 = next; }
-                ++len;
-                v = next;
+            }
+            __syncwarp();
+            int32_t* path = p.accept_path + (size_t)i * p.max_path;
+            for (int k = lane; k < p.max_path; k += 32) path[k] = (k < len) ? sm.path[k] : -1;
+            if (lane == 0) {
+                p.accept_len[i] = len;
+                p.bonus_token[i] = tstar;
+                sm.len = len;
             }
         }
-        for (int k = lane; k < p.max_path; k += 32) path[k] = (k < len) ? ((k < 32) ? p0 : p1) : -1;
-        if (lane == 0) {
-            p.accept_len[i] = len;
-            p.bonus_token[i] = tstar;
-        }
-        if (p.do_commit) commit_request(p, sm, i, len, p0, p1);
+        __syncthreads();
+        if (p.do_commit) commit_request(p, sm, i, sm.len);
     } else if (p.do_commit) {
         // COMMIT_ONLY over all requests [0, n_req)
-        const int i = wid;
+        const int i = blockIdx.x;
         if (i >= p.n_req) return;
         int len = p.accept_len[i];
         if (len > p.max_path) len = p.max_path;
         if (len > kAccMaxPath) len = kAccMaxPath;
         if (len < 0) len = 0;
         const int32_t* path = p.accept_path + (size_t)i * p.max_path;
-        const int p0 = (lane < len) ? path[lane] : -1;
-        const int p1 = (lane + 32 < len) ? path[lane + 32] : -1;
-        commit_request(p, sm, i, len, p0, p1);
+        if (tid < len) sm.path[tid] = path[tid];
+        __syncthreads();
+        commit_request(p, sm, i, len);
     }
 }
 
@@ -280,7 +282,7 @@ int launch_accept(const AcceptParams& p, const void* target_logits, int logits_b
     }
     const int nw = q.do_walk ? (q.req_end - q.req_begin) : q.n_req;
     if (nw <= 0) return 0;
-    walk_commit_kernel<<<(nw + kAccWarps - 1) / kAccWarps, kAccWarps * 32, 0, stream>>>(q);
+    walk_commit_kernel<<<nw, kAccThreads, 0, stream>>>(q);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -37,6 +37,7 @@ constexpr int kStages = 4;        // K and V ring depth
 constexpr int kThreads = 320;     // 10 warps: TMA, MMA, 2 x 4 softmax
 constexpr int kTmemCols = 512;    // S0 [0,64) S1 [64,128) O0 [128,128+D) O1 [128+D, 128+2D)
 constexpr int kOcol = 128;
+constexpr int kPtChunk = 512;     // page-table entries staged per refill
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
 
@@ -51,7 +52,9 @@ struct TcSmem {
     static constexpr int OFF_V = OFF_K + kStages * KV_BYTES;
     static constexpr int OFF_P = OFF_V + kStages * KV_BYTES;
     static constexpr int OFF_ML = OFF_P + 2 * P_BYTES;        // [2][2][2][128] f32 merge scratch
-    static constexpr int OFF_BAR = OFF_ML + 2 * 2 * 2 * 128 * 4;
+    static constexpr int OFF_PT = OFF_ML + 2 * 2 * 2 * 128 * 4;   // [kPtChunk] staged page-table row
+    static constexpr int OFF_TP = OFF_PT + kPtChunk * 4;           // [2][AS_MAX_TREE] staged tree parents
+    static constexpr int OFF_BAR = OFF_TP + 2 * AS_MAX_TREE * 4;
     static constexpr int N_BAR = 2 + 4 * kStages + 8 + 2;
     static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
     static constexpr int BYTES = OFF_TMEM + 16;
@@ -138,81 +141,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_holder;
 
     if (warp == 0) {
-        // ===================== TMA producer =====================
-        // Two cursors over the flattened (unit, tile) sequence of this CTA: the
-        // load cursor fills the smem rings; the prefetch cursor runs kPrefetch
-        // tiles ahead issuing L2 prefetches (no smem), so DRAM + TLB latency is
-        // covered by L2 capacity instead of shared memory.
-        if (lane == 0) {
-            uint32_t kv_it = 0, unit_it = 0;
-            const uint64_t pol = ptx::policy_evict_first();
-            auto next_unit = [&](int w, Unit& u) -> int {  // first non-empty unit at or after w
-                for (; w < p.n_units; w += gridDim.x) {
-                    if (decode_unit(p, w, u)) return w;
-                    if (u.K > AS_MAX_TREE && u.mt == 0 && u.g == 0) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, u.i);
-                }
-                return w;
-            };
-            auto prefetch_tile = [&](const Unit& u, int t) {
-                if (t == 0) {
-                    const int node0 = u.off + u.mt * (kBM / p.G);
-#pragma unroll
-                    for (int c = 0; c < NCH; ++c) ptx::tma_prefetch_3d(&tm_q, c * 64, u.g * p.G, node0);
-                }
-                if (t < u.n_prefix) {
-                    const int key0 = t * kBN;
-                    const int valid = min(kBN, u.L - key0);
-                    const int nbox = (valid + p.box_rows - 1) / p.box_rows;
-                    for (int b = 0; b < nbox; ++b) {
-                        const int kp = key0 + b * p.box_rows;
-                        const int page = __ldg(p.page_table + (size_t)u.i * p.max_pages + kp / p.page_size);
-                        const int slot = kp % p.page_size;
-#pragma unroll
-                        for (int c = 0; c < NCH; ++c) {
-                            ptx::tma_prefetch_4d(&tm_kc, c * 64, slot, u.g, page);
-                            ptx::tma_prefetch_4d(&tm_vc, c * 64, slot, u.g, page);
-                        }
-                    }
-                } else {
-                    const int row0 = u.off + (t - u.n_prefix) * kBN;
-#pragma unroll
-                    for (int c = 0; c < NCH; ++c) {
-                        ptx::tma_prefetch_3d(&tm_kt, c * 64, u.g, row0);
-                        ptx::tma_prefetch_3d(&tm_vt, c * 64, u.g, row0);
-                    }
-                }
-            };
-            // prefetch cursor
-            Unit pu;
-            int pw = next_unit(blockIdx.x, pu), pt = 0;
-            auto pf_step = [&]() {
-                if (pw >= p.n_units) return;
-                prefetch_tile(pu, pt);
-                if (++pt >= pu.nt) {
-                    pt = 0;
-                    pw = next_unit(pw + gridDim.x, pu);
-                }
-            };
-            for (int k = 0; k < p.prefetch_tiles; ++k) pf_step();
-            for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
-                Unit u;
-                if (!decode_unit(p, w, u)) continue;
-                if (u.mt == 0 && u.g == 0 && __ldg(p.kv_len + u.i) > p.max_pages * p.page_size)
-                    set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, u.i);
+        // ===================== TMA producer (whole warp) =====================
+        // Lane 0 issues every TMA; at each unit start (and every kPtChunk pages)
+        // the 32 lanes stage the request's page-table row in shared memory, so no
+        // global load sits on the per-tile issue path (that dependent load was the
+        // per-SM streaming limiter).  The 4-stage rings cover the staging bubble.
+        int* pt_s = reinterpret_cast<int*>(smem + S::OFF_PT);
+        uint32_t kv_it = 0, unit_it = 0;
+        const uint64_t pol = ptx::policy_evict_first();
+        for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
+            Unit u;
+            if (!decode_unit(p, w, u)) {
+                if (lane == 0 && u.K > AS_MAX_TREE && u.mt == 0 && u.g == 0)
+                    set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, u.i);
+                continue;
+            }
+            if (lane == 0 && u.mt == 0 && u.g == 0 && __ldg(p.kv_len + u.i) > p.max_pages * p.page_size)
+                set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, u.i);
+            const int n_pages_u = (u.L + p.page_size - 1) / p.page_size;
+            int chunk0 = -1;  // first page index currently staged
+            if (lane == 0) {
                 ptx::mbar_wait(q_empty, (unit_it & 1) ^ 1);
                 ptx::mbar_arrive_expect_tx(q_full, S::Q_BYTES);
                 const int node0 = u.off + u.mt * (kBM / p.G);
 #pragma unroll
                 for (int c = 0; c < NCH; ++c)
                     ptx::tma_load_3d(smem + S::OFF_Q + c * kBM * 128, &tm_q, q_full, c * 64, u.g * p.G, node0);
-                for (int t = 0; t < u.nt; ++t, ++kv_it) {
-                    pf_step();
-                    const int st = kv_it % kStages;
-                    const uint32_t ph = (kv_it / kStages) & 1;
-                    unsigned char* kdst = smem + S::OFF_K + st * S::KV_BYTES;
-                    unsigned char* vdst = smem + S::OFF_V + st * S::KV_BYTES;
-                    if (t < u.n_prefix) {
-                        const int key0 = t * kBN;
+            }
+            for (int t = 0; t < u.nt; ++t, ++kv_it) {
+                const int st = kv_it % kStages;
+                const uint32_t ph = (kv_it / kStages) & 1;
+                unsigned char* kdst = smem + S::OFF_K + st * S::KV_BYTES;
+                unsigned char* vdst = smem + S::OFF_V + st * S::KV_BYTES;
+                if (t < u.n_prefix) {
+                    const int key0 = t * kBN;
+                    const int pg_first = key0 / p.page_size;
+                    const int pg_last = (min(key0 + kBN, u.L) - 1) / p.page_size;
+                    if (chunk0 < 0 || pg_last >= chunk0 + kPtChunk) {  // warp-uniform
+                        chunk0 = pg_first;
+                        __syncwarp();
+                        for (int k = lane; k < kPtChunk && chunk0 + k < n_pages_u; k += 32)
+                            pt_s[k] = __ldg(p.page_table + (size_t)u.i * p.max_pages + chunk0 + k);
+                        __syncwarp();
+                    }
+                    if (lane == 0) {
                         const int valid = min(kBN, u.L - key0);
                         const int nbox = (valid + p.box_rows - 1) / p.box_rows;
                         const uint32_t bytes = (uint32_t)(nbox * NCH * p.box_rows * 128);
@@ -220,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::mbar_arrive_expect_tx(k_full + st, bytes);
                         for (int b = 0; b < nbox; ++b) {
                             const int kp = key0 + b * p.box_rows;
-                            const int page = __ldg(p.page_table + (size_t)u.i * p.max_pages + kp / p.page_size);
+                            const int page = pt_s[kp / p.page_size - chunk0];
                             const int slot = kp % p.page_size;
                             // out-of-range pages read as zeros (TMA bounds check); flag them
                             if (page < 0 || page >= p.num_pages) set_dev_error(p.ws, AS_DEV_BAD_PAGE, u.i);
@@ -233,30 +205,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::mbar_arrive_expect_tx(v_full + st, bytes);
                         for (int b = 0; b < nbox; ++b) {
                             const int kp = key0 + b * p.box_rows;
-                            const int page = __ldg(p.page_table + (size_t)u.i * p.max_pages + kp / p.page_size);
+                            const int page = pt_s[kp / p.page_size - chunk0];
                             const int slot = kp % p.page_size;
 #pragma unroll
                             for (int c = 0; c < NCH; ++c)
                                 ptx::tma_load_4d_hint(vdst + c * kBN * 128 + b * p.box_rows * 128, &tm_vc, v_full + st,
                                                       c * 64, slot, u.g, page, pol);
                         }
-                    } else {
-                        const int row0 = u.off + (t - u.n_prefix) * kBN;
-                        const uint32_t bytes = (uint32_t)(NCH * kBN * 128);
-                        ptx::mbar_wait(k_empty + st, ph ^ 1);
-                        ptx::mbar_arrive_expect_tx(k_full + st, bytes);
-#pragma unroll
-                        for (int c = 0; c < NCH; ++c)
-                            ptx::tma_load_3d(kdst + c * kBN * 128, &tm_kt, k_full + st, c * 64, u.g, row0);
-                        ptx::mbar_wait(v_empty + st, ph ^ 1);
-                        ptx::mbar_arrive_expect_tx(v_full + st, bytes);
-#pragma unroll
-                        for (int c = 0; c < NCH; ++c)
-                            ptx::tma_load_3d(vdst + c * kBN * 128, &tm_vt, v_full + st, c * 64, u.g, row0);
                     }
+                } else if (lane == 0) {
+                    const int row0 = u.off + (t - u.n_prefix) * kBN;
+                    const uint32_t bytes = (uint32_t)(NCH * kBN * 128);
+                    ptx::mbar_wait(k_empty + st, ph ^ 1);
+                    ptx::mbar_arrive_expect_tx(k_full + st, bytes);
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+                        ptx::tma_load_3d(kdst + c * kBN * 128, &tm_kt, k_full + st, c * 64, u.g, row0);
+                    ptx::mbar_wait(v_empty + st, ph ^ 1);
+                    ptx::mbar_arrive_expect_tx(v_full + st, bytes);
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+                        ptx::tma_load_3d(vdst + c * kBN * 128, &tm_vt, v_full + st, c * 64, u.g, row0);
                 }
-                ++unit_it;
             }
+            ++unit_it;
         }
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
@@ -377,14 +349,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool row_ok = rr < u.K * G;
             const int node = rr / G;
             const int hh = rr - node * G;
-            // ancestor-or-self bitmask of this row's node (R15)
+            // ancestor-or-self bitmask of this row's node (R15); parents staged in smem
+            int* tp_s = reinterpret_cast<int*>(smem + S::OFF_TP) + (unit_it & 1) * AS_MAX_TREE;
+            const int tid_sm = (warp - 2) * 32 + lane;
+            for (int j = tid_sm; j < u.K; j += 256) tp_s[j] = __ldg(p.tree_parent + u.off + j);
+            asm volatile("bar.sync 2, 256;" ::: "memory");
             uint64_t anc0 = 0, anc1 = 0;
             if (row_ok) {
                 int v = node, steps = 0;
                 for (;;) {
                     if (v < 64) anc0 |= 1ull << v; else anc1 |= 1ull << (v - 64);
                     if (v == 0) break;
-                    const int pv = __ldg(p.tree_parent + u.off + v);
+                    const int pv = tp_s[v];
                     if (pv < 0 || pv >= v || ++steps > u.K) {
                         set_dev_error(p.ws, AS_DEV_BAD_PARENT, u.i);
                         break;

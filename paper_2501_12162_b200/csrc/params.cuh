@@ -59,7 +59,6 @@ struct TcParams {
     float* lse;
     void* ws;
     int n_units;
-    int prefetch_tiles;  // L2 prefetch distance of the TMA producer, in 64-key tiles
     int debug_mode;  // 0 = normal; 1 = skip softmax math; 2 = also skip MMAs (timing experiments only)
 };
 

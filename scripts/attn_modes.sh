@@ -7,12 +7,8 @@ one() {
   timeout 200 python bench.py --config $CFG --steps 20 --warmup 5 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); r=d['roofline']
-print('$CFG mode=${AS_ATTN_DEBUG_MODE:-0} pf=${AS_ATTN_PREFETCH:-def} contig=${AS_BENCH_CONTIGUOUS_PAGES:-0}', 'attn_ms', r['attn_ms'], 'GB/s', r['achieved'], 'frac', r['frac'], 'bd', d['breakdown_ms'])"
+print('$CFG mode=${AS_ATTN_DEBUG_MODE:-0} contig=${AS_BENCH_CONTIGUOUS_PAGES:-0}', 'attn_ms', r['attn_ms'], 'GB/s', r['achieved'], 'frac', r['frac'], 'step_ms', d['ms_per_step'], 'bd', d['breakdown_ms'], 'clk', d['clocks'])"
 }
 for CFG in ${CFGS:-c2}; do
-  for PF in ${PFS:-0 8}; do for M in ${MODES:-0 2}; do
-    AS_ATTN_PREFETCH=$PF AS_ATTN_DEBUG_MODE=$M one
-  done; done
-  AS_BENCH_CONTIGUOUS_PAGES=1 AS_ATTN_PREFETCH=0 AS_ATTN_DEBUG_MODE=2 one
-  AS_BENCH_CONTIGUOUS_PAGES=1 AS_ATTN_PREFETCH=8 one
+  for M in ${MODES:-0 2}; do AS_ATTN_DEBUG_MODE=$M one; done
 done
