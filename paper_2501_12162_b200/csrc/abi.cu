@@ -126,7 +126,7 @@ as_status as_select_trees(int32_t n_req, int32_t n_cand_total, const int32_t* ca
 size_t as_attn_workspace_size(as_dtype dtype, int32_t n_req, int32_t n_tree_rows, int32_t n_q_heads,
                               int32_t head_dim, int32_t max_kv_len) {
     (void)dtype; (void)n_req; (void)n_tree_rows; (void)n_q_heads; (void)head_dim; (void)max_kv_len;
-    return kWsHeaderBytes;
+    return kWsHeaderBytes + kAttnTraceBytes;
 }
 
 as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows, int32_t n_q_heads,
@@ -198,6 +198,13 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     p.n_units = mt_max * n_req * n_kv_heads;
     const char* dbg = getenv("AS_ATTN_DEBUG_MODE");  // timing experiments only (wrong outputs)
     p.debug_mode = dbg ? atoi(dbg) : 0;
+    const char* tr = getenv("AS_ATTN_TRACE");  // CTA-0 pipeline timestamps into the workspace (debug)
+    p.trace = nullptr;
+    p.trace_cap = 0;
+    if (tr && atoi(tr) && workspace_bytes >= kWsHeaderBytes + kAttnTraceBytes) {
+        p.trace = reinterpret_cast<unsigned long long*>(reinterpret_cast<unsigned char*>(workspace) + kWsHeaderBytes);
+        p.trace_cap = (int)(kAttnTraceBytes / 64);
+    }
     return launch_attn_tc(maps, p, head_dim, sm_count(), S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
 }
 

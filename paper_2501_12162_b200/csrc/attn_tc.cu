@@ -61,6 +61,13 @@ struct TcSmem {
     static constexpr int ALLOC = BYTES + 1024;  // alignment slack
 };
 
+// CTA-0 pipeline trace (debug): event e of CTA-local tile index idx.
+#define AS_TRACE(e, idx)                                                                       \
+    do {                                                                                       \
+        if (p.trace != nullptr && blockIdx.x == 0 && (int)(idx) < p.trace_cap)                 \
+            p.trace[(size_t)(idx) * 8 + (e)] = clock64();                                      \
+    } while (0)
+
 struct Unit {
     int i, g, mt, off, K, L, nt, n_prefix;
 };
@@ -189,6 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int nbox = (valid + p.box_rows - 1) / p.box_rows;
                         const uint32_t bytes = (uint32_t)(nbox * NCH * p.box_rows * 128);
                         ptx::mbar_wait(k_empty + st, ph ^ 1);
+                        AS_TRACE(0, kv_it);
                         ptx::mbar_arrive_expect_tx(k_full + st, bytes);
                         for (int b = 0; b < nbox; ++b) {
                             const int kp = key0 + b * p.box_rows;
@@ -202,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                       c * 64, slot, u.g, page, pol);
                         }
                         ptx::mbar_wait(v_empty + st, ph ^ 1);
+                        AS_TRACE(1, kv_it);
                         ptx::mbar_arrive_expect_tx(v_full + st, bytes);
                         for (int b = 0; b < nbox; ++b) {
                             const int kp = key0 + b * p.box_rows;
@@ -217,11 +226,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int row0 = u.off + (t - u.n_prefix) * kBN;
                     const uint32_t bytes = (uint32_t)(NCH * kBN * 128);
                     ptx::mbar_wait(k_empty + st, ph ^ 1);
+                    AS_TRACE(0, kv_it);
                     ptx::mbar_arrive_expect_tx(k_full + st, bytes);
 #pragma unroll
                     for (int c = 0; c < NCH; ++c)
                         ptx::tma_load_3d(kdst + c * kBN * 128, &tm_kt, k_full + st, c * 64, u.g, row0);
                     ptx::mbar_wait(v_empty + st, ph ^ 1);
+                    AS_TRACE(1, kv_it);
                     ptx::mbar_arrive_expect_tx(v_full + st, bytes);
 #pragma unroll
                     for (int c = 0; c < NCH; ++c)
@@ -252,6 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int wg = t & 1;
                 const int st = k_it % kStages;
                 ptx::mbar_wait(k_full + st, (k_it / kStages) & 1);
+                if (lane == 0) AS_TRACE(2, k_it);
                 ptx::mbar_wait(s_empty + wg, ((s_ph >> wg) & 1) ^ 1);
                 ptx::tc_fence_after();
                 if (p.debug_mode >= 2) {
@@ -280,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int wg = t & 1;
                 const int st = v_it % kStages;
                 ptx::mbar_wait(v_full + st, (v_it / kStages) & 1);
+                if (lane == 0) AS_TRACE(3, v_it);
                 // zero V rows past the prefix end (stale/uninitialised smem or cache
                 // slots >= L may hold NaN; P is 0 there but 0 * NaN = NaN)
                 if (t < u.n_prefix) {
@@ -294,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 ptx::mbar_wait(p_full + wg, (p_ph >> wg) & 1);
+                if (lane == 0) AS_TRACE(4, v_it);
                 if (t == 0) ptx::mbar_wait(o_empty, (unit_it & 1) ^ 1);  // both O buffers drained
                 ptx::tc_fence_after();
                 __syncwarp();
@@ -341,6 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* ml = reinterpret_cast<float*>(smem + S::OFF_ML);  // [2 units][2 wg][2 (m,l)][128]
         const float sl2 = p.scale_log2;
         uint32_t s_cnt = 0, unit_it = 0;
+        int tbase = 0;  // CTA-local index of this unit's first tile (trace only)
         for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
             Unit u;
             if (!decode_unit(p, w, u)) continue;
@@ -372,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int t = wg; t < u.nt; t += 2, ++s_cnt) {
                 const uint32_t par = s_cnt & 1;
                 ptx::mbar_wait(s_full + wg, par);
+                if (lane == 0 && quad == 0) AS_TRACE(5, tbase + t);
                 ptx::tc_fence_after();
                 uint32_t sr[kBN];
                 ptx::tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
@@ -384,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(p_empty + wg, par ^ 1);
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(p_full + wg);
+                    if (lane == 0 && quad == 0) AS_TRACE(6, tbase + t);
                     continue;
                 }
                 float* x = reinterpret_cast<float*>(sr);
@@ -454,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(p_full + wg);
+                if (lane == 0 && quad == 0) AS_TRACE(6, tbase + t);
             }
             // ---- epilogue: merge the two warpgroups' partial softmax states ----
             float* mlu = ml + (unit_it & 1) * 512;
@@ -500,6 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(o_empty);
             ++unit_it;
+            tbase += u.nt;
         }
     }
     ptx::tc_fence_before();

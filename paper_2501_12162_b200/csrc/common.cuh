@@ -19,6 +19,7 @@ struct WsHeader {
 static_assert(sizeof(WsHeader) == 256, "header size");
 
 constexpr size_t kWsHeaderBytes = 256;
+constexpr size_t kAttnTraceBytes = 4096 * 64;  // debug pipeline trace area of the attention workspace
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 

@@ -60,6 +60,8 @@ struct TcParams {
     void* ws;
     int n_units;
     int debug_mode;  // 0 = normal; 1 = skip softmax math; 2 = also skip MMAs (timing experiments only)
+    unsigned long long* trace;  // CTA-0 pipeline timestamps [trace_cap][8] (clock64) or NULL
+    int trace_cap;
 };
 
 size_t select_ws_bytes(int n_req, int n_cand_total);

@@ -1,0 +1,54 @@
+"""Pipeline trace of the bf16 attention kernel (CTA 0), for tuning.
+
+    AS_ATTN_TRACE=1 python scripts/attn_trace.py [--config c2] [--mode 0]
+
+Events per CTA-local tile (clock64 cycles):
+  0 producer: K slot free, issuing K      1 producer: V slot free, issuing V
+  2 MMA: K landed (QK issued)             3 MMA: V landed
+  4 MMA: P ready (PV issued)              5 softmax: S ready (start)
+  6 softmax: P written (end)
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("AS_ATTN_TRACE", "1")
+import bench  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--ghz", type=float, default=1.965)
+args = ap.parse_args()
+W = bench.make_workload(args.config, "cuda")
+for _ in range(3):
+    bench.run_attention(W)
+torch.cuda.synchronize()
+W["ws_attn"].view[256:].zero_()
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s.record()
+bench.run_attention(W)
+e.record()
+torch.cuda.synchronize()
+print(f"{args.config} mode={os.environ.get('AS_ATTN_DEBUG_MODE', '0')} attention {s.elapsed_time(e) * 1e3:.1f} us")
+tr = W["ws_attn"].view[256:256 + 4096 * 64].view(torch.int64).cpu().numpy().reshape(4096, 8)
+n = int((tr[:, 0] != 0).sum())
+tr = tr[:n].astype(np.float64)
+t0 = tr[0, 0]
+tr = (tr - t0) / args.ghz  # ns
+ns = lambda x: f"{np.median(x):7.0f} (p10 {np.percentile(x, 10):6.0f}, p90 {np.percentile(x, 90):6.0f})"
+print(f"tiles traced on CTA 0: {n}; span {tr[n - 1, 6]:.0f} ns; per tile {tr[n - 1, 6] / n:.0f} ns")
+print("producer K issue interval     ", ns(np.diff(tr[:, 0])))
+print("K issue -> K landed (MMA sees)", ns(tr[:, 2] - tr[:, 0]))
+print("V issue -> V landed           ", ns(tr[:, 3] - tr[:, 1]))
+print("K landed -> softmax start     ", ns(tr[:, 5] - tr[:, 2]))
+print("softmax duration              ", ns(tr[:, 6] - tr[:, 5]))
+print("P ready -> MMA sees P         ", ns(tr[:, 4] - tr[:, 6]))
+print("V landed -> PV issue (wait P) ", ns(tr[:, 4] - tr[:, 3]))
+print("producer waits for K slot: K issue minus PV of tile-4 issue", ns(tr[4:, 0] - tr[:-4, 4]))
+np.set_printoptions(linewidth=200, suppress=True)
+print("first 12 tiles (ns):\n", np.round(tr[:12, :7]))
+print("tiles 40-52 (ns):\n", np.round(tr[40:52, :7]))
