@@ -164,33 +164,47 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
         return AS_ERR_INVALID_ARG;
     const uint64_t D = (uint64_t)head_dim;
     CUtensorMap maps[5];
+    const uint64_t NCH = D / 64;
+    // Every map carries the 64-element d-chunk index as its own dimension so one
+    // TMA box fills all chunks of a tile ([chunk][row][64] in smem, SW128): half
+    // the TMA issues of per-chunk boxes (the producer's issue rate bounded the
+    // per-SM streaming rate).
     {
-        uint64_t dims[3] = {D, (uint64_t)n_q_heads, (uint64_t)n_tree_rows};
-        uint64_t str[2] = {D * 2, (uint64_t)n_q_heads * D * 2};
-        uint32_t box[3] = {64, (uint32_t)G, (uint32_t)(128 / G)};
-        if (!make_map(&maps[0], q, 3, dims, str, box)) return AS_ERR_CUDA;
+        uint64_t dims[4] = {64, (uint64_t)n_q_heads, (uint64_t)n_tree_rows, NCH};
+        uint64_t str[3] = {D * 2, (uint64_t)n_q_heads * D * 2, 128};
+        uint32_t box[4] = {64, (uint32_t)G, (uint32_t)(128 / G), (uint32_t)NCH};
+        if (!make_map(&maps[0], q, 4, dims, str, box)) return AS_ERR_CUDA;
     }
     const int box_rows = page_size < 64 ? page_size : 64;
+    const int kv_split_d = page_size >= 64 ? 1 : 0;  // one box covers a whole 64-key tile
     {
         const uint64_t np = (uint64_t)(num_pages > 0 ? num_pages : 1);
-        uint64_t dims[4] = {D, (uint64_t)page_size, (uint64_t)n_kv_heads, np};
-        uint64_t str[3] = {D * 2, (uint64_t)page_size * D * 2, (uint64_t)n_kv_heads * page_size * D * 2};
-        uint32_t box[4] = {64, (uint32_t)box_rows, 1, 1};
         const void* kc = k_cache ? k_cache : k_tree;  // never dereferenced when there are no pages
         const void* vc = v_cache ? v_cache : v_tree;
-        if (!make_map(&maps[1], kc, 4, dims, str, box)) return AS_ERR_CUDA;
-        if (!make_map(&maps[2], vc, 4, dims, str, box)) return AS_ERR_CUDA;
+        if (kv_split_d) {
+            uint64_t dims[5] = {64, (uint64_t)page_size, NCH, (uint64_t)n_kv_heads, np};
+            uint64_t str[4] = {D * 2, 128, (uint64_t)page_size * D * 2, (uint64_t)n_kv_heads * page_size * D * 2};
+            uint32_t box[5] = {64, (uint32_t)box_rows, (uint32_t)NCH, 1, 1};
+            if (!make_map(&maps[1], kc, 5, dims, str, box)) return AS_ERR_CUDA;
+            if (!make_map(&maps[2], vc, 5, dims, str, box)) return AS_ERR_CUDA;
+        } else {
+            uint64_t dims[4] = {D, (uint64_t)page_size, (uint64_t)n_kv_heads, np};
+            uint64_t str[3] = {D * 2, (uint64_t)page_size * D * 2, (uint64_t)n_kv_heads * page_size * D * 2};
+            uint32_t box[4] = {64, (uint32_t)box_rows, 1, 1};
+            if (!make_map(&maps[1], kc, 4, dims, str, box)) return AS_ERR_CUDA;
+            if (!make_map(&maps[2], vc, 4, dims, str, box)) return AS_ERR_CUDA;
+        }
     }
     {
-        uint64_t dims[3] = {D, (uint64_t)n_kv_heads, (uint64_t)n_tree_rows};
-        uint64_t str[2] = {D * 2, (uint64_t)n_kv_heads * D * 2};
-        uint32_t box[3] = {64, 1, 64};
-        if (!make_map(&maps[3], k_tree, 3, dims, str, box)) return AS_ERR_CUDA;
-        if (!make_map(&maps[4], v_tree, 3, dims, str, box)) return AS_ERR_CUDA;
+        uint64_t dims[4] = {64, (uint64_t)n_tree_rows, NCH, (uint64_t)n_kv_heads};
+        uint64_t str[3] = {(uint64_t)n_kv_heads * D * 2, 128, D * 2};
+        uint32_t box[4] = {64, 64, (uint32_t)NCH, 1};
+        if (!make_map(&maps[3], k_tree, 4, dims, str, box)) return AS_ERR_CUDA;
+        if (!make_map(&maps[4], v_tree, 4, dims, str, box)) return AS_ERR_CUDA;
     }
     TcParams p;
     p.n_req = n_req; p.n_tree_rows = n_tree_rows; p.n_q = n_q_heads; p.n_kv = n_kv_heads; p.G = G;
-    p.page_size = page_size; p.box_rows = box_rows; p.max_pages = max_pages_per_req; p.num_pages = num_pages;
+    p.page_size = page_size; p.box_rows = box_rows; p.kv_split_d = kv_split_d; p.max_pages = max_pages_per_req; p.num_pages = num_pages;
     p.page_table = page_table; p.kv_len = kv_len; p.tree_offsets = tree_offsets; p.tree_parent = tree_parent;
     p.scale_log2 = sm_scale * 1.4426950408889634f;
     p.out = (__nv_bfloat16*)out; p.lse = lse; p.ws = workspace;

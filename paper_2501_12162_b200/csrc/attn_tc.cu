@@ -171,9 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(q_empty, (unit_it & 1) ^ 1);
                 ptx::mbar_arrive_expect_tx(q_full, S::Q_BYTES);
                 const int node0 = u.off + u.mt * (kBM / p.G);
-#pragma unroll
-                for (int c = 0; c < NCH; ++c)
-                    ptx::tma_load_3d(smem + S::OFF_Q + c * kBM * 128, &tm_q, q_full, c * 64, u.g * p.G, node0);
+                ptx::tma_load_4d(smem + S::OFF_Q, &tm_q, q_full, 0, u.g * p.G, node0, 0);
             }
             for (int t = 0; t < u.nt; ++t, ++kv_it) {
                 const int st = kv_it % kStages;
@@ -204,10 +202,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int slot = kp % p.page_size;
                             // out-of-range pages read as zeros (TMA bounds check); flag them
                             if (page < 0 || page >= p.num_pages) set_dev_error(p.ws, AS_DEV_BAD_PAGE, u.i);
+                            if (p.kv_split_d) {
+                                ptx::tma_load_5d_hint(kdst, &tm_kc, k_full + st, 0, slot, 0, u.g, page, pol);
+                            } else {
 #pragma unroll
-                            for (int c = 0; c < NCH; ++c)
-                                ptx::tma_load_4d_hint(kdst + c * kBN * 128 + b * p.box_rows * 128, &tm_kc, k_full + st,
-                                                      c * 64, slot, u.g, page, pol);
+                                for (int c = 0; c < NCH; ++c)
+                                    ptx::tma_load_4d_hint(kdst + c * kBN * 128 + b * p.box_rows * 128, &tm_kc,
+                                                          k_full + st, c * 64, slot, u.g, page, pol);
+                            }
                         }
                         ptx::mbar_wait(v_empty + st, ph ^ 1);
                         AS_TRACE(1, kv_it);
@@ -216,10 +218,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int kp = key0 + b * p.box_rows;
                             const int page = pt_s[kp / p.page_size - chunk0];
                             const int slot = kp % p.page_size;
+                            if (p.kv_split_d) {
+                                ptx::tma_load_5d_hint(vdst, &tm_vc, v_full + st, 0, slot, 0, u.g, page, pol);
+                            } else {
 #pragma unroll
-                            for (int c = 0; c < NCH; ++c)
-                                ptx::tma_load_4d_hint(vdst + c * kBN * 128 + b * p.box_rows * 128, &tm_vc, v_full + st,
-                                                      c * 64, slot, u.g, page, pol);
+                                for (int c = 0; c < NCH; ++c)
+                                    ptx::tma_load_4d_hint(vdst + c * kBN * 128 + b * p.box_rows * 128, &tm_vc,
+                                                          v_full + st, c * 64, slot, u.g, page, pol);
+                            }
                         }
                     }
                 } else if (lane == 0) {
@@ -228,15 +234,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(k_empty + st, ph ^ 1);
                     AS_TRACE(0, kv_it);
                     ptx::mbar_arrive_expect_tx(k_full + st, bytes);
-#pragma unroll
-                    for (int c = 0; c < NCH; ++c)
-                        ptx::tma_load_3d(kdst + c * kBN * 128, &tm_kt, k_full + st, c * 64, u.g, row0);
+                    ptx::tma_load_4d(kdst, &tm_kt, k_full + st, 0, row0, 0, u.g);
                     ptx::mbar_wait(v_empty + st, ph ^ 1);
                     AS_TRACE(1, kv_it);
                     ptx::mbar_arrive_expect_tx(v_full + st, bytes);
-#pragma unroll
-                    for (int c = 0; c < NCH; ++c)
-                        ptx::tma_load_3d(vdst + c * kBN * 128, &tm_vt, v_full + st, c * 64, u.g, row0);
+                    ptx::tma_load_4d(vdst, &tm_vt, v_full + st, 0, row0, 0, u.g);
                 }
             }
             ++unit_it;

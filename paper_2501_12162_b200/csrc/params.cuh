@@ -50,6 +50,7 @@ struct SimtParams {
 struct TcParams {
     int n_req, n_tree_rows, n_q, n_kv, G;
     int page_size, box_rows, max_pages, num_pages;
+    int kv_split_d;  // 1: cache maps are 5-D (d-chunk dim), one box per 64-key tile
     const int32_t* page_table;
     const int32_t* kv_len;
     const int32_t* tree_offsets;
