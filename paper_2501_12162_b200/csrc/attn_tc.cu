@@ -33,8 +33,10 @@ namespace as {
 
 constexpr int kBM = 128;          // query rows per tile (UMMA M)
 constexpr int kBN = 64;           // keys per tile
-constexpr int kStages = 4;        // K and V ring depth
-constexpr int kThreads = 320;     // 10 warps: TMA, MMA, 2 x 4 softmax
+constexpr int kKStages = 3;       // K ring depth (released right after QK)
+constexpr int kVStages = 6;       // V ring depth (held until PV)
+constexpr int kVWarp = 10;        // V producer warp
+constexpr int kThreads = 352;     // 11 warps: K/Q TMA, MMA, 2 x 4 softmax, V TMA
 constexpr int kTmemCols = 512;    // S0 [0,64) S1 [64,128) O0 [128,128+D) O1 [128+D, 128+2D)
 constexpr int kOcol = 128;
 constexpr int kPtChunk = 512;     // page-table entries staged per refill
@@ -49,13 +51,13 @@ struct TcSmem {
     static constexpr int P_BYTES = kBM * kBN * 2;             // 16 KB
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = OFF_Q + Q_BYTES;
-    static constexpr int OFF_V = OFF_K + kStages * KV_BYTES;
-    static constexpr int OFF_P = OFF_V + kStages * KV_BYTES;
+    static constexpr int OFF_V = OFF_K + kKStages * KV_BYTES;
+    static constexpr int OFF_P = OFF_V + kVStages * KV_BYTES;
     static constexpr int OFF_ML = OFF_P + 2 * P_BYTES;        // [2][2][2][128] f32 merge scratch
-    static constexpr int OFF_PT = OFF_ML + 2 * 2 * 2 * 128 * 4;   // [kPtChunk] staged page-table row
-    static constexpr int OFF_TP = OFF_PT + kPtChunk * 4;           // [2][AS_MAX_TREE] staged tree parents
+    static constexpr int OFF_PT = OFF_ML + 2 * 2 * 2 * 128 * 4;   // [2 producers][kPtChunk] staged page-table rows
+    static constexpr int OFF_TP = OFF_PT + 2 * kPtChunk * 4;       // [2][AS_MAX_TREE] staged tree parents
     static constexpr int OFF_BAR = OFF_TP + 2 * AS_MAX_TREE * 4;
-    static constexpr int N_BAR = 2 + 4 * kStages + 8 + 2;
+    static constexpr int N_BAR = 2 + 2 * kKStages + 2 * kVStages + 8 + 2;
     static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
     static constexpr int BYTES = OFF_TMEM + 16;
     static constexpr int ALLOC = BYTES + 1024;  // alignment slack
@@ -103,10 +105,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* q_full = bars + 0;
     uint64_t* q_empty = bars + 1;
     uint64_t* k_full = bars + 2;
-    uint64_t* k_empty = k_full + kStages;
-    uint64_t* v_full = k_empty + kStages;
-    uint64_t* v_empty = v_full + kStages;
-    uint64_t* s_full = v_empty + kStages;  // [2]
+    uint64_t* k_empty = k_full + kKStages;
+    uint64_t* v_full = k_empty + kKStages;
+    uint64_t* v_empty = v_full + kVStages;
+    uint64_t* s_full = v_empty + kVStages;  // [2]
     uint64_t* s_empty = s_full + 2;        // [2]
     uint64_t* p_full = s_empty + 2;        // [2]
     uint64_t* p_empty = p_full + 2;        // [2]
@@ -120,9 +122,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         ptx::mbar_init(q_full, 1);
         ptx::mbar_init(q_empty, 1);
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kKStages; ++s) {
             ptx::mbar_init(k_full + s, 1);
             ptx::mbar_init(k_empty + s, 1);
+        }
+        for (int s = 0; s < kVStages; ++s) {
             ptx::mbar_init(v_full + s, 1);
             ptx::mbar_init(v_empty + s, 1);
         }
@@ -147,37 +151,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
 
-    if (warp == 0) {
-        // ===================== TMA producer (whole warp) =====================
-        // Lane 0 issues every TMA; at each unit start (and every kPtChunk pages)
-        // the 32 lanes stage the request's page-table row in shared memory, so no
-        // global load sits on the per-tile issue path (that dependent load was the
-        // per-SM streaming limiter).  The 4-stage rings cover the staging bubble.
-        int* pt_s = reinterpret_cast<int*>(smem + S::OFF_PT);
-        uint32_t kv_it = 0, unit_it = 0;
+    if (warp == 0 || warp == kVWarp) {
+        // ===================== TMA producers (whole warps) =====================
+        // warp 0 loads Q and the K tiles, warp kVWarp the V tiles, each through its
+        // own ring (K: short residence, released by QK; V: held until PV), so K
+        // runs ahead independently of V-slot availability.  Lane 0 issues every
+        // TMA; at each unit start (and every kPtChunk pages) the 32 lanes stage
+        // the request's page-table row in shared memory, so no global load sits on
+        // the per-tile issue path.
+        const bool is_k = warp == 0;
+        int* pt_s = reinterpret_cast<int*>(smem + S::OFF_PT) + (is_k ? 0 : kPtChunk);
+        const int n_st = is_k ? kKStages : kVStages;
+        uint64_t* full = is_k ? k_full : v_full;
+        uint64_t* empty = is_k ? k_empty : v_empty;
+        const CUtensorMap* tm_c = is_k ? &tm_kc : &tm_vc;
+        const CUtensorMap* tm_t = is_k ? &tm_kt : &tm_vt;
+        unsigned char* ring = smem + (is_k ? S::OFF_K : S::OFF_V);
+        uint32_t it = 0, unit_it = 0;
         const uint64_t pol = ptx::policy_evict_first();
         for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
             Unit u;
             if (!decode_unit(p, w, u)) {
-                if (lane == 0 && u.K > AS_MAX_TREE && u.mt == 0 && u.g == 0)
+                if (is_k && lane == 0 && u.K > AS_MAX_TREE && u.mt == 0 && u.g == 0)
                     set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, u.i);
                 continue;
             }
-            if (lane == 0 && u.mt == 0 && u.g == 0 && __ldg(p.kv_len + u.i) > p.max_pages * p.page_size)
+            if (is_k && lane == 0 && u.mt == 0 && u.g == 0 && __ldg(p.kv_len + u.i) > p.max_pages * p.page_size)
                 set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, u.i);
             const int n_pages_u = (u.L + p.page_size - 1) / p.page_size;
             int chunk0 = -1;  // first page index currently staged
-            if (lane == 0) {
+            if (is_k && lane == 0) {
                 ptx::mbar_wait(q_empty, (unit_it & 1) ^ 1);
                 ptx::mbar_arrive_expect_tx(q_full, S::Q_BYTES);
                 const int node0 = u.off + u.mt * (kBM / p.G);
                 ptx::tma_load_4d(smem + S::OFF_Q, &tm_q, q_full, 0, u.g * p.G, node0, 0);
             }
-            for (int t = 0; t < u.nt; ++t, ++kv_it) {
-                const int st = kv_it % kStages;
-                const uint32_t ph = (kv_it / kStages) & 1;
-                unsigned char* kdst = smem + S::OFF_K + st * S::KV_BYTES;
-                unsigned char* vdst = smem + S::OFF_V + st * S::KV_BYTES;
+            for (int t = 0; t < u.nt; ++t, ++it) {
+                const int st = it % n_st;
+                const uint32_t ph = (it / n_st) & 1;
+                unsigned char* dst = ring + st * S::KV_BYTES;
                 if (t < u.n_prefix) {
                     const int key0 = t * kBN;
                     const int pg_first = key0 / p.page_size;
@@ -193,52 +205,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int valid = min(kBN, u.L - key0);
                         const int nbox = (valid + p.box_rows - 1) / p.box_rows;
                         const uint32_t bytes = (uint32_t)(nbox * NCH * p.box_rows * 128);
-                        ptx::mbar_wait(k_empty + st, ph ^ 1);
-                        AS_TRACE(0, kv_it);
-                        ptx::mbar_arrive_expect_tx(k_full + st, bytes);
+                        ptx::mbar_wait(empty + st, ph ^ 1);
+                        AS_TRACE(is_k ? 0 : 1, it);
+                        ptx::mbar_arrive_expect_tx(full + st, bytes);
                         for (int b = 0; b < nbox; ++b) {
                             const int kp = key0 + b * p.box_rows;
                             const int page = pt_s[kp / p.page_size - chunk0];
                             const int slot = kp % p.page_size;
                             // out-of-range pages read as zeros (TMA bounds check); flag them
-                            if (page < 0 || page >= p.num_pages) set_dev_error(p.ws, AS_DEV_BAD_PAGE, u.i);
+                            if (is_k && (page < 0 || page >= p.num_pages)) set_dev_error(p.ws, AS_DEV_BAD_PAGE, u.i);
                             if (p.kv_split_d) {
-                                ptx::tma_load_5d_hint(kdst, &tm_kc, k_full + st, 0, slot, 0, u.g, page, pol);
+                                ptx::tma_load_5d_hint(dst, tm_c, full + st, 0, slot, 0, u.g, page, pol);
                             } else {
 #pragma unroll
                                 for (int c = 0; c < NCH; ++c)
-                                    ptx::tma_load_4d_hint(kdst + c * kBN * 128 + b * p.box_rows * 128, &tm_kc,
-                                                          k_full + st, c * 64, slot, u.g, page, pol);
-                            }
-                        }
-                        ptx::mbar_wait(v_empty + st, ph ^ 1);
-                        AS_TRACE(1, kv_it);
-                        ptx::mbar_arrive_expect_tx(v_full + st, bytes);
-                        for (int b = 0; b < nbox; ++b) {
-                            const int kp = key0 + b * p.box_rows;
-                            const int page = pt_s[kp / p.page_size - chunk0];
-                            const int slot = kp % p.page_size;
-                            if (p.kv_split_d) {
-                                ptx::tma_load_5d_hint(vdst, &tm_vc, v_full + st, 0, slot, 0, u.g, page, pol);
-                            } else {
-#pragma unroll
-                                for (int c = 0; c < NCH; ++c)
-                                    ptx::tma_load_4d_hint(vdst + c * kBN * 128 + b * p.box_rows * 128, &tm_vc,
-                                                          v_full + st, c * 64, slot, u.g, page, pol);
+                                    ptx::tma_load_4d_hint(dst + c * kBN * 128 + b * p.box_rows * 128, tm_c, full + st,
+                                                          c * 64, slot, u.g, page, pol);
                             }
                         }
                     }
                 } else if (lane == 0) {
                     const int row0 = u.off + (t - u.n_prefix) * kBN;
-                    const uint32_t bytes = (uint32_t)(NCH * kBN * 128);
-                    ptx::mbar_wait(k_empty + st, ph ^ 1);
-                    AS_TRACE(0, kv_it);
-                    ptx::mbar_arrive_expect_tx(k_full + st, bytes);
-                    ptx::tma_load_4d(kdst, &tm_kt, k_full + st, 0, row0, 0, u.g);
-                    ptx::mbar_wait(v_empty + st, ph ^ 1);
-                    AS_TRACE(1, kv_it);
-                    ptx::mbar_arrive_expect_tx(v_full + st, bytes);
-                    ptx::tma_load_4d(vdst, &tm_vt, v_full + st, 0, row0, 0, u.g);
+                    ptx::mbar_wait(empty + st, ph ^ 1);
+                    AS_TRACE(is_k ? 0 : 1, it);
+                    ptx::mbar_arrive_expect_tx(full + st, (uint32_t)(NCH * kBN * 128));
+                    ptx::tma_load_4d(dst, tm_t, full + st, 0, row0, 0, u.g);
                 }
             }
             ++unit_it;
@@ -263,8 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(q_full, unit_it & 1);
             auto do_qk = [&](int t) {
                 const int wg = t & 1;
-                const int st = k_it % kStages;
-                ptx::mbar_wait(k_full + st, (k_it / kStages) & 1);
+                const int st = k_it % kKStages;
+                ptx::mbar_wait(k_full + st, (k_it / kKStages) & 1);
                 if (lane == 0) AS_TRACE(2, k_it);
                 ptx::mbar_wait(s_empty + wg, ((s_ph >> wg) & 1) ^ 1);
                 ptx::tc_fence_after();
@@ -292,8 +283,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             auto do_pv = [&](int t) {
                 const int wg = t & 1;
-                const int st = v_it % kStages;
-                ptx::mbar_wait(v_full + st, (v_it / kStages) & 1);
+                const int st = v_it % kVStages;
+                ptx::mbar_wait(v_full + st, (v_it / kVStages) & 1);
                 if (lane == 0) AS_TRACE(3, v_it);
                 // zero V rows past the prefix end (stale/uninitialised smem or cache
                 // slots >= L may hold NaN; P is 0 there but 0 * NaN = NaN)
