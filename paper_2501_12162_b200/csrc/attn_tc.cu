@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(k_full + st, (k_it / kKStages) & 1);
                 if (lane == 0) AS_TRACE(2, k_it);
                 ptx::mbar_wait(s_empty + wg, ((s_ph >> wg) & 1) ^ 1);
+                if (lane == 0) AS_TRACE(7, k_it);
                 ptx::tc_fence_after();
                 if (p.debug_mode >= 2) {
                     if (lane == 0) {

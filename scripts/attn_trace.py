@@ -39,6 +39,7 @@ n = int((tr[:, 0] != 0).sum())
 tr = tr[:n].astype(np.float64)
 t0 = tr[0, 0]
 tr = (tr - t0) / args.ghz  # ns
+# columns: 0 K issue, 1 V issue, 2 MMA: K landed, 3 MMA: V landed, 4 PV issue, 5 softmax start, 6 softmax end, 7 QK issue
 ns = lambda x: f"{np.median(x):7.0f} (p10 {np.percentile(x, 10):6.0f}, p90 {np.percentile(x, 90):6.0f})"
 print(f"tiles traced on CTA 0: {n}; span {tr[n - 1, 6]:.0f} ns; per tile {tr[n - 1, 6] / n:.0f} ns")
 print("producer K issue interval     ", ns(np.diff(tr[:, 0])))
@@ -50,5 +51,7 @@ print("P ready -> MMA sees P         ", ns(tr[:, 4] - tr[:, 6]))
 print("V landed -> PV issue (wait P) ", ns(tr[:, 4] - tr[:, 3]))
 print("producer waits for K slot: K issue minus PV of tile-4 issue", ns(tr[4:, 0] - tr[:-4, 4]))
 np.set_printoptions(linewidth=200, suppress=True)
-print("first 12 tiles (ns):\n", np.round(tr[:12, :7]))
-print("tiles 40-52 (ns):\n", np.round(tr[40:52, :7]))
+print("QK issue -> softmax start      ", ns(tr[:, 5] - tr[:, 7]))
+print("QK issue interval             ", ns(np.diff(tr[:, 7])))
+print("cols: Kiss Viss Kland Vland PViss Sstart Send QKiss ; rows = tiles 20..36 (ns rel. to tile 20 K issue)")
+print(np.round(tr[20:37, :8] - tr[20, 0]))
