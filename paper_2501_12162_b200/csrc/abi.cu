@@ -212,6 +212,8 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     p.n_units = mt_max * n_req * n_kv_heads;
     const char* dbg = getenv("AS_ATTN_DEBUG_MODE");  // timing experiments only (wrong outputs)
     p.debug_mode = dbg ? atoi(dbg) : 0;
+    const char* pf = getenv("AS_ATTN_PREFETCH");  // tuning override of the L2 prefetch distance
+    p.prefetch_tiles = pf ? atoi(pf) : 8;
     const char* tr = getenv("AS_ATTN_TRACE");  // CTA-0 pipeline timestamps into the workspace (debug)
     p.trace = nullptr;
     p.trace_cap = 0;

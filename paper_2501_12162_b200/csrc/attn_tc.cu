@@ -186,6 +186,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int node0 = u.off + u.mt * (kBM / p.G);
                 ptx::tma_load_4d(smem + S::OFF_Q, &tm_q, q_full, 0, u.g * p.G, node0, 0);
             }
+            // L2 prefetch of tile tp of this unit (no smem; hides DRAM latency beyond
+            // what the rings cover).  Only tiles whose page entries are staged.
+            auto prefetch = [&](int tp) {
+                if (tp >= u.nt) return;
+                if (tp < u.n_prefix) {
+                    const int key0 = tp * kBN;
+                    const int valid = min(kBN, u.L - key0);
+                    const int nbox = (valid + p.box_rows - 1) / p.box_rows;
+                    for (int b = 0; b < nbox; ++b) {
+                        const int kp = key0 + b * p.box_rows;
+                        const int pi = kp / p.page_size - chunk0;
+                        if (pi < 0 || pi >= kPtChunk) return;
+                        const int page = pt_s[pi];
+                        const int slot = kp % p.page_size;
+                        if (p.kv_split_d) {
+                            ptx::tma_prefetch_5d(tm_c, 0, slot, 0, u.g, page);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < NCH; ++c) ptx::tma_prefetch_4d(tm_c, c * 64, slot, u.g, page);
+                        }
+                    }
+                } else {
+                    ptx::tma_prefetch_4d(tm_t, 0, u.off + (tp - u.n_prefix) * kBN, 0, u.g);
+                }
+            };
             for (int t = 0; t < u.nt; ++t, ++it) {
                 const int st = it % n_st;
                 const uint32_t ph = (it / n_st) & 1;
@@ -200,8 +225,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int k = lane; k < kPtChunk && chunk0 + k < n_pages_u; k += 32)
                             pt_s[k] = __ldg(p.page_table + (size_t)u.i * p.max_pages + chunk0 + k);
                         __syncwarp();
+                        if (lane == 0 && t == 0)
+                            for (int tp = 1; tp <= p.prefetch_tiles; ++tp) prefetch(tp);
                     }
                     if (lane == 0) {
+                        prefetch(t + 1 + p.prefetch_tiles);
                         const int valid = min(kBN, u.L - key0);
                         const int nbox = (valid + p.box_rows - 1) / p.box_rows;
                         const uint32_t bytes = (uint32_t)(nbox * NCH * p.box_rows * 128);
@@ -225,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 } else if (lane == 0) {
+                    prefetch(t + 1 + p.prefetch_tiles);
                     const int row0 = u.off + (t - u.n_prefix) * kBN;
                     ptx::mbar_wait(empty + st, ph ^ 1);
                     AS_TRACE(is_k ? 0 : 1, it);

@@ -60,6 +60,7 @@ struct TcParams {
     float* lse;
     void* ws;
     int n_units;
+    int prefetch_tiles;  // L2 prefetch distance of the TMA producers (tiles)
     int debug_mode;  // 0 = normal; 1 = skip softmax math; 2 = also skip MMAs (timing experiments only)
     unsigned long long* trace;  // CTA-0 pipeline timestamps [trace_cap][8] (clock64) or NULL
     int trace_cap;
