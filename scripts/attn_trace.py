@@ -23,6 +23,19 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--ghz", type=float, default=1.965)
 args = ap.parse_args()
+# calibration: HBM copy bandwidth on this box right now (read+write bytes)
+_a = torch.empty(1 << 29, dtype=torch.bfloat16, device="cuda")
+_b = torch.empty_like(_a)
+for _ in range(3):
+    _b.copy_(_a)
+_s, _e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+_s.record()
+for _ in range(5):
+    _b.copy_(_a)
+_e.record()
+torch.cuda.synchronize()
+print(f"calibration: torch copy {2 * _a.numel() * 2 * 5 / (_s.elapsed_time(_e) / 1e3) / 1e9:.0f} GB/s")
+del _a, _b
 W = bench.make_workload(args.config, "cuda")
 for _ in range(3):
     bench.run_attention(W)
