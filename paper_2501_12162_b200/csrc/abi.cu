@@ -277,6 +277,16 @@ as_status as_accept_tokens(as_accept_phase phase, int32_t n_req, int32_t req_beg
                                                                                                       : AS_ERR_CUDA;
 }
 
+// ----------------------------------------------------------------- debug
+as_status as_debug_stream_bw(const void* src, const int32_t* order, int32_t n_chunks, int32_t chunk_bytes,
+                             int32_t stages, int32_t mode, unsigned long long* sink, int32_t grid, void* stream) {
+    if (!src || !order || !sink || n_chunks <= 0 || chunk_bytes <= 0 || chunk_bytes % 16 || stages <= 0 || grid <= 0)
+        return AS_ERR_INVALID_ARG;
+    if ((size_t)stages * chunk_bytes > 200 * 1024) return AS_ERR_UNSUPPORTED;
+    return launch_stream_bw(src, order, n_chunks, chunk_bytes, stages, mode, sink, grid, S(stream)) == 0 ? AS_OK
+                                                                                                       : AS_ERR_CUDA;
+}
+
 // ----------------------------------------------------------------- selftest
 as_status as_selftest_umma(const void* a, const void* b, float* d, int32_t n, int32_t k, int32_t b_mn_major,
                            void* stream) {
