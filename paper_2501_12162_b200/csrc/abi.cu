@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "params.cuh"
@@ -283,8 +284,18 @@ as_status as_debug_stream_bw(const void* src, const int32_t* order, int32_t n_ch
     if (!src || !order || !sink || n_chunks <= 0 || chunk_bytes <= 0 || chunk_bytes % 16 || stages <= 0 || grid <= 0)
         return AS_ERR_INVALID_ARG;
     if ((size_t)stages * chunk_bytes > 200 * 1024) return AS_ERR_UNSUPPORTED;
-    return launch_stream_bw(src, order, n_chunks, chunk_bytes, stages, mode, sink, grid, S(stream)) == 0 ? AS_OK
-                                                                                                       : AS_ERR_CUDA;
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof(tm));
+    if (mode >= 3) {  // [rows][128] bf16 view, box {64, rows_per_chunk, 2}, SW128
+        const uint64_t rows = (uint64_t)n_chunks * (chunk_bytes / 256);
+        uint64_t dims[3] = {64, rows, 2};
+        uint64_t str[2] = {256, 128};
+        uint32_t box[3] = {64, (uint32_t)(chunk_bytes / 256), 2};
+        if (chunk_bytes / 256 > 256 || !make_map(&tm, src, 3, dims, str, box)) return AS_ERR_UNSUPPORTED;
+    }
+    return launch_stream_bw(src, order, n_chunks, chunk_bytes, stages, mode, sink, grid, &tm, S(stream)) == 0
+               ? AS_OK
+               : AS_ERR_CUDA;
 }
 
 // ----------------------------------------------------------------- selftest

@@ -19,12 +19,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// mode 3/4: like 0/1 but each chunk is fetched as a 3-D TENSOR box
+// {64 elems, rows, 2 halves} with SWIZZLE_128B from a [rows][128] bf16 view
+// (exactly the attention kernel's K/V tile loads); chunk_bytes = rows * 256.
 __global__ void __launch_bounds__(256, 1)
     stream_bw_kernel(const unsigned char* __restrict__ src, const int* __restrict__ order, int n_chunks,
-                     int chunk_bytes, int stages, int mode, unsigned long long* sink) {
-    extern __shared__ __align__(1024) unsigned char smem[];
+                     int chunk_bytes, int stages, int mode, unsigned long long* sink,
+                     const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)stages * chunk_bytes);
     const int tid = threadIdx.x;
+    const bool tensor = mode >= 3;
+    const int rows_per_chunk = chunk_bytes / 256;
+    if (tensor) mode -= 3;
     if (mode <= 1) {
         if (tid == 0) {
             for (int s = 0; s < stages; ++s) ptx::mbar_init(bars + s, 1);
@@ -41,14 +49,20 @@ __global__ void __launch_bounds__(256, 1)
             for (int j = 0; j < my_stages && k < n_chunks; ++j, k += kstep, ++primed) {
                 const int st = tid + j * nthr;
                 ptx::mbar_arrive_expect_tx(bars + st, chunk_bytes);
-                bulk_g2s(smem + (size_t)st * chunk_bytes, src + (size_t)order[k] * chunk_bytes, chunk_bytes, bars + st);
+                if (tensor)
+                    ptx::tma_load_3d(smem + (size_t)st * chunk_bytes, &tmap, bars + st, 0, order[k] * rows_per_chunk, 0);
+                else
+                    bulk_g2s(smem + (size_t)st * chunk_bytes, src + (size_t)order[k] * chunk_bytes, chunk_bytes, bars + st);
             }
             uint32_t it = 0;
             for (; k < n_chunks; k += kstep, ++it) {
                 const int st = tid + (int)(it % my_stages) * nthr;
                 ptx::mbar_wait(bars + st, (it / my_stages) & 1);
                 ptx::mbar_arrive_expect_tx(bars + st, chunk_bytes);
-                bulk_g2s(smem + (size_t)st * chunk_bytes, src + (size_t)order[k] * chunk_bytes, chunk_bytes, bars + st);
+                if (tensor)
+                    ptx::tma_load_3d(smem + (size_t)st * chunk_bytes, &tmap, bars + st, 0, order[k] * rows_per_chunk, 0);
+                else
+                    bulk_g2s(smem + (size_t)st * chunk_bytes, src + (size_t)order[k] * chunk_bytes, chunk_bytes, bars + st);
             }
             for (int d = 0; d < primed; ++d, ++it) {
                 const int st = tid + (int)(it % my_stages) * nthr;
@@ -73,13 +87,13 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 int launch_stream_bw(const void* src, const int* order, int n_chunks, int chunk_bytes, int stages, int mode,
-                     unsigned long long* sink, int grid, cudaStream_t stream) {
-    size_t smem = mode <= 1 ? (size_t)stages * chunk_bytes + stages * 8 + 64 : 0;
+                     unsigned long long* sink, int grid, const CUtensorMap* tmap, cudaStream_t stream) {
+    size_t smem = mode != 2 ? (size_t)stages * chunk_bytes + stages * 8 + 64 + 1024 : 0;
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(stream_bw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;
     stream_bw_kernel<<<grid, 256, smem, stream>>>(reinterpret_cast<const unsigned char*>(src), order, n_chunks,
-                                                  chunk_bytes, stages, mode, sink);
+                                                  chunk_bytes, stages, mode, sink, *tmap);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

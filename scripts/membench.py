@@ -34,15 +34,12 @@ def run(chunk, stages, mode, rand, grid=nsm, reps=3):
 
 
 print("SMs", nsm)
-for mode in (0, 1):
+for mode in (0, 1, 3, 4):
     for chunk in (8192, 16384, 32768):
-        for stages in (2, 4, 6, 8, 12):
+        for stages in (4, 8):
             if stages * chunk > 200 * 1024:
                 continue
             r = [run(chunk, stages, mode, rand) for rand in (False, True)]
             print(f"mode {mode} chunk {chunk // 1024:2d}KB stages {stages:2d} ({stages * chunk // 1024:3d}KB in flight): "
                   f"seq {r[0]:6.0f} GB/s  random {r[1]:6.0f} GB/s")
-for chunk in (16384,):
-    for grid in (nsm, 2 * nsm, 4 * nsm):
-        r = [run(chunk, 1, 2, rand, grid=grid) for rand in (False, True)]
-        print(f"mode 2 (LDG) chunk {chunk // 1024}KB grid {grid}: seq {r[0]:6.0f}  random {r[1]:6.0f} GB/s")
+print("modes: 0 bulk-1thr 1 bulk-2thr 3 tensor-1thr 4 tensor-2thr")
