@@ -32,14 +32,19 @@ __global__ void __launch_bounds__(256, 1)
     const int tid = threadIdx.x;
     const bool tensor = mode >= 3;
     const int rows_per_chunk = chunk_bytes / 256;
-    if (tensor) mode -= 3;
+    int nthr_sel = 1;
+    if (mode == 1 || mode == 4) nthr_sel = 2;
+    if (mode == 5) nthr_sel = 4;
+    if (mode == 6) nthr_sel = 8;
+    if (tensor) mode = 0;
+    else if (mode == 1) mode = 0;
     if (mode <= 1) {
         if (tid == 0) {
             for (int s = 0; s < stages; ++s) ptx::mbar_init(bars + s, 1);
             ptx::fence_mbar_init();
         }
         __syncthreads();
-        const int nthr = mode == 0 ? 1 : 2;
+        const int nthr = nthr_sel;
         if (tid < nthr) {
             // thread tid owns stages tid, tid+nthr, ... and chunks k = blockIdx + (tid + j*nthr)*grid
             const int my_stages = (stages - tid + nthr - 1) / nthr;

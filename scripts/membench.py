@@ -34,12 +34,12 @@ def run(chunk, stages, mode, rand, grid=nsm, reps=3):
 
 
 print("SMs", nsm)
-for mode in (0, 1, 3, 4):
-    for chunk in (8192, 16384, 32768):
-        for stages in (4, 8):
+for mode in (3, 4, 5, 6):
+    for chunk in (16384, 32768):
+        for stages in (4, 8, 12):
             if stages * chunk > 200 * 1024:
                 continue
             r = [run(chunk, stages, mode, rand) for rand in (False, True)]
             print(f"mode {mode} chunk {chunk // 1024:2d}KB stages {stages:2d} ({stages * chunk // 1024:3d}KB in flight): "
                   f"seq {r[0]:6.0f} GB/s  random {r[1]:6.0f} GB/s")
-print("modes: 0 bulk-1thr 1 bulk-2thr 3 tensor-1thr 4 tensor-2thr")
+print("modes: 3 tensor-1thr 4 tensor-2thr 5 tensor-4thr 6 tensor-8thr")
