@@ -221,8 +221,9 @@ as_status as_check_device_error(const void* workspace, int32_t* code, int32_t* r
 as_status as_reset_workspace(void* workspace, size_t workspace_bytes, void* stream);
 /* Self-test of the tcgen05/TMA building blocks used by the bf16 attention:
  * D[M=128, N] = A[128, K] . B[N, K]^T with bf16 A/B (device, K-major rows) and
- * fp32 D (device), N in {64,128}, K in {64,128}; b_mn_major != 0 treats B as
- * [K, N] (N contiguous), as the PV product does with V.  Debug/tests only. */
+ * fp32 D (device), N in {64,128}, K in {64,128}; bit 0 of b_mn_major treats B
+ * as [K, N] (N contiguous), as the PV product does with V; bit 1 stages A in
+ * tensor memory (the A-from-TMEM form used for P).  Debug/tests only. */
 as_status as_selftest_umma(const void* a, const void* b, float* d, int32_t n, int32_t k,
                            int32_t b_mn_major, void* stream);
 

@@ -321,7 +321,9 @@ as_status as_selftest_umma(const void* a, const void* b, float* d, int32_t n, in
         uint32_t box[2] = {64, (uint32_t)k};
         if (!make_map(&mb, b, 2, dims, str, box)) return AS_ERR_CUDA;
     }
-    return launch_umma_selftest(&ma, &mb, d, n, k, b_mn_major ? 1 : 0, S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
+    return launch_umma_selftest(&ma, &mb, d, n, k, (b_mn_major & 1) ? 1 : 0, a, (b_mn_major & 2) ? 1 : 0, S(stream)) == 0
+               ? AS_OK
+               : AS_ERR_CUDA;
 }
 
 }  // extern "C"

@@ -76,6 +76,6 @@ int launch_attn_tc(const CUtensorMap* maps, const TcParams& p, int head_dim, int
 int launch_stream_bw(const void* src, const int* order, int n_chunks, int chunk_bytes, int stages, int mode,
                      unsigned long long* sink, int grid, const CUtensorMap* tmap, cudaStream_t stream);
 int launch_umma_selftest(const CUtensorMap* ma, const CUtensorMap* mb, float* d, int N, int K, int b_mn,
-                         cudaStream_t stream);
+                         const void* a_g, int a_tmem, cudaStream_t stream);
 
 }  // namespace as

@@ -9,7 +9,7 @@ namespace as {
 
 __global__ void __launch_bounds__(128, 1)
     umma_selftest_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                         float* d, int N, int K, int b_mn) {
+                         float* d, int N, int K, int b_mn, const __nv_bfloat16* a_g, int a_tmem) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* sa = smem;                  // (K/64) chunks of [128 x 64]
@@ -22,11 +22,28 @@ __global__ void __launch_bounds__(128, 1)
         ptx::mbar_init(bar + 1, 1);
         ptx::fence_mbar_init();
     }
-    if (warp == 0) ptx::tmem_alloc(holder, 256);
+    if (warp == 0) ptx::tmem_alloc(holder, 512);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *holder;
+    if (a_tmem) {
+        // stage A into TMEM columns [256, 256 + K/2): lane = row, bf16 pairs packed per column
+        const int row = warp * 32 + lane;
+        for (int c0 = 0; c0 < K / 2; c0 += 32) {
+            uint32_t r[32];
+            for (int j = 0; j < 32; ++j) {
+                const int k = 2 * (c0 + j);
+                __nv_bfloat162 h2 = __halves2bfloat162(a_g[(size_t)row * K + k], a_g[(size_t)row * K + k + 1]);
+                r[j] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            ptx::tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + 256 + c0, r);
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncthreads();
+        ptx::tc_fence_after();
+    }
     if (threadIdx.x == 0) {
         const int kch = K / 64;
         const uint32_t bytes = (uint32_t)(kch * 128 * 128 + K * N * 2);
@@ -47,7 +64,8 @@ __global__ void __launch_bounds__(128, 1)
             uint64_t bd;
             if (!b_mn) bd = ptx::sw128_desc(b0 + c * N * 128 + kk * 32, 0, 1024);
             else bd = ptx::sw128_desc(b0 + ks * 16 * 128, K * 128, 1024);
-            ptx::mma_bf16_ss(tmem, ad, bd, idesc, ks > 0 ? 1u : 0u);
+            if (a_tmem) ptx::mma_bf16_ts(tmem, tmem + 256 + ks * 8, bd, idesc, ks > 0 ? 1u : 0u);
+            else ptx::mma_bf16_ss(tmem, ad, bd, idesc, ks > 0 ? 1u : 0u);
         }
         ptx::mma_commit(bar + 1);
     }
@@ -65,16 +83,17 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     if (warp == 0) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem, 256);
+        ptx::tmem_dealloc(tmem, 512);
     }
 }
 
 int launch_umma_selftest(const CUtensorMap* ma, const CUtensorMap* mb, float* d, int N, int K, int b_mn,
-                         cudaStream_t stream) {
+                         const void* a_g, int a_tmem, cudaStream_t stream) {
     const int smem = 4 * 128 * 128 + 64 + 1024;
     if (cudaFuncSetAttribute(umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return -1;
-    umma_selftest_kernel<<<1, 128, smem, stream>>>(*ma, *mb, d, N, K, b_mn);
+    umma_selftest_kernel<<<1, 128, smem, stream>>>(*ma, *mb, d, N, K, b_mn,
+                                                   reinterpret_cast<const __nv_bfloat16*>(a_g), a_tmem);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

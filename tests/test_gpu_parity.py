@@ -28,13 +28,14 @@ def ada():
 
 # --------------------------------------------------------------------------- tcgen05 building blocks
 @pytest.mark.parametrize("n,k,mn", [(64, 128, 0), (128, 128, 0), (64, 64, 0), (128, 64, 1), (64, 64, 1),
-                                    (128, 128, 1)])
+                                    (128, 128, 1), (128, 128, 3), (64, 64, 3), (128, 64, 2)])
 def test_umma_selftest(ada, n, k, mn):
+    """bit 0: B MN-major (the PV/V form); bit 1: A staged in TMEM (the P form)."""
     g = torch.Generator(device="cpu").manual_seed(n * 7 + k + mn)
     a = torch.randn(128, k, generator=g).to(torch.bfloat16)
-    b = torch.randn((k, n) if mn else (n, k), generator=g).to(torch.bfloat16)
+    b = torch.randn((k, n) if mn & 1 else (n, k), generator=g).to(torch.bfloat16)
     d = ada.selftest_umma(a.cuda(), b.cuda(), n, k, mn).cpu()
-    ref = a.double() @ (b.double() if mn else b.double().T)
+    ref = a.double() @ (b.double() if mn & 1 else b.double().T)
     torch.cuda.synchronize()
     assert torch.allclose(d.double(), ref, atol=1e-3, rtol=1e-4), (d - ref).abs().max()
 
