@@ -126,8 +126,13 @@ as_status as_select_trees(int32_t n_req, int32_t n_cand_total, const int32_t* ca
 // ----------------------------------------------------------------- attention
 size_t as_attn_workspace_size(as_dtype dtype, int32_t n_req, int32_t n_tree_rows, int32_t n_q_heads,
                               int32_t head_dim, int32_t max_kv_len) {
-    (void)dtype; (void)n_req; (void)n_tree_rows; (void)n_q_heads; (void)head_dim; (void)max_kv_len;
-    return kWsHeaderBytes + kAttnTraceBytes;
+    (void)dtype; (void)n_tree_rows; (void)max_kv_len;
+    if (n_req < 0 || n_q_heads < 0 || head_dim <= 0) return 0;
+    // header + debug trace + stream-K counters (one per unit: n_units = n_q * n_req
+    // for every GQA ratio) + 2 partial-state slots per SM
+    const size_t units = (size_t)n_q_heads * (size_t)n_req;
+    const size_t slot = ((size_t)128 * head_dim + 256) * 4;
+    return kWsHeaderBytes + kAttnTraceBytes + align_up(units * 4, 256) + 2 * (size_t)sm_count() * slot;
 }
 
 as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows, int32_t n_q_heads,
@@ -211,6 +216,18 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     p.out = (__nv_bfloat16*)out; p.lse = lse; p.ws = workspace;
     const int mt_max = (AS_MAX_TREE * G + 127) / 128;
     p.n_units = mt_max * n_req * n_kv_heads;
+    {
+        const int nsm = sm_count();
+        const size_t slot = ((size_t)128 * head_dim + 256) * 4;
+        const size_t cnt_bytes = align_up((size_t)p.n_units * 4, 256);
+        const size_t need = kWsHeaderBytes + kAttnTraceBytes + cnt_bytes + 2 * (size_t)nsm * slot;
+        unsigned char* base = reinterpret_cast<unsigned char*>(workspace) + kWsHeaderBytes + kAttnTraceBytes;
+        const char* skenv = getenv("AS_ATTN_STREAMK");  // A/B switch (debug)
+        p.stream_k = (workspace_bytes >= need && !(skenv && atoi(skenv) == 0)) ? 1 : 0;
+        p.cnt = reinterpret_cast<int*>(base);
+        p.partial = reinterpret_cast<float*>(base + cnt_bytes);
+        p.slot_floats = 128 * head_dim + 256;
+    }
     const char* dbg = getenv("AS_ATTN_DEBUG_MODE");  // timing experiments only (wrong outputs)
     p.debug_mode = dbg ? atoi(dbg) : 0;
     const char* pf = getenv("AS_ATTN_PREFETCH");  // tuning override of the L2 prefetch distance

@@ -40,6 +40,7 @@ constexpr int kThreads = 352;     // 11 warps: K/Q TMA, MMA, 2 x 4 softmax, V TM
 constexpr int kTmemCols = 512;    // S0 [0,64) S1 [64,128) O0 [128,128+D) O1 [128+D, 128+2D)
 constexpr int kOcol = 128;
 constexpr int kPtChunk = 512;     // page-table entries staged per refill
+constexpr int kPlanCap = 12288;   // stream-K plan entries (long long) that fit in the V ring scratch
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
 
@@ -90,6 +91,83 @@ __device__ __forceinline__ bool decode_unit(const TcParams& p, int w, Unit& u) {
     u.n_prefix = (u.L + kBN - 1) / kBN;
     u.nt = u.n_prefix + (u.K + kBN - 1) / kBN;
     return true;
+}
+
+// ---------------------------------------------------------------------------
+// Work schedule.  A "piece" is a contiguous tile range [tb, te) of one unit.
+// stream-K mode: the non-empty units' tiles, in unit order (mt, i, g), are
+// concatenated and CTA b processes global tiles [T*b/G, T*(b+1)/G), so every
+// SM streams the same number of KV tiles whatever the tree/prefix sizes; a unit
+// cut between CTAs is finished by the last CTA to complete a piece of it (its
+// partial (O, m, l) states are merged in fp32 through the workspace).
+// static mode (fallback when the plan does not fit in shared memory): whole
+// units round-robin.
+// ---------------------------------------------------------------------------
+struct Piece {
+    Unit u;
+    int w;         // unit index (mt, i, g)
+    int tb, te;    // tile range of this piece
+    long long x;   // global tile index of (u, tb) in stream-K mode
+};
+
+struct Sched {
+    int stream;
+    int beta, g, t;      // stream-K cursor: block (mt, i), kv head, tile
+    long long rem, x;    // tiles left for this CTA, global index of the cursor
+    int w;               // static cursor
+};
+
+__device__ __forceinline__ bool sched_next(const TcParams& p, Sched& sc, Piece& pc) {
+    if (!sc.stream) {
+        for (; sc.w < p.n_units; sc.w += gridDim.x) {
+            if (decode_unit(p, sc.w, pc.u)) {
+                pc.w = sc.w;
+                pc.tb = 0;
+                pc.te = pc.u.nt;
+                pc.x = -1;
+                sc.w += gridDim.x;
+                return true;
+            }
+        }
+        return false;
+    }
+    const int nb = p.n_units / p.n_kv;
+    while (sc.rem > 0 && sc.beta < nb) {
+        const int w = sc.beta * p.n_kv + sc.g;
+        if (!decode_unit(p, w, pc.u)) {  // empty block: all its kv heads are empty
+            ++sc.beta;
+            sc.g = 0;
+            sc.t = 0;
+            continue;
+        }
+        pc.w = w;
+        pc.tb = sc.t;
+        const long long avail = pc.u.nt - sc.t;
+        pc.te = sc.t + (int)(avail < sc.rem ? avail : sc.rem);
+        pc.x = sc.x;
+        const int n = pc.te - pc.tb;
+        sc.rem -= n;
+        sc.x += n;
+        sc.t = pc.te;
+        if (sc.t >= pc.u.nt) {
+            sc.t = 0;
+            if (++sc.g >= p.n_kv) {
+                sc.g = 0;
+                ++sc.beta;
+            }
+        }
+        return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ long long sk_start(long long T, int b, int G) { return T * (long long)b / G; }
+__device__ __forceinline__ int sk_owner(long long T, int G, long long x) {
+    int b = (int)((x * G) / (T > 0 ? T : 1));
+    if (b >= G) b = G - 1;
+    while (b + 1 < G && sk_start(T, b + 1, G) <= x) ++b;
+    while (b > 0 && sk_start(T, b, G) > x) --b;
+    return b;
 }
 
 template <int D>
@@ -151,6 +229,91 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
 
+    // ---------------- stream-K plan (all threads; V ring used as scratch) ----------------
+    __shared__ long long sk_T, sk_x0;
+    __shared__ int sk_cur[3];
+    __shared__ long long sk_rem;
+    __shared__ long long scan_tmp[33];
+    __shared__ int sk_last;
+    Sched sched0;
+    sched0.w = blockIdx.x;
+    sched0.stream = 0;
+    {
+        const int nb = p.n_units / p.n_kv;
+        if (p.stream_k && nb <= kPlanCap) {
+            long long* pre = reinterpret_cast<long long*>(smem + S::OFF_V);
+            for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+                Unit u;
+                const bool ok = decode_unit(p, b * p.n_kv, u);
+                if (!ok && u.K > AS_MAX_TREE && u.mt == 0) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, u.i);
+                pre[b] = ok ? (long long)u.nt * p.n_kv : 0;
+            }
+            __syncthreads();
+            // exclusive scan of pre[0..nb): per-thread chunks, then warp and block totals
+            const int chunk = (nb + blockDim.x - 1) / blockDim.x;
+            const int lo = threadIdx.x * chunk, hi = min(nb, lo + chunk);
+            long long loc = 0;
+            for (int b = lo; b < hi; ++b) loc += pre[b];
+            long long inc = loc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+                if ((int)lane >= o) inc += y;
+            }
+            if (lane == 31) scan_tmp[warp] = inc;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                long long acc = 0;
+                for (int k = 0; k < (int)(blockDim.x / 32); ++k) {
+                    const long long v = scan_tmp[k];
+                    scan_tmp[k] = acc;
+                    acc += v;
+                }
+                scan_tmp[32] = acc;  // T
+            }
+            __syncthreads();
+            long long run = scan_tmp[warp] + inc - loc;
+            for (int b = lo; b < hi; ++b) {
+                const long long v = pre[b];
+                pre[b] = run;
+                run += v;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const long long T = scan_tmp[32];
+                const int G = gridDim.x;
+                const long long x0 = sk_start(T, blockIdx.x, G), x1 = sk_start(T, blockIdx.x + 1, G);
+                sk_T = T;
+                sk_x0 = x0;
+                sk_rem = x1 - x0;
+                int beta = 0, g = 0, t = 0;
+                if (x1 > x0) {
+                    int lo_b = 0, hi_b = nb - 1;  // last b with pre[b] <= x0
+                    while (lo_b < hi_b) {
+                        const int mid = (lo_b + hi_b + 1) >> 1;
+                        if (pre[mid] <= x0) lo_b = mid; else hi_b = mid - 1;
+                    }
+                    beta = lo_b;
+                    const long long next = (beta + 1 < nb) ? pre[beta + 1] : T;
+                    const long long ntu = (next - pre[beta]) / p.n_kv;
+                    const long long off = x0 - pre[beta];
+                    g = (int)(off / ntu);
+                    t = (int)(off - (long long)g * ntu);
+                }
+                sk_cur[0] = beta;
+                sk_cur[1] = g;
+                sk_cur[2] = t;
+            }
+            __syncthreads();
+            sched0.stream = 1;
+            sched0.beta = sk_cur[0];
+            sched0.g = sk_cur[1];
+            sched0.t = sk_cur[2];
+            sched0.rem = sk_rem;
+            sched0.x = sk_x0;
+        }
+    }
+
     if (warp == 0 || warp == kVWarp) {
         // ===================== TMA producers (whole warps) =====================
         // warp 0 loads Q and the K tiles, warp kVWarp the V tiles, each through its
@@ -169,13 +332,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         unsigned char* ring = smem + (is_k ? S::OFF_K : S::OFF_V);
         uint32_t it = 0, unit_it = 0;
         const uint64_t pol = ptx::policy_evict_first();
-        for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
-            Unit u;
-            if (!decode_unit(p, w, u)) {
-                if (is_k && lane == 0 && u.K > AS_MAX_TREE && u.mt == 0 && u.g == 0)
-                    set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, u.i);
-                continue;
-            }
+        Sched sc = sched0;
+        Piece pc;
+        while (sched_next(p, sc, pc)) {
+            const Unit& u = pc.u;
             if (is_k && lane == 0 && u.mt == 0 && u.g == 0 && __ldg(p.kv_len + u.i) > p.max_pages * p.page_size)
                 set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, u.i);
             const int n_pages_u = (u.L + p.page_size - 1) / p.page_size;
@@ -189,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // L2 prefetch of tile tp of this unit (no smem; hides DRAM latency beyond
             // what the rings cover).  Only tiles whose page entries are staged.
             auto prefetch = [&](int tp) {
-                if (tp >= u.nt) return;
+                if (tp >= pc.te) return;
                 if (tp < u.n_prefix) {
                     const int key0 = tp * kBN;
                     const int valid = min(kBN, u.L - key0);
@@ -211,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tma_prefetch_4d(tm_t, 0, u.off + (tp - u.n_prefix) * kBN, 0, u.g);
                 }
             };
-            for (int t = 0; t < u.nt; ++t, ++it) {
+            for (int t = pc.tb; t < pc.te; ++t, ++it) {
                 const int st = it % n_st;
                 const uint32_t ph = (it / n_st) & 1;
                 unsigned char* dst = ring + st * S::KV_BYTES;
@@ -225,8 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int k = lane; k < kPtChunk && chunk0 + k < n_pages_u; k += 32)
                             pt_s[k] = __ldg(p.page_table + (size_t)u.i * p.max_pages + chunk0 + k);
                         __syncwarp();
-                        if (lane == 0 && t == 0)
-                            for (int tp = 1; tp <= p.prefetch_tiles; ++tp) prefetch(tp);
+                        if (lane == 0 && t == pc.tb)
+                            for (int tp = t + 1; tp <= t + p.prefetch_tiles && tp < pc.te; ++tp) prefetch(tp);
                     }
                     if (lane == 0) {
                         prefetch(t + 1 + p.prefetch_tiles);
@@ -277,12 +437,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t p_base = ptx::smem_u32(smem + S::OFF_P);
         uint32_t k_it = 0, v_it = 0, unit_it = 0;
         uint32_t s_ph = 0, p_ph = 0;  // bit wg = phase parity of S[wg] / P[wg] uses
-        for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
-            Unit u;
-            if (!decode_unit(p, w, u)) continue;
+        Sched sc = sched0;
+        Piece pc;
+        while (sched_next(p, sc, pc)) {
+            const Unit& u = pc.u;
             ptx::mbar_wait(q_full, unit_it & 1);
             auto do_qk = [&](int t) {
-                const int wg = t & 1;
+                const int wg = (t - pc.tb) & 1;
                 const int st = k_it % kKStages;
                 ptx::mbar_wait(k_full + st, (k_it / kKStages) & 1);
                 if (lane == 0) AS_TRACE(2, k_it);
@@ -293,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0) {
                         ptx::mbar_arrive(k_empty + st);
                         ptx::mbar_arrive(s_full + wg);
-                        if (t == u.nt - 1) ptx::mbar_arrive(q_empty);
+                        if (t == pc.te - 1) ptx::mbar_arrive(q_empty);
                     }
                 } else if (lane == 0) {
 #pragma unroll
@@ -305,14 +466,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     ptx::mma_commit(k_empty + st);
                     ptx::mma_commit(s_full + wg);
-                    if (t == u.nt - 1) ptx::mma_commit(q_empty);
+                    if (t == pc.te - 1) ptx::mma_commit(q_empty);
                 }
                 __syncwarp();
                 ++k_it;
                 s_ph ^= 1u << wg;
             };
             auto do_pv = [&](int t) {
-                const int wg = t & 1;
+                const int wg = (t - pc.tb) & 1;
                 const int st = v_it % kVStages;
                 ptx::mbar_wait(v_full + st, (v_it / kVStages) & 1);
                 if (lane == 0) AS_TRACE(3, v_it);
@@ -331,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::mbar_wait(p_full + wg, (p_ph >> wg) & 1);
                 if (lane == 0) AS_TRACE(4, v_it);
-                if (t == 0) ptx::mbar_wait(o_empty, (unit_it & 1) ^ 1);  // both O buffers drained
+                if (t == pc.tb) ptx::mbar_wait(o_empty, (unit_it & 1) ^ 1);  // both O buffers drained
                 ptx::tc_fence_after();
                 __syncwarp();
                 if (p.debug_mode >= 2) {
@@ -344,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int kk = 0; kk < kBN / 16; ++kk) {
                         const uint64_t a = ptx::sw128_desc(p_base + wg * S::P_BYTES + kk * 32, 0, 1024);
                         const uint64_t b = ptx::sw128_desc(v_base + st * S::KV_BYTES + kk * 16 * 128, kBN * 128, 1024);
-                        ptx::mma_bf16_ss(tmem + kOcol + wg * D, a, b, idesc_pv, (t >= 2 || kk > 0) ? 1u : 0u);
+                        ptx::mma_bf16_ss(tmem + kOcol + wg * D, a, b, idesc_pv, (t - pc.tb >= 2 || kk > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(v_empty + st);
                     ptx::mma_commit(p_empty + wg);
@@ -353,11 +514,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ++v_it;
                 p_ph ^= 1u << wg;
             };
-            do_qk(0);
-            if (u.nt > 1) do_qk(1);
-            for (int t = 0; t < u.nt; ++t) {
+            do_qk(pc.tb);
+            if (pc.te - pc.tb > 1) do_qk(pc.tb + 1);
+            for (int t = pc.tb; t < pc.te; ++t) {
                 do_pv(t);
-                if (t + 2 < u.nt) do_qk(t + 2);
+                if (t + 2 < pc.te) do_qk(t + 2);
             }
             if (lane == 0) {
                 if (p.debug_mode >= 2) ptx::mbar_arrive(o_full);
@@ -379,9 +540,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float sl2 = p.scale_log2;
         uint32_t s_cnt = 0, unit_it = 0;
         int tbase = 0;  // CTA-local index of this unit's first tile (trace only)
-        for (int w = blockIdx.x; w < p.n_units; w += gridDim.x) {
-            Unit u;
-            if (!decode_unit(p, w, u)) continue;
+        Sched sc = sched0;
+        Piece pc;
+        while (sched_next(p, sc, pc)) {
+            const Unit& u = pc.u;
             const int G = p.G;
             const int rr = u.mt * kBM + r;
             const bool row_ok = rr < u.K * G;
@@ -407,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             float m_ref = -INFINITY, l_sum = 0.f;
-            for (int t = wg; t < u.nt; t += 2, ++s_cnt) {
+            for (int t = pc.tb + wg; t < pc.te; t += 2, ++s_cnt) {
                 const uint32_t par = s_cnt & 1;
                 ptx::mbar_wait(s_full + wg, par);
                 if (lane == 0 && quad == 0) AS_TRACE(5, tbase + t);
@@ -449,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float m_new = fmaxf(m_ref, tmax);
                 // P buffer wg is free (and O[wg] stable) once PV of this warpgroup's previous tile completed
                 ptx::mbar_wait(p_empty + wg, par ^ 1);
-                if (t >= 2) {
+                if (t - pc.tb >= 2) {
                     const bool need = m_new > m_ref + kRescaleThresh;
                     if (__any_sync(0xffffffffu, need)) {
                         ptx::tc_fence_after();
@@ -508,40 +670,123 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float a0 = (m0 == -INFINITY) ? 0.f : ptx::ex2(m0 - mm);
             const float a1 = (m1 == -INFINITY) ? 0.f : ptx::ex2(m1 - mm);
             const float lt = l0 * a0 + l1 * a1;
-            const float inv = 1.f / lt;
+            const bool full = (pc.tb == 0 && pc.te == u.nt);
+            // full unit: normalise here; partial piece: keep (O, m, l) unnormalised
+            const float inv = full ? 1.f / lt : 1.f;
             const float f0 = a0 * inv, f1 = a1 * inv;
             const size_t orow = (size_t)(u.off + node) * p.n_q + (size_t)u.g * G + hh;
             const uint32_t o0_addr = tmem + lane_addr + kOcol;
             const uint32_t o1_addr = o0_addr + D;
+            const int slot = 2 * blockIdx.x + (pc.x == sk_x0 ? 0 : 1);
+            float* part = p.partial + (size_t)slot * p.slot_floats;  // [128][D] O, then m[128], l[128]
 #pragma unroll
             for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
                 uint32_t oa[32], ob[32];
                 ptx::tmem_ld32(o0_addr + c0, oa);
                 ptx::tmem_ld32(o1_addr + c0, ob);
                 ptx::tmem_ld_wait();
-                if (row_ok) {
-                    uint32_t pk[16];
+                float v[32];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        float v0 = __uint_as_float(oa[2 * j]) * f0, v1 = __uint_as_float(oa[2 * j + 1]) * f0;
-                        if (f1 != 0.f) {  // warpgroup 1 may have had no tile (garbage O[1])
-                            v0 = fmaf(__uint_as_float(ob[2 * j]), f1, v0);
-                            v1 = fmaf(__uint_as_float(ob[2 * j + 1]), f1, v1);
+                for (int j = 0; j < 32; ++j) {
+                    v[j] = __uint_as_float(oa[j]) * f0;
+                    if (f1 != 0.f) v[j] = fmaf(__uint_as_float(ob[j]), f1, v[j]);  // wg 1 may have had no tile
+                }
+                if (full) {
+                    if (row_ok) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+                            pk[j] = *reinterpret_cast<uint32_t*>(&h2);
                         }
-                        __nv_bfloat162 h2 = __floats2bfloat162_rn(v0, v1);
-                        pk[j] = *reinterpret_cast<uint32_t*>(&h2);
-                    }
-                    uint4* dst = reinterpret_cast<uint4*>(p.out + orow * D + c0);
+                        uint4* dst = reinterpret_cast<uint4*>(p.out + orow * D + c0);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+                        for (int j = 0; j < 4; ++j)
+                            dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+                    }
+                } else {
+                    float4* dst = reinterpret_cast<float4*>(part + (size_t)r * D + c0);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                 }
             }
-            if (row_ok && p.lse && wg == 0) p.lse[orow] = (mm + __log2f(lt)) * 0.6931471805599453f;
+            if (full && row_ok && p.lse && wg == 0) p.lse[orow] = (mm + __log2f(lt)) * 0.6931471805599453f;
+            if (!full && wg == 0) {
+                part[128 * D + r] = mm;
+                part[128 * D + 128 + r] = lt;
+            }
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(o_empty);
+            if (!full) {
+                // stream-K fix-up: the CTA that completes the unit's last piece merges
+                // every piece's (O, m, l) (fp32, through L2) and writes the output.
+                __threadfence();
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (warp == 2 && lane == 0) {
+                    const int n = pc.te - pc.tb;
+                    const int old = atomicAdd(p.cnt + pc.w, n);
+                    sk_last = (old + n == u.nt) ? 1 : 0;
+                }
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (sk_last) {
+                    __threadfence();
+                    const long long T = sk_T;
+                    const int Gd = gridDim.x;
+                    const long long U0 = pc.x - pc.tb;
+                    const int b_first = sk_owner(T, Gd, U0), b_last = sk_owner(T, Gd, U0 + u.nt - 1);
+                    float M = -INFINITY;
+                    for (int b = b_first; b <= b_last; ++b) {
+                        const float* pb = p.partial + (size_t)(2 * b + (sk_start(T, b, Gd) < U0 ? 1 : 0)) * p.slot_floats;
+                        M = fmaxf(M, __ldcg(pb + 128 * D + r));
+                    }
+                    float Ltot = 0.f;
+                    for (int b = b_first; b <= b_last; ++b) {
+                        const float* pb = p.partial + (size_t)(2 * b + (sk_start(T, b, Gd) < U0 ? 1 : 0)) * p.slot_floats;
+                        const float mb = __ldcg(pb + 128 * D + r);
+                        if (mb != -INFINITY) Ltot += __ldcg(pb + 128 * D + 128 + r) * ptx::ex2(mb - M);
+                    }
+                    const float invL = 1.f / Ltot;
+#pragma unroll
+                    for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
+                        float acc[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+                        for (int b = b_first; b <= b_last; ++b) {
+                            const float* pb =
+                                p.partial + (size_t)(2 * b + (sk_start(T, b, Gd) < U0 ? 1 : 0)) * p.slot_floats;
+                            const float mb = __ldcg(pb + 128 * D + r);
+                            if (mb == -INFINITY) continue;
+                            const float fb = ptx::ex2(mb - M) * invL;
+                            const float4* src = reinterpret_cast<const float4*>(pb + (size_t)r * D + c0);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const float4 q4 = __ldcg(src + j);
+                                acc[4 * j] = fmaf(q4.x, fb, acc[4 * j]);
+                                acc[4 * j + 1] = fmaf(q4.y, fb, acc[4 * j + 1]);
+                                acc[4 * j + 2] = fmaf(q4.z, fb, acc[4 * j + 2]);
+                                acc[4 * j + 3] = fmaf(q4.w, fb, acc[4 * j + 3]);
+                            }
+                        }
+                        if (row_ok) {
+                            uint32_t pk[16];
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                __nv_bfloat162 h2 = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
+                                pk[j] = *reinterpret_cast<uint32_t*>(&h2);
+                            }
+                            uint4* dst = reinterpret_cast<uint4*>(p.out + orow * D + c0);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+                        }
+                    }
+                    if (row_ok && p.lse && wg == 0) p.lse[orow] = (M + __log2f(Ltot)) * 0.6931471805599453f;
+                    if (warp == 2 && lane == 0) atomicExch(p.cnt + pc.w, 0);  // reusable workspace
+                }
+            }
             ++unit_it;
-            tbase += u.nt;
+            tbase += pc.te - pc.tb;
         }
     }
     ptx::tc_fence_before();

@@ -60,6 +60,10 @@ struct TcParams {
     float* lse;
     void* ws;
     int n_units;
+    int stream_k;         // 1: stream-K tile ranges (needs cnt/partial), 0: static whole units
+    int* cnt;             // [n_units] tiles completed per split unit (zeroed, self-resetting)
+    float* partial;       // [2 * gridDim.x][slot_floats] partial (O, m, l) of split units
+    int slot_floats;      // 128 * D + 256
     int prefetch_tiles;  // L2 prefetch distance of the TMA producers (tiles)
     int debug_mode;  // 0 = normal; 1 = skip softmax math; 2 = also skip MMAs (timing experiments only)
     unsigned long long* trace;  // CTA-0 pipeline timestamps [trace_cap][8] (clock64) or NULL
