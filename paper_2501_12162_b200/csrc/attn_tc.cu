@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const CUtensorMap* tm_t = is_k ? &tm_kt : &tm_vt;
         unsigned char* ring = smem + (is_k ? S::OFF_K : S::OFF_V);
         uint32_t it = 0, unit_it = 0;
-        const uint64_t pol = ptx::policy_evict_first();
+        const uint64_t pol = p.evict_first ? ptx::policy_evict_first() : ptx::policy_evict_normal();
         Sched sc = sched0;
         Piece pc;
         while (sched_next(p, sc, pc)) {
