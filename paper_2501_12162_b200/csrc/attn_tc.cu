@@ -33,8 +33,8 @@ namespace as {
 
 constexpr int kBM = 128;          // query rows per tile (UMMA M)
 constexpr int kBN = 64;           // keys per tile
-constexpr int kKStages = 3;       // K ring depth (released right after QK)
-constexpr int kVStages = 6;       // V ring depth (held until PV)
+constexpr int kKStages = 4;       // K ring depth (released right after QK)
+constexpr int kVStages = 7;       // V ring depth (held until PV)
 constexpr int kVWarp = 10;        // V producer warp
 constexpr int kThreads = 352;     // 11 warps: K/Q TMA, MMA, 2 x 4 softmax, V TMA
 constexpr int kTmemCols = 512;    // S0 [0,64) S1 [64,128) O0 [128,128+D) O1 [128+D, 128+2D)
@@ -49,12 +49,10 @@ struct TcSmem {
     static constexpr int NCH = D / 64;                        // 128-byte swizzle chunks along d
     static constexpr int Q_BYTES = NCH * kBM * 128;           // 16 KB per chunk
     static constexpr int KV_BYTES = NCH * kBN * 128;          // 8 KB per chunk
-    static constexpr int P_BYTES = kBM * kBN * 2;             // 16 KB
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = OFF_Q + Q_BYTES;
     static constexpr int OFF_V = OFF_K + kKStages * KV_BYTES;
-    static constexpr int OFF_P = OFF_V + kVStages * KV_BYTES;
-    static constexpr int OFF_ML = OFF_P + 2 * P_BYTES;        // [2][2][2][128] f32 merge scratch
+    static constexpr int OFF_ML = OFF_V + kVStages * KV_BYTES;  // [2][2][2][128] f32 merge scratch
     static constexpr int OFF_PT = OFF_ML + 2 * 2 * 2 * 128 * 4;   // [2 producers][kPtChunk] staged page-table rows
     static constexpr int OFF_TP = OFF_PT + 2 * kPtChunk * 4;       // [2][AS_MAX_TREE] staged tree parents
     static constexpr int OFF_BAR = OFF_TP + 2 * AS_MAX_TREE * 4;
@@ -434,7 +432,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t q_base = ptx::smem_u32(smem + S::OFF_Q);
         const uint32_t k_base = ptx::smem_u32(smem + S::OFF_K);
         const uint32_t v_base = ptx::smem_u32(smem + S::OFF_V);
-        const uint32_t p_base = ptx::smem_u32(smem + S::OFF_P);
         uint32_t k_it = 0, v_it = 0, unit_it = 0;
         uint32_t s_ph = 0, p_ph = 0;  // bit wg = phase parity of S[wg] / P[wg] uses
         Sched sc = sched0;
@@ -503,9 +500,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else if (lane == 0) {
 #pragma unroll
                     for (int kk = 0; kk < kBN / 16; ++kk) {
-                        const uint64_t a = ptx::sw128_desc(p_base + wg * S::P_BYTES + kk * 32, 0, 1024);
+                        // A = P_t, bf16 pairs packed in the first kBN/2 columns of S[wg] (TMEM)
                         const uint64_t b = ptx::sw128_desc(v_base + st * S::KV_BYTES + kk * 16 * 128, kBN * 128, 1024);
-                        ptx::mma_bf16_ss(tmem + kOcol + wg * D, a, b, idesc_pv, (t - pc.tb >= 2 || kk > 0) ? 1u : 0u);
+                        ptx::mma_bf16_ts(tmem + kOcol + wg * D, tmem + wg * kBN + kk * 8, b, idesc_pv,
+                                         (t - pc.tb >= 2 || kk > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(v_empty + st);
                     ptx::mma_commit(p_empty + wg);
@@ -535,7 +533,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
         const uint32_t s_addr = tmem + lane_addr + wg * kBN;
         const uint32_t o_addr = tmem + lane_addr + kOcol + wg * D;
-        unsigned char* p_row = smem + S::OFF_P + wg * S::P_BYTES + r * 128;
         float* ml = reinterpret_cast<float*>(smem + S::OFF_ML);  // [2 units][2 wg][2 (m,l)][128]
         const float sl2 = p.scale_log2;
         uint32_t s_cnt = 0, unit_it = 0;
@@ -647,13 +644,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pk[c >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                 }
                 l_sum += (rs[0] + rs[1]) + (rs[2] + rs[3]);
-#pragma unroll
-                for (int ch = 0; ch < 8; ++ch) {
-                    const int phys = ch ^ (r & 7);
-                    *reinterpret_cast<uint4*>(p_row + phys * 16) =
-                        make_uint4(pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
-                }
-                ptx::fence_proxy_async_smem();
+                // P_t overwrites the first kBN/2 columns of S[wg] (already in registers);
+                // the PV MMA reads it from TMEM as its A operand.
+                ptx::tmem_st32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(p_full + wg);
                 if (lane == 0 && quad == 0) AS_TRACE(6, tbase + t);

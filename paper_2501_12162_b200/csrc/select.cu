@@ -18,11 +18,13 @@
 //   (5) tree i = root + pi_i[0 : s_i + m_i], emitted in ascending candidate
 //       index (topological; ancestor-closed by App. B).
 //
-// One kernel launch:  every CTA sorts/thresholds 32 requests (one warp each:
-// register bitonic sort with __shfl_xor_sync, lane-uniform fp64 prefix loop);
-// the last CTA to finish (threadfence + ticket) does (3)-(5): rank by A,
-// block scan, an 8-bit-digit radix select over the 64-bit tail keys with
-// warp-aggregated shared-memory histograms, ballot counts, and the emit.
+// One cooperative kernel launch:  every CTA sorts/thresholds 32 requests (one
+// warp each: register bitonic sort with __shfl_xor_sync, lane-uniform fp64
+// prefix loop); the last CTA to finish (threadfence + ticket) does (3)-(4):
+// rank by A, block scan, an 8-bit-digit radix select over the 64-bit tail keys
+// with warp-aggregated shared-memory histograms, ballot counts and the tree
+// offsets; it then releases a generation flag and every CTA emits (5) its own
+// 32 trees in parallel.
 #include "common.cuh"
 
 namespace as {
@@ -231,23 +233,23 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
         }
     }
     __syncthreads();
+    WsHeader* hdr = reinterpret_cast<WsHeader*>(p.ws);
+    __shared__ unsigned s_gen0;
     if (threadIdx.x == 0) {
+        s_gen0 = *reinterpret_cast<volatile unsigned*>(&hdr->pad[0]);  // generation before arriving
         __threadfence();
-        WsHeader* h = reinterpret_cast<WsHeader*>(p.ws);
-        unsigned t = atomicAdd(&h->ticket, 1u);
+        unsigned t = atomicAdd(&hdr->ticket, 1u);
         s_is_last = (t == gridDim.x - 1);
+        if (s_is_last) atomicExch(&hdr->ticket, 0u);  // everyone has arrived: reusable
     }
     __syncthreads();
-    if (!s_is_last) return;
+    if (s_is_last) {
     __threadfence();
 
     // ---- phase 2 (last CTA) ----
     double* A_s = reinterpret_cast<double*>(smem_raw);                    // [n]
     int* ord_s = reinterpret_cast<int*>(A_s + n);                         // [n] desired in A order -> cum
     int* rank_s = ord_s + n;                                              // [n]
-    int* remap_all = rank_s + n;                                          // [32][kRemapWords]
-    unsigned* bitmap_all = reinterpret_cast<unsigned*>(remap_all + kSelWarps * kRemapWords);  // [32][kBitmapWords]
-    int* parent_all = reinterpret_cast<int*>(bitmap_all + kSelWarps * kBitmapWords);          // [32][kRemapWords]
 
     for (int i = threadIdx.x; i < n; i += kSelThreads) A_s[i] = p.A[i];
     __syncthreads();
@@ -380,18 +382,32 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
         p.tree_offsets[i] = ord_s[i];
     }
     if (threadIdx.x == 0) p.tree_offsets[n] = used;
-    __threadfence_block();
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(&hdr->pad[0], 1u);  // release phase 3 in every CTA
+    }  // last CTA
+    // ---- phase 3 (every CTA, its own 32 requests): wait for the global phase ----
+    if (threadIdx.x == 0) {
+        while (*reinterpret_cast<volatile unsigned*>(&hdr->pad[0]) == s_gen0) __nanosleep(64);
+        __threadfence();
+    }
     __syncthreads();
 
     // (5) emit: warp per request.
+    double* A_s2 = reinterpret_cast<double*>(smem_raw);
+    int* remap_all = reinterpret_cast<int*>(A_s2 + n) + 2 * n;                                 // [32][kRemapWords]
+    unsigned* bitmap_all = reinterpret_cast<unsigned*>(remap_all + kSelWarps * kRemapWords);  // [32][kBitmapWords]
+    int* parent_all = reinterpret_cast<int*>(bitmap_all + kSelWarps * kBitmapWords);          // [32][kRemapWords]
     int* remap = remap_all + warp_id() * kRemapWords;
     unsigned* bits = bitmap_all + warp_id() * kBitmapWords;
     int* cpar = parent_all + warp_id() * kRemapWords;
-    for (int i = warp_id(); i < n; i += kSelWarps) {
+    {
+        const int i = blockIdx.x * kSelWarps + (int)warp_id();
+        if (i < n) {
         int off;
         const int nr = n_nonroot(p, i, &off);
         const int take = __ldcg(p.take + i);
-        const int tbase = ord_s[i];
+        const int tbase = __ldcg(p.tree_offsets + i);
         const int sbase = off - i;
         for (int w = lane; w < kBitmapWords; w += 32) bits[w] = 0u;
         for (int c = lane; c <= nr; c += 32) cpar[c] = p.cand_parent[off + c];  // staged: depth walks stay on chip
@@ -439,10 +455,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
             }
         }
         __syncwarp();
-    }
-    if (threadIdx.x == 0) {
-        WsHeader* h = reinterpret_cast<WsHeader*>(p.ws);
-        atomicExch(&h->ticket, 0u);  // reusable workspace
+        }
     }
 }
 
@@ -494,7 +507,19 @@ int launch_select(int n_req, int n_cand_total, const int32_t* cand_offsets, cons
             cudaSuccess)
         return -1;
     const int grid = (n_req + kSelWarps - 1) / kSelWarps;
-    select_trees_kernel<<<grid, kSelThreads, smem, stream>>>(p);
+    // cooperative launch: every CTA waits for the global phase run by the last
+    // one to arrive, so all CTAs must be co-resident (grid <= 128 CTAs)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kSelThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, select_trees_kernel, p) != cudaSuccess) return -1;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
