@@ -234,6 +234,10 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     p.prefetch_tiles = pf ? atoi(pf) : 0;
     const char* ef = getenv("AS_ATTN_EVICT_FIRST");  // A/B: L2 evict-first hint on KV loads
     p.evict_first = ef ? atoi(ef) : 1;
+    const char* ig = getenv("AS_ATTN_ISSUE_GROUP");  // A/B: TMA ops issued per warp instruction
+    p.issue_group = ig ? atoi(ig) : 2;
+    if (p.issue_group < 1) p.issue_group = 1;
+    if (p.issue_group > 4) p.issue_group = 4;
     const char* tr = getenv("AS_ATTN_TRACE");  // CTA-0 pipeline timestamps into the workspace (debug)
     p.trace = nullptr;
     p.trace_cap = 0;

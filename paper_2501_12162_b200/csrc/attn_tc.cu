@@ -369,30 +369,37 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tma_prefetch_4d(tm_t, 0, u.off + (tp - u.n_prefix) * kBN, 0, u.g);
                 }
             };
-            for (int t = pc.tb; t < pc.te; ++t, ++it) {
-                const int st = it % n_st;
-                const uint32_t ph = (it / n_st) & 1;
-                unsigned char* dst = ring + st * S::KV_BYTES;
-                if (t < u.n_prefix) {
-                    const int key0 = t * kBN;
-                    const int pg_first = key0 / p.page_size;
-                    const int pg_last = (min(key0 + kBN, u.L) - 1) / p.page_size;
-                    if (chunk0 < 0 || pg_last >= chunk0 + kPtChunk) {  // warp-uniform
+            // Tiles are issued in groups of `grp` (lanes 0..grp-1 issue one tile each
+            // in the same warp instructions): several TMA operations per issue slot.
+            const int grp = p.issue_group;
+            for (int t0 = pc.tb; t0 < pc.te; t0 += grp) {
+                const int nt_here = min(grp, pc.te - t0);
+                if (t0 < u.n_prefix) {  // stage page-table entries covering the group (warp-uniform)
+                    const int tp_last = min(t0 + nt_here - 1, u.n_prefix - 1);
+                    const int pg_first = t0 * kBN / p.page_size;
+                    const int pg_last = (min(tp_last * kBN + kBN, u.L) - 1) / p.page_size;
+                    if (chunk0 < 0 || pg_first < chunk0 || pg_last >= chunk0 + kPtChunk) {
                         chunk0 = pg_first;
                         __syncwarp();
                         for (int k = lane; k < kPtChunk && chunk0 + k < n_pages_u; k += 32)
                             pt_s[k] = __ldg(p.page_table + (size_t)u.i * p.max_pages + chunk0 + k);
                         __syncwarp();
-                        if (lane == 0 && t == pc.tb)
-                            for (int tp = t + 1; tp <= t + p.prefetch_tiles && tp < pc.te; ++tp) prefetch(tp);
                     }
-                    if (lane == 0) {
+                }
+                if (lane < nt_here) {
+                    const int t = t0 + lane;
+                    const uint32_t myit = it + lane;
+                    const int st = myit % n_st;
+                    const uint32_t ph = (myit / n_st) & 1;
+                    unsigned char* dst = ring + st * S::KV_BYTES;
+                    if (t < u.n_prefix) {
                         prefetch(t + 1 + p.prefetch_tiles);
+                        const int key0 = t * kBN;
                         const int valid = min(kBN, u.L - key0);
                         const int nbox = (valid + p.box_rows - 1) / p.box_rows;
                         const uint32_t bytes = (uint32_t)(nbox * NCH * p.box_rows * 128);
                         ptx::mbar_wait(empty + st, ph ^ 1);
-                        AS_TRACE(is_k ? 0 : 1, it);
+                        AS_TRACE(is_k ? 0 : 1, myit);
                         ptx::mbar_arrive_expect_tx(full + st, bytes);
                         for (int b = 0; b < nbox; ++b) {
                             const int kp = key0 + b * p.box_rows;
@@ -409,15 +416,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                           c * 64, slot, u.g, page, pol);
                             }
                         }
+                    } else {
+                        prefetch(t + 1 + p.prefetch_tiles);
+                        const int row0 = u.off + (t - u.n_prefix) * kBN;
+                        ptx::mbar_wait(empty + st, ph ^ 1);
+                        AS_TRACE(is_k ? 0 : 1, myit);
+                        ptx::mbar_arrive_expect_tx(full + st, (uint32_t)(NCH * kBN * 128));
+                        ptx::tma_load_4d(dst, tm_t, full + st, 0, row0, 0, u.g);
                     }
-                } else if (lane == 0) {
-                    prefetch(t + 1 + p.prefetch_tiles);
-                    const int row0 = u.off + (t - u.n_prefix) * kBN;
-                    ptx::mbar_wait(empty + st, ph ^ 1);
-                    AS_TRACE(is_k ? 0 : 1, it);
-                    ptx::mbar_arrive_expect_tx(full + st, (uint32_t)(NCH * kBN * 128));
-                    ptx::tma_load_4d(dst, tm_t, full + st, 0, row0, 0, u.g);
                 }
+                __syncwarp();
+                it += nt_here;
             }
             ++unit_it;
         }
