@@ -47,6 +47,8 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, 
     return res == CUDA_SUCCESS;
 }
 
+constexpr int kMaxKLead = 3;  // must stay < the K ring depth
+
 int sm_count() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 148;
@@ -234,10 +236,10 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     p.prefetch_tiles = pf ? atoi(pf) : 0;
     const char* ef = getenv("AS_ATTN_EVICT_FIRST");  // A/B: L2 evict-first hint on KV loads
     p.evict_first = ef ? atoi(ef) : 1;
-    const char* ig = getenv("AS_ATTN_ISSUE_GROUP");  // A/B: TMA ops issued per warp instruction
-    p.issue_group = ig ? atoi(ig) : 2;
-    if (p.issue_group < 1) p.issue_group = 1;
-    if (p.issue_group > 4) p.issue_group = 4;
+    const char* kl = getenv("AS_ATTN_KLEAD");  // tuning: K stream lead over V (tiles)
+    p.k_lead = kl ? atoi(kl) : 2;
+    if (p.k_lead < 0) p.k_lead = 0;
+    if (p.k_lead > kMaxKLead) p.k_lead = kMaxKLead;
     const char* tr = getenv("AS_ATTN_TRACE");  // CTA-0 pipeline timestamps into the workspace (debug)
     p.trace = nullptr;
     p.trace_cap = 0;

@@ -35,8 +35,7 @@ constexpr int kBM = 128;          // query rows per tile (UMMA M)
 constexpr int kBN = 64;           // keys per tile
 constexpr int kKStages = 4;       // K ring depth (released right after QK)
 constexpr int kVStages = 7;       // V ring depth (held until PV)
-constexpr int kVWarp = 10;        // V producer warp
-constexpr int kThreads = 352;     // 11 warps: K/Q TMA, MMA, 2 x 4 softmax, V TMA
+constexpr int kThreads = 320;     // 10 warps: TMA producer, MMA, 2 x 4 softmax
 constexpr int kTmemCols = 512;    // S0 [0,64) S1 [64,128) O0 [128,128+D) O1 [128+D, 128+2D)
 constexpr int kOcol = 128;
 constexpr int kPtChunk = 512;     // page-table entries staged per refill
@@ -53,8 +52,8 @@ struct TcSmem {
     static constexpr int OFF_K = OFF_Q + Q_BYTES;
     static constexpr int OFF_V = OFF_K + kKStages * KV_BYTES;
     static constexpr int OFF_ML = OFF_V + kVStages * KV_BYTES;  // [2][2][2][128] f32 merge scratch
-    static constexpr int OFF_PT = OFF_ML + 2 * 2 * 2 * 128 * 4;   // [2 producers][kPtChunk] staged page-table rows
-    static constexpr int OFF_TP = OFF_PT + 2 * kPtChunk * 4;       // [2][AS_MAX_TREE] staged tree parents
+    static constexpr int OFF_PT = OFF_ML + 2 * 2 * 2 * 128 * 4;   // [kPtChunk] staged page-table row
+    static constexpr int OFF_TP = OFF_PT + kPtChunk * 4;           // [2][AS_MAX_TREE] staged tree parents
     static constexpr int OFF_BAR = OFF_TP + 2 * AS_MAX_TREE * 4;
     static constexpr int N_BAR = 2 + 2 * kKStages + 2 * kVStages + 8 + 2;
     static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
@@ -312,72 +311,42 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
 
-    if (warp == 0 || warp == kVWarp) {
-        // ===================== TMA producers (whole warps) =====================
-        // warp 0 loads Q and the K tiles, warp kVWarp the V tiles, each through its
-        // own ring (K: short residence, released by QK; V: held until PV), so K
-        // runs ahead independently of V-slot availability.  Lane 0 issues every
-        // TMA; at each unit start (and every kPtChunk pages) the 32 lanes stage
-        // the request's page-table row in shared memory, so no global load sits on
+    if (warp == 0) {
+        // ===================== TMA producer (whole warp) =====================
+        // One warp issues Q and every K/V tile in CONSUMPTION order -- K_{t+lead}
+        // together with V_t, as two lanes of the same warp instructions -- so the
+        // per-SM TMA queue (which serves operations roughly in order at a bounded
+        // rate) never holds far-ahead V tiles in front of K tiles the MMA needs
+        // next.  At each unit start (and every kPtChunk pages) the 32 lanes stage
+        // the request's page-table row in shared memory: no global load sits on
         // the per-tile issue path.
-        const bool is_k = warp == 0;
-        int* pt_s = reinterpret_cast<int*>(smem + S::OFF_PT) + (is_k ? 0 : kPtChunk);
-        const int n_st = is_k ? kKStages : kVStages;
-        uint64_t* full = is_k ? k_full : v_full;
-        uint64_t* empty = is_k ? k_empty : v_empty;
-        const CUtensorMap* tm_c = is_k ? &tm_kc : &tm_vc;
-        const CUtensorMap* tm_t = is_k ? &tm_kt : &tm_vt;
-        unsigned char* ring = smem + (is_k ? S::OFF_K : S::OFF_V);
-        uint32_t it = 0, unit_it = 0;
+        int* pt_s = reinterpret_cast<int*>(smem + S::OFF_PT);
+        uint32_t itk = 0, itv = 0, unit_it = 0;
         const uint64_t pol = p.evict_first ? ptx::policy_evict_first() : ptx::policy_evict_normal();
+        const int lead = p.k_lead;
         Sched sc = sched0;
         Piece pc;
         while (sched_next(p, sc, pc)) {
             const Unit& u = pc.u;
-            if (is_k && lane == 0 && u.mt == 0 && u.g == 0 && __ldg(p.kv_len + u.i) > p.max_pages * p.page_size)
+            if (lane == 0 && u.mt == 0 && u.g == 0 && __ldg(p.kv_len + u.i) > p.max_pages * p.page_size)
                 set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, u.i);
             const int n_pages_u = (u.L + p.page_size - 1) / p.page_size;
             int chunk0 = -1;  // first page index currently staged
-            if (is_k && lane == 0) {
+            if (lane == 0) {
                 ptx::mbar_wait(q_empty, (unit_it & 1) ^ 1);
                 ptx::mbar_arrive_expect_tx(q_full, S::Q_BYTES);
                 const int node0 = u.off + u.mt * (kBM / p.G);
                 ptx::tma_load_4d(smem + S::OFF_Q, &tm_q, q_full, 0, u.g * p.G, node0, 0);
             }
-            // L2 prefetch of tile tp of this unit (no smem; hides DRAM latency beyond
-            // what the rings cover).  Only tiles whose page entries are staged.
-            auto prefetch = [&](int tp) {
-                if (tp >= pc.te) return;
-                if (tp < u.n_prefix) {
-                    const int key0 = tp * kBN;
-                    const int valid = min(kBN, u.L - key0);
-                    const int nbox = (valid + p.box_rows - 1) / p.box_rows;
-                    for (int b = 0; b < nbox; ++b) {
-                        const int kp = key0 + b * p.box_rows;
-                        const int pi = kp / p.page_size - chunk0;
-                        if (pi < 0 || pi >= kPtChunk) return;
-                        const int page = pt_s[pi];
-                        const int slot = kp % p.page_size;
-                        if (p.kv_split_d) {
-                            ptx::tma_prefetch_5d(tm_c, 0, slot, 0, u.g, page);
-                        } else {
-#pragma unroll
-                            for (int c = 0; c < NCH; ++c) ptx::tma_prefetch_4d(tm_c, c * 64, slot, u.g, page);
-                        }
-                    }
-                } else {
-                    ptx::tma_prefetch_4d(tm_t, 0, u.off + (tp - u.n_prefix) * kBN, 0, u.g);
-                }
-            };
-            // Tiles are issued in groups of `grp` (lanes 0..grp-1 issue one tile each
-            // in the same warp instructions): several TMA operations per issue slot.
-            const int grp = p.issue_group;
-            for (int t0 = pc.tb; t0 < pc.te; t0 += grp) {
-                const int nt_here = min(grp, pc.te - t0);
-                if (t0 < u.n_prefix) {  // stage page-table entries covering the group (warp-uniform)
-                    const int tp_last = min(t0 + nt_here - 1, u.n_prefix - 1);
-                    const int pg_first = t0 * kBN / p.page_size;
-                    const int pg_last = (min(tp_last * kBN + kBN, u.L) - 1) / p.page_size;
+            const int n = pc.te - pc.tb;
+            for (int j = 0; j < n + lead; ++j) {
+                const int tk = pc.tb + j;         // K tile issued at this step (lane 0)
+                const int tv = pc.tb + j - lead;  // V tile issued at this step (lane 1)
+                // stage page-table entries covering both tiles (warp-uniform)
+                const int tlo = max(tv, pc.tb), thi = min(tk, pc.te - 1);
+                if (tlo < u.n_prefix) {
+                    const int pg_first = tlo * kBN / p.page_size;
+                    const int pg_last = (min(min(thi, u.n_prefix - 1) * kBN + kBN, u.L) - 1) / p.page_size;
                     if (chunk0 < 0 || pg_first < chunk0 || pg_last >= chunk0 + kPtChunk) {
                         chunk0 = pg_first;
                         __syncwarp();
@@ -386,21 +355,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __syncwarp();
                     }
                 }
-                if (lane < nt_here) {
-                    const int t = t0 + lane;
-                    const uint32_t myit = it + lane;
+                const bool is_k = lane == 0;
+                const int t = is_k ? tk : tv;
+                if (lane < 2 && t >= pc.tb && t < pc.te) {
+                    const uint32_t myit = is_k ? itk : itv;
+                    const int n_st = is_k ? kKStages : kVStages;
                     const int st = myit % n_st;
                     const uint32_t ph = (myit / n_st) & 1;
-                    unsigned char* dst = ring + st * S::KV_BYTES;
+                    uint64_t* full = (is_k ? k_full : v_full) + st;
+                    uint64_t* empty = (is_k ? k_empty : v_empty) + st;
+                    unsigned char* dst = smem + (is_k ? S::OFF_K : S::OFF_V) + st * S::KV_BYTES;
                     if (t < u.n_prefix) {
-                        prefetch(t + 1 + p.prefetch_tiles);
+                        const CUtensorMap* tm_c = is_k ? &tm_kc : &tm_vc;
                         const int key0 = t * kBN;
                         const int valid = min(kBN, u.L - key0);
                         const int nbox = (valid + p.box_rows - 1) / p.box_rows;
                         const uint32_t bytes = (uint32_t)(nbox * NCH * p.box_rows * 128);
-                        ptx::mbar_wait(empty + st, ph ^ 1);
+                        ptx::mbar_wait(empty, ph ^ 1);
                         AS_TRACE(is_k ? 0 : 1, myit);
-                        ptx::mbar_arrive_expect_tx(full + st, bytes);
+                        ptx::mbar_arrive_expect_tx(full, bytes);
                         for (int b = 0; b < nbox; ++b) {
                             const int kp = key0 + b * p.box_rows;
                             const int page = pt_s[kp / p.page_size - chunk0];
@@ -408,25 +381,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // out-of-range pages read as zeros (TMA bounds check); flag them
                             if (is_k && (page < 0 || page >= p.num_pages)) set_dev_error(p.ws, AS_DEV_BAD_PAGE, u.i);
                             if (p.kv_split_d) {
-                                ptx::tma_load_5d_hint(dst, tm_c, full + st, 0, slot, 0, u.g, page, pol);
+                                ptx::tma_load_5d_hint(dst, tm_c, full, 0, slot, 0, u.g, page, pol);
                             } else {
 #pragma unroll
                                 for (int c = 0; c < NCH; ++c)
-                                    ptx::tma_load_4d_hint(dst + c * kBN * 128 + b * p.box_rows * 128, tm_c, full + st,
+                                    ptx::tma_load_4d_hint(dst + c * kBN * 128 + b * p.box_rows * 128, tm_c, full,
                                                           c * 64, slot, u.g, page, pol);
                             }
                         }
                     } else {
-                        prefetch(t + 1 + p.prefetch_tiles);
+                        const CUtensorMap* tm_t = is_k ? &tm_kt : &tm_vt;
                         const int row0 = u.off + (t - u.n_prefix) * kBN;
-                        ptx::mbar_wait(empty + st, ph ^ 1);
+                        ptx::mbar_wait(empty, ph ^ 1);
                         AS_TRACE(is_k ? 0 : 1, myit);
-                        ptx::mbar_arrive_expect_tx(full + st, (uint32_t)(NCH * kBN * 128));
-                        ptx::tma_load_4d(dst, tm_t, full + st, 0, row0, 0, u.g);
+                        ptx::mbar_arrive_expect_tx(full, (uint32_t)(NCH * kBN * 128));
+                        ptx::tma_load_4d(dst, tm_t, full, 0, row0, 0, u.g);
                     }
                 }
                 __syncwarp();
-                it += nt_here;
+                if (tk < pc.te) ++itk;
+                if (tv >= pc.tb && tv < pc.te) ++itv;
             }
             ++unit_it;
         }

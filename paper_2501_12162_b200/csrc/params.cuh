@@ -66,7 +66,7 @@ struct TcParams {
     int slot_floats;      // 128 * D + 256
     int prefetch_tiles;
     int evict_first;
-    int issue_group;      // tiles issued per producer warp instruction (lanes 0..n-1)      // L2 evict-first policy on the KV tile loads  // L2 prefetch distance of the TMA producers (tiles)
+    int k_lead;           // tiles by which the K stream leads the V stream in the producer      // L2 evict-first policy on the KV tile loads  // L2 prefetch distance of the TMA producers (tiles)
     int debug_mode;  // 0 = normal; 1 = skip softmax math; 2 = also skip MMAs (timing experiments only)
     unsigned long long* trace;  // CTA-0 pipeline timestamps [trace_cap][8] (clock64) or NULL
     int trace_cap;

@@ -33,9 +33,9 @@ d=json.loads(sys.stdin.read()); r=d['roofline']
 print('${CFG:-c2} $TAG', 'attn_ms', r['attn_ms'], 'GB/s', r['achieved'], 'frac', r['frac'], 'step_ms', d['ms_per_step'], 'bd', d['breakdown_ms'])"
 }
 for CFG in ${CFGS:-c2}; do
-for IG in 1 2 4; do
-TAG="group$IG" AS_ATTN_ISSUE_GROUP=$IG one
-TAG="group${IG}_mode2" AS_ATTN_ISSUE_GROUP=$IG AS_ATTN_DEBUG_MODE=2 one
+for KL in 1 2 3; do
+TAG="klead$KL" AS_ATTN_KLEAD=$KL one
 done
+TAG="mode2" AS_ATTN_DEBUG_MODE=2 one
 TAG="streamk0" AS_ATTN_STREAMK=0 one
 done
