@@ -36,8 +36,9 @@ constexpr int kBN = 64;           // keys per tile
 constexpr int kKStages = 4;       // K ring depth (released right after QK)
 constexpr int kVStages = 7;       // V ring depth (held until PV)
 constexpr int kThreads = 320;     // 10 warps: TMA producer, MMA, 2 x 4 softmax
-constexpr int kTmemCols = 512;    // S0 [0,64) S1 [64,128) O0 [128,128+D) O1 [128+D, 128+2D)
-constexpr int kOcol = 128;
+constexpr int kTmemCols = 512;    // S0 [0,64) S1 [64,128) P0 [128,160) P1 [160,192) O0 [256,256+D) O1 [256+D,256+2D)
+constexpr int kPcol = 128;        // P (bf16 pairs) of warpgroup w at kPcol + 32 w
+constexpr int kOcol = 256;
 constexpr int kPtChunk = 512;     // page-table entries staged per refill
 constexpr int kPlanCap = 12288;   // stream-K plan entries (long long) that fit in the V ring scratch
 constexpr float kRescaleThresh = 8.0f;  // log2 units
@@ -408,8 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===================== MMA issuer =====================
         // Softmax warpgroup w (0/1) owns the tiles t = w (mod 2) of every unit, with
         // its own TMEM S buffer S[w], smem P buffer P[w] and TMEM accumulator O[w].
-        // Issue order per unit: QK0 QK1 | PV0 QK2 | PV1 QK3 | ... so that S_{t+2}
-        // is computed while warpgroup w^1 runs the softmax of tile t+1.
+        // Issue order per piece: QK0 QK1 | QK2 PV0 | QK3 PV1 | ...
         constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(kBM, kBN, 0);
         constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(kBM, D, 1);
         const uint32_t q_base = ptx::smem_u32(smem + S::OFF_Q);
@@ -483,9 +483,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else if (lane == 0) {
 #pragma unroll
                     for (int kk = 0; kk < kBN / 16; ++kk) {
-                        // A = P_t, bf16 pairs packed in the first kBN/2 columns of S[wg] (TMEM)
+                        // A = P_t: bf16 pairs in TMEM columns kPcol + 32 wg (its own region, so
+                        // QK_{t+2} may overwrite S[wg] before PV_t runs)
                         const uint64_t b = ptx::sw128_desc(v_base + st * S::KV_BYTES + kk * 16 * 128, kBN * 128, 1024);
-                        ptx::mma_bf16_ts(tmem + kOcol + wg * D, tmem + wg * kBN + kk * 8, b, idesc_pv,
+                        ptx::mma_bf16_ts(tmem + kOcol + wg * D, tmem + kPcol + wg * (kBN / 2) + kk * 8, b, idesc_pv,
                                          (t - pc.tb >= 2 || kk > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(v_empty + st);
@@ -495,11 +496,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ++v_it;
                 p_ph ^= 1u << wg;
             };
+            // QK_{t+2} is issued as soon as warpgroup wg has READ S_t (start of its
+            // softmax), PV_t when P_t is written: each warpgroup finds its next S
+            // ready when it finishes a tile.
             do_qk(pc.tb);
             if (pc.te - pc.tb > 1) do_qk(pc.tb + 1);
             for (int t = pc.tb; t < pc.te; ++t) {
-                do_pv(t);
                 if (t + 2 < pc.te) do_qk(t + 2);
+                do_pv(t);
             }
             if (lane == 0) {
                 if (p.debug_mode >= 2) ptx::mbar_arrive(o_full);
@@ -627,9 +631,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pk[c >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                 }
                 l_sum += (rs[0] + rs[1]) + (rs[2] + rs[3]);
-                // P_t overwrites the first kBN/2 columns of S[wg] (already in registers);
-                // the PV MMA reads it from TMEM as its A operand.
-                ptx::tmem_st32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+                // P_t goes to this warpgroup's TMEM P region; the PV MMA reads it as A.
+                ptx::tmem_st32(tmem + lane_addr + kPcol + wg * (kBN / 2), *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
