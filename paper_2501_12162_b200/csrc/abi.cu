@@ -47,7 +47,7 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, 
     return res == CUDA_SUCCESS;
 }
 
-constexpr int kMaxKLead = 3;  // must stay < the K ring depth
+constexpr int kMaxKLead = 1;  // must stay < the K ring depth (2)
 
 int sm_count() {
     int dev = 0;
@@ -134,7 +134,8 @@ size_t as_attn_workspace_size(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     // for every GQA ratio) + 2 partial-state slots per SM
     const size_t units = (size_t)n_q_heads * (size_t)n_req;
     const size_t slot = ((size_t)128 * head_dim + 256) * 4;
-    return kWsHeaderBytes + kAttnTraceBytes + align_up(units * 4, 256) + 2 * (size_t)sm_count() * slot;
+    return kWsHeaderBytes + kAttnTraceBytes + align_up(units * 4, 256) +
+           2 * (size_t)sm_count() * (size_t)tc_ctas_per_sm() * slot;
 }
 
 as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows, int32_t n_q_heads,
@@ -222,7 +223,7 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
         const int nsm = sm_count();
         const size_t slot = ((size_t)128 * head_dim + 256) * 4;
         const size_t cnt_bytes = align_up((size_t)p.n_units * 4, 256);
-        const size_t need = kWsHeaderBytes + kAttnTraceBytes + cnt_bytes + 2 * (size_t)nsm * slot;
+        const size_t need = kWsHeaderBytes + kAttnTraceBytes + cnt_bytes + 2 * (size_t)nsm * tc_ctas_per_sm() * slot;
         unsigned char* base = reinterpret_cast<unsigned char*>(workspace) + kWsHeaderBytes + kAttnTraceBytes;
         const char* skenv = getenv("AS_ATTN_STREAMK");  // A/B switch (debug)
         p.stream_k = (workspace_bytes >= need && !(skenv && atoi(skenv) == 0)) ? 1 : 0;
@@ -237,7 +238,7 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     const char* ef = getenv("AS_ATTN_EVICT_FIRST");  // A/B: L2 evict-first hint on KV loads
     p.evict_first = ef ? atoi(ef) : 1;
     const char* kl = getenv("AS_ATTN_KLEAD");  // tuning: K stream lead over V (tiles)
-    p.k_lead = kl ? atoi(kl) : 2;
+    p.k_lead = kl ? atoi(kl) : 1;
     if (p.k_lead < 0) p.k_lead = 0;
     if (p.k_lead > kMaxKLead) p.k_lead = kMaxKLead;
     const char* tr = getenv("AS_ATTN_TRACE");  // CTA-0 pipeline timestamps into the workspace (debug)

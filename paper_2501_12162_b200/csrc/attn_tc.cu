@@ -6,26 +6,28 @@
 // all K_i nodes form Q rows r = node*G + hh, so one kv head's keys are read
 // from HBM once for all G*K_i rows (c2: 4*32 = 128 rows = one UMMA M tile).
 //
-// Structure (persistent, one 192-thread CTA per SM, static unit schedule):
-//   warp 0      TMA producer: Q tile (3-D map, box 64 x G x 128/G, SW128) and
-//               K/V tiles of 64 keys, one 4-D box per page fragment
-//               [d 64 x page rows x 1 head x 1 page] through the page table,
-//               or from k_tree/v_tree (3-D map) for the tree tile(s);
-//               4-stage K and V rings, mbarrier complete_tx.
+// Structure: persistent, TWO 192-thread CTAs per SM (measured: one CTA's TMA
+// stream tops out near 4.7 TB/s chip-wide with 16 KB operations, two CTAs per
+// SM reach 6.5-6.9 TB/s -- DESIGN.md §5), stream-K tile schedule.
+//   warp 0      TMA producer: Q tile (4-D map, box 64 x G x 128/G x 2 chunks,
+//               SW128) and 64-key K/V tiles (5-D map over [page][head][row]
+//               [chunk][64] -> one 16 KB box per tile, coordinates from the
+//               page-table row staged in shared memory; k_tree/v_tree for the
+//               tree tile).  K_{t+1} and V_t are issued by two lanes of the
+//               same instructions (consumption order).  2+2-stage rings.
 //   warp 1      TMEM owner + single-thread tcgen05.mma issuer:
-//               S_t = Q K_t^T  (M=128, N=64, K=d; both K-major SW128) into one of
-//               two TMEM S buffers; O += P_t V_t (M=128, N=d, K=64; P K-major,
-//               V MN-major SW128) into the TMEM O accumulator.  QK_{t+1} is
-//               issued before PV_t so softmax(t+1) overlaps PV_t.
+//               S_t = Q K_t^T (M=128, N=64, K=d; SS, both K-major SW128) into
+//               TMEM; O += P_t V_t (M=128, N=d, K=64; A = P from TMEM, V
+//               MN-major SW128).  QK_{t+1} is issued as soon as the softmax has
+//               read S_t, PV_t as soon as P_t is written.
 //   warps 2-5   softmax + epilogue, one TMEM lane (= Q row) per thread:
 //               tcgen05.ld S -> mask (prefix length / ancestor bitmask) ->
 //               online softmax in the log2 domain with lazy O rescaling
 //               (only when the running max grows by > 8, i.e. 256x) ->
-//               P (bf16) written to shared memory in the SW128 K-major layout
-//               -> fence.proxy.async -> PV.  Epilogue: tcgen05.ld O, * 1/l,
-//               bf16 store, optional natural-log LSE.
-// Units: (q-tile mt, request i, kv head g), mt slowest so that the non-empty
-// units are spread round-robin over the SMs.
+//               P (bf16 pairs) tcgen05.st to TMEM -> PV.  Epilogue:
+//               tcgen05.ld O, * 1/l, bf16 store, optional natural-log LSE; or,
+//               for a unit split across CTAs, the fp32 partial (O, m, l) and
+//               the stream-K fix-up by the CTA that completes the unit.
 #include "params.cuh"
 #include "tc_ptx.cuh"
 
@@ -33,16 +35,16 @@ namespace as {
 
 constexpr int kBM = 128;          // query rows per tile (UMMA M)
 constexpr int kBN = 64;           // keys per tile
-constexpr int kKStages = 4;       // K ring depth (released right after QK)
-constexpr int kVStages = 7;       // V ring depth (held until PV)
-constexpr int kThreads = 320;     // 10 warps: TMA producer, MMA, 2 x 4 softmax
-constexpr int kTmemCols = 512;    // S0 [0,64) S1 [64,128) P0 [128,160) P1 [160,192) O0 [256,256+D) O1 [256+D,256+2D)
-constexpr int kPcol = 128;        // P (bf16 pairs) of warpgroup w at kPcol + 32 w
-constexpr int kOcol = 256;
-constexpr int kPtChunk = 512;     // page-table entries staged per refill
-constexpr int kPlanCap = 12288;   // stream-K plan entries (long long) that fit in the V ring scratch
+constexpr int kKStages = 2;       // K ring depth (released right after QK)
+constexpr int kVStages = 2;       // V ring depth (held until PV)
+constexpr int kThreads = 192;     // 6 warps: TMA producer, MMA, 4 softmax
+constexpr int kCtasPerSm = 2;
+constexpr int kTmemCols = 256;    // S [0,64) P [64,96) O [128,128+D)
+constexpr int kScol = 0;
+constexpr int kPcol = 64;
+constexpr int kOcol = 128;
+constexpr int kPtChunk = 256;     // page-table entries staged per refill
 constexpr float kRescaleThresh = 8.0f;  // log2 units
-
 
 template <int D>
 struct TcSmem {
@@ -52,14 +54,15 @@ struct TcSmem {
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = OFF_Q + Q_BYTES;
     static constexpr int OFF_V = OFF_K + kKStages * KV_BYTES;
-    static constexpr int OFF_ML = OFF_V + kVStages * KV_BYTES;  // [2][2][2][128] f32 merge scratch
-    static constexpr int OFF_PT = OFF_ML + 2 * 2 * 2 * 128 * 4;   // [kPtChunk] staged page-table row
+    static constexpr int OFF_PT = OFF_V + kVStages * KV_BYTES;     // [kPtChunk] staged page-table row
     static constexpr int OFF_TP = OFF_PT + kPtChunk * 4;           // [2][AS_MAX_TREE] staged tree parents
     static constexpr int OFF_BAR = OFF_TP + 2 * AS_MAX_TREE * 4;
-    static constexpr int N_BAR = 2 + 2 * kKStages + 2 * kVStages + 8 + 2;
+    static constexpr int N_BAR = 2 + 2 * kKStages + 2 * kVStages + 4 + 2;
     static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
     static constexpr int BYTES = OFF_TMEM + 16;
     static constexpr int ALLOC = BYTES + 1024;  // alignment slack
+    // stream-K plan scratch (long long per block) aliases the K+V rings before any TMA
+    static constexpr int PLAN_CAP = (kKStages + kVStages) * KV_BYTES / 8;
 };
 
 // CTA-0 pipeline trace (debug): event e of CTA-local tile index idx.
@@ -95,11 +98,10 @@ __device__ __forceinline__ bool decode_unit(const TcParams& p, int w, Unit& u) {
 // Work schedule.  A "piece" is a contiguous tile range [tb, te) of one unit.
 // stream-K mode: the non-empty units' tiles, in unit order (mt, i, g), are
 // concatenated and CTA b processes global tiles [T*b/G, T*(b+1)/G), so every
-// SM streams the same number of KV tiles whatever the tree/prefix sizes; a unit
-// cut between CTAs is finished by the last CTA to complete a piece of it (its
-// partial (O, m, l) states are merged in fp32 through the workspace).
-// static mode (fallback when the plan does not fit in shared memory): whole
-// units round-robin.
+// CTA streams the same number of KV tiles whatever the tree/prefix sizes; a
+// unit cut between CTAs is finished by the last CTA to complete a piece of it
+// (the partial (O, m, l) states are merged in fp32 through the workspace).
+// static mode (fallback when the plan does not fit): whole units round-robin.
 // ---------------------------------------------------------------------------
 struct Piece {
     Unit u;
@@ -169,7 +171,7 @@ __device__ __forceinline__ int sk_owner(long long T, int G, long long x) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
                         const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kt,
                         const __grid_constant__ CUtensorMap tm_vt, const TcParams p) {
@@ -184,11 +186,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* k_empty = k_full + kKStages;
     uint64_t* v_full = k_empty + kKStages;
     uint64_t* v_empty = v_full + kVStages;
-    uint64_t* s_full = v_empty + kVStages;  // [2]
-    uint64_t* s_empty = s_full + 2;        // [2]
-    uint64_t* p_full = s_empty + 2;        // [2]
-    uint64_t* p_empty = p_full + 2;        // [2]
-    uint64_t* o_full = p_empty + 2;
+    uint64_t* s_full = v_empty + kVStages;
+    uint64_t* s_empty = s_full + 1;
+    uint64_t* p_full = s_empty + 1;
+    uint64_t* p_empty = p_full + 1;
+    uint64_t* o_full = p_empty + 1;
     uint64_t* o_empty = o_full + 1;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + S::OFF_TMEM);
 
@@ -206,14 +208,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(v_full + s, 1);
             ptx::mbar_init(v_empty + s, 1);
         }
-        for (int b = 0; b < 2; ++b) {
-            ptx::mbar_init(s_full + b, 1);
-            ptx::mbar_init(s_empty + b, 4);  // the 4 warps of softmax warpgroup b
-            ptx::mbar_init(p_full + b, 4);
-            ptx::mbar_init(p_empty + b, 1);
-        }
+        ptx::mbar_init(s_full, 1);
+        ptx::mbar_init(s_empty, 4);  // the 4 softmax warps
+        ptx::mbar_init(p_full, 4);
+        ptx::mbar_init(p_empty, 1);
         ptx::mbar_init(o_full, 1);
-        ptx::mbar_init(o_empty, 8);
+        ptx::mbar_init(o_empty, 4);
         ptx::fence_mbar_init();
         ptx::tma_prefetch(&tm_q);
         ptx::tma_prefetch(&tm_kc);
@@ -227,10 +227,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
 
-    // ---------------- stream-K plan (all threads; V ring used as scratch) ----------------
-    __shared__ long long sk_T, sk_x0;
+    // ---------------- stream-K plan (all threads; K/V rings used as scratch) ----------------
+    __shared__ long long sk_T, sk_x0, sk_rem;
     __shared__ int sk_cur[3];
-    __shared__ long long sk_rem;
     __shared__ long long scan_tmp[33];
     __shared__ int sk_last;
     Sched sched0;
@@ -238,8 +237,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     sched0.stream = 0;
     {
         const int nb = p.n_units / p.n_kv;
-        if (p.stream_k && nb <= kPlanCap) {
-            long long* pre = reinterpret_cast<long long*>(smem + S::OFF_V);
+        if (p.stream_k && nb <= S::PLAN_CAP) {
+            long long* pre = reinterpret_cast<long long*>(smem + S::OFF_K);
             for (int b = threadIdx.x; b < nb; b += blockDim.x) {
                 Unit u;
                 const bool ok = decode_unit(p, b * p.n_kv, u);
@@ -314,13 +313,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         // ===================== TMA producer (whole warp) =====================
-        // One warp issues Q and every K/V tile in CONSUMPTION order -- K_{t+lead}
-        // together with V_t, as two lanes of the same warp instructions -- so the
-        // per-SM TMA queue (which serves operations roughly in order at a bounded
-        // rate) never holds far-ahead V tiles in front of K tiles the MMA needs
-        // next.  At each unit start (and every kPtChunk pages) the 32 lanes stage
-        // the request's page-table row in shared memory: no global load sits on
-        // the per-tile issue path.
+        // K_{t+lead} (lane 0) and V_t (lane 1) are issued by the same
+        // instructions, in consumption order.  At each piece start (and every
+        // kPtChunk pages) the 32 lanes stage the request's page-table row in
+        // shared memory: no global load sits on the per-tile issue path.
         int* pt_s = reinterpret_cast<int*>(smem + S::OFF_PT);
         uint32_t itk = 0, itv = 0, unit_it = 0;
         const uint64_t pol = p.evict_first ? ptx::policy_evict_first() : ptx::policy_evict_normal();
@@ -343,9 +339,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < n + lead; ++j) {
                 const int tk = pc.tb + j;         // K tile issued at this step (lane 0)
                 const int tv = pc.tb + j - lead;  // V tile issued at this step (lane 1)
-                // stage page-table entries covering both tiles (warp-uniform)
                 const int tlo = max(tv, pc.tb), thi = min(tk, pc.te - 1);
-                if (tlo < u.n_prefix) {
+                if (tlo < u.n_prefix) {  // stage page-table entries covering both tiles (warp-uniform)
                     const int pg_first = tlo * kBN / p.page_size;
                     const int pg_last = (min(min(thi, u.n_prefix - 1) * kBN + kBN, u.L) - 1) / p.page_size;
                     if (chunk0 < 0 || pg_first < chunk0 || pg_last >= chunk0 + kPtChunk) {
@@ -407,33 +402,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
-        // Softmax warpgroup w (0/1) owns the tiles t = w (mod 2) of every unit, with
-        // its own TMEM S buffer S[w], smem P buffer P[w] and TMEM accumulator O[w].
-        // Issue order per piece: QK0 QK1 | QK2 PV0 | QK3 PV1 | ...
+        // Issue order per piece: QK0 | QK1 PV0 | QK2 PV1 | ...  QK_{t+1} waits for
+        // the softmax to have READ S_t (start of its tile), PV_t for P_t.
         constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(kBM, kBN, 0);
         constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(kBM, D, 1);
         const uint32_t q_base = ptx::smem_u32(smem + S::OFF_Q);
         const uint32_t k_base = ptx::smem_u32(smem + S::OFF_K);
         const uint32_t v_base = ptx::smem_u32(smem + S::OFF_V);
-        uint32_t k_it = 0, v_it = 0, unit_it = 0;
-        uint32_t s_ph = 0, p_ph = 0;  // bit wg = phase parity of S[wg] / P[wg] uses
+        uint32_t k_it = 0, v_it = 0, unit_it = 0, s_it = 0, p_it = 0;
         Sched sc = sched0;
         Piece pc;
         while (sched_next(p, sc, pc)) {
             const Unit& u = pc.u;
             ptx::mbar_wait(q_full, unit_it & 1);
             auto do_qk = [&](int t) {
-                const int wg = (t - pc.tb) & 1;
                 const int st = k_it % kKStages;
                 ptx::mbar_wait(k_full + st, (k_it / kKStages) & 1);
                 if (lane == 0) AS_TRACE(2, k_it);
-                ptx::mbar_wait(s_empty + wg, ((s_ph >> wg) & 1) ^ 1);
+                ptx::mbar_wait(s_empty, (s_it & 1) ^ 1);
                 if (lane == 0) AS_TRACE(7, k_it);
                 ptx::tc_fence_after();
                 if (p.debug_mode >= 2) {
                     if (lane == 0) {
                         ptx::mbar_arrive(k_empty + st);
-                        ptx::mbar_arrive(s_full + wg);
+                        ptx::mbar_arrive(s_full);
                         if (t == pc.te - 1) ptx::mbar_arrive(q_empty);
                     }
                 } else if (lane == 0) {
@@ -442,18 +434,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int c = ks >> 2, kk = ks & 3;
                         const uint64_t a = ptx::sw128_desc(q_base + c * kBM * 128 + kk * 32, 0, 1024);
                         const uint64_t b = ptx::sw128_desc(k_base + st * S::KV_BYTES + c * kBN * 128 + kk * 32, 0, 1024);
-                        ptx::mma_bf16_ss(tmem + wg * kBN, a, b, idesc_qk, ks > 0 ? 1u : 0u);
+                        ptx::mma_bf16_ss(tmem + kScol, a, b, idesc_qk, ks > 0 ? 1u : 0u);
                     }
                     ptx::mma_commit(k_empty + st);
-                    ptx::mma_commit(s_full + wg);
+                    ptx::mma_commit(s_full);
                     if (t == pc.te - 1) ptx::mma_commit(q_empty);
                 }
                 __syncwarp();
                 ++k_it;
-                s_ph ^= 1u << wg;
+                ++s_it;
             };
             auto do_pv = [&](int t) {
-                const int wg = (t - pc.tb) & 1;
                 const int st = v_it % kVStages;
                 ptx::mbar_wait(v_full + st, (v_it / kVStages) & 1);
                 if (lane == 0) AS_TRACE(3, v_it);
@@ -470,39 +461,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::fence_proxy_async_smem();
                     }
                 }
-                ptx::mbar_wait(p_full + wg, (p_ph >> wg) & 1);
+                ptx::mbar_wait(p_full, p_it & 1);
                 if (lane == 0) AS_TRACE(4, v_it);
-                if (t == pc.tb) ptx::mbar_wait(o_empty, (unit_it & 1) ^ 1);  // both O buffers drained
+                if (t == pc.tb) ptx::mbar_wait(o_empty, (unit_it & 1) ^ 1);  // O drained by the previous epilogue
                 ptx::tc_fence_after();
                 __syncwarp();
                 if (p.debug_mode >= 2) {
                     if (lane == 0) {
                         ptx::mbar_arrive(v_empty + st);
-                        ptx::mbar_arrive(p_empty + wg);
+                        ptx::mbar_arrive(p_empty);
                     }
                 } else if (lane == 0) {
 #pragma unroll
                     for (int kk = 0; kk < kBN / 16; ++kk) {
-                        // A = P_t: bf16 pairs in TMEM columns kPcol + 32 wg (its own region, so
-                        // QK_{t+2} may overwrite S[wg] before PV_t runs)
+                        // A = P_t: bf16 pairs in TMEM columns [kPcol, kPcol + kBN/2)
                         const uint64_t b = ptx::sw128_desc(v_base + st * S::KV_BYTES + kk * 16 * 128, kBN * 128, 1024);
-                        ptx::mma_bf16_ts(tmem + kOcol + wg * D, tmem + kPcol + wg * (kBN / 2) + kk * 8, b, idesc_pv,
-                                         (t - pc.tb >= 2 || kk > 0) ? 1u : 0u);
+                        ptx::mma_bf16_ts(tmem + kOcol, tmem + kPcol + kk * 8, b, idesc_pv,
+                                         (t > pc.tb || kk > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(v_empty + st);
-                    ptx::mma_commit(p_empty + wg);
+                    ptx::mma_commit(p_empty);
                 }
                 __syncwarp();
                 ++v_it;
-                p_ph ^= 1u << wg;
+                ++p_it;
             };
-            // QK_{t+2} is issued as soon as warpgroup wg has READ S_t (start of its
-            // softmax), PV_t when P_t is written: each warpgroup finds its next S
-            // ready when it finishes a tile.
             do_qk(pc.tb);
-            if (pc.te - pc.tb > 1) do_qk(pc.tb + 1);
             for (int t = pc.tb; t < pc.te; ++t) {
-                if (t + 2 < pc.te) do_qk(t + 2);
+                if (t + 1 < pc.te) do_qk(t + 1);
                 do_pv(t);
             }
             if (lane == 0) {
@@ -513,17 +499,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++unit_it;
         }
     } else {
-        // ===================== softmax + epilogue (warps 2..9) =====================
-        const int wg = (warp - 2) >> 2;  // warpgroup: tiles t = wg (mod 2)
+        // ===================== softmax + epilogue (warps 2..5) =====================
         const int quad = warp & 3;       // TMEM lane quadrant this warp may access
         const int r = quad * 32 + lane;  // Q row in the tile == TMEM lane
         const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-        const uint32_t s_addr = tmem + lane_addr + wg * kBN;
-        const uint32_t o_addr = tmem + lane_addr + kOcol + wg * D;
-        float* ml = reinterpret_cast<float*>(smem + S::OFF_ML);  // [2 units][2 wg][2 (m,l)][128]
+        const uint32_t s_addr = tmem + lane_addr + kScol;
+        const uint32_t p_addr = tmem + lane_addr + kPcol;
+        const uint32_t o_addr = tmem + lane_addr + kOcol;
         const float sl2 = p.scale_log2;
         uint32_t s_cnt = 0, unit_it = 0;
-        int tbase = 0;  // CTA-local index of this unit's first tile (trace only)
+        int tbase = 0;  // CTA-local index of the piece's first tile (trace only)
         Sched sc = sched0;
         Piece pc;
         while (sched_next(p, sc, pc)) {
@@ -535,9 +520,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int hh = rr - node * G;
             // ancestor-or-self bitmask of this row's node (R15); parents staged in smem
             int* tp_s = reinterpret_cast<int*>(smem + S::OFF_TP) + (unit_it & 1) * AS_MAX_TREE;
-            const int tid_sm = (warp - 2) * 32 + lane;
-            for (int j = tid_sm; j < u.K; j += 256) tp_s[j] = __ldg(p.tree_parent + u.off + j);
-            asm volatile("bar.sync 2, 256;" ::: "memory");
+            for (int j = (int)threadIdx.x - 64; j < u.K; j += 128) tp_s[j] = __ldg(p.tree_parent + u.off + j);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
             uint64_t anc0 = 0, anc1 = 0;
             if (row_ok) {
                 int v = node, steps = 0;
@@ -553,10 +537,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             float m_ref = -INFINITY, l_sum = 0.f;
-            for (int t = pc.tb + wg; t < pc.te; t += 2, ++s_cnt) {
+            for (int t = pc.tb; t < pc.te; ++t, ++s_cnt) {
                 const uint32_t par = s_cnt & 1;
-                ptx::mbar_wait(s_full + wg, par);
-                if (lane == 0 && quad == 0) AS_TRACE(5, tbase + t);
+                ptx::mbar_wait(s_full, par);
+                if (lane == 0 && quad == 0) AS_TRACE(5, tbase + t - pc.tb);
                 ptx::tc_fence_after();
                 uint32_t sr[kBN];
                 ptx::tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
@@ -564,12 +548,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tmem_ld_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(s_empty + wg);
+                if (lane == 0) ptx::mbar_arrive(s_empty);
                 if (p.debug_mode >= 1) {  // timing experiment: no softmax math
-                    ptx::mbar_wait(p_empty + wg, par ^ 1);
+                    ptx::mbar_wait(p_empty, par ^ 1);
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(p_full + wg);
-                    if (lane == 0 && quad == 0) AS_TRACE(6, tbase + t);
+                    if (lane == 0) ptx::mbar_arrive(p_full);
                     continue;
                 }
                 float* x = reinterpret_cast<float*>(sr);
@@ -593,26 +576,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                          fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
                 const float m_new = fmaxf(m_ref, tmax);
-                // P buffer wg is free (and O[wg] stable) once PV of this warpgroup's previous tile completed
-                ptx::mbar_wait(p_empty + wg, par ^ 1);
-                if (t - pc.tb >= 2) {
+                // P is free (and O stable) once PV_{t-1} completed
+                ptx::mbar_wait(p_empty, par ^ 1);
+                if (t > pc.tb) {
                     const bool need = m_new > m_ref + kRescaleThresh;
                     if (__any_sync(0xffffffffu, need)) {
                         ptx::tc_fence_after();
-                        const float sc = need ? ptx::ex2(m_ref - m_new) : 1.f;
+                        const float sc2 = need ? ptx::ex2(m_ref - m_new) : 1.f;
 #pragma unroll
                         for (int c0 = 0; c0 < D; c0 += 32) {
                             uint32_t o[32];
                             ptx::tmem_ld32(o_addr + c0, o);
                             ptx::tmem_ld_wait();
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * sc);
+                            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * sc2);
                             ptx::tmem_st32(o_addr + c0, o);
                         }
                         ptx::tmem_st_wait();
                         ptx::tc_fence_before();
                         if (need) {
-                            l_sum *= sc;
+                            l_sum *= sc2;
                             m_ref = m_new;
                         }
                     }
@@ -631,70 +614,52 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pk[c >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                 }
                 l_sum += (rs[0] + rs[1]) + (rs[2] + rs[3]);
-                // P_t goes to this warpgroup's TMEM P region; the PV MMA reads it as A.
-                ptx::tmem_st32(tmem + lane_addr + kPcol + wg * (kBN / 2), *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+                ptx::tmem_st32(p_addr, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(p_full + wg);
-                if (lane == 0 && quad == 0) AS_TRACE(6, tbase + t);
+                if (lane == 0) ptx::mbar_arrive(p_full);
+                if (lane == 0 && quad == 0) AS_TRACE(6, tbase + t - pc.tb);
             }
-            // ---- epilogue: merge the two warpgroups' partial softmax states ----
-            float* mlu = ml + (unit_it & 1) * 512;
-            mlu[wg * 256 + r] = m_ref;
-            mlu[wg * 256 + 128 + r] = l_sum;
+            // ---- epilogue ----
             ptx::mbar_wait(o_full, unit_it & 1);
             ptx::tc_fence_after();
-            asm volatile("bar.sync 1, 256;" ::: "memory");
-            const float m0 = mlu[r], l0 = mlu[128 + r], m1 = mlu[256 + r], l1 = mlu[384 + r];
-            const float mm = fmaxf(m0, m1);
-            const float a0 = (m0 == -INFINITY) ? 0.f : ptx::ex2(m0 - mm);
-            const float a1 = (m1 == -INFINITY) ? 0.f : ptx::ex2(m1 - mm);
-            const float lt = l0 * a0 + l1 * a1;
             const bool full = (pc.tb == 0 && pc.te == u.nt);
-            // full unit: normalise here; partial piece: keep (O, m, l) unnormalised
-            const float inv = full ? 1.f / lt : 1.f;
-            const float f0 = a0 * inv, f1 = a1 * inv;
+            const float inv = full ? 1.f / l_sum : 1.f;  // partial piece: keep (O, m, l) unnormalised
             const size_t orow = (size_t)(u.off + node) * p.n_q + (size_t)u.g * G + hh;
-            const uint32_t o0_addr = tmem + lane_addr + kOcol;
-            const uint32_t o1_addr = o0_addr + D;
             const int slot = 2 * blockIdx.x + (pc.x == sk_x0 ? 0 : 1);
             float* part = p.partial + (size_t)slot * p.slot_floats;  // [128][D] O, then m[128], l[128]
 #pragma unroll
-            for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
-                uint32_t oa[32], ob[32];
-                ptx::tmem_ld32(o0_addr + c0, oa);
-                ptx::tmem_ld32(o1_addr + c0, ob);
+            for (int c0 = 0; c0 < D; c0 += 32) {
+                uint32_t oa[32];
+                ptx::tmem_ld32(o_addr + c0, oa);
                 ptx::tmem_ld_wait();
-                float v[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    v[j] = __uint_as_float(oa[j]) * f0;
-                    if (f1 != 0.f) v[j] = fmaf(__uint_as_float(ob[j]), f1, v[j]);  // wg 1 may have had no tile
-                }
                 if (full) {
                     if (row_ok) {
-                        uint32_t pk[16];
+                        uint32_t pkk[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
-                            __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-                            pk[j] = *reinterpret_cast<uint32_t*>(&h2);
+                            __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(oa[2 * j]) * inv,
+                                                                      __uint_as_float(oa[2 * j + 1]) * inv);
+                            pkk[j] = *reinterpret_cast<uint32_t*>(&h2);
                         }
                         uint4* dst = reinterpret_cast<uint4*>(p.out + orow * D + c0);
 #pragma unroll
                         for (int j = 0; j < 4; ++j)
-                            dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+                            dst[j] = make_uint4(pkk[4 * j], pkk[4 * j + 1], pkk[4 * j + 2], pkk[4 * j + 3]);
                     }
                 } else {
                     float4* dst = reinterpret_cast<float4*>(part + (size_t)r * D + c0);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    for (int j = 0; j < 8; ++j)
+                        dst[j] = make_float4(__uint_as_float(oa[4 * j]), __uint_as_float(oa[4 * j + 1]),
+                                             __uint_as_float(oa[4 * j + 2]), __uint_as_float(oa[4 * j + 3]));
                 }
             }
-            if (full && row_ok && p.lse && wg == 0) p.lse[orow] = (mm + __log2f(lt)) * 0.6931471805599453f;
-            if (!full && wg == 0) {
-                part[128 * D + r] = mm;
-                part[128 * D + 128 + r] = lt;
+            if (full && row_ok && p.lse) p.lse[orow] = (m_ref + __log2f(l_sum)) * 0.6931471805599453f;
+            if (!full) {
+                part[128 * D + r] = m_ref;
+                part[128 * D + 128 + r] = l_sum;
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -703,39 +668,38 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // stream-K fix-up: the CTA that completes the unit's last piece merges
                 // every piece's (O, m, l) (fp32, through L2) and writes the output.
                 __threadfence();
-                asm volatile("bar.sync 1, 256;" ::: "memory");
+                asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (warp == 2 && lane == 0) {
                     const int n = pc.te - pc.tb;
                     const int old = atomicAdd(p.cnt + pc.w, n);
                     sk_last = (old + n == u.nt) ? 1 : 0;
                 }
-                asm volatile("bar.sync 1, 256;" ::: "memory");
+                asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (sk_last) {
                     __threadfence();
                     const long long T = sk_T;
                     const int Gd = gridDim.x;
                     const long long U0 = pc.x - pc.tb;
                     const int b_first = sk_owner(T, Gd, U0), b_last = sk_owner(T, Gd, U0 + u.nt - 1);
+                    auto slot_of = [&](int b) {
+                        return p.partial + (size_t)(2 * b + (sk_start(T, b, Gd) < U0 ? 1 : 0)) * p.slot_floats;
+                    };
                     float M = -INFINITY;
-                    for (int b = b_first; b <= b_last; ++b) {
-                        const float* pb = p.partial + (size_t)(2 * b + (sk_start(T, b, Gd) < U0 ? 1 : 0)) * p.slot_floats;
-                        M = fmaxf(M, __ldcg(pb + 128 * D + r));
-                    }
+                    for (int b = b_first; b <= b_last; ++b) M = fmaxf(M, __ldcg(slot_of(b) + 128 * D + r));
                     float Ltot = 0.f;
                     for (int b = b_first; b <= b_last; ++b) {
-                        const float* pb = p.partial + (size_t)(2 * b + (sk_start(T, b, Gd) < U0 ? 1 : 0)) * p.slot_floats;
+                        const float* pb = slot_of(b);
                         const float mb = __ldcg(pb + 128 * D + r);
                         if (mb != -INFINITY) Ltot += __ldcg(pb + 128 * D + 128 + r) * ptx::ex2(mb - M);
                     }
                     const float invL = 1.f / Ltot;
-#pragma unroll
-                    for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 32) {
+#pragma unroll 1
+                    for (int c0 = 0; c0 < D; c0 += 32) {
                         float acc[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) acc[j] = 0.f;
                         for (int b = b_first; b <= b_last; ++b) {
-                            const float* pb =
-                                p.partial + (size_t)(2 * b + (sk_start(T, b, Gd) < U0 ? 1 : 0)) * p.slot_floats;
+                            const float* pb = slot_of(b);
                             const float mb = __ldcg(pb + 128 * D + r);
                             if (mb == -INFINITY) continue;
                             const float fb = ptx::ex2(mb - M) * invL;
@@ -750,19 +714,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                         if (row_ok) {
-                            uint32_t pk[16];
+                            uint32_t pkk[16];
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
                                 __nv_bfloat162 h2 = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
-                                pk[j] = *reinterpret_cast<uint32_t*>(&h2);
+                                pkk[j] = *reinterpret_cast<uint32_t*>(&h2);
                             }
                             uint4* dst = reinterpret_cast<uint4*>(p.out + orow * D + c0);
 #pragma unroll
                             for (int j = 0; j < 4; ++j)
-                                dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+                                dst[j] = make_uint4(pkk[4 * j], pkk[4 * j + 1], pkk[4 * j + 2], pkk[4 * j + 3]);
                         }
                     }
-                    if (row_ok && p.lse && wg == 0) p.lse[orow] = (M + __log2f(Ltot)) * 0.6931471805599453f;
+                    if (row_ok && p.lse) p.lse[orow] = (M + __log2f(Ltot)) * 0.6931471805599453f;
                     if (warp == 2 && lane == 0) atomicExch(p.cnt + pc.w, 0);  // reusable workspace
                 }
             }
@@ -784,10 +748,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 int tc_smem_bytes(int head_dim) {
     return head_dim == 64 ? TcSmem<64>::ALLOC : TcSmem<128>::ALLOC;
 }
+int tc_ctas_per_sm() { return kCtasPerSm; }
 
 int launch_attn_tc(const CUtensorMap* maps, const TcParams& p, int head_dim, int n_sms, cudaStream_t stream) {
     const int smem = tc_smem_bytes(head_dim);
-    int grid = p.n_units < n_sms ? p.n_units : n_sms;
+    int grid = n_sms * kCtasPerSm;
+    if (!p.stream_k && p.n_units < grid) grid = p.n_units;
     if (grid <= 0) return 0;
     if (head_dim == 128) {
         if (cudaFuncSetAttribute(tree_attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
