@@ -219,6 +219,7 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     p.out = (__nv_bfloat16*)out; p.lse = lse; p.ws = workspace;
     const int mt_max = (AS_MAX_TREE * G + 127) / 128;
     p.n_units = mt_max * n_req * n_kv_heads;
+    p.mt_max = mt_max;
     {
         const int nsm = sm_count();
         const size_t slot = ((size_t)128 * head_dim + 256) * 4;

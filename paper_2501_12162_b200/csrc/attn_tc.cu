@@ -76,71 +76,88 @@ struct Unit {
     int i, g, mt, off, K, L, nt, n_prefix;
 };
 
-__device__ __forceinline__ bool decode_unit(const TcParams& p, int w, Unit& u) {
-    const int per_mt = p.n_req * p.n_kv;
-    u.mt = w / per_mt;
-    const int rem = w - u.mt * per_mt;
-    u.i = rem / p.n_kv;
-    u.g = rem - u.i * p.n_kv;
-    u.off = __ldg(p.tree_offsets + u.i);
-    u.K = __ldg(p.tree_offsets + u.i + 1) - u.off;
-    if (u.K <= 0 || u.K > AS_MAX_TREE || u.off + u.K > p.n_tree_rows) return false;
-    if (u.K * p.G <= u.mt * kBM) return false;
-    u.L = __ldg(p.kv_len + u.i);
-    if (u.L < 0) u.L = 0;
-    if (u.L > p.max_pages * p.page_size) u.L = p.max_pages * p.page_size;
-    u.n_prefix = (u.L + kBN - 1) / kBN;
-    u.nt = u.n_prefix + (u.K + kBN - 1) / kBN;
-    return true;
+// Per-request geometry: MT q-tiles of 128 rows (rows = node*G + hh), nt KV tiles.
+struct Req {
+    int off, K, L, MT, nt, n_prefix;
+};
+
+__device__ __forceinline__ void load_req(const TcParams& p, int i, Req& r) {
+    r.off = __ldg(p.tree_offsets + i);
+    r.K = __ldg(p.tree_offsets + i + 1) - r.off;
+    r.L = __ldg(p.kv_len + i);
+    if (r.L < 0) r.L = 0;
+    if (r.L > p.max_pages * p.page_size) r.L = p.max_pages * p.page_size;
+    r.n_prefix = (r.L + kBN - 1) / kBN;
+    const bool ok = r.K > 0 && r.K <= AS_MAX_TREE && r.off + r.K <= p.n_tree_rows;
+    r.MT = ok ? (r.K * p.G + kBM - 1) / kBM : 0;
+    r.nt = r.n_prefix + (r.K + kBN - 1) / kBN;
+}
+
+__device__ __forceinline__ void make_unit(const Req& r, int i, int j, Unit& u) {
+    u.i = i;
+    u.g = j / r.MT;
+    u.mt = j - u.g * r.MT;
+    u.off = r.off;
+    u.K = r.K;
+    u.L = r.L;
+    u.nt = r.nt;
+    u.n_prefix = r.n_prefix;
 }
 
 // ---------------------------------------------------------------------------
-// Work schedule.  A "piece" is a contiguous tile range [tb, te) of one unit.
-// stream-K mode: the non-empty units' tiles, in unit order (mt, i, g), are
-// concatenated and CTA b processes global tiles [T*b/G, T*(b+1)/G), so every
-// CTA streams the same number of KV tiles whatever the tree/prefix sizes; a
-// unit cut between CTAs is finished by the last CTA to complete a piece of it
-// (the partial (O, m, l) states are merged in fp32 through the workspace).
-// static mode (fallback when the plan does not fit): whole units round-robin.
+// Work schedule.  Units are (request i, kv head g, q-tile mt) in that order --
+// the q-tiles of one (i, g) are adjacent, so CTAs running them side by side
+// read that head's KV from L2 the second time.  A "piece" is a contiguous tile
+// range [tb, te) of one unit.
+//  static mode: non-empty unit k goes to CTA k mod G (whole units);
+//  stream-K mode: the units' tiles are concatenated and CTA b processes global
+//   tiles [T*b/G, T*(b+1)/G); a unit cut between CTAs is finished by the last
+//   CTA to complete a piece of it (partial (O, m, l) merged in fp32 through
+//   the workspace).  Chosen per launch by a makespan model (prologue).
 // ---------------------------------------------------------------------------
 struct Piece {
     Unit u;
-    int w;         // unit index (mt, i, g)
+    int w;         // unit id (i, g, mt) -> counter index
     int tb, te;    // tile range of this piece
     long long x;   // global tile index of (u, tb) in stream-K mode
 };
 
 struct Sched {
     int stream;
-    int beta, g, t;      // stream-K cursor: block (mt, i), kv head, tile
-    long long rem, x;    // tiles left for this CTA, global index of the cursor
-    int w;               // static cursor
+    int i, j, t;         // cursor: request, unit within request (g*MT + mt), tile
+    long long rem, x;    // stream-K: tiles left for this CTA, global tile index of the cursor
+    long long k, ucum;   // static: next unit index, units before request i
+    Req r;               // geometry of request i
 };
 
 __device__ __forceinline__ bool sched_next(const TcParams& p, Sched& sc, Piece& pc) {
+    const int units_per_req = p.n_kv;  // times MT
     if (!sc.stream) {
-        for (; sc.w < p.n_units; sc.w += gridDim.x) {
-            if (decode_unit(p, sc.w, pc.u)) {
-                pc.w = sc.w;
-                pc.tb = 0;
-                pc.te = pc.u.nt;
-                pc.x = -1;
-                sc.w += gridDim.x;
-                return true;
-            }
+        // advance the request cursor to the request holding unit k
+        while (sc.i < p.n_req && sc.k >= sc.ucum + (long long)units_per_req * sc.r.MT) {
+            sc.ucum += (long long)units_per_req * sc.r.MT;
+            if (++sc.i < p.n_req) load_req(p, sc.i, sc.r);
         }
-        return false;
+        if (sc.i >= p.n_req) return false;
+        const int j = (int)(sc.k - sc.ucum);
+        make_unit(sc.r, sc.i, j, pc.u);
+        pc.w = (sc.i * p.n_kv + pc.u.g) * p.mt_max + pc.u.mt;
+        pc.tb = 0;
+        pc.te = pc.u.nt;
+        pc.x = -1;
+        sc.k += gridDim.x;
+        return true;
     }
-    const int nb = p.n_units / p.n_kv;
-    while (sc.rem > 0 && sc.beta < nb) {
-        const int w = sc.beta * p.n_kv + sc.g;
-        if (!decode_unit(p, w, pc.u)) {  // empty block: all its kv heads are empty
-            ++sc.beta;
-            sc.g = 0;
+    while (sc.rem > 0 && sc.i < p.n_req) {
+        if (sc.j >= units_per_req * sc.r.MT) {  // next request (empty requests have no units)
+            if (++sc.i >= p.n_req) return false;
+            load_req(p, sc.i, sc.r);
+            sc.j = 0;
             sc.t = 0;
             continue;
         }
-        pc.w = w;
+        make_unit(sc.r, sc.i, sc.j, pc.u);
+        pc.w = (sc.i * p.n_kv + pc.u.g) * p.mt_max + pc.u.mt;
         pc.tb = sc.t;
         const long long avail = pc.u.nt - sc.t;
         pc.te = sc.t + (int)(avail < sc.rem ? avail : sc.rem);
@@ -151,10 +168,7 @@ __device__ __forceinline__ bool sched_next(const TcParams& p, Sched& sc, Piece& 
         sc.t = pc.te;
         if (sc.t >= pc.u.nt) {
             sc.t = 0;
-            if (++sc.g >= p.n_kv) {
-                sc.g = 0;
-                ++sc.beta;
-            }
+            ++sc.j;
         }
         return true;
     }
@@ -227,28 +241,50 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
 
-    // ---------------- stream-K plan (all threads; K/V rings used as scratch) ----------------
+    // ---------------- schedule plan (all threads; K/V rings used as scratch) ----------------
     __shared__ long long sk_T, sk_x0, sk_rem;
     __shared__ int sk_cur[3];
+    __shared__ int sk_stream;
     __shared__ long long scan_tmp[33];
+    __shared__ int red_tmp[2][8];
     __shared__ int sk_last;
     Sched sched0;
-    sched0.w = blockIdx.x;
-    sched0.stream = 0;
     {
-        const int nb = p.n_units / p.n_kv;
-        if (p.stream_k && nb <= S::PLAN_CAP) {
-            long long* pre = reinterpret_cast<long long*>(smem + S::OFF_K);
-            for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-                Unit u;
-                const bool ok = decode_unit(p, b * p.n_kv, u);
-                if (!ok && u.K > AS_MAX_TREE && u.mt == 0) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, u.i);
-                pre[b] = ok ? (long long)u.nt * p.n_kv : 0;
-            }
-            __syncthreads();
-            // exclusive scan of pre[0..nb): per-thread chunks, then warp and block totals
-            const int chunk = (nb + blockDim.x - 1) / blockDim.x;
-            const int lo = threadIdx.x * chunk, hi = min(nb, lo + chunk);
+        const int n = p.n_req;
+        long long* pre = reinterpret_cast<long long*>(smem + S::OFF_K);  // per-request tiles -> prefix
+        const bool can_stream = p.stream_k && n <= S::PLAN_CAP;
+        int my_units = 0, my_maxnt = 0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            Req r;
+            load_req(p, i, r);
+            if (r.MT == 0 && r.K > AS_MAX_TREE) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, i);
+            my_units += p.n_kv * r.MT;
+            if (r.MT > 0) my_maxnt = max(my_maxnt, r.nt);
+            if (can_stream) pre[i] = (long long)p.n_kv * r.MT * r.nt;
+        }
+        // block reductions: total units, max unit tiles
+        int wu = my_units, wm = my_maxnt;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            wu += __shfl_xor_sync(0xffffffffu, wu, o);
+            wm = max(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+        }
+        if (lane == 0) {
+            red_tmp[0][warp] = wu;
+            red_tmp[1][warp] = wm;
+        }
+        __syncthreads();
+        int U = 0, maxnt = 0;
+        for (int k = 0; k < (int)(blockDim.x / 32); ++k) {
+            U += red_tmp[0][k];
+            maxnt = max(maxnt, red_tmp[1][k]);
+        }
+        const int G = gridDim.x;
+        long long T = 0;
+        if (can_stream) {
+            // exclusive scan of pre[0..n): per-thread chunks, then warp and block totals
+            const int chunk = (n + blockDim.x - 1) / blockDim.x;
+            const int lo = threadIdx.x * chunk, hi = min(n, lo + chunk);
             long long loc = 0;
             for (int b = lo; b < hi; ++b) loc += pre[b];
             long long inc = loc;
@@ -266,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                     scan_tmp[k] = acc;
                     acc += v;
                 }
-                scan_tmp[32] = acc;  // T
+                scan_tmp[32] = acc;
             }
             __syncthreads();
             long long run = scan_tmp[warp] + inc - loc;
@@ -276,39 +312,54 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 run += v;
             }
             __syncthreads();
-            if (threadIdx.x == 0) {
-                const long long T = scan_tmp[32];
-                const int G = gridDim.x;
+            T = scan_tmp[32];
+        }
+        if (threadIdx.x == 0) {
+            // makespan model (tiles): static = ceil(U/G) whole units of <= maxnt tiles;
+            // stream-K = T/G plus ~30% for the split fix-ups (measured on c2).
+            const long long static_ms = (long long)((U + G - 1) / G) * maxnt;
+            const bool stream = can_stream && T > 0 && (T * 13 / 10) / G + 1 < static_ms;
+            sk_stream = stream ? 1 : 0;
+            sk_T = T;
+            sk_x0 = 0;
+            sk_rem = 0;
+            int i0 = 0, j0 = 0, t0 = 0;
+            if (stream) {
                 const long long x0 = sk_start(T, blockIdx.x, G), x1 = sk_start(T, blockIdx.x + 1, G);
-                sk_T = T;
                 sk_x0 = x0;
                 sk_rem = x1 - x0;
-                int beta = 0, g = 0, t = 0;
                 if (x1 > x0) {
-                    int lo_b = 0, hi_b = nb - 1;  // last b with pre[b] <= x0
+                    int lo_b = 0, hi_b = n - 1;  // last i with pre[i] <= x0
                     while (lo_b < hi_b) {
                         const int mid = (lo_b + hi_b + 1) >> 1;
                         if (pre[mid] <= x0) lo_b = mid; else hi_b = mid - 1;
                     }
-                    beta = lo_b;
-                    const long long next = (beta + 1 < nb) ? pre[beta + 1] : T;
-                    const long long ntu = (next - pre[beta]) / p.n_kv;
-                    const long long off = x0 - pre[beta];
-                    g = (int)(off / ntu);
-                    t = (int)(off - (long long)g * ntu);
+                    i0 = lo_b;
+                    Req r;
+                    load_req(p, i0, r);
+                    const long long off = x0 - pre[i0];
+                    j0 = (int)(off / r.nt);
+                    t0 = (int)(off - (long long)j0 * r.nt);
                 }
-                sk_cur[0] = beta;
-                sk_cur[1] = g;
-                sk_cur[2] = t;
             }
-            __syncthreads();
-            sched0.stream = 1;
-            sched0.beta = sk_cur[0];
-            sched0.g = sk_cur[1];
-            sched0.t = sk_cur[2];
-            sched0.rem = sk_rem;
-            sched0.x = sk_x0;
+            sk_cur[0] = i0;
+            sk_cur[1] = j0;
+            sk_cur[2] = t0;
         }
+        __syncthreads();
+        sched0.stream = sk_stream;
+        sched0.i = sk_cur[0];
+        sched0.j = sk_cur[1];
+        sched0.t = sk_cur[2];
+        sched0.rem = sk_rem;
+        sched0.x = sk_x0;
+        sched0.k = blockIdx.x;
+        sched0.ucum = 0;
+        if (n > 0) load_req(p, sched0.i, sched0.r);
+        else sched0.r.MT = 0;
+        if (!sched0.stream) sched0.i = 0;
+        if (!sched0.stream && n > 0) load_req(p, 0, sched0.r);
+        __syncthreads();  // plan scratch (K/V rings) is free again
     }
 
     if (warp == 0) {
