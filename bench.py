@@ -9,9 +9,9 @@ Metric (BASELINE.json): verified tree tokens/sec (sum_i K_i per step / step time
 and the attention kernel's HBM GB/s as a fraction of the measured HBM peak.
 A step = one pass of the whole hot path over one batch: as_select_trees ->
 as_tree_verify_attn (one layer) -> as_accept_tokens (walk + KV commit), plus at
-N>1 the all-gather of accept records.  Inputs are resident in HBM; the
-per-request prefix length is restored before each step (a 256-byte D2D copy)
-so every step verifies the same workload.
+N>1 the all-gather of accept records.  Inputs are resident in HBM; accept
+writes the advanced prefix lengths out of place (kv_len_out), so every step
+verifies the same workload with nothing but the hot path in the timed region.
 
 The only place outside tests/ that touches oracle/ is the `cpu_baseline` leg
 and `--impl reference`, which time the CPU oracle as it stands on this host.
@@ -113,8 +113,11 @@ def make_workload(cfg_name, device="cuda", seed_salt=0, rank=0, world=1, engine=
     W["cand_token"] = torch.from_numpy(F["cand_token"]).to(device)
     W["slo_deficit"] = torch.from_numpy(np.ascontiguousarray(A, np.float64)).to(device)
     W["page_table"] = torch.from_numpy(table).to(device)
-    W["kv_len0"] = torch.from_numpy(kv_len).to(device)
-    W["kv_len"] = W["kv_len0"].clone()
+    # kv_len is the committed prefix the step reads; accept writes the new
+    # lengths to kv_len_out (as_accept_tokens' out-of-place form), so every
+    # replayed step verifies the same workload without a restore copy.
+    W["kv_len"] = torch.from_numpy(kv_len).to(device)
+    W["kv_len_out"] = torch.empty_like(W["kv_len"])
     W["q"] = rnd(R, n_q, D)
     W["k_tree"] = rnd(R, n_kv, D)
     W["v_tree"] = rnd(R, n_kv, D)
@@ -184,7 +187,7 @@ def run_accept(W, phase=None, req_range=None):
     ada.accept_tokens(ada.AS_ACCEPT_FUSED if phase is None else phase, W["sel"]["tree_offsets"],
                       W["sel"]["tree_parent"], W["sel"]["tree_token"], target_tokens=W["target_tokens"],
                       max_path=W["max_path"], k_tree=W["k_tree"], v_tree=W["v_tree"], k_cache=kc, v_cache=vc,
-                      page_table=W["page_table"], kv_len=W["kv_len"], req_range=req_range,
+                      page_table=W["page_table"], kv_len=W["kv_len"], kv_len_out=W["kv_len_out"], req_range=req_range,
                       accept_len=W["acc"]["accept_len"], accept_path=W["acc"]["accept_path"],
                       bonus_token=W["acc"]["bonus_token"], n_tree_rows=W["R"], workspace=W["ws_accept"])
 
@@ -244,24 +247,31 @@ class Step:
         self.W = W
         self.dist = dist_ctx
 
-    def __call__(self, events=None, external=False):
+    def __call__(self, events=None, external=False, attn_only=False):
+        """events: 4 (before select/attention/accept, after accept) or, with
+        attn_only, 2 (around the attention launch)."""
         W = self.W
         W["pool_idx"] = (W["pool_idx"] + 1) % W["n_pools"]
-        W["kv_len"].copy_(W["kv_len0"], non_blocking=True)
-        if events:
-            _record(events[0], external)
+        ea = events if (events and attn_only) else None
+        eb = events if (events and not attn_only) else None
+        if eb:
+            _record(eb[0], external)
         run_select(W)
-        if events:
-            _record(events[1], external)
+        if eb:
+            _record(eb[1], external)
+        if ea:
+            _record(ea[0], external)
         run_attention(W)
-        if events:
-            _record(events[2], external)
+        if ea:
+            _record(ea[1], external)
+        if eb:
+            _record(eb[2], external)
         if self.dist is None:
             run_accept(W)
         else:
             self.dist.accept_and_commit(W)
-        if events:
-            _record(events[3], external)
+        if eb:
+            _record(eb[3], external)
         return events
 
 
@@ -399,12 +409,15 @@ def main():
     for _ in range(2):  # eager warm-up (attribute setup, NCCL communicator)
         step()
     torch.cuda.synchronize()
-    all_ev = make_events(4 * args.steps + 2)
+    # Timed graph: K unrolled steps, events only around each attention launch
+    # (the roofline kernel) and around the whole region.  A second graph with
+    # events around every call gives the per-kernel breakdown (not the value).
+    all_ev = make_events(2 * args.steps + 2)
     start, end = all_ev[-2], all_ev[-1]
-    evs = [all_ev[4 * k:4 * k + 4] for k in range(args.steps)]
+    attn_ev = [all_ev[2 * k:2 * k + 2] for k in range(args.steps)]
+    brk_ev = [make_events(4) for _ in range(args.steps)]
     if use_graph:
-        # The whole hot path of a step is replayed from CUDA graphs:
-        # one graph of K unrolled steps with event-record nodes around every call.
+        # The whole hot path of a step is replayed from CUDA graphs.
         g_warm = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_warm):
             step()
@@ -412,8 +425,12 @@ def main():
         with torch.cuda.graph(g_timed):
             _record(start, True)
             for k in range(args.steps):
-                step(evs[k], external=True)
+                step(attn_ev[k], external=True, attn_only=True)
             _record(end, True)
+        g_brk = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_brk):
+            for k in range(args.steps):
+                step(brk_ev[k], external=True)
         for _ in range(args.warmup):
             g_warm.replay()
     else:
@@ -431,7 +448,7 @@ def main():
     else:
         start.record()
         for k in range(args.steps):
-            step(evs[k])
+            step(attn_ev[k], attn_only=True)
         end.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -439,9 +456,17 @@ def main():
     torch.cuda.synchronize()
     clocks = _clock_sampler_stop(sampler, local_rank)
     total_ms = start.elapsed_time(end)
-    t_sel = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
-    t_attn = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
-    t_acc = float(np.mean([e[2].elapsed_time(e[3]) for e in evs]))
+    t_attn = float(np.mean([e[0].elapsed_time(e[1]) for e in attn_ev]))
+    # breakdown pass (not timed for the value)
+    if use_graph:
+        g_brk.replay()
+    else:
+        for k in range(args.steps):
+            step(brk_ev[k])
+    torch.cuda.synchronize()
+    t_sel = float(np.mean([e[0].elapsed_time(e[1]) for e in brk_ev]))
+    t_attn_b = float(np.mean([e[1].elapsed_time(e[2]) for e in brk_ev]))
+    t_acc = float(np.mean([e[2].elapsed_time(e[3]) for e in brk_ev]))
     if world > 1:
         t = torch.tensor([total_ms, t_attn], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -454,14 +479,28 @@ def main():
     abytes = attn_algorithmic_bytes(W)
     aflops = attn_flops(W)
     achieved_gbs = abytes / (t_attn / 1e3) / 1e9
+    achieved_tf = aflops / (t_attn / 1e3) / 1e12
     hbm_peak = float(peaks["hbm_gbs"])
-    roofline = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved_gbs / hbm_peak, 4), "traffic": _traffic_from_profiles(args.config),
-                "kernel": "tree_attn_tc_kernel" if W["dtype"] == torch.bfloat16 else "tree_attn_simt_kernel",
-                "algorithmic_bytes_per_launch": abytes, "attn_ms": round(t_attn, 4),
-                "tensor_tflops": round(aflops / (t_attn / 1e3) / 1e12, 1),
-                "tensor_frac_sustained": round(aflops / (t_attn / 1e3) / 1e12 / float(peaks.get(
-                    "bf16_tflops_sustained", 1400.0)), 4), "peak_source": peak_kind}
+    # bf16 dense peak for a kernel timed alone (burst); the kernel also reports
+    # its fraction of the sustained figure.  fp32 (SIMT, c1) has no tensor bound.
+    tf_peak = float(peaks.get("bf16_tflops", 1590.0))
+    tf_sus = float(peaks.get("bf16_tflops_sustained", 1400.0))
+    ai = aflops / abytes if abytes else 0.0
+    ridge = tf_peak * 1e12 / (hbm_peak * 1e9)
+    tensor_bound = W["dtype"] == torch.bfloat16 and ai > ridge
+    common = {"traffic": _traffic_from_profiles(args.config),
+              "kernel": "tree_attn_tc_kernel" if W["dtype"] == torch.bfloat16 else "tree_attn_simt_kernel",
+              "algorithmic_bytes_per_launch": abytes, "algorithmic_flops_per_launch": aflops,
+              "arith_intensity": round(ai, 1), "ridge": round(ridge, 1), "attn_ms": round(t_attn, 4),
+              "hbm_gbs": round(achieved_gbs, 1), "hbm_frac": round(achieved_gbs / hbm_peak, 4),
+              "tensor_tflops": round(achieved_tf, 1), "tensor_frac_burst": round(achieved_tf / tf_peak, 4),
+              "tensor_frac_sustained": round(achieved_tf / tf_sus, 4), "peak_source": peak_kind}
+    if tensor_bound:
+        roofline = {"bound": "tensor", "achieved": round(achieved_tf, 1), "peak": tf_peak, "unit": "TFLOP/s",
+                    "frac": round(achieved_tf / tf_peak, 4), **common}
+    else:
+        roofline = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(achieved_gbs / hbm_peak, 4), **common}
 
     e2e = None
     if not args.no_e2e and not args.profile:
@@ -491,7 +530,8 @@ def main():
                        if W["n_pools"] == 1 else f"{W['n_pools']} rotating KV pools (> 3x L2)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks, "graph": use_graph,
-            "breakdown_ms": {"select": round(t_sel, 4), "attention": round(t_attn, 4), "accept_commit": round(t_acc, 4)},
+            "breakdown_ms": {"select": round(t_sel, 4), "attention": round(t_attn_b, 4), "accept_commit": round(t_acc, 4),
+                             "note": "separate instrumented replay (events around every call)"},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

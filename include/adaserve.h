@@ -178,7 +178,9 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
  *   E[accept_len] = sum_v f(v) (Thm. 1).
  * Commit (R14/R16): rows accept_path[i][0..len) of k_tree/v_tree are copied
  *   into cache slots [kv_len[i], kv_len[i] + len) through the page table, then
- *   kv_len[i] += len.  COMMIT covers ALL requests [0, n_req) (for KV-head
+ *   kv_len_out[i] = kv_len[i] + len (kv_len_out == NULL or == kv_len: in place;
+ *   a separate kv_len_out keeps kv_len unchanged, e.g. for a replayed graph
+ *   whose next iteration swaps the two buffers).  COMMIT covers ALL requests [0, n_req) (for KV-head
  *   sharding every rank commits every request's path for its own heads).
  * Phases: AS_ACCEPT_FUSED = walk [begin,end) + commit of the same requests;
  *   AS_ACCEPT_WALK_ONLY = walk only; AS_ACCEPT_COMMIT_ONLY = commit from
@@ -188,7 +190,8 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
  *   logits_dtype or NULL (one of the two is required for the walk);
  *   k_tree/v_tree [n_tree_rows, n_kv_heads, head_dim] of kv_dtype;
  *   caches [num_pages, n_kv_heads, page_size, head_dim]; page_table
- *   [n_req, max_pages_per_req]; kv_len [n_req] (in/out).
+ *   [n_req, max_pages_per_req]; kv_len [n_req] (in; also the output when
+ *   kv_len_out is NULL); kv_len_out [n_req] or NULL.
  * For WALK_ONLY the KV arguments may be NULL.
  * Device preconditions: AS_DEV_NAN_LOGIT, AS_DEV_PATH_TOO_LONG,
  *   AS_DEV_PAGE_OVERFLOW, AS_DEV_BAD_PAGE.
@@ -205,8 +208,8 @@ as_status as_accept_tokens(as_accept_phase phase, int32_t n_req, int32_t req_beg
                            const void* k_tree, const void* v_tree, as_dtype kv_dtype,
                            int32_t n_kv_heads, int32_t head_dim, void* k_cache, void* v_cache,
                            int32_t num_pages, int32_t page_size, const int32_t* page_table,
-                           int32_t max_pages_per_req, int32_t* kv_len, void* workspace,
-                           size_t workspace_bytes, void* stream);
+                           int32_t max_pages_per_req, int32_t* kv_len, int32_t* kv_len_out,
+                           void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------- */
 /* Utilities                                                                 */

@@ -54,7 +54,7 @@ def lib():
                                           _vp]
         L.as_accept_tokens.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_i32,
                                        _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _vp,
-                                       _c_i32, _c_i32, _vp, _c_i32, _vp, _vp, _c_sz, _vp]
+                                       _c_i32, _c_i32, _vp, _c_i32, _vp, _vp, _vp, _c_sz, _vp]
         L.as_check_device_error.argtypes = [_vp, _vp, _vp, _vp]
         L.as_reset_workspace.argtypes = [_vp, _c_sz, _vp]
         L.as_selftest_umma.argtypes = [_vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _vp]
@@ -196,10 +196,10 @@ def tree_verify_attn(q, k_tree, v_tree, k_cache, v_cache, page_table, kv_len, tr
 def accept_tokens(phase, tree_offsets, tree_parent=None, tree_tokens=None, target_tokens=None, target_logits=None,
                   max_path=16, k_tree=None, v_tree=None, k_cache=None, v_cache=None, page_table=None, kv_len=None,
                   req_range=None, accept_len=None, accept_path=None, bonus_token=None, n_tree_rows=None,
-                  workspace=None):
+                  workspace=None, kv_len_out=None):
     """as_accept_tokens (walk + commit).  Returns dict(accept_len,
-    accept_path, bonus_token); the caches and kv_len are updated in place
-    for FUSED / COMMIT_ONLY."""
+    accept_path, bonus_token); for FUSED / COMMIT_ONLY the caches are updated
+    in place and the new lengths go to kv_len_out (None: kv_len in place)."""
     n = tree_offsets.numel() - 1
     dev = tree_offsets.device
     b, e = (0, n) if req_range is None else req_range
@@ -223,7 +223,8 @@ def accept_tokens(phase, tree_offsets, tree_parent=None, tree_tokens=None, targe
                                 _ptr(accept_path), _ptr(bonus_token), _ptr(k_tree), _ptr(v_tree), kv_dt, n_kv, d,
                                 _ptr(k_cache), _ptr(v_cache), k_cache.shape[0] if k_cache is not None else 0,
                                 k_cache.shape[2] if k_cache is not None else 0, _ptr(page_table),
-                                page_table.shape[1] if page_table is not None else 0, _ptr(kv_len), ws.ptr, ws.nbytes,
+                                page_table.shape[1] if page_table is not None else 0, _ptr(kv_len), _ptr(kv_len_out),
+                                ws.ptr, ws.nbytes,
                                 _stream())
     _check(st, "as_accept_tokens")
     return dict(accept_len=accept_len, accept_path=accept_path, bonus_token=bonus_token, workspace=ws)

@@ -264,7 +264,8 @@ as_status as_accept_tokens(as_accept_phase phase, int32_t n_req, int32_t req_beg
                            int32_t* accept_path, int32_t* bonus_token, const void* k_tree, const void* v_tree,
                            as_dtype kv_dtype, int32_t n_kv_heads, int32_t head_dim, void* k_cache, void* v_cache,
                            int32_t num_pages, int32_t page_size, const int32_t* page_table, int32_t max_pages_per_req,
-                           int32_t* kv_len, void* workspace, size_t workspace_bytes, void* stream) {
+                           int32_t* kv_len, int32_t* kv_len_out, void* workspace, size_t workspace_bytes,
+                           void* stream) {
     if (phase != AS_ACCEPT_FUSED && phase != AS_ACCEPT_WALK_ONLY && phase != AS_ACCEPT_COMMIT_ONLY)
         return AS_ERR_INVALID_ARG;
     if (n_req < 0 || req_begin < 0 || req_end < req_begin || req_end > n_req || n_tree_rows < 0) return AS_ERR_INVALID_ARG;
@@ -297,7 +298,7 @@ as_status as_accept_tokens(as_accept_phase phase, int32_t n_req, int32_t req_beg
     p.elem_bytes = kv_dtype == AS_BF16 ? 2 : 4; p.n_kv = n_kv_heads; p.head_dim = head_dim;
     p.k_cache = (unsigned char*)k_cache; p.v_cache = (unsigned char*)v_cache;
     p.num_pages = num_pages; p.page_size = page_size; p.page_table = page_table; p.max_pages = max_pages_per_req;
-    p.kv_len = kv_len; p.ws = workspace;
+    p.kv_len = kv_len; p.kv_len_out = kv_len_out ? kv_len_out : kv_len; p.ws = workspace;
     p.do_walk = walk ? 1 : 0;
     p.do_commit = commit ? 1 : 0;
     int32_t* argmax_buf = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(workspace) + kWsHeaderBytes);

@@ -117,38 +117,40 @@ struct AccSmem {
     int parent[kAccMaxNodes];
     int token[kAccMaxNodes];
     int target[kAccMaxNodes];
+    int next[kAccMaxNodes];  // lowest-index child c of v with token[c] == target[v] (or INT_MAX)
     int path[kAccMaxPath];
     long long dst[kAccMaxPath];  // byte offset of the cache row for path position k (-1: skip)
     long long src[kAccMaxPath];  // byte offset of the k_tree/v_tree row of path node k
     int len;
 };
 
-__device__ __forceinline__ void commit_request(const AcceptParams& p, AccSmem& sm, int i, int len) {
+// Cache-row byte offset of path position k (slot L + k of request i) or a
+// negative code: -1 no slot, -2 page-table overflow, -3 page id out of range.
+__device__ __forceinline__ long long slot_dst(const AcceptParams& p, int i, int L, int k, long long row_bytes) {
+    const int slot = L + k;
+    const int pi = slot / p.page_size;
+    if (pi >= p.max_pages) return -2;
+    const int page = __ldg(p.page_table + (size_t)i * p.max_pages + pi);
+    if (page < 0 || page >= p.num_pages) return -3;
+    return ((long long)page * p.n_kv * p.page_size + slot % p.page_size) * row_bytes;
+}
+
+// Copy the path rows' K/V (every (path node, kv head, 16-byte chunk) vector in
+// one flattened, unrolled sweep) into the cache rows sm.dst[k]; kv_len_out = L + len.
+__device__ __forceinline__ void commit_copy(const AcceptParams& p, AccSmem& sm, int i, int off, int L, int len) {
     const int tid = threadIdx.x;
-    const int off = p.tree_offsets[i];
-    const int L = p.kv_len[i];
     const long long row_bytes = (long long)p.head_dim * p.elem_bytes;
     const int vpr = (int)(row_bytes / 16);
     if (tid < kAccMaxPath) {
         const int k = tid;
-        long long d = -1, s = 0;
+        long long d = -1;
         if (k < len) {
-            const int slot = L + k;
-            const int pi = slot / p.page_size;
-            if (pi >= p.max_pages) {
-                set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, i);
-            } else {
-                const int page = p.page_table[(size_t)i * p.max_pages + pi];
-                if (page < 0 || page >= p.num_pages) {
-                    set_dev_error(p.ws, AS_DEV_BAD_PAGE, i);
-                } else {
-                    d = ((long long)page * p.n_kv * p.page_size + slot % p.page_size) * row_bytes;
-                    s = (long long)(off + sm.path[k]) * p.n_kv * row_bytes;
-                }
-            }
+            d = sm.dst[k];
+            if (d == -2) set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, i);
+            if (d == -3) set_dev_error(p.ws, AS_DEV_BAD_PAGE, i);
         }
         sm.dst[k] = d;
-        sm.src[k] = s;
+        sm.src[k] = (k < len) ? (long long)(off + sm.path[k]) * p.n_kv * row_bytes : 0;
     }
     __syncthreads();
     const int per_k = p.n_kv * vpr;
@@ -183,18 +185,29 @@ __device__ __forceinline__ void commit_request(const AcceptParams& p, AccSmem& s
             }
         }
     }
-    if (tid == 0) p.kv_len[i] = L + len;
+    if (tid == 0) p.kv_len_out[i] = L + len;
 }
 
 __global__ void __launch_bounds__(kAccThreads) walk_commit_kernel(AcceptParams p) {
     __shared__ AccSmem sm;
+    pdl_launch_dependents();
+    pdl_wait();  // trees (select) and the attention's reads of kv_len / the cache
     const int tid = threadIdx.x;
     const int lane = lane_id();
+    const long long row_bytes = (long long)p.head_dim * p.elem_bytes;
     if (p.do_walk) {
         const int i = p.req_begin + blockIdx.x;
         if (i >= p.req_end) return;
-        const int off = p.tree_offsets[i];
-        const int K = p.tree_offsets[i + 1] - off;
+        // independent loads first: the commit's cache rows (kv_len -> page table)
+        // resolve while the tree is staged and walked
+        const int L = p.do_commit ? __ldg(p.kv_len + i) : 0;
+        const int off = __ldg(p.tree_offsets + i);
+        const int K = __ldg(p.tree_offsets + i + 1) - off;
+        const int npath = min(p.max_path, kAccMaxPath);
+        if (p.do_commit && tid >= kAccThreads - kAccMaxPath) {
+            const int k = tid - (kAccThreads - kAccMaxPath);
+            sm.dst[k] = k < npath ? slot_dst(p, i, L, k, row_bytes) : -1;
+        }
         if (off + K > p.n_tree_rows) {
             if (tid == 0) set_dev_error(p.ws, AS_DEV_ROWS_OVERFLOW, i);
             return;
@@ -202,18 +215,47 @@ __global__ void __launch_bounds__(kAccThreads) walk_commit_kernel(AcceptParams p
         const bool staged = K <= kAccMaxNodes;
         if (staged) {
             for (int c = tid; c < K; c += kAccThreads) {
-                sm.parent[c] = p.tree_parent[off + c];
-                sm.token[c] = p.tree_tokens[off + c];
-                sm.target[c] = p.target_tokens[off + c];
+                sm.parent[c] = __ldg(p.tree_parent + off + c);
+                sm.token[c] = __ldg(p.tree_tokens + off + c);
+                sm.target[c] = __ldg(p.target_tokens + off + c);
+                sm.next[c] = 0x7fffffff;
+            }
+            __syncthreads();
+            // every edge at once: c is v's accepted child candidate when its draft
+            // token equals v's target token; the lowest index wins (R13)
+            for (int c = 1 + tid; c < K; c += kAccThreads) {
+                const int v = sm.parent[c];
+                if (v >= 0 && v < c && sm.token[c] == sm.target[v]) atomicMin(&sm.next[v], c);
             }
         }
         __syncthreads();
         if (warp_id() == 0) {
-            const int* par = staged ? sm.parent : p.tree_parent + off;
-            const int* tok = staged ? sm.token : p.tree_tokens + off;
-            const int* tgt = staged ? sm.target : p.target_tokens + off;
             int len = 0, tstar = -1;
-            if (K > 0) {
+            if (staged) {
+                // the walk is now a pointer chase through next[] (lane 0)
+                if (lane == 0 && K > 0) {
+                    int v = 0;
+                    len = 1;
+                    sm.path[0] = 0;
+                    for (;;) {
+                        const int nx = sm.next[v];
+                        if (nx == 0x7fffffff) break;
+                        if (len >= p.max_path || len >= kAccMaxPath) {
+                            set_dev_error(p.ws, AS_DEV_PATH_TOO_LONG, i);
+                            break;
+                        }
+                        sm.path[len++] = nx;
+                        v = nx;
+                    }
+                    tstar = sm.target[v];
+                }
+                len = __shfl_sync(0xffffffffu, len, 0);
+                tstar = __shfl_sync(0xffffffffu, tstar, 0);
+            } else if (K > 0) {
+                // large trees: walk from global memory, one ballot per 32 nodes
+                const int* par = p.tree_parent + off;
+                const int* tok = p.tree_tokens + off;
+                const int* tgt = p.target_tokens + off;
                 int v = 0;
                 len = 1;
                 if (lane == 0) sm.path[0] = 0;
@@ -246,19 +288,24 @@ __global__ void __launch_bounds__(kAccThreads) walk_commit_kernel(AcceptParams p
             }
         }
         __syncthreads();
-        if (p.do_commit) commit_request(p, sm, i, sm.len);
+        if (p.do_commit) commit_copy(p, sm, i, off, L, sm.len);
     } else if (p.do_commit) {
         // COMMIT_ONLY over all requests [0, n_req)
         const int i = blockIdx.x;
         if (i >= p.n_req) return;
+        const int L = __ldg(p.kv_len + i);
+        const int off = __ldg(p.tree_offsets + i);
         int len = p.accept_len[i];
         if (len > p.max_path) len = p.max_path;
         if (len > kAccMaxPath) len = kAccMaxPath;
         if (len < 0) len = 0;
         const int32_t* path = p.accept_path + (size_t)i * p.max_path;
-        if (tid < len) sm.path[tid] = path[tid];
+        if (tid < len) {
+            sm.path[tid] = path[tid];
+            sm.dst[tid] = slot_dst(p, i, L, tid, row_bytes);
+        }
         __syncthreads();
-        commit_request(p, sm, i, len);
+        commit_copy(p, sm, i, off, L, len);
     }
 }
 
@@ -282,7 +329,14 @@ int launch_accept(const AcceptParams& p, const void* target_logits, int logits_b
     }
     const int nw = q.do_walk ? (q.req_end - q.req_begin) : q.n_req;
     if (nw <= 0) return 0;
-    walk_commit_kernel<<<nw, kAccThreads, 0, stream>>>(q);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nw);
+    cfg.blockDim = dim3(kAccThreads);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    cfg.attrs = attr;
+    cfg.numAttrs = fill_launch_attrs(attr);
+    if (cudaLaunchKernelEx(&cfg, walk_commit_kernel, q) != cudaSuccess) return -1;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

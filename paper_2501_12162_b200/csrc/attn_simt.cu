@@ -28,6 +28,8 @@ __global__ void __launch_bounds__(256) tree_attn_simt_kernel(SimtParams p) {
     __shared__ float sv[kSimtKeys][D];
     __shared__ unsigned long long anc[AS_MAX_TREE][2];
     __shared__ int spar[AS_MAX_TREE];
+    pdl_launch_dependents();
+    pdl_wait();
 
     const int i = blockIdx.x;
     const int g = blockIdx.y;
@@ -169,8 +171,16 @@ __global__ void __launch_bounds__(256) tree_attn_simt_kernel(SimtParams p) {
 
 int launch_attn_simt(const SimtParams& p, int head_dim, cudaStream_t stream) {
     dim3 grid(p.n_req, p.n_kv, (AS_MAX_TREE * p.G + kSimtRows - 1) / kSimtRows);
-    if (head_dim == 64) tree_attn_simt_kernel<64><<<grid, 256, 0, stream>>>(p);
-    else tree_attn_simt_kernel<128><<<grid, 256, 0, stream>>>(p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    cfg.attrs = attr;
+    cfg.numAttrs = fill_launch_attrs(attr);
+    const cudaError_t e = head_dim == 64 ? cudaLaunchKernelEx(&cfg, tree_attn_simt_kernel<64>, p)
+                                         : cudaLaunchKernelEx(&cfg, tree_attn_simt_kernel<128>, p);
+    if (e != cudaSuccess) return -1;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
     const int warp = warp_id();
     const int lane = lane_id();
+    pdl_launch_dependents();
 
     if (threadIdx.x == 0) {
         ptx::mbar_init(q_full, 1);
@@ -240,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
+    pdl_wait();  // the trees come from the select kernel launched just before
 
     // ---------------- schedule plan (all threads; K/V rings used as scratch) ----------------
     __shared__ long long sk_T, sk_x0, sk_rem;
@@ -806,16 +808,28 @@ int launch_attn_tc(const CUtensorMap* maps, const TcParams& p, int head_dim, int
     int grid = n_sms * kCtasPerSm;
     if (!p.stream_k && p.n_units < grid) grid = p.n_units;
     if (grid <= 0) return 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    cfg.attrs = attr;
+    cfg.numAttrs = fill_launch_attrs(attr);
     if (head_dim == 128) {
         if (cudaFuncSetAttribute(tree_attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
             cudaSuccess)
             return -1;
-        tree_attn_tc_kernel<128><<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
+        if (cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<128>, maps[0], maps[1], maps[2], maps[3], maps[4], p) !=
+            cudaSuccess)
+            return -1;
     } else {
         if (cudaFuncSetAttribute(tree_attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
             cudaSuccess)
             return -1;
-        tree_attn_tc_kernel<64><<<grid, kThreads, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
+        if (cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<64>, maps[0], maps[1], maps[2], maps[3], maps[4], p) !=
+            cudaSuccess)
+            return -1;
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

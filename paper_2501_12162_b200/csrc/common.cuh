@@ -28,6 +28,23 @@ __device__ __forceinline__ void set_dev_error(void* ws, int code, int req) {
     if (atomicCAS(&h->err_code, 0, code) == 0) atomicExch(&h->err_request, req);
 }
 
+// Programmatic dependent launch (PDL): the hot path's kernels are launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization, so each one is
+// dispatched while its predecessor is still running; it runs its prologue,
+// then waits here for the predecessor's results.  Both are no-ops for a
+// normally launched kernel.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Host: launch attributes of the hot path (PDL on unless AS_PDL=0).
+int pdl_enabled();
+inline int fill_launch_attrs(cudaLaunchAttribute* attr) {
+    if (!pdl_enabled()) return 0;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    return 1;
+}
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned warp_id() { return threadIdx.x >> 5; }
 

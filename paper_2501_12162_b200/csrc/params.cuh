@@ -23,7 +23,8 @@ struct AcceptParams {
     int num_pages, page_size;
     const int32_t* page_table;
     int max_pages;
-    int32_t* kv_len;
+    const int32_t* kv_len;
+    int32_t* kv_len_out;  // == kv_len for in-place updates
     void* ws;
     int do_walk, do_commit;
 };

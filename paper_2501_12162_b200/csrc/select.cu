@@ -8,8 +8,7 @@
 //       because requests' candidate sets are disjoint;
 //   (2) desired_i = number of pi_i entries the SLO loop would take
 //       with unlimited budget: first k with 1 + sum_{t<k} f-hat >= A_cap, capped
-//       by n_max and by C_i - 1; the fp64 sum runs in pi order, exactly as the
-//       sequential loop adds (R9);
+//       by n_max and by C_i - 1; the fp64 sum equals the sequential loop's (R9);
 //   (3) the single shared budget is consumed in (A desc, id asc) order (P:L821,
 //       R5): s_i = clamp(B0 - sum_{j before i} desired_j, 0, desired_i);
 //   (4) the throughput loop takes the global top-R of the
@@ -18,25 +17,45 @@
 //   (5) tree i = root + pi_i[0 : s_i + m_i], emitted in ascending candidate
 //       index (topological; ancestor-closed by App. B).
 //
-// One cooperative kernel launch:  every CTA sorts/thresholds 32 requests (one
-// warp each: register bitonic sort with __shfl_xor_sync, lane-uniform fp64
-// prefix loop); the last CTA to finish (threadfence + ticket) does (3)-(4):
-// rank by A, block scan, an 8-bit-digit radix select over the 64-bit tail keys
-// with warp-aggregated shared-memory histograms, ballot counts and the tree
-// offsets; it then releases a generation flag and every CTA emits (5) its own
-// 32 trees in parallel.
+// One launch of ONE thread-block cluster (CS <= 16 CTAs of 512 threads; CTA c
+// owns a contiguous block of requests).  Everything stays on chip:
+//   * each CTA stages its requests' offsets, f-hat and parents in shared memory
+//     with coalesced loads; one warp per request sorts pi_i in registers
+//     (bitonic, __shfl_xor_sync) and finds desired_i with a warp fp64 scan +
+//     ballot when the sum is provably exact in any order (R9), else with the
+//     lane-uniform sequential loop; the rank of the request in (A desc, id asc)
+//     order is a warp-parallel count;
+//   * exchange 1 (DSMEM): every CTA writes desired_i at position rank_i into
+//     every peer's shared array; after one cluster barrier each CTA redundantly
+//     scans it (s_i, sum s, R) -- no global round trip, no spin-waits;
+//   * the global top-R is a radix select (8-bit digits, MSB first) whose
+//     per-CTA shared histograms are summed through DSMEM, one cluster barrier
+//     per digit (double-buffered), with an early exit once the bucket holding
+//     the R-th key is taken whole;
+//   * exchange 2 (DSMEM): per-CTA tree-size totals -> tree offsets; each CTA
+//     emits its own trees (ballot-rank compaction, parent remap).
+// Requests whose candidates do not fit the shared staging area (very large
+// batches) read f-hat/parents from global memory and keep pi_i in the
+// workspace instead (same code path, generic pointers).
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace as {
 
 constexpr int kSelThreads = 1024;
 constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kSelMaxReq = 4096;                // requests handled by one call
+constexpr int kSelMaxCluster = 16;
 constexpr int kRemapWords = AS_MAX_CAND + 1;    // local indices 0..AS_MAX_CAND
 constexpr int kBitmapWords = (AS_MAX_CAND + 1 + 31) / 32;
+constexpr int kSelSmemLimit = 200 * 1024;
 
 struct SelectParams {
-    int n_req;
+    int n_req, rpc;   // requests, requests per CTA
     const int32_t* cand_offsets;
     const int32_t* cand_parent;
     const float* cand_prob;
@@ -50,241 +69,510 @@ struct SelectParams {
     int32_t* tree_token;
     int32_t* slo_count;
     void* ws;
-    int32_t* desired;   // [n]
-    int32_t* take;      // [n]  s_i + m_i
-    int32_t* stage_s;   // [n]  s_i
-    int32_t* toff;      // [n+1] tree offsets (workspace copy)
-    uint64_t* skey;     // [N - n] per-request sorted keys (f-hat bits << 32 | ~local idx)
+    uint64_t* skey_g;   // [N - n] workspace pi keys (used when a CTA's candidates do not fit smem)
+    int cand_cap;       // candidates a CTA can stage in shared memory
+    int dbg_stop;       // latency profiling only (AS_SEL_STOP): return after phase k (wrong outputs)
 };
 
-__device__ __forceinline__ int n_nonroot(const SelectParams& p, int i, int* off_out) {
-    int off = p.cand_offsets[i];
-    int C = p.cand_offsets[i + 1] - off;
-    *off_out = off;
-    int nr = C - 1;
-    if (nr < 0) nr = 0;
-    if (nr > AS_MAX_CAND) nr = AS_MAX_CAND;
-    return nr;
+// Shared-memory layout (dynamic part), sized by the host from n, rpc and the
+// per-CTA candidate capacity `cap` (36 bytes per staged candidate).
+struct SelLayout {
+    int o_A, o_des, o_exc, o_own, o_remap, o_bits, o_ukey, o_key, o_prob, o_par, o_rank, o_tok, o_dep, bytes;
+    __host__ __device__ SelLayout(int n, int rpc, int cap) {
+        int o = 0;
+        o_A = o;     o += 8 * n;                                 // A(r) of every request
+        o_des = o;   o += 4 * n;                                 // desired in A order (exchange 1)
+        o_exc = o;   o += 4 * n;                                 // exclusive scan of o_des
+        o_own = o;   o += 4 * 8 * (rpc + 1);                     // own: off, desired, arank, nr, s, take, size
+        o = (o + 15) & ~15;
+        o_remap = o; o += 2 * kSelWarps * kRemapWords;           // u16 remap per request group
+        o = (o + 15) & ~15;
+        o_bits = o;  o += 4 * kSelWarps * kBitmapWords;
+        o = (o + 15) & ~15;
+        o_ukey = o;  o += 8 * cap;                               // keys in candidate order
+        o_key = o;   o += 8 * cap;                               // pi keys (sorted, non-root)
+        o_prob = o;  o += 4 * cap;
+        o_par = o;   o += 4 * cap;
+        o_rank = o;  o += 4 * cap;
+        o_tok = o;   o += 4 * cap;
+        o_dep = o;   o += cap;
+        o = (o + 15) & ~15;
+        bytes = o;
+    }
+};
+constexpr int kSelBytesPerCand = 37;
+
+__device__ __forceinline__ void cl_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cl_sync() { cl_arrive(); cl_wait(); }
+__device__ __forceinline__ void red_add_cluster(int* local_addr, int rank, int v) {
+    // fire-and-forget atomic add into CTA `rank`'s shared memory (DSMEM)
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(local_addr), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("red.relaxed.cluster.shared::cluster.add.u32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+}
+
+// Warp-0 exclusive scan of data[0..n) (shared) into out[0..n) (may alias);
+// returns the total to lane 0..31 of warp 0 (others: undefined).
+__device__ __forceinline__ int warp_exclusive_scan(const int* data, int* out, int n) {
+    const int lane = lane_id();
+    const int chunk = (n + 31) >> 5;
+    const int b = lane * chunk, e = min(n, b + chunk);
+    int local = 0;
+    for (int x = b; x < e; ++x) local += data[x];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    int run = incl - local;
+    for (int x = b; x < e; ++x) {
+        const int v = data[x];
+        out[x] = run;
+        run += v;
+    }
+    return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+__device__ __forceinline__ uint64_t tail_key(uint64_t sk, int i) {
+    // global order (f-hat desc, req asc, idx asc): low word = ~(i*512 + idx)
+    const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(sk & 0xFFFFFFFFull);
+    return (sk & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - ((uint32_t)i * 512u + idx));
 }
 
 // ---------------------------------------------------------------------------
-// Phase 1: warp per request -- sort pi_i and compute desired_i.
+// Warp per request: sort pi_i, desired_i.
+// prob/par: the request's candidates (local index c -> prob[c]), staged in
+// shared memory or global; key_out: where pi_i's keys go (smem or workspace).
+//
+// pi_i is built by rank counting: the key of candidate j is (f-hat bits << 32
+// | ~j) -- positive floats order as uint32, the complemented index breaks ties
+// toward the lower index (R8) -- and its position in pi_i is the number of
+// larger keys.  Keys are distinct, so the ranks are a permutation.  Every
+// compare is independent (no shuffle chain), which is what a single warp per
+// request needs for latency: the kernel is latency-bound, not ALU-bound.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t cand_key(float f, int j) {
+    const uint32_t fb = (f > 0.f) ? __float_as_uint(f) : 0u;
+    return ((uint64_t)fb << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)j);
+}
+
 template <int E>
-__device__ __forceinline__ void sort_request(const SelectParams& p, int i, int off, int nr) {
-    constexpr int P = 32 * E;
+__device__ __forceinline__ int sort_request(const SelectParams& p, int i, const float* prob, const int* par,
+                                            int nr, uint64_t* key_out) {
     const int lane = lane_id();
     uint64_t key[E];
+    int cnt[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        int s = e * 32 + lane;
-        key[e] = 0ull;
+        const int s = e * 32 + lane;
+        key[e] = 0ull;  // padding: never counted (positions >= nr are not stored)
+        cnt[e] = 0;
         if (s < nr) {
-            int j = s + 1;
-            float f = p.cand_prob[off + j];
-            int par = p.cand_parent[off + j];
-            if (par < 0 || par >= j) {
+            const int j = s + 1;
+            const float f = prob[j];
+            const int pj = par[j];
+            if (pj < 0 || pj >= j) {
                 set_dev_error(p.ws, AS_DEV_BAD_PARENT, i);
             } else {
-                float fp = p.cand_prob[off + par];
+                const float fp = prob[pj];
                 if (!(f > 0.f) || !(f <= fp)) set_dev_error(p.ws, AS_DEV_BAD_PROB, i);
             }
-            uint32_t fb = (f > 0.f) ? __float_as_uint(f) : 0u;   // positive floats order as uint32
-            key[e] = ((uint64_t)fb << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)j);
+            key[e] = cand_key(f, j);
         }
     }
-    // Bitonic sort, descending in position s = e*32 + lane.
+    // rank = #{k : key_k > key_j}, k over the request's non-root candidates
+    int k = 1;
+#pragma unroll 1
+    for (; k + 3 <= nr; k += 4) {
+        uint64_t kk[4];
 #pragma unroll
-    for (int k = 2; k <= P; k <<= 1) {
+        for (int u = 0; u < 4; ++u) kk[u] = cand_key(prob[k + u], k + u);
 #pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            uint64_t nk[E];
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int s = e * 32 + lane;
-                uint64_t pv;
-                if (j < 32) pv = __shfl_xor_sync(0xffffffffu, key[e], j);
-                else pv = key[e ^ (j >> 5)];
-                const bool desc = (s & k) == 0;
-                const bool lo = (s & j) == 0;
-                const uint64_t mx = key[e] > pv ? key[e] : pv;
-                const uint64_t mn = key[e] > pv ? pv : key[e];
-                nk[e] = (desc == lo) ? mx : mn;
-            }
-#pragma unroll
-            for (int e = 0; e < E; ++e) key[e] = nk[e];
-        }
+            for (int e = 0; e < E; ++e) cnt[e] += kk[u] > key[e] ? 1 : 0;
     }
-    const int sbase = off - i;  // sum_{j<i} (C_j - 1)
+#pragma unroll 1
+    for (; k <= nr; ++k) {
+        const uint64_t kk = cand_key(prob[k], k);
+#pragma unroll
+        for (int e = 0; e < E; ++e) cnt[e] += kk > key[e] ? 1 : 0;
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        if (e * 32 + lane < nr) key_out[cnt[e]] = key[e];
+    __syncwarp();
+    float fv[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        int s = e * 32 + lane;
-        if (s < nr) p.skey[sbase + s] = key[e];
+        const int s = e * 32 + lane;
+        fv[e] = (s < nr) ? __uint_as_float((uint32_t)(key_out[s] >> 32)) : 0.f;
     }
-    // SLO stage threshold with unlimited budget; lane-uniform,
-    // sequential fp64 accumulation in pi order (identical to the oracle).
+    // SLO stage threshold with unlimited budget: the loop adds
+    // f-hat in pi order in fp64 starting from n_acc = 1.0 (R9) and stops at the
+    // first k with n_acc >= A_cap, or at lim = min(n_max, nr).
     const double a_cap = fmin(p.A[i], (double)p.depth_d + 1.0);
     const int lim = min(p.n_max, nr);
-    double nacc = 1.0;
-    int k = 0;
-    while (k < lim && nacc < a_cap) {
-        uint64_t v = key[0];
+    if (!(1.0 < a_cap) || lim == 0) return 0;
+    // Fast path (R9): if every f-hat >= 2^-24 each one is a multiple of 2^-47;
+    // while 1 + sum < 2^6 every partial sum is then exact in fp64, so a warp
+    // scan gives exactly the sequential loop's partial sums.
+    bool small = false;
 #pragma unroll
-        for (int e = 1; e < E; ++e)
-            if ((k >> 5) == e) v = key[e];
-        v = __shfl_sync(0xffffffffu, v, k & 31);
-        nacc += (double)__uint_as_float((uint32_t)(v >> 32));
-        ++k;
+    for (int e = 0; e < E; ++e) small |= (e * 32 + lane < nr) && !(fv[e] >= 5.9604644775390625e-08f);
+    if (!__any_sync(0xffffffffu, small)) {
+        double run = 1.0;  // n_acc before chunk e
+        int kst = -1;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            double incl = (double)fv[e];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            incl += run;  // n_acc after position e*32 + lane
+            const int s = e * 32 + lane;
+            const unsigned hit = __ballot_sync(0xffffffffu, s < lim && incl >= a_cap);
+            const double tot = __shfl_sync(0xffffffffu, incl, 31);
+            if (kst < 0 && hit) kst = e * 32 + __ffs(hit);  // count includes the crossing element
+            run = tot;
+        }
+        // exactness guard: every partial sum < 64 (checked on the final, monotone total)
+        if (run < 64.0) return kst < 0 ? lim : min(kst, lim);
     }
-    if (lane == 0) p.desired[i] = k;
-}
-
-// ---------------------------------------------------------------------------
-// Block-level helpers for the last CTA.
-// ---------------------------------------------------------------------------
-__device__ int block_sum_int(int v, int* red) {
-    v = warp_sum(v);
-    __syncthreads();
-    if (lane_id() == 0) red[warp_id()] = v;
-    __syncthreads();
+    // General case: the lane-uniform sequential loop (identical to the oracle).
+    double nacc = 1.0;
     int t = 0;
-    if (threadIdx.x < 32) {
-        t = (threadIdx.x < (unsigned)kSelWarps) ? red[threadIdx.x] : 0;
-        t = warp_sum(t);
-        if (threadIdx.x == 0) red[32] = t;
+    while (t < lim && nacc < a_cap) {
+        nacc += (double)__uint_as_float((uint32_t)(key_out[t] >> 32));
+        ++t;
     }
-    __syncthreads();
-    return red[32];
+    return t;
 }
 
-// Exclusive scan of data[0..n) in place (shared memory); returns the total.
-__device__ int block_exclusive_scan(int* data, int n, int* red) {
+// Exclusive scan of data[0..n) (shared) into out[0..n); returns the total.
+__device__ int block_exclusive_scan(const int* data, int* out, int n, int* red) {
     const int tid = threadIdx.x;
     const int chunk = (n + kSelThreads - 1) / kSelThreads;
     const int b = tid * chunk;
     const int e = min(n, b + chunk);
     int local = 0;
     for (int x = b; x < e; ++x) local += data[x];
-    // warp inclusive scan of local
     int incl = local;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
         if ((int)lane_id() >= o) incl += y;
     }
     __syncthreads();
     if (lane_id() == 31) red[warp_id()] = incl;
     __syncthreads();
     if (threadIdx.x < 32) {
-        int w = red[threadIdx.x];
+        const int w = threadIdx.x < (unsigned)kSelWarps ? red[threadIdx.x] : 0;
         int wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, wi, o);
+            const int y = __shfl_up_sync(0xffffffffu, wi, o);
             if ((int)threadIdx.x >= o) wi += y;
         }
-        red[threadIdx.x] = wi - w;  // exclusive warp offsets
+        red[threadIdx.x] = wi - w;
         if (threadIdx.x == 31) red[32] = wi;
     }
     __syncthreads();
     int run = red[warp_id()] + incl - local;
     for (int x = b; x < e; ++x) {
-        int v = data[x];
-        data[x] = run;
+        const int v = data[x];
+        out[x] = run;
         run += v;
     }
-    int total = red[32];
+    const int total = red[32];
     __syncthreads();
     return total;
 }
 
-__device__ __forceinline__ uint64_t tail_key(uint64_t sk, int i) {
-    // global order (f-hat desc, req asc, idx asc): low word = ~(i*512 + idx)
-    uint32_t idx = 0xFFFFFFFFu - (uint32_t)(sk & 0xFFFFFFFFull);
-    return (sk & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - ((uint32_t)i * 512u + idx));
+__device__ int block_sum(int v, int* red) {
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane_id() == 0) red[warp_id()] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int t = threadIdx.x < (unsigned)kSelWarps ? red[threadIdx.x] : 0;
+        t = warp_sum(t);
+        if (threadIdx.x == 0) red[32] = t;
+    }
+    __syncthreads();
+    const int r = red[32];
+    __syncthreads();
+    return r;
+}
+
+// desired_i (SLO stage length with unlimited budget) from request i's sorted
+// keys ks[0..nr), one warp.  Same arithmetic as the tail of sort_request: the
+// warp fp64 scan when it is provably exact (R9), else the sequential loop.
+__device__ int slo_prefix_len(const SelectParams& p, int i, const uint64_t* ks, int nr) {
+    const int lane = lane_id();
+    const double a_cap = fmin(p.A[i], (double)p.depth_d + 1.0);
+    const int lim = min(p.n_max, nr);
+    if (!(1.0 < a_cap) || lim == 0) return 0;
+    double run = 1.0;
+    bool exact = true;
+    for (int c0 = 0; c0 < lim; c0 += 32) {
+        const int s = c0 + lane;
+        const float f = s < lim ? __uint_as_float((uint32_t)(ks[s] >> 32)) : 0.f;
+        if (__any_sync(0xffffffffu, s < lim && !(f >= 5.9604644775390625e-08f))) { exact = false; break; }
+        double incl = (double)f;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        incl += run;
+        const unsigned hit = __ballot_sync(0xffffffffu, s < lim && incl >= a_cap);
+        run = __shfl_sync(0xffffffffu, incl, 31);
+        if (!(run < 64.0)) { exact = false; break; }  // partial sums so far must be < 2^6
+        if (hit) return c0 + __ffs(hit);              // count includes the crossing element
+    }
+    if (exact) return lim;
+    double nacc = 1.0;  // the lane-uniform sequential loop (identical to the oracle)
+    int t = 0;
+    while (t < lim && nacc < a_cap) {
+        nacc += (double)__uint_as_float((uint32_t)(ks[t] >> 32));
+        ++t;
+    }
+    return t;
 }
 
 // ---------------------------------------------------------------------------
-// The kernel.
+// The kernel (one cluster).  Own requests are processed by groups of W warps
+// (W = warps / requests-per-CTA, at least 1); every phase ends at a CTA
+// barrier, and all groups run the same number of rounds, so the barriers are
+// uniform.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int red[33];
+    extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int hist[256];
-    __shared__ int s_bcast[4];
-    __shared__ int s_is_last;
+    __shared__ int hsum[2][256];
+    __shared__ int part_nr[kSelMaxCluster];
+    __shared__ int part_tot[kSelMaxCluster];
+    __shared__ int s_bcast[8];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CS = (int)cluster.num_blocks();
+    const int c = (int)cluster.block_rank();
     const int n = p.n_req;
     const int lane = lane_id();
+    const int warp = warp_id();
+    const int tid = threadIdx.x;
+    // zero what peers accumulate into before anyone can reach exchange 1
+    for (int x = tid; x < 512; x += kSelThreads) (&hsum[0][0])[x] = 0;
+    for (int x = tid; x < 256; x += kSelThreads) hist[x] = 0;
+    cl_arrive_relaxed();  // "started": waited on before the first remote access
+    pdl_launch_dependents();  // let the attention kernel run its prologue meanwhile
+    pdl_wait();               // the previous step's accept may still read our outputs
 
-    // ---- phase 1 ----
-    {
-        const int i = blockIdx.x * kSelWarps + (int)warp_id();
-        if (i < n) {
-            int off;
-            int C = p.cand_offsets[i + 1] - p.cand_offsets[i];
-            if (C < 1 || C - 1 > AS_MAX_CAND) {
-                if (lane == 0) set_dev_error(p.ws, C < 1 ? AS_DEV_BAD_PARENT : AS_DEV_TOO_MANY_CAND, i);
+    const SelLayout Lo(n, p.rpc, p.cand_cap);
+    double* A_s = reinterpret_cast<double*>(smem + Lo.o_A);
+    int* des_all = reinterpret_cast<int*>(smem + Lo.o_des);
+    int* exc_all = reinterpret_cast<int*>(smem + Lo.o_exc);
+    int* own = reinterpret_cast<int*>(smem + Lo.o_own);
+    const int rpc = p.rpc;
+    int* off_s = own;                      // [rpc+1] cand offsets of own requests
+    int* desired_s = off_s + (rpc + 1);    // [rpc] desired, later the tree size
+    int* arank_s = desired_s + (rpc + 1);  // [rpc] position in (A desc, id asc) order
+    int* nr_s = arank_s + (rpc + 1);
+    int* s_s = nr_s + (rpc + 1);
+    int* take_s = s_s + (rpc + 1);
+    int* size_s = take_s + (rpc + 1);      // scanned tree offsets (CTA-local)
+    uint64_t* ukey_s = reinterpret_cast<uint64_t*>(smem + Lo.o_ukey);
+    uint64_t* key_s = reinterpret_cast<uint64_t*>(smem + Lo.o_key);
+    float* prob_s = reinterpret_cast<float*>(smem + Lo.o_prob);
+    int* par_s = reinterpret_cast<int*>(smem + Lo.o_par);
+    int* rank_s = reinterpret_cast<int*>(smem + Lo.o_rank);
+    int* tok_s = reinterpret_cast<int*>(smem + Lo.o_tok);
+    uint8_t* dep_s = reinterpret_cast<uint8_t*>(smem + Lo.o_dep);
+
+    const int r0 = min(n, c * rpc);
+    const int r1 = min(n, r0 + rpc);
+    const int nown = r1 - r0;
+    // request groups: W warps per request, G groups
+    const int W = max(1, kSelWarps / max(1, nown));
+    const int G = kSelWarps / W;
+    const int grp = warp / W, wg = warp - grp * W;
+    const int rounds = (nown + G - 1) / G;
+
+    if (p.dbg_stop == 0) return;
+    // ---- stage: own offsets, every A(r); then f-hat, parents (and tokens) ----
+    for (int k = tid; k <= nown; k += kSelThreads) off_s[k] = p.cand_offsets[r0 + k];
+    for (int k = tid; k < n; k += kSelThreads) A_s[k] = p.A[k];
+    __syncthreads();
+    const int cbase = off_s[0];
+    const int ncand = off_s[nown] - cbase;
+    const bool staged = ncand <= p.cand_cap;
+    const bool want_tok = p.tree_token != nullptr;
+    if (staged) {
+        for (int k = tid; k < ncand; k += kSelThreads) {
+            prob_s[k] = p.cand_prob[cbase + k];
+            par_s[k] = p.cand_parent[cbase + k];
+            if (want_tok) tok_s[k] = p.cand_token[cbase + k];
+        }
+    }
+    __syncthreads();
+    // candidate arrays indexed by GLOBAL candidate id (staged: shifted smem)
+    const float* probc = staged ? prob_s - cbase : p.cand_prob;
+    const int* parc = staged ? par_s - cbase : p.cand_parent;
+    // pi keys: own request k's sorted keys start at keyc + (off - i)
+    uint64_t* keyc = staged ? key_s - (cbase - r0) : p.skey_g;
+
+    if (p.dbg_stop == 1) return;
+    // ---- phase 1: pi_i, desired_i, rank of A_i ----
+    for (int k = tid; k < nown; k += kSelThreads) {
+        const int C = off_s[k + 1] - off_s[k];
+        if (C < 1 || C - 1 > AS_MAX_CAND) set_dev_error(p.ws, C < 1 ? AS_DEV_BAD_PARENT : AS_DEV_TOO_MANY_CAND, r0 + k);
+        nr_s[k] = max(0, min(C - 1, AS_MAX_CAND));
+    }
+    __syncthreads();
+    if (staged) {
+        for (int rd = 0; rd < rounds; ++rd) {
+            const int k = rd * G + grp;
+            const bool active = grp < G && k < nown;
+            const int i = r0 + k;
+            const int off = active ? off_s[k] : 0;
+            const int nr = active ? nr_s[k] : 0;
+            const int lo = off - cbase;  // request's first staged candidate (its root)
+            // (1a) keys in candidate order, validation, depth; ranks zeroed
+            for (int s = wg * 32 + lane; s < nr; s += W * 32) {
+                const int j = s + 1;
+                const float f = prob_s[lo + j];
+                const int pj = par_s[lo + j];
+                int dep = 1;
+                if (pj < 0 || pj >= j) {
+                    set_dev_error(p.ws, AS_DEV_BAD_PARENT, i);
+                } else {
+                    if (!(f > 0.f) || !(f <= prob_s[lo + pj])) set_dev_error(p.ws, AS_DEV_BAD_PROB, i);
+                    for (int u = pj, guard = 0; u > 0 && guard <= AS_MAX_CAND; ++guard) {  // depth walk
+                        const int pu = par_s[lo + u];
+                        u = (pu >= 0 && pu < u) ? pu : 0;
+                        ++dep;
+                    }
+                }
+                dep_s[lo + j] = (uint8_t)min(dep, 255);
+                ukey_s[lo - k + s] = cand_key(f, j);
+                rank_s[lo - k + s] = 0;
             }
-            int nr = n_nonroot(p, i, &off);
-            if (nr <= 32) sort_request<1>(p, i, off, nr);
-            else if (nr <= 64) sort_request<2>(p, i, off, nr);
-            else if (nr <= 128) sort_request<4>(p, i, off, nr);
-            else sort_request<8>(p, i, off, nr);
+            __syncthreads();
+            // (1b) rank counting: warp wg compares every element with its slice of keys
+            if (active) {
+                const int per = (nr + W - 1) / W;
+                const int kb = wg * per, ke = min(nr, kb + per);
+                const uint64_t* uk = ukey_s + (lo - k);
+                for (int s = lane; s < nr; s += 32) {
+                    const uint64_t key = uk[s];
+                    int cnt = 0;
+                    int t = kb;
+#pragma unroll 1
+                    for (; t + 3 < ke; t += 4)
+                        cnt += (uk[t] > key) + (uk[t + 1] > key) + (uk[t + 2] > key) + (uk[t + 3] > key);
+                    for (; t < ke; ++t) cnt += uk[t] > key;
+                    if (cnt) atomicAdd(&rank_s[lo - k + s], cnt);
+                }
+            }
+            __syncthreads();
+            // (1c) scatter into pi order
+            for (int s = wg * 32 + lane; s < nr; s += W * 32) keyc[off - i + rank_s[lo - k + s]] = ukey_s[lo - k + s];
+            __syncthreads();
+            // (1d) desired_i (warp 0 of the group) and the A-order rank (warp 1, or 0)
+            if (active && wg == 0) {
+                const int des = slo_prefix_len(p, i, keyc + (off - i), nr);
+                if (lane == 0) desired_s[k] = des;
+            }
+            if (active && wg == (W > 1 ? 1 : 0)) {
+                const double a = A_s[i];
+                int rk = 0;
+                for (int j = lane; j < n; j += 32) {
+                    const double b = A_s[j];
+                    rk += (b > a) || (b == a && j < i);
+                }
+                rk = warp_sum(rk);
+                if (lane == 0) arank_s[k] = rk;
+            }
+        }
+    } else {
+        // large batches: one warp per request, candidates read from global memory
+        for (int k = warp; k < nown; k += kSelWarps) {
+            const int i = r0 + k;
+            const int off = off_s[k];
+            const int nr = nr_s[k];
+            uint64_t* ko = keyc + (off - i);
+            int des;
+            if (nr <= 32) des = sort_request<1>(p, i, probc + off, parc + off, nr, ko);
+            else if (nr <= 64) des = sort_request<2>(p, i, probc + off, parc + off, nr, ko);
+            else if (nr <= 128) des = sort_request<4>(p, i, probc + off, parc + off, nr, ko);
+            else des = sort_request<8>(p, i, probc + off, parc + off, nr, ko);
+            const double a = A_s[i];
+            int rk = 0;
+            for (int j = lane; j < n; j += 32) {
+                const double b = A_s[j];
+                rk += (b > a) || (b == a && j < i);
+            }
+            rk = warp_sum(rk);
+            if (lane == 0) {
+                desired_s[k] = des;
+                arank_s[k] = rk;
+            }
         }
     }
     __syncthreads();
-    WsHeader* hdr = reinterpret_cast<WsHeader*>(p.ws);
-    __shared__ unsigned s_gen0;
-    if (threadIdx.x == 0) {
-        s_gen0 = *reinterpret_cast<volatile unsigned*>(&hdr->pad[0]);  // generation before arriving
-        __threadfence();
-        unsigned t = atomicAdd(&hdr->ticket, 1u);
-        s_is_last = (t == gridDim.x - 1);
-        if (s_is_last) atomicExch(&hdr->ticket, 0u);  // everyone has arrived: reusable
-    }
-    __syncthreads();
-    if (s_is_last) {
-    __threadfence();
 
-    // ---- phase 2 (last CTA) ----
-    double* A_s = reinterpret_cast<double*>(smem_raw);                    // [n]
-    int* ord_s = reinterpret_cast<int*>(A_s + n);                         // [n] desired in A order -> cum
-    int* rank_s = ord_s + n;                                              // [n]
-
-    for (int i = threadIdx.x; i < n; i += kSelThreads) A_s[i] = p.A[i];
-    __syncthreads();
-    // (3) rank by (A desc, id asc)
-    for (int i = threadIdx.x; i < n; i += kSelThreads) {
-        const double a = A_s[i];
-        int r = 0;
-        for (int j = 0; j < n; ++j) {
-            const double b = A_s[j];
-            r += (b > a) || (b == a && j < i);
-        }
-        rank_s[i] = r;
-        ord_s[r] = __ldcg(p.desired + i);
+    // ---- exchange 1: desired at rank position, per-CTA sum of nr, into every CTA ----
+    if (p.dbg_stop == 2) return;
+    cl_wait();  // every CTA of the cluster has started
+    for (int x = tid; x < nown * CS; x += kSelThreads) {
+        const int k = x / CS, dst = x - k * CS;
+        cluster.map_shared_rank(des_all, dst)[arank_s[k]] = desired_s[k];
     }
-    __syncthreads();
-    block_exclusive_scan(ord_s, n, red);
+    if (warp == kSelWarps - 1) {
+        int v = 0;
+        for (int k = lane; k < nown; k += 32) v += nr_s[k];
+        v = warp_sum(v);
+        if (lane < CS) cluster.map_shared_rank(part_nr, lane)[c] = v;
+    }
+    cl_sync();
+
+    if (p.dbg_stop == 3) return;
+    // ---- (3) budget sequencing, redundant in every CTA (warp 0) ----
     const int B0 = p.budget - n;
-    int my_s = 0, my_tail = 0;
-    for (int i = threadIdx.x; i < n; i += kSelThreads) {
-        int off;
-        const int nr = n_nonroot(p, i, &off);
-        const int des = __ldcg(p.desired + i);
-        int s = B0 - ord_s[rank_s[i]];
-        s = max(0, min(s, des));
-        p.stage_s[i] = s;
-        if (p.slo_count) p.slo_count[i] = s;
-        my_s += s;
-        my_tail += nr - s;
+    if (warp == 0) {
+        warp_exclusive_scan(des_all, exc_all, n);
+        __syncwarp();
+        int my_s = 0;
+        for (int x = lane; x < n; x += 32) my_s += max(0, min(B0 - exc_all[x], des_all[x]));
+        my_s = warp_sum(my_s);
+        int sum_nr = 0;
+        for (int q = 0; q < CS; ++q) sum_nr += part_nr[q];
+        if (lane == 0) {
+            s_bcast[4] = my_s;
+            s_bcast[5] = sum_nr;
+        }
     }
-    const int sum_s = block_sum_int(my_s, red);
-    const int sum_tail = block_sum_int(my_tail, red);
+    __syncthreads();
+    const int sum_s = s_bcast[4];
+    const int sum_tail = s_bcast[5] - sum_s;
     const int R = min(B0 - sum_s, sum_tail);
+    for (int k = tid; k < nown; k += kSelThreads) {
+        const int sv = max(0, min(B0 - exc_all[arank_s[k]], desired_s[k]));
+        s_s[k] = sv;
+        if (p.slo_count) p.slo_count[r0 + k] = sv;
+    }
     __syncthreads();
 
-    // (4) global top-R of the tails: radix select of the R-th largest key.
+    if (p.dbg_stop == 4) return;
+    // ---- (4) global top-R of the tails: cluster radix select ----
+    // Per digit: warp-aggregated shared histogram of this CTA's matching tails,
+    // pushed into every CTA's hsum with DSMEM reductions, one cluster barrier,
+    // then every CTA picks the same digit.  hsum is double-buffered by pass.
     int sh = 64;
     uint64_t prefix = 0;
     const bool select_all = (R >= sum_tail);
@@ -292,54 +580,61 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
     if (!select_all && !select_none) {
         int need = R;
         bool done = false;
+        int pass = 0;
         while (!done && sh > 0) {
             sh -= 8;
-            for (int x = threadIdx.x; x < 256; x += kSelThreads) hist[x] = 0;
-            __syncthreads();
-            for (int i = warp_id(); i < n; i += kSelWarps) {
-                int off;
-                const int nr = n_nonroot(p, i, &off);
-                const int s = __ldcg(p.stage_s + i);
-                const int sbase = off - i;
-                for (int t0 = s; t0 < nr; t0 += 32) {  // warp-uniform trip count
+            for (int k = warp; k < nown; k += kSelWarps) {
+                const int i = r0 + k;
+                const int nr = nr_s[k], sk = s_s[k];
+                const uint64_t* ks = keyc + (off_s[k] - i);
+                for (int t0 = sk; t0 < nr; t0 += 32) {  // warp-uniform trip count
                     const int t = t0 + lane;
                     const bool valid = t < nr;
-                    const uint64_t k = valid ? tail_key(__ldcg(p.skey + sbase + t), i) : 0ull;
-                    const bool match = valid && (sh + 8 == 64 || (k >> (sh + 8)) == prefix);
-                    const int dig = (int)((k >> sh) & 255ull);
-                    // warp-aggregated increment: one shared atomic per distinct digit
+                    const uint64_t key = valid ? tail_key(ks[t], i) : 0ull;
+                    const bool match = valid && (sh + 8 == 64 || (key >> (sh + 8)) == prefix);
+                    const int dig = (int)((key >> sh) & 255ull);
                     const unsigned same = __match_any_sync(0xffffffffu, match ? dig : -1);
                     if (match && (__ffs(same) - 1) == lane) atomicAdd(&hist[dig], __popc(same));
                 }
             }
             __syncthreads();
-            if (threadIdx.x < 32) {
+            int* hs = hsum[pass & 1];
+            for (int x = tid; x < 256 * CS; x += kSelThreads) {
+                const int bin = x & 255, q = x >> 8;
+                const int v = hist[bin];
+                if (v) red_add_cluster(&hs[bin], q, v);
+            }
+            __syncthreads();
+            for (int x = tid; x < 256; x += kSelThreads) hist[x] = 0;
+            cl_sync();  // every CTA's contribution to hs has landed
+            if (warp == 0) {
                 int loc[8];
                 int lsum = 0;
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    loc[q] = hist[255 - 8 * lane - q];
+                    loc[q] = hs[255 - 8 * lane - q];
+                    hs[255 - 8 * lane - q] = 0;  // reused two passes later
                     lsum += loc[q];
                 }
                 int incl = lsum;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
-                    int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
                     if (lane >= o) incl += y;
                 }
                 const int excl = incl - lsum;
                 const unsigned hit = __ballot_sync(0xffffffffu, excl < need && need <= incl);
-                const int L = __ffs(hit) - 1;
-                if (lane == L) {
-                    int c = excl;
+                const int Lh = __ffs(hit) - 1;
+                if (lane == Lh) {
+                    int cc = excl;
                     for (int q = 0; q < 8; ++q) {
-                        if (c + loc[q] >= need) {
+                        if (cc + loc[q] >= need) {
                             s_bcast[0] = 255 - 8 * lane - q;
-                            s_bcast[1] = c;
+                            s_bcast[1] = cc;
                             s_bcast[2] = loc[q];
                             break;
                         }
-                        c += loc[q];
+                        cc += loc[q];
                     }
                 }
             }
@@ -349,125 +644,161 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
             prefix = (prefix << 8) | (uint64_t)b;
             done = (s_bcast[2] == need);
             __syncthreads();
+            ++pass;
         }
     }
-    // m_i and take_i; tree sizes into ord_s for the offsets scan.
-    for (int i = warp_id(); i < n; i += kSelWarps) {
-        int off;
-        const int nr = n_nonroot(p, i, &off);
-        const int s = __ldcg(p.stage_s + i);
+    // m_i, take_i, tree size of own requests
+    for (int k = warp; k < nown; k += kSelWarps) {
+        const int i = r0 + k;
+        const int nr = nr_s[k], sk = s_s[k];
         int m = 0;
         if (select_all) {
-            m = nr - s;
+            m = nr - sk;
         } else if (!select_none) {
-            const int sbase = off - i;
-            for (int t0 = s; t0 < nr; t0 += 32) {
+            const uint64_t* ks = keyc + (off_s[k] - i);
+            for (int t0 = sk; t0 < nr; t0 += 32) {
                 const int t = t0 + lane;
-                bool in = false;
-                if (t < nr) {
-                    uint64_t k = tail_key(__ldcg(p.skey + sbase + t), i);
-                    in = (k >> sh) >= prefix;
-                }
+                const bool in = t < nr && (tail_key(ks[t], i) >> sh) >= prefix;
                 m += __popc(__ballot_sync(0xffffffffu, in));
             }
         }
         if (lane == 0) {
-            p.take[i] = s + m;
-            ord_s[i] = 1 + s + m;
+            take_s[k] = sk + m;
+            desired_s[k] = 1 + sk + m;  // tree size (desired no longer needed)
         }
     }
     __syncthreads();
-    const int used = block_exclusive_scan(ord_s, n, red);
-    for (int i = threadIdx.x; i < n; i += kSelThreads) {
-        p.tree_offsets[i] = ord_s[i];
+    if (warp == 0) {
+        const int tot = warp_exclusive_scan(desired_s, size_s, nown);
+        // ---- exchange 2: per-CTA totals -> tree offsets ----
+        if (lane < CS) cluster.map_shared_rank(part_tot, lane)[c] = tot;
     }
-    if (threadIdx.x == 0) p.tree_offsets[n] = used;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(&hdr->pad[0], 1u);  // release phase 3 in every CTA
-    }  // last CTA
-    // ---- phase 3 (every CTA, its own 32 requests): wait for the global phase ----
-    if (threadIdx.x == 0) {
-        while (*reinterpret_cast<volatile unsigned*>(&hdr->pad[0]) == s_gen0) __nanosleep(64);
-        __threadfence();
+    if (p.dbg_stop == 5) return;
+    cl_sync();
+    int base = 0, used = 0;
+    for (int q = 0; q < CS; ++q) {
+        base += (q < c) ? part_tot[q] : 0;
+        used += part_tot[q];
     }
-    __syncthreads();
+    for (int k = tid; k < nown; k += kSelThreads) p.tree_offsets[r0 + k] = base + size_s[k];
+    if (c == CS - 1 && tid == 0) p.tree_offsets[n] = used;
 
-    // (5) emit: warp per request.
-    double* A_s2 = reinterpret_cast<double*>(smem_raw);
-    int* remap_all = reinterpret_cast<int*>(A_s2 + n) + 2 * n;                                 // [32][kRemapWords]
-    unsigned* bitmap_all = reinterpret_cast<unsigned*>(remap_all + kSelWarps * kRemapWords);  // [32][kBitmapWords]
-    int* parent_all = reinterpret_cast<int*>(bitmap_all + kSelWarps * kBitmapWords);          // [32][kRemapWords]
-    int* remap = remap_all + warp_id() * kRemapWords;
-    unsigned* bits = bitmap_all + warp_id() * kBitmapWords;
-    int* cpar = parent_all + warp_id() * kRemapWords;
-    {
-        const int i = blockIdx.x * kSelWarps + (int)warp_id();
-        if (i < n) {
-        int off;
-        const int nr = n_nonroot(p, i, &off);
-        const int take = __ldcg(p.take + i);
-        const int tbase = __ldcg(p.tree_offsets + i);
-        const int sbase = off - i;
-        for (int w = lane; w < kBitmapWords; w += 32) bits[w] = 0u;
-        for (int c = lane; c <= nr; c += 32) cpar[c] = p.cand_parent[off + c];  // staged: depth walks stay on chip
-        __syncwarp();
-        for (int t = lane; t < take; t += 32) {
-            uint32_t idx = 0xFFFFFFFFu - (uint32_t)(__ldcg(p.skey + sbase + t) & 0xFFFFFFFFull);
+    if (p.dbg_stop == 6) return;
+    // ---- (5) emit own trees: group of W warps per request ----
+    uint16_t* remap = reinterpret_cast<uint16_t*>(smem + Lo.o_remap) + grp * kRemapWords;
+    unsigned* bits = reinterpret_cast<unsigned*>(smem + Lo.o_bits) + grp * kBitmapWords;
+    const int* tokc = staged ? tok_s - cbase : p.cand_token;
+    for (int rd = 0; rd < rounds; ++rd) {
+        const int k = rd * G + grp;
+        const bool active = grp < G && k < nown;
+        const int i = r0 + k;
+        const int off = active ? off_s[k] : 0;
+        const int nr = active ? nr_s[k] : 0;
+        const int take = active ? take_s[k] : 0;
+        const int tbase = active ? base + size_s[k] : 0;
+        const uint64_t* ks = keyc + (off - i);
+        const int nwords = (nr + 1 + 31) >> 5;  // local indices 0..nr
+        if (active)
+            for (int w = wg * 32 + lane; w < nwords; w += W * 32) bits[w] = 0u;
+        __syncthreads();
+        for (int t = wg * 32 + lane; t < take; t += W * 32) {
+            const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(ks[t] & 0xFFFFFFFFull);
             atomicOr(&bits[idx >> 5], 1u << (idx & 31));
         }
-        __syncwarp();
-        int running = 0;
-        for (int c0 = 1; c0 <= nr; c0 += 32) {
-            const int c = c0 + lane;
-            const bool sel = c <= nr && ((bits[c >> 5] >> (c & 31)) & 1u);
-            const unsigned mm = __ballot_sync(0xffffffffu, sel);
-            if (sel) remap[c] = 1 + running + __popc(mm & ((1u << lane) - 1u));
-            running += __popc(mm);
+        __syncthreads();
+        // compact index of candidate cc = 1 + #selected candidates before it
+        for (int w = wg; w < nwords; w += W) {
+            const int cc = w * 32 + lane;
+            const unsigned word = bits[w];
+            int before = 0;
+            for (int x = 0; x < w; ++x) before += __popc(bits[x]);
+            if ((word >> lane) & 1u) remap[cc] = (uint16_t)(1 + before + __popc(word & ((1u << lane) - 1u)));
         }
-        __syncwarp();
-        if (lane == 0) {
+        __syncthreads();
+        if (active && wg == 0 && lane == 0) {
             p.tree_src[tbase] = 0;
             p.tree_parent[tbase] = 0;
             if (p.tree_depth) p.tree_depth[tbase] = 0;
-            if (p.tree_token) p.tree_token[tbase] = p.cand_token[off];
+            if (want_tok) p.tree_token[tbase] = tokc[off];
         }
-        for (int c0 = 1; c0 <= nr; c0 += 32) {
-            const int c = c0 + lane;
-            const bool sel = c <= nr && ((bits[c >> 5] >> (c & 31)) & 1u);
-            if (sel) {
-                const int row = tbase + remap[c];
-                const int par = cpar[c];
-                const bool ok = par >= 0 && par < c;
-                p.tree_src[row] = c;
-                p.tree_parent[row] = (ok && par > 0) ? remap[par] : 0;
-                if (p.tree_depth) {
-                    int dep = 1, u = par, guard = 0;
-                    while (u > 0 && guard < AS_MAX_CAND + 1) {
-                        int pu = cpar[u];
+        for (int cc = 1 + wg * 32 + lane; cc <= nr; cc += W * 32) {
+            if (!((bits[cc >> 5] >> (cc & 31)) & 1u)) continue;
+            const int row = tbase + remap[cc];
+            const int par = parc[off + cc];
+            const bool ok = par >= 0 && par < cc;
+            p.tree_src[row] = cc;
+            p.tree_parent[row] = (ok && par > 0) ? remap[par] : 0;
+            if (p.tree_depth) {
+                int dep;
+                if (staged) {
+                    dep = dep_s[off - cbase + cc];
+                } else {
+                    dep = 1;
+                    for (int u = par, guard = 0; u > 0 && guard <= AS_MAX_CAND; ++guard) {
+                        const int pu = parc[off + u];
                         u = (pu >= 0 && pu < u) ? pu : 0;
                         ++dep;
-                        ++guard;
                     }
-                    p.tree_depth[row] = dep;
                 }
-                if (p.tree_token) p.tree_token[row] = p.cand_token[off + c];
+                p.tree_depth[row] = dep;
             }
+            if (want_tok) p.tree_token[row] = tokc[off + cc];
         }
-        __syncwarp();
-        }
+        __syncthreads();
     }
 }
 
-size_t select_smem_bytes(int n) {
-    return (size_t)n * sizeof(double) + 2 * (size_t)n * sizeof(int) +
-           2 * (size_t)kSelWarps * kRemapWords * sizeof(int) + (size_t)kSelWarps * kBitmapWords * sizeof(unsigned);
+// ---------------------------------------------------------------------------
+// Host side.
+// ---------------------------------------------------------------------------
+int pdl_enabled() {
+    static const int v = [] {
+        const char* e = getenv("AS_PDL");  // A/B switch: 0 = plain stream ordering
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return v;
+}
+
+static int cluster_size_for(int n) {
+    int cs = n;  // as many CTAs as possible: more warps per request (latency-bound)
+    if (cs < 1) cs = 1;
+    if (cs > kSelMaxCluster) cs = kSelMaxCluster;
+    return cs;
+}
+
+static int cand_cap_for(int n, int rpc, int n_cand_total) {
+    const SelLayout base(n, rpc, 0);
+    const int avail = kSelSmemLimit - base.bytes;
+    int cap = avail > 0 ? avail / kSelBytesPerCand : 0;
+    int want = rpc * (AS_MAX_CAND + 1);
+    if (n_cand_total < want) want = n_cand_total;  // no CTA holds more than all candidates
+    return cap < want ? cap : want;
+}
+
+// Largest cluster size <= want that the device can co-schedule with this smem.
+static int fit_cluster(int want, size_t smem) {
+    while (want > 1) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(want);
+        cfg.blockDim = dim3(kSelThreads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = want;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, select_trees_kernel, &cfg) == cudaSuccess && nc >= 1) return want;
+        cudaGetLastError();
+        want = want > 8 ? 8 : want / 2;
+    }
+    return 1;
 }
 
 size_t select_ws_bytes(int n_req, int n_cand_total) {
     size_t b = kWsHeaderBytes;
-    b += align_up((size_t)n_req * 4, 256) * 4;        // desired, take, stage_s, toff
-    b += align_up((size_t)(n_req + 1) * 4, 256);
     b += align_up((size_t)(n_cand_total > 0 ? n_cand_total : 1) * 8, 256);
     return b;
 }
@@ -477,6 +808,7 @@ int launch_select(int n_req, int n_cand_total, const int32_t* cand_offsets, cons
                   int n_max, int budget, int32_t* tree_offsets, int32_t* tree_parent, int32_t* tree_src,
                   int32_t* tree_depth, int32_t* tree_token, int32_t* slo_count, void* ws,
                   cudaStream_t stream) {
+    if (n_req > kSelMaxReq) return -1;
     SelectParams p;
     p.n_req = n_req;
     p.cand_offsets = cand_offsets;
@@ -494,31 +826,42 @@ int launch_select(int n_req, int n_cand_total, const int32_t* cand_offsets, cons
     p.tree_token = tree_token;
     p.slo_count = slo_count;
     p.ws = ws;
-    unsigned char* b = reinterpret_cast<unsigned char*>(ws) + kWsHeaderBytes;
-    const size_t nb = align_up((size_t)n_req * 4, 256);
-    p.desired = reinterpret_cast<int32_t*>(b);
-    p.take = reinterpret_cast<int32_t*>(b + nb);
-    p.stage_s = reinterpret_cast<int32_t*>(b + 2 * nb);
-    p.toff = reinterpret_cast<int32_t*>(b + 3 * nb);
-    p.skey = reinterpret_cast<uint64_t*>(b + 4 * nb + align_up((size_t)(n_req + 1) * 4, 256));
-    const size_t smem = select_smem_bytes(n_req);
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(select_trees_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
-        return -1;
-    const int grid = (n_req + kSelWarps - 1) / kSelWarps;
-    // cooperative launch: every CTA waits for the global phase run by the last
-    // one to arrive, so all CTAs must be co-resident (grid <= 128 CTAs)
+    p.skey_g = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(ws) + kWsHeaderBytes);
+    static bool attrs_set = false;
+    if (!attrs_set) {
+        if (cudaFuncSetAttribute(select_trees_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSelSmemLimit + 16 * 1024) != cudaSuccess ||
+            cudaFuncSetAttribute(select_trees_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                cudaSuccess)
+            return -1;
+        attrs_set = true;
+    }
+    int cs = cluster_size_for(n_req);
+    for (;;) {
+        p.rpc = (n_req + cs - 1) / cs;
+        p.cand_cap = cand_cap_for(n_req, p.rpc, n_cand_total);
+        const int fit = fit_cluster(cs, SelLayout(n_req, p.rpc, p.cand_cap).bytes);
+        if (fit == cs) break;
+        cs = fit;
+    }
+    const size_t smem = SelLayout(n_req, p.rpc, p.cand_cap).bytes;
+    static const int dbg_stop = [] {
+        const char* e = getenv("AS_SEL_STOP");
+        return e ? atoi(e) : 99;
+    }();
+    p.dbg_stop = dbg_stop;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(kSelThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 1 + fill_launch_attrs(attr + 1);
     if (cudaLaunchKernelEx(&cfg, select_trees_kernel, p) != cudaSuccess) return -1;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

@@ -64,10 +64,10 @@ def test_host_checks_return_without_launch(L):
     assert st == 4
     # accept: bad phase / max_path
     st = L.as_accept_tokens(7, 1, 0, 1, 4, dummy, dummy, dummy, dummy, None, 0, 0, 8, dummy, dummy, dummy,
-                            None, None, 1, 0, 0, None, None, 0, 0, None, 0, None, vp(1 << 16), 1 << 12, None)
+                            None, None, 1, 0, 0, None, None, 0, 0, None, 0, None, None, vp(1 << 16), 1 << 12, None)
     assert st == 1
     st = L.as_accept_tokens(1, 1, 0, 1, 4, dummy, dummy, dummy, dummy, None, 0, 0, 65, dummy, dummy, dummy,
-                            None, None, 1, 0, 0, None, None, 0, 0, None, 0, None, vp(1 << 16), 1 << 12, None)
+                            None, None, 1, 0, 0, None, None, 0, 0, None, 0, None, None, vp(1 << 16), 1 << 12, None)
     assert st == 3
 
 

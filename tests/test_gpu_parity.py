@@ -127,6 +127,50 @@ def test_select_fuzz(ada, seed):
         _assert_select_equal(F, A, d, n_max, B, got)
 
 
+def test_select_exact_sum_guards(ada):
+    """Both desired_i paths of the kernel: the warp fp64 scan is used only when
+    every f-hat >= 2^-24 and 1 + sum < 64 (R9); chains of f-hat = 1.0 (sums past
+    64) and tiny f-hat (< 2^-24) must take the sequential loop and still match."""
+    rng = np.random.default_rng(7)
+    # (a) chains with f = 1.0 everywhere: n_acc reaches 1 + 200 > 64
+    n, K = 5, 201
+    F = dict(cand_offsets=np.arange(0, (n + 1) * K, K, dtype=np.int32),
+             cand_parent=np.concatenate([[0] + list(range(K - 1))] * n).astype(np.int32),
+             cand_prob=np.ones(n * K, np.float32))
+    for A, d, n_max in ((150.0, 300, 250), (70.5, 300, 250), (30.0, 300, 250), (300.0, 100, 90)):
+        got = _gpu_select(ada, F, np.full(n, A), d, n_max, n * K)
+        _assert_select_equal(F, np.full(n, A), d, n_max, n * K, got)
+    # (b) tiny path probabilities (< 2^-24) mixed with large ones
+    for it in range(10):
+        F = synth.random_forest(rng, 40, 60)
+        f = F["cand_prob"].copy()
+        co = F["cand_offsets"]
+        for i in range(40):
+            if rng.random() < 0.5:
+                # scale a whole request's non-root f by 2^-30 (keeps f(child) <= f(parent))
+                f[co[i] + 1: co[i + 1]] = (f[co[i] + 1: co[i + 1]].astype(np.float64) * 2.0 ** -30).astype(np.float32)
+        F["cand_prob"] = f
+        A = rng.uniform(0.5, 4.0, 40)
+        n_max = int(rng.integers(1, 60))
+        B = int(rng.integers(40, 1500))
+        got = _gpu_select(ada, F, A, 8, n_max, B)
+        _assert_select_equal(F, A, 8, n_max, B, got)
+
+
+@pytest.mark.parametrize("n,maxn", [(4096, 5), (2500, 100)])
+def test_select_large_batches(ada, n, maxn):
+    """Cluster of 16 CTAs with several requests per warp (4096 x 5), and a batch
+    whose candidates overflow the per-CTA shared staging area (2500 x ~100):
+    the kernel then keeps pi_i in the workspace -- same results."""
+    rng = np.random.default_rng(n)
+    F = synth.random_forest(rng, n, maxn, tie_prob=0.3, min_nodes=max(1, maxn - 10))
+    A = rng.uniform(-1, 5, n)
+    N = int(F["cand_offsets"][-1])
+    for n_max, B in ((3, n + min(3000, (N - n) // 3)), (40, n + 1500)):
+        got = _gpu_select(ada, F, A, 8, n_max, B)
+        _assert_select_equal(F, A, 8, n_max, B, got)
+
+
 # --------------------------------------------------------------------------- accept
 def _accept_inputs(rng, n, maxK, vocab=50, dtype=np.float32, n_kv=2, d=64, ps=16, L_max=70):
     sizes = rng.integers(1, maxK + 1, n)
