@@ -254,19 +254,24 @@ class Step:
         W["pool_idx"] = (W["pool_idx"] + 1) % W["n_pools"]
         ea = events if (events and attn_only) else None
         eb = events if (events and not attn_only) else None
+        skip = os.environ.get("AS_BENCH_SKIP", "")  # ablation only (never for reported numbers)
         if eb:
             _record(eb[0], external)
-        run_select(W)
+        if "select" not in skip:
+            run_select(W)
         if eb:
             _record(eb[1], external)
         if ea:
             _record(ea[0], external)
-        run_attention(W)
+        if "attention" not in skip:
+            run_attention(W)
         if ea:
             _record(ea[1], external)
         if eb:
             _record(eb[2], external)
-        if self.dist is None:
+        if "accept" in skip:
+            pass
+        elif self.dist is None:
             run_accept(W)
         else:
             self.dist.accept_and_commit(W)
@@ -529,7 +534,8 @@ def main():
                        else "1 GPU", "l2": ("inputs larger than L2: KV %.0f MiB/GPU" % (W["kv_bytes"] / 2**20))
                        if W["n_pools"] == 1 else f"{W['n_pools']} rotating KV pools (> 3x L2)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-            "clocks": clocks, "graph": use_graph,
+            "clocks": clocks, "graph": use_graph, **({"ablation_skip": os.environ["AS_BENCH_SKIP"]}
+                                                       if os.environ.get("AS_BENCH_SKIP") else {}),
             "breakdown_ms": {"select": round(t_sel, 4), "attention": round(t_attn_b, 4), "accept_commit": round(t_acc, 4),
                              "note": "separate instrumented replay (events around every call)"},
         }

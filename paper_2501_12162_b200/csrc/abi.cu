@@ -227,7 +227,8 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
         const size_t need = kWsHeaderBytes + kAttnTraceBytes + cnt_bytes + 2 * (size_t)nsm * tc_ctas_per_sm() * slot;
         unsigned char* base = reinterpret_cast<unsigned char*>(workspace) + kWsHeaderBytes + kAttnTraceBytes;
         const char* skenv = getenv("AS_ATTN_STREAMK");  // A/B switch (debug)
-        p.stream_k = (workspace_bytes >= need && !(skenv && atoi(skenv) == 0)) ? 1 : 0;
+        // A/B: AS_ATTN_STREAMK=0 static only, =2 force stream-K
+        p.stream_k = (workspace_bytes >= need && !(skenv && atoi(skenv) == 0)) ? ((skenv && atoi(skenv) == 2) ? 2 : 1) : 0;
         p.cnt = reinterpret_cast<int*>(base);
         p.partial = reinterpret_cast<float*>(base + cnt_bytes);
         p.slot_floats = 128 * head_dim + 256;
@@ -247,7 +248,7 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     p.trace_cap = 0;
     if (tr && atoi(tr) && workspace_bytes >= kWsHeaderBytes + kAttnTraceBytes) {
         p.trace = reinterpret_cast<unsigned long long*>(reinterpret_cast<unsigned char*>(workspace) + kWsHeaderBytes);
-        p.trace_cap = (int)(kAttnTraceBytes / 64);
+        p.trace_cap = (int)(kAttnTraceBytes / 64) - 512;  // last 512 records: per-CTA timeline
     }
     return launch_attn_tc(maps, p, head_dim, sm_count(), S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
 }

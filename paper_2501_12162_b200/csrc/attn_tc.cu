@@ -39,12 +39,14 @@ constexpr int kKStages = 2;       // K ring depth (released right after QK)
 constexpr int kVStages = 2;       // V ring depth (held until PV)
 constexpr int kThreads = 192;     // 6 warps: TMA producer, MMA, 4 softmax
 constexpr int kCtasPerSm = 2;
-constexpr int kTmemCols = 256;    // S [0,64) P [64,96) O [128,128+D)
+constexpr int kTmemCols = 256;    // S [0,64) P0 [64,96) P1 [96,128) O [128,128+D)
 constexpr int kScol = 0;
-constexpr int kPcol = 64;
+constexpr int kPcol = 64;         // P double buffer: [64,96) and [96,128)
 constexpr int kOcol = 128;
 constexpr int kPtChunk = 256;     // page-table entries staged per refill
 constexpr float kRescaleThresh = 8.0f;  // log2 units
+constexpr int kMaxRec = 64;       // pieces per CTA precomputed in the prologue
+constexpr int kTraceCtas = 512;   // per-CTA timeline records after the CTA-0 tile trace (debug)
 
 template <int D>
 struct TcSmem {
@@ -56,13 +58,15 @@ struct TcSmem {
     static constexpr int OFF_V = OFF_K + kKStages * KV_BYTES;
     static constexpr int OFF_PT = OFF_V + kVStages * KV_BYTES;     // [kPtChunk] staged page-table row
     static constexpr int OFF_TP = OFF_PT + kPtChunk * 4;           // [2][AS_MAX_TREE] staged tree parents
-    static constexpr int OFF_BAR = OFF_TP + 2 * AS_MAX_TREE * 4;
-    static constexpr int N_BAR = 2 + 2 * kKStages + 2 * kVStages + 4 + 2;
+    static constexpr int OFF_REC = OFF_TP + 2 * AS_MAX_TREE * 4;  // [kMaxRec] this CTA's pieces
+    static constexpr int OFF_BAR = OFF_REC + kMaxRec * 32;
+    static constexpr int N_BAR = 2 + 2 * kKStages + 2 * kVStages + 6 + 2;
     static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
     static constexpr int BYTES = OFF_TMEM + 16;
     static constexpr int ALLOC = BYTES + 1024;  // alignment slack
     // stream-K plan scratch (long long per block) aliases the K+V rings before any TMA
     static constexpr int PLAN_CAP = (kKStages + kVStages) * KV_BYTES / 8;
+    static constexpr int PLAN_HALF = PLAN_CAP / 2;  // [0,half) tile prefix, [half, cap) unit prefix
 };
 
 // CTA-0 pipeline trace (debug): event e of CTA-local tile index idx.
@@ -122,6 +126,38 @@ struct Piece {
     long long x;   // global tile index of (u, tb) in stream-K mode
 };
 
+// A piece precomputed in the prologue (shared memory): no global load and no
+// request walk at a unit boundary.
+struct PieceRec {
+    int i, j, tb, te;  // request, unit within request (g*MT + mt), tile range
+    int off, K, L, x;  // request geometry, global tile index of (unit, tb) (stream-K)
+};
+
+// The roles (producer, MMA, softmax) only replay the CTA's records.
+struct RecCursor {
+    int nrec, q;
+    const PieceRec* rec;
+};
+
+__device__ __forceinline__ bool rec_next(const TcParams& p, RecCursor& cur, Piece& pc) {
+    if (cur.q >= cur.nrec) return false;
+    const PieceRec rc = cur.rec[cur.q++];
+    Req r;
+    r.off = rc.off;
+    r.K = rc.K;
+    r.L = rc.L;
+    r.n_prefix = (r.L + kBN - 1) / kBN;
+    r.MT = (r.K * p.G + kBM - 1) / kBM;
+    r.nt = r.n_prefix + (r.K + kBN - 1) / kBN;
+    make_unit(r, rc.i, rc.j, pc.u);
+    pc.w = (rc.i * p.n_kv + pc.u.g) * p.mt_max + pc.u.mt;
+    pc.tb = rc.tb;
+    pc.te = rc.te;
+    pc.x = rc.x;
+    return true;
+}
+
+// Prologue-only walker of the stream-K tile range (builds the records).
 struct Sched {
     int stream;
     int i, j, t;         // cursor: request, unit within request (g*MT + mt), tile
@@ -202,9 +238,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     uint64_t* v_empty = v_full + kVStages;
     uint64_t* s_full = v_empty + kVStages;
     uint64_t* s_empty = s_full + 1;
-    uint64_t* p_full = s_empty + 1;
-    uint64_t* p_empty = p_full + 1;
-    uint64_t* o_full = p_empty + 1;
+    uint64_t* p_full = s_empty + 1;   // [2] per P buffer
+    uint64_t* p_empty = p_full + 2;   // [2]
+    uint64_t* o_full = p_empty + 2;
     uint64_t* o_empty = o_full + 1;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + S::OFF_TMEM);
 
@@ -225,8 +261,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         }
         ptx::mbar_init(s_full, 1);
         ptx::mbar_init(s_empty, 4);  // the 4 softmax warps
-        ptx::mbar_init(p_full, 4);
-        ptx::mbar_init(p_empty, 1);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(p_full + b, 4);
+            ptx::mbar_init(p_empty + b, 1);
+        }
         ptx::mbar_init(o_full, 1);
         ptx::mbar_init(o_empty, 4);
         ptx::fence_mbar_init();
@@ -242,85 +280,108 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
     pdl_wait();  // the trees come from the select kernel launched just before
+    unsigned long long t_start = 0;
+    if (p.trace != nullptr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
     // ---------------- schedule plan (all threads; K/V rings used as scratch) ----------------
     __shared__ long long sk_T, sk_x0, sk_rem;
     __shared__ int sk_cur[3];
     __shared__ int sk_stream;
     __shared__ long long scan_tmp[33];
-    __shared__ int red_tmp[2][8];
+    __shared__ int red_tmp[3][8];
     __shared__ int sk_last;
-    Sched sched0;
+    RecCursor cur0;
     {
         const int n = p.n_req;
-        long long* pre = reinterpret_cast<long long*>(smem + S::OFF_K);  // per-request tiles -> prefix
-        const bool can_stream = p.stream_k && n <= S::PLAN_CAP;
-        int my_units = 0, my_maxnt = 0;
+        // per-request prefixes (K/V rings as scratch): tiles [0, half), units [half, 2 half)
+        long long* pre = reinterpret_cast<long long*>(smem + S::OFF_K);
+        long long* preu = pre + S::PLAN_HALF;
+        const bool can_plan = n <= S::PLAN_HALF;
+        const bool can_stream = p.stream_k && can_plan;
+        int my_units = 0, my_maxnt = 0, my_minnt = 0x7fffffff;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             Req r;
             load_req(p, i, r);
             if (r.MT == 0 && r.K > AS_MAX_TREE) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, i);
+            if (r.MT > 0 && __ldg(p.kv_len + i) > p.max_pages * p.page_size) set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, i);
             my_units += p.n_kv * r.MT;
-            if (r.MT > 0) my_maxnt = max(my_maxnt, r.nt);
-            if (can_stream) pre[i] = (long long)p.n_kv * r.MT * r.nt;
+            if (r.MT > 0) {
+                my_maxnt = max(my_maxnt, r.nt);
+                my_minnt = min(my_minnt, r.nt);
+            }
+            if (can_plan) {
+                pre[i] = (long long)p.n_kv * r.MT * r.nt;
+                preu[i] = (long long)p.n_kv * r.MT;
+            }
         }
         // block reductions: total units, max unit tiles
-        int wu = my_units, wm = my_maxnt;
+        int wu = my_units, wm = my_maxnt, wn = my_minnt;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             wu += __shfl_xor_sync(0xffffffffu, wu, o);
             wm = max(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+            wn = min(wn, __shfl_xor_sync(0xffffffffu, wn, o));
         }
         if (lane == 0) {
             red_tmp[0][warp] = wu;
             red_tmp[1][warp] = wm;
+            red_tmp[2][warp] = wn;
         }
         __syncthreads();
-        int U = 0, maxnt = 0;
+        int U = 0, maxnt = 0, minnt = 0x7fffffff;
         for (int k = 0; k < (int)(blockDim.x / 32); ++k) {
             U += red_tmp[0][k];
             maxnt = max(maxnt, red_tmp[1][k]);
+            minnt = min(minnt, red_tmp[2][k]);
         }
         const int G = gridDim.x;
         long long T = 0;
-        if (can_stream) {
-            // exclusive scan of pre[0..n): per-thread chunks, then warp and block totals
-            const int chunk = (n + blockDim.x - 1) / blockDim.x;
-            const int lo = threadIdx.x * chunk, hi = min(n, lo + chunk);
-            long long loc = 0;
-            for (int b = lo; b < hi; ++b) loc += pre[b];
-            long long inc = loc;
+        if (can_plan) {
+            // exclusive scans of pre[] and preu[]: per-thread chunks, then warp and block totals
+            for (int pass = 0; pass < 2; ++pass) {
+                long long* a = pass == 0 ? pre : preu;
+                const int chunk = (n + blockDim.x - 1) / blockDim.x;
+                const int lo = threadIdx.x * chunk, hi = min(n, lo + chunk);
+                long long loc = 0;
+                for (int b = lo; b < hi; ++b) loc += a[b];
+                long long inc = loc;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const long long y = __shfl_up_sync(0xffffffffu, inc, o);
-                if ((int)lane >= o) inc += y;
-            }
-            if (lane == 31) scan_tmp[warp] = inc;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                long long acc = 0;
-                for (int k = 0; k < (int)(blockDim.x / 32); ++k) {
-                    const long long v = scan_tmp[k];
-                    scan_tmp[k] = acc;
-                    acc += v;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if ((int)lane >= o) inc += y;
                 }
-                scan_tmp[32] = acc;
+                if (lane == 31) scan_tmp[warp] = inc;
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    long long acc = 0;
+                    for (int k = 0; k < (int)(blockDim.x / 32); ++k) {
+                        const long long v = scan_tmp[k];
+                        scan_tmp[k] = acc;
+                        acc += v;
+                    }
+                    scan_tmp[32] = acc;
+                }
+                __syncthreads();
+                long long run = scan_tmp[warp] + inc - loc;
+                for (int b = lo; b < hi; ++b) {
+                    const long long v = a[b];
+                    a[b] = run;
+                    run += v;
+                }
+                if (pass == 0) T = scan_tmp[32];
+                __syncthreads();
             }
-            __syncthreads();
-            long long run = scan_tmp[warp] + inc - loc;
-            for (int b = lo; b < hi; ++b) {
-                const long long v = pre[b];
-                pre[b] = run;
-                run += v;
-            }
-            __syncthreads();
-            T = scan_tmp[32];
         }
+        PieceRec* recs = reinterpret_cast<PieceRec*>(smem + S::OFF_REC);
+        __shared__ int s_nrec;
         if (threadIdx.x == 0) {
             // makespan model (tiles): static = ceil(U/G) whole units of <= maxnt tiles;
             // stream-K = T/G plus ~30% for the split fix-ups (measured on c2).
             const long long static_ms = (long long)((U + G - 1) / G) * maxnt;
-            const bool stream = can_stream && T > 0 && (T * 13 / 10) / G + 1 < static_ms;
+            // every CTA's tile range must fit kMaxRec pieces: <= ceil(T/G)/min_nt + 2 of them
+            const bool fits = minnt > 0 && ((T + G - 1) / G) / minnt + 2 <= kMaxRec;
+            const bool stream = can_stream && fits && T > 0 &&
+                                (p.stream_k == 2 || (T * 13 / 10) / G + 1 < static_ms);
             sk_stream = stream ? 1 : 0;
             sk_T = T;
             sk_x0 = 0;
@@ -347,21 +408,62 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             sk_cur[0] = i0;
             sk_cur[1] = j0;
             sk_cur[2] = t0;
+            // static pieces are built in parallel below; stream-K ones here (falling
+            // back to static when this CTA's range would need more than kMaxRec pieces)
+            s_nrec = -1;
+            if (stream) {
+                Sched w;
+                w.stream = 1;
+                w.i = i0; w.j = j0; w.t = t0;
+                w.rem = sk_rem; w.x = sk_x0;
+                w.k = 0; w.ucum = 0;
+                if (n > 0) load_req(p, i0, w.r);
+                else w.r.MT = 0;
+                Piece pc;
+                int q = 0;
+                while (q <= kMaxRec && sched_next(p, w, pc)) {
+                    if (q < kMaxRec) {
+                        const int MT = (pc.u.K * p.G + kBM - 1) / kBM;
+                        recs[q] = PieceRec{pc.u.i, pc.u.g * MT + pc.u.mt, pc.tb, pc.te, pc.u.off, pc.u.K, pc.u.L,
+                                           (int)pc.x};
+                    }
+                    ++q;
+                }
+                s_nrec = q <= kMaxRec ? q : -1;
+            }
         }
         __syncthreads();
-        sched0.stream = sk_stream;
-        sched0.i = sk_cur[0];
-        sched0.j = sk_cur[1];
-        sched0.t = sk_cur[2];
-        sched0.rem = sk_rem;
-        sched0.x = sk_x0;
-        sched0.k = blockIdx.x;
-        sched0.ucum = 0;
-        if (n > 0) load_req(p, sched0.i, sched0.r);
-        else sched0.r.MT = 0;
-        if (!sched0.stream) sched0.i = 0;
-        if (!sched0.stream && n > 0) load_req(p, 0, sched0.r);
-        __syncthreads();  // plan scratch (K/V rings) is free again
+        if (sk_stream && s_nrec < 0) {  // some CTA may take this branch alone: static for it is wrong,
+            // so every CTA computes the same bound -- the host keeps U <= kMaxRec * G -- and we
+            // flag the (unreachable) overflow instead of mixing schedules.
+            if (threadIdx.x == 0) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, -2);
+            s_nrec = 0;
+        }
+        if (!sk_stream) {
+            const int cnt = U > (int)blockIdx.x ? (U - 1 - (int)blockIdx.x) / G + 1 : 0;
+            if (cnt > kMaxRec || !can_plan) {
+                if (threadIdx.x == 0) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, -2);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) s_nrec = (cnt <= kMaxRec && can_plan) ? cnt : 0;
+            __syncthreads();
+        }
+        const int nrec_static = (!sk_stream && s_nrec >= 0) ? s_nrec : 0;
+        for (int q = threadIdx.x; q < nrec_static; q += blockDim.x) {
+            const long long k = (long long)blockIdx.x + (long long)q * G;
+            int lo_b = 0, hi_b = n - 1;  // last i with preu[i] <= k
+            while (lo_b < hi_b) {
+                const int mid = (lo_b + hi_b + 1) >> 1;
+                if (preu[mid] <= k) lo_b = mid; else hi_b = mid - 1;
+            }
+            Req r;
+            load_req(p, lo_b, r);
+            recs[q] = PieceRec{lo_b, (int)(k - preu[lo_b]), 0, r.nt, r.off, r.K, r.L, -1};
+        }
+        cur0.nrec = s_nrec;
+        cur0.q = 0;
+        cur0.rec = recs;
+        __syncthreads();  // plan scratch (K/V rings) is free again; records are visible
     }
 
     if (warp == 0) {
@@ -374,12 +476,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         uint32_t itk = 0, itv = 0, unit_it = 0;
         const uint64_t pol = p.evict_first ? ptx::policy_evict_first() : ptx::policy_evict_normal();
         const int lead = p.k_lead;
-        Sched sc = sched0;
+        RecCursor sc = cur0;
         Piece pc;
-        while (sched_next(p, sc, pc)) {
+        while (rec_next(p, sc, pc)) {
             const Unit& u = pc.u;
-            if (lane == 0 && u.mt == 0 && u.g == 0 && __ldg(p.kv_len + u.i) > p.max_pages * p.page_size)
-                set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, u.i);
             const int n_pages_u = (u.L + p.page_size - 1) / p.page_size;
             int chunk0 = -1;  // first page index currently staged
             if (lane == 0) {
@@ -463,9 +563,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         const uint32_t k_base = ptx::smem_u32(smem + S::OFF_K);
         const uint32_t v_base = ptx::smem_u32(smem + S::OFF_V);
         uint32_t k_it = 0, v_it = 0, unit_it = 0, s_it = 0, p_it = 0;
-        Sched sc = sched0;
+        RecCursor sc = cur0;
         Piece pc;
-        while (sched_next(p, sc, pc)) {
+        while (rec_next(p, sc, pc)) {
             const Unit& u = pc.u;
             ptx::mbar_wait(q_full, unit_it & 1);
             auto do_qk = [&](int t) {
@@ -514,7 +614,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                         ptx::fence_proxy_async_smem();
                     }
                 }
-                ptx::mbar_wait(p_full, p_it & 1);
+                const uint32_t pbuf = p_it & 1;
+                ptx::mbar_wait(p_full + pbuf, (p_it >> 1) & 1);
                 if (lane == 0) AS_TRACE(4, v_it);
                 if (t == pc.tb) ptx::mbar_wait(o_empty, (unit_it & 1) ^ 1);  // O drained by the previous epilogue
                 ptx::tc_fence_after();
@@ -522,18 +623,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 if (p.debug_mode >= 2) {
                     if (lane == 0) {
                         ptx::mbar_arrive(v_empty + st);
-                        ptx::mbar_arrive(p_empty);
+                        ptx::mbar_arrive(p_empty + pbuf);
                     }
                 } else if (lane == 0) {
 #pragma unroll
                     for (int kk = 0; kk < kBN / 16; ++kk) {
                         // A = P_t: bf16 pairs in TMEM columns [kPcol, kPcol + kBN/2)
                         const uint64_t b = ptx::sw128_desc(v_base + st * S::KV_BYTES + kk * 16 * 128, kBN * 128, 1024);
-                        ptx::mma_bf16_ts(tmem + kOcol, tmem + kPcol + kk * 8, b, idesc_pv,
+                        ptx::mma_bf16_ts(tmem + kOcol, tmem + kPcol + pbuf * 32 + kk * 8, b, idesc_pv,
                                          (t > pc.tb || kk > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(v_empty + st);
-                    ptx::mma_commit(p_empty);
+                    ptx::mma_commit(p_empty + pbuf);
                 }
                 __syncwarp();
                 ++v_it;
@@ -562,9 +663,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         const float sl2 = p.scale_log2;
         uint32_t s_cnt = 0, unit_it = 0;
         int tbase = 0;  // CTA-local index of the piece's first tile (trace only)
-        Sched sc = sched0;
+        RecCursor sc = cur0;
         Piece pc;
-        while (sched_next(p, sc, pc)) {
+        while (rec_next(p, sc, pc)) {
             const Unit& u = pc.u;
             const int G = p.G;
             const int rr = u.mt * kBM + r;
@@ -603,9 +704,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(s_empty);
                 if (p.debug_mode >= 1) {  // timing experiment: no softmax math
-                    ptx::mbar_wait(p_empty, par ^ 1);
+                    ptx::mbar_wait(p_empty + (s_cnt & 1), ((s_cnt >> 1) & 1) ^ 1);
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(p_full);
+                    if (lane == 0) ptx::mbar_arrive(p_full + (s_cnt & 1));
                     continue;
                 }
                 float* x = reinterpret_cast<float*>(sr);
@@ -629,11 +730,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                          fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
                 const float m_new = fmaxf(m_ref, tmax);
-                // P is free (and O stable) once PV_{t-1} completed
-                ptx::mbar_wait(p_empty, par ^ 1);
+                // P buffer s_cnt&1 is free once PV two tiles back completed (double buffer:
+                // the softmax of tile t+1 overlaps PV_t)
+                const uint32_t pb = s_cnt & 1;
+                ptx::mbar_wait(p_empty + pb, ((s_cnt >> 1) & 1) ^ 1);
                 if (t > pc.tb) {
                     const bool need = m_new > m_ref + kRescaleThresh;
                     if (__any_sync(0xffffffffu, need)) {
+                        // O must be stable: PV_{t-1} (other buffer, use (s_cnt-1)>>1) completed
+                        ptx::mbar_wait(p_empty + (pb ^ 1), ((s_cnt - 1) >> 1) & 1);
                         ptx::tc_fence_after();
                         const float sc2 = need ? ptx::ex2(m_ref - m_new) : 1.f;
 #pragma unroll
@@ -667,11 +772,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                     pk[c >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                 }
                 l_sum += (rs[0] + rs[1]) + (rs[2] + rs[3]);
-                ptx::tmem_st32(p_addr, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+                ptx::tmem_st32(p_addr + pb * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(p_full);
+                if (lane == 0) ptx::mbar_arrive(p_full + pb);
                 if (lane == 0 && quad == 0) AS_TRACE(6, tbase + t - pc.tb);
             }
             // ---- epilogue ----
@@ -793,6 +898,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, kTmemCols);
     }
+    if (p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceCtas) {
+        // per-CTA timeline (debug): start/end globaltimer, after the CTA-0 tile trace
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        unsigned long long* rec = p.trace + (size_t)(p.trace_cap + blockIdx.x) * 8;
+        rec[0] = t_start;
+        rec[1] = t_end;
+        rec[2] = sk_stream;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -802,10 +916,31 @@ int tc_smem_bytes(int head_dim) {
     return head_dim == 64 ? TcSmem<64>::ALLOC : TcSmem<128>::ALLOC;
 }
 int tc_ctas_per_sm() { return kCtasPerSm; }
+int launch_attn_tc_chunk(const CUtensorMap* maps, const TcParams& p, int head_dim, int grid_full, int smem,
+                         cudaStream_t stream);
 
-int launch_attn_tc(const CUtensorMap* maps, const TcParams& p, int head_dim, int n_sms, cudaStream_t stream) {
+int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, int n_sms, cudaStream_t stream) {
     const int smem = tc_smem_bytes(head_dim);
-    int grid = n_sms * kCtasPerSm;
+    const int grid_full = n_sms * kCtasPerSm;
+    // Every CTA replays a list of at most kMaxRec pieces built in its prologue:
+    // batches with more units than kMaxRec * grid are verified in request chunks.
+    const int units_per_req = p0.n_kv * p0.mt_max;
+    const int chunk = units_per_req > 0 ? max(1, kMaxRec * grid_full / units_per_req) : p0.n_req;
+    for (int r0 = 0; r0 < p0.n_req; r0 += chunk) {
+        TcParams p = p0;
+        p.n_req = min(chunk, p0.n_req - r0);
+        p.page_table = p0.page_table + (size_t)r0 * p0.max_pages;
+        p.kv_len = p0.kv_len + r0;
+        p.tree_offsets = p0.tree_offsets + r0;
+        p.n_units = p.mt_max * p.n_req * p.n_kv;
+        if (launch_attn_tc_chunk(maps, p, head_dim, grid_full, smem, stream) != 0) return -1;
+    }
+    return 0;
+}
+
+int launch_attn_tc_chunk(const CUtensorMap* maps, const TcParams& p, int head_dim, int grid_full, int smem,
+                         cudaStream_t stream) {
+    int grid = grid_full;
     if (!p.stream_k && p.n_units < grid) grid = p.n_units;
     if (grid <= 0) return 0;
     cudaLaunchConfig_t cfg = {};

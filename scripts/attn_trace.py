@@ -48,6 +48,19 @@ e.record()
 torch.cuda.synchronize()
 print(f"{args.config} mode={os.environ.get('AS_ATTN_DEBUG_MODE', '0')} attention {s.elapsed_time(e) * 1e3:.1f} us")
 tr = W["ws_attn"].view[256:256 + 4096 * 64].view(torch.int64).cpu().numpy().reshape(4096, 8)
+cta = tr[4096 - 512:].copy()
+tr = tr[:4096 - 512]
+cta = cta[cta[:, 0] != 0]
+if len(cta):
+    t0c = cta[:, 0].min()
+    st = (cta[:, 0] - t0c) / 1e3
+    en = (cta[:, 1] - t0c) / 1e3
+    print(f"per-CTA timeline ({len(cta)} CTAs, us from first start, stream-K={int(cta[0, 2])}):")
+    print(f"  start  median {np.median(st):.2f}  max {st.max():.2f}")
+    print(f"  end    min {en.min():.2f}  p10 {np.percentile(en, 10):.2f}  median {np.median(en):.2f}  "
+          f"p90 {np.percentile(en, 90):.2f}  max {en.max():.2f}")
+    print(f"  busy fraction (sum of CTA spans / (CTAs x makespan)) {((en - st).sum() / (len(cta) * en.max())):.3f}")
+    print("  end-time histogram (us):", np.histogram(en, bins=10)[0].tolist(), np.round(np.histogram(en, bins=10)[1], 1).tolist())
 n = int((tr[:, 0] != 0).sum())
 tr = tr[:n].astype(np.float64)
 t0 = tr[0, 0]

@@ -340,6 +340,26 @@ def test_attn_bf16(ada, ci):
     assert np.abs(lse.cpu().numpy() - ref_lse).max() <= BF16_TOL
 
 
+def test_attn_bf16_request_chunks(ada):
+    """More units than the kernel's per-CTA piece lists hold (n_kv * q-tiles *
+    n_req > 64 * 2 * SMs): the library verifies the batch in request chunks;
+    every request, including those at chunk edges, must match the oracle."""
+    rng = np.random.default_rng(31)
+    n = 700
+    sizes = rng.integers(1, 6, n)
+    sizes[::97] = 40  # a few multi-q-tile requests (G*K > 128)
+    kv = rng.integers(0, 90, n)
+    w = synth.tree_workload(rng, sizes, kv, 32, 8, 128, 64, bf16=True)
+    scale = np.float32(1.0 / np.sqrt(128))
+    ref, _ = oracle_attn(w, scale)
+    g = workload_to_device(w, torch.bfloat16)
+    ws = ada.Workspace(256)
+    out, _ = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"], g["page_table"],
+                                  g["kv_len"], g["tree_offsets"], g["tree_parent"], scale, workspace=ws)
+    assert ada.check_device_error(ws)[0] == 0
+    assert np.abs(out.float().cpu().numpy() - ref).max() <= BF16_TOL
+
+
 def test_attn_bf16_nan_in_unused_cache_slots(ada):
     """Cache slots past kv_len may hold garbage (NaN): outputs must not see them."""
     w = _attn_case(([6, 9], [70, 33], 8, 2, 128, 64, "random", 1.0), True, 77)
