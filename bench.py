@@ -392,6 +392,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-spec", action="store_true", help="skip the NEXT-1 speculation-layer measurement")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e / cpu legs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -510,6 +511,9 @@ def main():
     e2e = None
     if not args.no_e2e and not args.profile:
         e2e = measure_e2e(W, step, args.steps, world)
+    spec = None
+    if rank == 0 and not args.profile and not args.no_spec:
+        spec = measure_speculation(W, args.steps)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         threads = os.cpu_count() or 1
@@ -534,7 +538,7 @@ def main():
                        else "1 GPU", "l2": ("inputs larger than L2: KV %.0f MiB/GPU" % (W["kv_bytes"] / 2**20))
                        if W["n_pools"] == 1 else f"{W['n_pools']} rotating KV pools (> 3x L2)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-            "clocks": clocks, "graph": use_graph, **({"ablation_skip": os.environ["AS_BENCH_SKIP"]}
+            "clocks": clocks, "graph": use_graph, "speculation": spec, **({"ablation_skip": os.environ["AS_BENCH_SKIP"]}
                                                        if os.environ.get("AS_BENCH_SKIP") else {}),
             "breakdown_ms": {"select": round(t_sel, 4), "attention": round(t_attn_b, 4), "accept_commit": round(t_acc, 4),
                              "note": "separate instrumented replay (events around every call)"},
@@ -542,6 +546,59 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def measure_speculation(W, steps):
+    """NEXT-1: one Step 1 beam layer at this config's
+    shapes -- n requests x w kept nodes x |V| = 128 256 draft probabilities
+    (fp32, synthetic, > L2) -> top-w per request written into a candidate
+    forest.  HBM-bound: algorithmic bytes = the probabilities read once."""
+    ada = W["ada"]
+    c = W["c"]
+    n, w, V = W["n"], c["w"], synth.LLAMA3_VOCAB
+    if c["dtype"] != "bf16":
+        return None
+    dev = torch.device(W["device"])
+    gen = torch.Generator(device=dev).manual_seed(synth.SEED_BASE + 99)
+    # draft distributions as in the forest generator (DESIGN.md §Inputs): softmax of
+    # z ~ N(0, sigma^2) over the vocabulary, sigma ~ U(1, 4) per request
+    if os.environ.get("AS_BENCH_SPEC_DIST") == "uniform":  # A/B only
+        probs = torch.rand((n, w, V), generator=gen, device=dev, dtype=torch.float32)
+        probs /= probs.sum(dim=-1, keepdim=True)
+    else:
+        sigma = torch.empty((n, 1, 1), device=dev).uniform_(1.0, 4.0, generator=gen)
+        z = torch.randn((n, w, V), generator=gen, device=dev, dtype=torch.float32) * sigma
+        probs = torch.softmax(z, dim=-1)
+        del z
+    stride = 1 + c["d"] * w
+    par = torch.zeros(n * stride, dtype=torch.int32, device=dev)
+    prob = torch.zeros(n * stride, dtype=torch.float32, device=dev)
+    prob[::stride] = 1.0
+    tok = torch.zeros(n * stride, dtype=torch.int32, device=dev)
+    root = probs[:, :1, :].contiguous()
+    ws = ada.beam_step(1, w, root, par, prob, tok, stride)
+    for _ in range(3):
+        ada.beam_step(2, w, probs, par, prob, tok, stride, workspace=ws)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()  # replayed: no host launch overhead between layers
+    with torch.cuda.graph(g):
+        for _ in range(steps):
+            ada.beam_step(2, w, probs, par, prob, tok, stride, workspace=ws)
+    g.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    us = s.elapsed_time(e) * 1e3 / steps
+    nbytes = probs.numel() * 4
+    peak = float(_peaks()[0]["hbm_gbs"])
+    gbs = nbytes / (us * 1e-6) / 1e9
+    return {"step": "beam layer (as_beam_step, layer 2)", "n_req": n, "width": w, "vocab": V,
+            "draft_probs": "softmax(N(0, sigma^2)), sigma ~ U(1,4) per request, fp32",
+            "layer_us": round(us, 2), "algorithmic_bytes": nbytes, "hbm_gbs": round(gbs, 1),
+            "hbm_frac": round(gbs / peak, 4), "launches": 2}
 
 
 def measure_e2e(W, step, steps, world):

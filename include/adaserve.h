@@ -71,6 +71,41 @@ enum {
 
 #define AS_MAX_TREE 128 /* nodes per tree (incl. root) accepted by as_tree_verify_attn */
 #define AS_MAX_CAND 256 /* non-root candidates per request accepted by as_select_trees */
+#define AS_MAX_BEAM 16  /* beam width accepted by as_beam_step */
+
+/* ------------------------------------------------------------------------- */
+/* Speculation: one beam-search layer (Step 1)                    */
+/* ------------------------------------------------------------------------- */
+/*
+ * Builds layer `layer` (1..d) of every request's candidate tree (the input of
+ * as_select_trees) from the draft model's distributions at the kept nodes of
+ * layer-1.  Every expansion (parent k, token t) gets the approximated path
+ * probability f-hat = fl32(f-hat(k) * draft_probs[i][k][t]) (the product of
+ * draft conditionals along the path); the layer keeps the `width`
+ * largest by (f-hat desc, parent rank asc, token asc) (R8).
+ *
+ * Forest layout (the one as_select_trees reads): request i owns candidates
+ * [i*cand_stride, (i+1)*cand_stride), cand_stride >= 1 + layer*width; local
+ * node 0 is the root (caller-initialised: parent 0, prob 1.0, its token);
+ * layer l occupies local nodes 1 + (l-1)*width + r, r = rank (0 = best), so the
+ * kept nodes of layer l-1 are the w_in = (l == 1 ? 1 : width) nodes before it.
+ * Inputs (device):
+ *   draft_probs [n_req][w_in][vocab] fp32  M_q(t | X, Path(node)) of the kept
+ *                nodes of layer-1 in rank order; finite and >= 0.
+ *   cand_prob    read: f-hat of the layer-1 nodes.
+ * Outputs (device): cand_parent / cand_prob / cand_token of the layer's
+ *   `width` nodes (parent = local index of the kept parent).
+ * Scalars: 1 <= width <= AS_MAX_BEAM, width <= vocab (every layer then keeps
+ *   exactly `width` nodes), layer >= 1, w_in*vocab < 2^32.
+ * Workspace >= as_beam_workspace_size(n_req, width, vocab) (chunk top-w lists).
+ * Device preconditions: AS_DEV_BAD_PROB (a negative probability); a NaN
+ *   probability is treated as 0 (never preferred to a real one).
+ */
+size_t as_beam_workspace_size(int32_t n_req, int32_t width, int32_t vocab);
+as_status as_beam_step(int32_t n_req, int32_t layer, int32_t width, int32_t vocab,
+                       const float* draft_probs, int32_t cand_stride, int32_t* cand_parent,
+                       float* cand_prob, int32_t* cand_token, void* workspace,
+                       size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------- */
 /* Select: Alg. 2                                                */

@@ -19,6 +19,11 @@ Contents
 * ``accept_walk`` / ``commit`` -- the sequential acceptance walk and KV commit (C).
 * ``expected_accept_exact`` -- Thm. 1 by exhaustive enumeration of
   per-node target samples, in exact rationals.
+* ``beam_step`` / ``beam_search`` -- Step 1 speculation: one
+  beam layer = the top-w of the w x |V| expansions by approximated path
+  probability f-hat = fl32(f-hat(parent) * M_q(token | X, Path(parent)))
+  (P:L691-694), ties (parent asc, token asc) (R8); pinned by exhaustive
+  enumeration, the complete-tree case and Thm. 2 containment.
 
 Parity unpinned: none (see DESIGN.md §Oracle pins).
 """
@@ -232,6 +237,53 @@ def brute_force_optimal(cand_offsets, cand_parent, cand_prob, slo_deficit, budge
         if best is None or val > best[0]:
             best = (val, [set(c[2]) for c in combo])
     return best
+
+
+# ---------------------------------------------------------------------------
+# Speculation (Step 1): beam search over the draft model's distributions
+# ---------------------------------------------------------------------------
+def beam_step(probs, f_parent, width):
+    """One beam layer for ONE request.  probs [w_in, V] fp32:
+    the draft conditional M_q(token | X, Path(parent)) of every kept node of the
+    previous layer (rows in rank order); f_parent [w_in] fp32 their f-hat.
+    Every expansion (parent k, token t) gets f-hat = fl32(f_parent[k] *
+    probs[k, t]) (the product of conditionals along the path, P:L691-694);
+    the layer keeps the `width` largest by (f-hat desc, parent asc, token asc)
+    (R8; P:L752-753 "the w with the highest approximated path probabilities").
+    Returns (parent_rank [width], token [width], f-hat [width]) in rank order."""
+    probs = np.asarray(probs, np.float32)
+    f_parent = np.asarray(f_parent, np.float32)
+    w_in, V = probs.shape
+    f = (f_parent[:, None] * probs).astype(np.float32)        # fp32 products
+    par = np.repeat(np.arange(w_in), V)
+    tok = np.tile(np.arange(V), w_in)
+    ff = f.reshape(-1)
+    order = np.lexsort((tok, par, -ff.astype(np.float64)))[:width]
+    return par[order].astype(np.int32), tok[order].astype(np.int32), ff[order].astype(np.float32)
+
+
+def beam_search(root_probs_fn, depth, width):
+    """Step 1 for one request: d beam layers.  root_probs_fn(path)
+    returns the draft distribution [V] after the token path `path` (a tuple of
+    token ids from the root).  Returns the candidate tree in the forest layout
+    the select kernel consumes: node 0 = root (f-hat 1), then layer by layer in
+    rank order -- (parent [N], token [N] (root token = -1), prob [N] fp32)."""
+    parent, token, prob, paths = [0], [-1], [np.float32(1.0)], [()]
+    layer = [0]
+    for _ in range(depth):
+        probs = np.stack([np.asarray(root_probs_fn(paths[u]), np.float32) for u in layer])
+        fpar = np.array([prob[u] for u in layer], np.float32)
+        pr, tk, fv = beam_step(probs, fpar, width)
+        new = []
+        for k in range(len(pr)):
+            u = layer[int(pr[k])]
+            parent.append(u)
+            token.append(int(tk[k]))
+            prob.append(np.float32(fv[k]))
+            paths.append(paths[u] + (int(tk[k]),))
+            new.append(len(parent) - 1)
+        layer = new
+    return np.array(parent, np.int32), np.array(token, np.int32), np.array(prob, np.float32)
 
 
 # ---------------------------------------------------------------------------

@@ -42,8 +42,11 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         L.as_status_string.restype = ctypes.c_char_p
         L.as_version.restype = ctypes.c_char_p
-        for name in ("as_select_workspace_size", "as_attn_workspace_size", "as_accept_workspace_size"):
+        for name in ("as_select_workspace_size", "as_attn_workspace_size", "as_accept_workspace_size",
+                     "as_beam_workspace_size"):
             getattr(L, name).restype = _c_sz
+        L.as_beam_workspace_size.argtypes = [_c_i32, _c_i32, _c_i32]
+        L.as_beam_step.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _vp, _c_i32, _vp, _vp, _vp, _vp, _c_sz, _vp]
         L.as_select_workspace_size.argtypes = [_c_i32, _c_i32]
         L.as_attn_workspace_size.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32]
         L.as_accept_workspace_size.argtypes = [_c_i32]
@@ -92,6 +95,28 @@ def _dt(t):
 def _need(t, dtype, name):
     if t.dtype != dtype:
         raise AdaServeError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def beam_workspace_size(n_req, width, vocab):
+    return int(lib().as_beam_workspace_size(n_req, width, vocab))
+
+
+def beam_step(layer, width, draft_probs, cand_parent, cand_prob, cand_token, cand_stride, workspace=None):
+    """as_beam_step: speculation layer `layer` (Step 1) for every
+    request, written in place into the candidate forest (stride cand_stride).
+    draft_probs [n_req, w_in, vocab] fp32, w_in = 1 at layer 1 else width."""
+    _need(draft_probs, torch.float32, "draft_probs")
+    n, w_in, vocab = draft_probs.shape
+    if w_in != (1 if layer == 1 else width):
+        raise AdaServeError(f"draft_probs must have {1 if layer == 1 else width} rows per request at layer {layer}")
+    _need(cand_parent, torch.int32, "cand_parent")
+    _need(cand_prob, torch.float32, "cand_prob")
+    _need(cand_token, torch.int32, "cand_token")
+    ws = workspace if workspace is not None else Workspace(beam_workspace_size(n, width, vocab), draft_probs.device)
+    ws.ensure(beam_workspace_size(n, width, vocab))
+    _check(lib().as_beam_step(n, layer, width, vocab, _ptr(draft_probs), cand_stride, _ptr(cand_parent),
+                              _ptr(cand_prob), _ptr(cand_token), ws.ptr, ws.nbytes, _stream()), "as_beam_step")
+    return ws
 
 
 def select_workspace_size(n_req, n_cand_total):

@@ -97,6 +97,28 @@ as_status as_reset_workspace(void* workspace, size_t workspace_bytes, void* stre
     return cudaMemsetAsync(workspace, 0, workspace_bytes, S(stream)) == cudaSuccess ? AS_OK : AS_ERR_CUDA;
 }
 
+// ----------------------------------------------------------------- speculation (beam layer)
+size_t as_beam_workspace_size(int32_t n_req, int32_t width, int32_t vocab) {
+    if (n_req < 0 || width < 1 || width > AS_MAX_BEAM || vocab < 1) return 0;
+    return beam_ws_bytes(n_req, width, vocab);
+}
+
+as_status as_beam_step(int32_t n_req, int32_t layer, int32_t width, int32_t vocab, const float* draft_probs,
+                       int32_t cand_stride, int32_t* cand_parent, float* cand_prob, int32_t* cand_token,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+    if (n_req < 0 || layer < 1 || vocab < 1) return AS_ERR_INVALID_ARG;
+    if (width < 1 || width > AS_MAX_BEAM || vocab < width) return AS_ERR_UNSUPPORTED;
+    const long long w_in = layer == 1 ? 1 : width;
+    if (w_in * (long long)vocab >= (1ll << 32) - 1) return AS_ERR_UNSUPPORTED;
+    if ((long long)cand_stride < 1 + (long long)layer * width) return AS_ERR_INVALID_ARG;
+    if (n_req == 0) return AS_OK;
+    if (!draft_probs || !cand_parent || !cand_prob || !cand_token) return AS_ERR_INVALID_ARG;
+    if (!workspace || !al256(workspace) || workspace_bytes < beam_ws_bytes(n_req, width, vocab))
+        return AS_ERR_WORKSPACE;
+    return launch_beam(n_req, layer, width, vocab, draft_probs, cand_stride, cand_parent, cand_prob, cand_token,
+                       workspace, S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
+}
+
 // ----------------------------------------------------------------- select
 size_t as_select_workspace_size(int32_t n_req, int32_t n_cand_total) {
     if (n_req < 0 || n_cand_total < 0) return 0;

@@ -82,6 +82,9 @@ int launch_accept(const AcceptParams& p, const void* target_logits, int logits_b
 int launch_attn_simt(const SimtParams& p, int head_dim, cudaStream_t stream);
 int launch_attn_tc(const CUtensorMap* maps, const TcParams& p, int head_dim, int n_sms, cudaStream_t stream);
 int tc_ctas_per_sm();
+size_t beam_ws_bytes(int n_req, int width, int vocab);
+int launch_beam(int n_req, int layer, int width, int vocab, const float* probs, int stride, int32_t* cand_parent,
+                float* cand_prob, int32_t* cand_token, void* ws, cudaStream_t stream);
 int launch_stream_bw(const void* src, const int* order, int n_chunks, int chunk_bytes, int stages, int mode,
                      unsigned long long* sink, int grid, const CUtensorMap* tmap, cudaStream_t stream);
 int launch_umma_selftest(const CUtensorMap* ma, const CUtensorMap* mb, float* d, int N, int K, int b_mn,

@@ -40,6 +40,71 @@ def test_umma_selftest(ada, n, k, mn):
     assert torch.allclose(d.double(), ref, atol=1e-3, rtol=1e-4), (d - ref).abs().max()
 
 
+# --------------------------------------------------------------------------- speculation (beam)
+def _rand_probs(rng, shape, sigma, ties):
+    z = rng.normal(0.0, sigma, shape)
+    e = np.exp(z - z.max(axis=-1, keepdims=True))
+    p = e / e.sum(axis=-1, keepdims=True)
+    if ties:  # quantise: many exactly equal probabilities (and zeros) -> key ties resolved by index
+        p = np.floor(p * 64.0) / 64.0
+    return p.astype(np.float32)
+
+
+@pytest.mark.parametrize("V,width,n,d,ties", [(1000, 8, 6, 4, False), (1000, 8, 5, 3, True),
+                                              (8195, 2, 3, 3, False), (20, 16, 4, 3, False),
+                                              (5, 1, 3, 4, True), (128256, 8, 3, 2, False)])
+def test_beam_layers_bit_exact(ada, V, width, n, d, ties):
+    """d speculation layers on the GPU (as_beam_step) == the oracle's beam step
+    applied layer by layer: parents, tokens and f-hat bit-exact."""
+    rng = np.random.default_rng(V + width + d)
+    stride = 1 + d * width
+    par = np.zeros(n * stride, np.int32)
+    prob = np.zeros(n * stride, np.float32)
+    tok = np.zeros(n * stride, np.int32)
+    prob[::stride] = 1.0
+    tok[::stride] = rng.integers(0, V, n)
+    g_par, g_prob, g_tok = dev(par), dev(prob), dev(tok)
+    ws = None
+    for layer in range(1, d + 1):
+        w_in = 1 if layer == 1 else width
+        P = _rand_probs(rng, (n, w_in, V), float(rng.uniform(0.5, 4.0)), ties)
+        ws = ada.beam_step(layer, width, dev(P), g_par, g_prob, g_tok, stride, workspace=ws)
+        base_prev = 0 if layer == 1 else 1 + (layer - 2) * width
+        base_new = 1 + (layer - 1) * width
+        for i in range(n):
+            fpar = prob[i * stride + base_prev: i * stride + base_prev + w_in]
+            pr, tk, fv = oracle.beam_step(P[i], fpar, width)
+            k = len(pr)
+            o = i * stride + base_new
+            par[o:o + k] = base_prev + pr
+            tok[o:o + k] = tk
+            prob[o:o + k] = fv
+    assert ada.check_device_error(ws)[0] == 0
+    np.testing.assert_array_equal(g_par.cpu().numpy(), par)
+    np.testing.assert_array_equal(g_tok.cpu().numpy(), tok)
+    np.testing.assert_array_equal(g_prob.cpu().numpy().view(np.int32), prob.view(np.int32))
+
+
+def test_beam_then_select(ada):
+    """Speculation feeds selection: the GPU-built forest selected on the GPU ==
+    the oracle's select on the oracle-built forest."""
+    rng = np.random.default_rng(5)
+    n, d, width, V = 16, 5, 4, 3000
+    stride = 1 + d * width
+    prob = np.zeros(n * stride, np.float32)
+    prob[::stride] = 1.0
+    g_par, g_prob = dev(np.zeros(n * stride, np.int32)), dev(prob)
+    g_tok = dev(np.zeros(n * stride, np.int32))
+    for layer in range(1, d + 1):
+        P = _rand_probs(rng, (n, 1 if layer == 1 else width, V), 2.0, False)
+        ada.beam_step(layer, width, dev(P), g_par, g_prob, g_tok, stride)
+    F = dict(cand_offsets=np.arange(0, (n + 1) * stride, stride, dtype=np.int32),
+             cand_parent=g_par.cpu().numpy(), cand_prob=g_prob.cpu().numpy())
+    A = rng.uniform(0.5, 3.0, n)
+    got = _gpu_select(ada, F, A, d, 10, n * 8)
+    _assert_select_equal(F, A, d, 10, n * 8, got)
+
+
 # --------------------------------------------------------------------------- select
 def _gpu_select(ada, F, A, d, n_max, B):
     co, cp, cf = F["cand_offsets"], F["cand_parent"], F["cand_prob"]
