@@ -192,6 +192,17 @@ def run_accept(W, phase=None, req_range=None):
                       bonus_token=W["acc"]["bonus_token"], n_tree_rows=W["R"], workspace=W["ws_accept"])
 
 
+def run_accept_records(W, phase, records, req_range=None):
+    """Multi-GPU form: walk / commit through the contiguous record rows."""
+    ada = W["ada"]
+    kc, vc = W["pools"][W["pool_idx"]]
+    ada.accept_tokens(phase, W["sel"]["tree_offsets"], W["sel"]["tree_parent"], W["sel"]["tree_token"],
+                      target_tokens=W["target_tokens"], max_path=W["max_path"], k_tree=W["k_tree"],
+                      v_tree=W["v_tree"], k_cache=kc, v_cache=vc, page_table=W["page_table"], kv_len=W["kv_len"],
+                      kv_len_out=W["kv_len_out"], req_range=req_range, accept_path=records, n_tree_rows=W["R"],
+                      workspace=W["ws_accept"])
+
+
 def attn_algorithmic_bytes(W):
     """Per launch: K and V of every (request, kv head) prefix + tree (read once),
     Q read and O written once."""
@@ -404,8 +415,14 @@ def main():
         return main_reference(args, rank, world)
     torch.cuda.set_device(local_rank)
     dist_ctx = None
-    if world > 1:
+    force_dist = os.environ.get("AS_BENCH_FORCE_DIST") == "1"  # test only: the N>1 code path on one GPU
+    if world > 1 or force_dist:
         import torch.distributed as dist
+        if force_dist and world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         from paper_2501_12162_b200.dist import ShardedAccept
         dist_ctx = ShardedAccept(rank, world)
@@ -524,7 +541,7 @@ def main():
             toks_t, secs_t, reps = toks_t + toks, secs_t + secs, reps + 1
         cpu = {"value": round(toks_t / secs_t, 2), "unit": "verified tree tokens/s", "cores": threads,
                "kind": "oracle", "sample": f"{desc}; repeated {reps}x", "seconds": round(secs_t, 3)}
-    launches_per_step = 3
+    launches_per_step = 3 if world == 1 else 4  # select, attention, walk, commit (+ the NCCL all-gather)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "verified tree tokens/s", "n_gpus": world,
@@ -608,8 +625,10 @@ def measure_e2e(W, step, steps, world):
     names = ["cand_offsets", "cand_parent", "cand_prob", "cand_token", "slo_deficit", "q", "k_tree", "v_tree",
              "target_tokens"]
     host = {k: W[k].cpu().pin_memory() for k in names}
-    outs = ["accept_len", "accept_path", "bonus_token"]
-    host_out = {k: torch.empty_like(W["acc"][k], device="cpu").pin_memory() for k in outs}
+    # accept results: the three arrays at N=1, the all-gathered record rows at N>1
+    res = dict(W["acc"]) if step.dist is None else {"records": step.dist.records}
+    outs = list(res)
+    host_out = {k: torch.empty_like(res[k], device="cpu").pin_memory() for k in outs}
     h2d = sum(host[k].numel() * host[k].element_size() for k in names)
     d2h = sum(host_out[k].numel() * host_out[k].element_size() for k in outs)
     for _ in range(2):
@@ -617,7 +636,7 @@ def measure_e2e(W, step, steps, world):
             W[k].copy_(host[k], non_blocking=True)
         step()
         for k in outs:
-            host_out[k].copy_(W["acc"][k], non_blocking=True)
+            host_out[k].copy_(res[k], non_blocking=True)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -629,7 +648,7 @@ def measure_e2e(W, step, steps, world):
             W[k].copy_(host[k], non_blocking=True)
         step()
         for k in outs:
-            host_out[k].copy_(W["acc"][k], non_blocking=True)
+            host_out[k].copy_(res[k], non_blocking=True)
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e)

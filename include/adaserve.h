@@ -220,6 +220,10 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
  * Phases: AS_ACCEPT_FUSED = walk [begin,end) + commit of the same requests;
  *   AS_ACCEPT_WALK_ONLY = walk only; AS_ACCEPT_COMMIT_ONLY = commit from
  *   accept_len/accept_path given as inputs (e.g. after an all-gather).
+ *   *_RECORDS: the walk result of request i is ONE contiguous int32 row
+ *   accept_path[i*(max_path+2) ..] = {len, bonus, path[max_path]} (accept_len
+ *   and bonus_token unused, may be NULL) -- a request shard's rows are then a
+ *   contiguous slice, all-gathered in place with no packing (multi-GPU).
  * Inputs: tree_offsets [n_req+1], tree_parent/tree_tokens [n_tree_rows];
  *   target_tokens [n_tree_rows] or NULL; target_logits [n_tree_rows, vocab] of
  *   logits_dtype or NULL (one of the two is required for the walk);
@@ -231,7 +235,13 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
  * Device preconditions: AS_DEV_NAN_LOGIT, AS_DEV_PATH_TOO_LONG,
  *   AS_DEV_PAGE_OVERFLOW, AS_DEV_BAD_PAGE.
  */
-typedef enum { AS_ACCEPT_FUSED = 0, AS_ACCEPT_WALK_ONLY = 1, AS_ACCEPT_COMMIT_ONLY = 2 } as_accept_phase;
+typedef enum {
+    AS_ACCEPT_FUSED = 0,
+    AS_ACCEPT_WALK_ONLY = 1,
+    AS_ACCEPT_COMMIT_ONLY = 2,
+    AS_ACCEPT_WALK_RECORDS = 3,   /* walk [begin,end) into records (see below)        */
+    AS_ACCEPT_COMMIT_RECORDS = 4  /* commit all requests from records                 */
+} as_accept_phase;
 
 size_t as_accept_workspace_size(int32_t n_tree_rows);
 as_status as_accept_tokens(as_accept_phase phase, int32_t n_req, int32_t req_begin,

@@ -14,7 +14,8 @@ import os
 import torch
 
 __all__ = ["lib", "select_trees", "tree_verify_attn", "accept_tokens", "Workspace", "check_device_error",
-           "selftest_umma", "AS_ACCEPT_FUSED", "AS_ACCEPT_WALK_ONLY", "AS_ACCEPT_COMMIT_ONLY", "AdaServeError",
+           "selftest_umma", "AS_ACCEPT_FUSED", "AS_ACCEPT_WALK_ONLY", "AS_ACCEPT_COMMIT_ONLY",
+           "AS_ACCEPT_WALK_RECORDS", "AS_ACCEPT_COMMIT_RECORDS", "beam_step", "beam_workspace_size", "AdaServeError",
            "select_workspace_size", "attn_workspace_size", "accept_workspace_size", "DEVICE_ERRORS"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -22,6 +23,7 @@ LIB_PATH = os.path.join(_PKG, "libadaserve.so")
 
 AS_F32, AS_BF16 = 0, 1
 AS_ACCEPT_FUSED, AS_ACCEPT_WALK_ONLY, AS_ACCEPT_COMMIT_ONLY = 0, 1, 2
+AS_ACCEPT_WALK_RECORDS, AS_ACCEPT_COMMIT_RECORDS = 3, 4
 DEVICE_ERRORS = {0: "ok", 1: "bad parent", 2: "bad f-hat", 3: "too many candidates", 4: "tree too big",
                  5: "rows overflow", 6: "page overflow", 7: "NaN logit", 8: "path too long", 9: "bad page"}
 
@@ -230,12 +232,20 @@ def accept_tokens(phase, tree_offsets, tree_parent=None, tree_tokens=None, targe
     b, e = (0, n) if req_range is None else req_range
     R = int(n_tree_rows if n_tree_rows is not None else
             (tree_parent.numel() if tree_parent is not None else (k_tree.shape[0] if k_tree is not None else 0)))
-    if accept_len is None:
-        accept_len = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    if accept_path is None:
-        accept_path = torch.empty((max(n, 1), max_path), dtype=torch.int32, device=dev)
-    if bonus_token is None:
-        bonus_token = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    records = phase in (AS_ACCEPT_WALK_RECORDS, AS_ACCEPT_COMMIT_RECORDS)
+    if records:
+        # accept_path = int32 [rows >= n, 2 + max_path] records {len, bonus, path}
+        if accept_path is None:
+            accept_path = torch.empty((max(n, 1), 2 + max_path), dtype=torch.int32, device=dev)
+        if accept_path.dim() != 2 or accept_path.shape[0] < n or accept_path.shape[1] != 2 + max_path:
+            raise AdaServeError("records must be int32 [>= n_req, 2 + max_path]")
+    else:
+        if accept_len is None:
+            accept_len = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        if accept_path is None:
+            accept_path = torch.empty((max(n, 1), max_path), dtype=torch.int32, device=dev)
+        if bonus_token is None:
+            bonus_token = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     ws = workspace if workspace is not None else Workspace(accept_workspace_size(R), dev)
     ws.ensure(accept_workspace_size(R))
     kv_dt = _dt(k_tree) if k_tree is not None else AS_BF16
@@ -252,6 +262,8 @@ def accept_tokens(phase, tree_offsets, tree_parent=None, tree_tokens=None, targe
                                 ws.ptr, ws.nbytes,
                                 _stream())
     _check(st, "as_accept_tokens")
+    if records:
+        return dict(records=accept_path, workspace=ws)
     return dict(accept_len=accept_len, accept_path=accept_path, bonus_token=bonus_token, workspace=ws)
 
 

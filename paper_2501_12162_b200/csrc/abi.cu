@@ -289,17 +289,19 @@ as_status as_accept_tokens(as_accept_phase phase, int32_t n_req, int32_t req_beg
                            int32_t num_pages, int32_t page_size, const int32_t* page_table, int32_t max_pages_per_req,
                            int32_t* kv_len, int32_t* kv_len_out, void* workspace, size_t workspace_bytes,
                            void* stream) {
-    if (phase != AS_ACCEPT_FUSED && phase != AS_ACCEPT_WALK_ONLY && phase != AS_ACCEPT_COMMIT_ONLY)
+    if (phase != AS_ACCEPT_FUSED && phase != AS_ACCEPT_WALK_ONLY && phase != AS_ACCEPT_COMMIT_ONLY &&
+        phase != AS_ACCEPT_WALK_RECORDS && phase != AS_ACCEPT_COMMIT_RECORDS)
         return AS_ERR_INVALID_ARG;
+    const bool records = phase == AS_ACCEPT_WALK_RECORDS || phase == AS_ACCEPT_COMMIT_RECORDS;
     if (n_req < 0 || req_begin < 0 || req_end < req_begin || req_end > n_req || n_tree_rows < 0) return AS_ERR_INVALID_ARG;
     if (max_path < 1 || max_path > 64) return AS_ERR_UNSUPPORTED;
     if (!workspace || !al256(workspace) || workspace_bytes < as_accept_workspace_size(n_tree_rows))
         return AS_ERR_WORKSPACE;
-    if (!tree_offsets || !accept_len || !accept_path) return AS_ERR_INVALID_ARG;
-    const bool walk = phase != AS_ACCEPT_COMMIT_ONLY;
-    const bool commit = phase != AS_ACCEPT_WALK_ONLY;
+    if (!tree_offsets || !accept_path || (!records && !accept_len)) return AS_ERR_INVALID_ARG;
+    const bool walk = phase == AS_ACCEPT_FUSED || phase == AS_ACCEPT_WALK_ONLY || phase == AS_ACCEPT_WALK_RECORDS;
+    const bool commit = phase == AS_ACCEPT_FUSED || phase == AS_ACCEPT_COMMIT_ONLY || phase == AS_ACCEPT_COMMIT_RECORDS;
     if (walk) {
-        if (!tree_parent || !tree_tokens || !bonus_token) return AS_ERR_INVALID_ARG;
+        if (!tree_parent || !tree_tokens || (!records && !bonus_token)) return AS_ERR_INVALID_ARG;
         if (!target_tokens && !target_logits) return AS_ERR_INVALID_ARG;
         if (!target_tokens && (vocab <= 0 || (logits_dtype != AS_F32 && logits_dtype != AS_BF16)))
             return AS_ERR_INVALID_ARG;
@@ -324,6 +326,7 @@ as_status as_accept_tokens(as_accept_phase phase, int32_t n_req, int32_t req_beg
     p.kv_len = kv_len; p.kv_len_out = kv_len_out ? kv_len_out : kv_len; p.ws = workspace;
     p.do_walk = walk ? 1 : 0;
     p.do_commit = commit ? 1 : 0;
+    p.records = records ? 1 : 0;
     int32_t* argmax_buf = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(workspace) + kWsHeaderBytes);
     return launch_accept(p, target_logits, logits_dtype == AS_BF16, vocab, argmax_buf, S(stream)) == 0 ? AS_OK
                                                                                                       : AS_ERR_CUDA;

@@ -279,11 +279,18 @@ __global__ void __launch_bounds__(kAccThreads) walk_commit_kernel(AcceptParams p
                 }
             }
             __syncwarp();
-            int32_t* path = p.accept_path + (size_t)i * p.max_path;
+            // records: row i = {len, bonus, path[max_path]} (one contiguous int32 row per request)
+            int32_t* rec = p.records ? p.accept_path + (size_t)i * (p.max_path + 2) : nullptr;
+            int32_t* path = p.records ? rec + 2 : p.accept_path + (size_t)i * p.max_path;
             for (int k = lane; k < p.max_path; k += 32) path[k] = (k < len) ? sm.path[k] : -1;
             if (lane == 0) {
-                p.accept_len[i] = len;
-                p.bonus_token[i] = tstar;
+                if (p.records) {
+                    rec[0] = len;
+                    rec[1] = tstar;
+                } else {
+                    p.accept_len[i] = len;
+                    p.bonus_token[i] = tstar;
+                }
                 sm.len = len;
             }
         }
@@ -295,11 +302,12 @@ __global__ void __launch_bounds__(kAccThreads) walk_commit_kernel(AcceptParams p
         if (i >= p.n_req) return;
         const int L = __ldg(p.kv_len + i);
         const int off = __ldg(p.tree_offsets + i);
-        int len = p.accept_len[i];
+        const int32_t* rec = p.accept_path + (size_t)i * (p.max_path + 2);
+        int len = p.records ? rec[0] : p.accept_len[i];
         if (len > p.max_path) len = p.max_path;
         if (len > kAccMaxPath) len = kAccMaxPath;
         if (len < 0) len = 0;
-        const int32_t* path = p.accept_path + (size_t)i * p.max_path;
+        const int32_t* path = p.records ? rec + 2 : p.accept_path + (size_t)i * p.max_path;
         if (tid < len) {
             sm.path[tid] = path[tid];
             sm.dst[tid] = slot_dst(p, i, L, tid, row_bytes);

@@ -27,6 +27,7 @@ struct AcceptParams {
     int32_t* kv_len_out;  // == kv_len for in-place updates
     void* ws;
     int do_walk, do_commit;
+    int records;  // 1: accept_path is int32 [rows][2 + max_path] records {len, bonus, path}
 };
 
 struct SimtParams {

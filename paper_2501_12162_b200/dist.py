@@ -5,9 +5,12 @@ NCCL exchange of the hot path (BASELINE north_star).
 * attention is sharded by KV head: rank p owns kv heads
   [p*n_kv/P, (p+1)*n_kv/P) and their G query heads (no collective);
 * the acceptance walk is sharded by request (rank p walks requests
-  [p*s, (p+1)*s), s = ceil(n/P)), then ONE all_gather_into_tensor of fixed-size
-  int32 accept records {accept_len, bonus_token, path[max_path]} over NCCL /
-  NVLink; every rank then commits ALL requests' paths for ITS OWN kv heads.
+  [p*s, (p+1)*s), s = ceil(n/P)) and writes fixed-size int32 records
+  {accept_len, bonus_token, path[max_path]} straight into its rows of a
+  [P*s, 2 + max_path] buffer (as_accept_tokens AS_ACCEPT_WALK_RECORDS), ONE
+  in-place all_gather_into_tensor over NCCL / NVLink fills the other ranks'
+  rows, and every rank commits ALL requests' paths for ITS OWN kv heads from
+  the records (AS_ACCEPT_COMMIT_RECORDS): 2 kernels + 1 collective, no packing.
 Nothing else crosses NVLink: no KV, no activations, no logits.
 
 The packing helpers are plain torch ops (device-agnostic) so the protocol is
@@ -60,20 +63,34 @@ def all_gather_records(rec, world, group=None):
     return out
 
 
+def record_shard(records, rank, s):
+    """This rank's rows of the [world*s, 2+mp] record buffer (a contiguous view)."""
+    return records[rank * s:(rank + 1) * s]
+
+
+def all_gather_in_place(records, rank, world, group=None):
+    """Fill every rank's rows of `records` from the owner rank (in place)."""
+    s = records.shape[0] // world
+    dist.all_gather_into_tensor(records, record_shard(records, rank, s), group=group)
+    return records
+
+
 class ShardedAccept:
-    """WALK_ONLY on this rank's request shard -> all-gather -> COMMIT_ONLY."""
+    """WALK_RECORDS on this rank's request shard -> in-place all-gather ->
+    COMMIT_RECORDS (every rank, its own kv heads)."""
 
     def __init__(self, rank: int, world: int, group=None):
         self.rank, self.world, self.group = rank, world, group
+        self.records = None
 
     def accept_and_commit(self, W):
         import paper_2501_12162_b200 as ada
-        from bench import run_accept  # the bench's call wrapper (same arguments)
+        from bench import run_accept_records  # the bench's call wrapper (same arguments)
         n = W["n"]
         b, e, s = request_range(n, self.rank, self.world)
-        acc = W["acc"]
-        run_accept(W, phase=ada.AS_ACCEPT_WALK_ONLY, req_range=(b, e))
-        rec = pack_records(acc["accept_len"], acc["accept_path"], acc["bonus_token"], b, e, s)
-        g = all_gather_records(rec, self.world, self.group)
-        unpack_records(g, n, acc["accept_len"], acc["accept_path"], acc["bonus_token"])
-        run_accept(W, phase=ada.AS_ACCEPT_COMMIT_ONLY)
+        if self.records is None:
+            self.records = torch.zeros((self.world * s, 2 + W["max_path"]), dtype=torch.int32,
+                                       device=W["kv_len"].device)
+        run_accept_records(W, ada.AS_ACCEPT_WALK_RECORDS, self.records, req_range=(b, e))
+        all_gather_in_place(self.records, self.rank, self.world, self.group)
+        run_accept_records(W, ada.AS_ACCEPT_COMMIT_RECORDS, self.records)

@@ -12,8 +12,8 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from paper_2501_12162_b200.dist import (all_gather_records, head_range, pack_records, request_range,
-                                        unpack_records)
+from paper_2501_12162_b200.dist import (all_gather_in_place, all_gather_records, head_range, pack_records,
+                                        record_shard, request_range, unpack_records)
 
 
 def _free_port():
@@ -60,6 +60,69 @@ def _worker(rank, world, port, n, q):
           and np.array_equal(bt2.numpy(), full["bonus_token"]))
     q.put((rank, ok))
     dist.destroy_process_group()
+
+
+def _worker_records(rank, world, port, n, q):
+    """The record protocol the GPU path uses (AS_ACCEPT_WALK_RECORDS ->
+    in-place all_gather_into_tensor -> AS_ACCEPT_COMMIT_RECORDS), with the
+    oracle standing in for the two kernels: every rank ends with every
+    request's record, and committing them for this rank's kv heads equals the
+    single-process commit of those heads."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    to, par, toks, tgt = _walk_inputs(9, n)
+    mpth = 20
+    b, e, s = request_range(n, rank, world)
+    rec = torch.full((world * s, 2 + mpth), -7, dtype=torch.int32)
+    sub_to = (to[b:e + 1] - to[b]).astype(np.int32)
+    rows = slice(int(to[b]), int(to[e]))
+    if e > b:
+        r = oracle.accept_walk(sub_to, par[rows], toks[rows], target_tokens=tgt[rows], max_path=mpth)
+        mine = record_shard(rec, rank, s)
+        mine[:e - b, 0] = torch.from_numpy(r["accept_len"])
+        mine[:e - b, 1] = torch.from_numpy(r["bonus_token"])
+        mine[:e - b, 2:] = torch.from_numpy(r["accept_path"])
+    all_gather_in_place(rec, rank, world)
+    full = oracle.accept_walk(to, par, toks, target_tokens=tgt, max_path=mpth)
+    ok = (np.array_equal(rec[:n, 0].numpy(), full["accept_len"]) and
+          np.array_equal(rec[:n, 1].numpy(), full["bonus_token"]) and
+          np.array_equal(rec[:n, 2:].numpy(), full["accept_path"]))
+    # commit from the gathered records for this rank's heads == the full commit's head slice
+    rng = np.random.default_rng(4)
+    R = int(to[-1])
+    n_kv, d, ps = 4, 8, 4
+    kv_len = rng.integers(0, 9, n).astype(np.int32)
+    table, n_pages = synth.paged_kv(rng, kv_len, ps, extra_slots=mpth + 2)
+    kt = rng.standard_normal((R, n_kv, d)).astype(np.float32)
+    vt = rng.standard_normal((R, n_kv, d)).astype(np.float32)
+    kc = rng.standard_normal((n_pages, n_kv, ps, d)).astype(np.float32)
+    vc = rng.standard_normal((n_pages, n_kv, ps, d)).astype(np.float32)
+    h0, h1 = head_range(n_kv, rank, world)
+    kc_all, vc_all, kl_all = kc.copy(), vc.copy(), kv_len.copy()
+    oracle.commit(to, full["accept_len"], full["accept_path"], kt, vt, kc_all, vc_all, table, kl_all)
+    kc_me = np.ascontiguousarray(kc[:, h0:h1])
+    vc_me = np.ascontiguousarray(vc[:, h0:h1])
+    kl_me = kv_len.copy()
+    oracle.commit(to, rec[:n, 0].numpy().copy(), rec[:n, 2:].numpy().copy(), np.ascontiguousarray(kt[:, h0:h1]),
+                  np.ascontiguousarray(vt[:, h0:h1]), kc_me, vc_me, table, kl_me)
+    ok = ok and np.array_equal(kc_me, kc_all[:, h0:h1]) and np.array_equal(vc_me, vc_all[:, h0:h1])
+    ok = ok and np.array_equal(kl_me, kl_all)
+    q.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,world", [(7, 2), (64, 2), (1, 2), (10, 4)])
+def test_record_protocol_gloo(n, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_records, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
 
 
 @pytest.mark.parametrize("n", [7, 64, 1])

@@ -351,6 +351,23 @@ def test_accept_sharded_walk_then_commit_equals_fused(ada):
     assert torch.equal(al, fused["accept_len"]) and torch.equal(ap, fused["accept_path"])
     assert torch.equal(bt, fused["bonus_token"])
     assert torch.equal(kl1, kl2) and torch.equal(kc1, kc2) and torch.equal(vc1, vc2)
+    # the record form used across GPUs: shards walk into their rows of one
+    # [world*s, 2 + max_path] buffer (the all-gather is the identity on one GPU),
+    # then every request is committed from the records; kv_len_out out of place
+    world, s = 3, 17
+    rec = torch.full((world * s, 26), -7, dtype=torch.int32, device="cuda")
+    for r in range(world):
+        b, e = min(n, r * s), min(n, r * s + s)
+        ada.accept_tokens(ada.AS_ACCEPT_WALK_RECORDS, dev(X["to"]), dev(X["par"]), dev(X["toks"]),
+                          target_tokens=dev(X["tgt"]), max_path=24, req_range=(b, e), accept_path=rec)
+    assert torch.equal(rec[:n, 0], fused["accept_len"]) and torch.equal(rec[:n, 1], fused["bonus_token"])
+    assert torch.equal(rec[:n, 2:], fused["accept_path"])
+    kc3, vc3, kl3 = dev(X["kc"], torch.bfloat16), dev(X["vc"], torch.bfloat16), dev(X["kv_len"])
+    kl3_out = torch.full_like(kl3, -1)
+    ada.accept_tokens(ada.AS_ACCEPT_COMMIT_RECORDS, dev(X["to"]), max_path=24, accept_path=rec, k_cache=kc3,
+                      v_cache=vc3, kv_len=kl3, kv_len_out=kl3_out, n_tree_rows=int(X["to"][-1]), **args)
+    assert torch.equal(kl3, dev(X["kv_len"]))  # input untouched
+    assert torch.equal(kl3_out, kl1) and torch.equal(kc3, kc1) and torch.equal(vc3, vc1)
 
 
 # --------------------------------------------------------------------------- attention
