@@ -242,6 +242,14 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     const int mt_max = (AS_MAX_TREE * G + 127) / 128;
     p.n_units = mt_max * n_req * n_kv_heads;
     p.mt_max = mt_max;
+    // CTA shape: pair the q-tiles of a (request, kv head) -- each K/V tile loaded
+    // once for both -- when the trees on average span more than one 128-row
+    // q-tile (n_tree_rows / n_req: the caller's row allocation per request).
+    {
+        const char* nqe = getenv("AS_ATTN_NQ");  // A/B override: 1 or 2
+        const long long rows_per_req = n_req > 0 ? (long long)n_tree_rows / n_req : 0;
+        p.nq = (nqe && (atoi(nqe) == 1 || atoi(nqe) == 2)) ? atoi(nqe) : (G * rows_per_req > 128 ? 2 : 1);
+    }
     {
         const int nsm = sm_count();
         const size_t slot = ((size_t)128 * head_dim + 256) * 4;

@@ -35,37 +35,48 @@ namespace as {
 
 constexpr int kBM = 128;          // query rows per tile (UMMA M)
 constexpr int kBN = 64;           // keys per tile
-constexpr int kKStages = 2;       // K ring depth (released right after QK)
-constexpr int kVStages = 2;       // V ring depth (held until PV)
-constexpr int kThreads = 192;     // 6 warps: TMA producer, MMA, 4 softmax
-constexpr int kCtasPerSm = 2;
-constexpr int kTmemCols = 256;    // S [0,64) P0 [64,96) P1 [96,128) O [128,128+D)
-constexpr int kScol = 0;
-constexpr int kPcol = 64;         // P double buffer: [64,96) and [96,128)
-constexpr int kOcol = 128;
+// Two CTA shapes (template NQ = q-tiles processed per CTA):
+//  NQ = 1: 192 threads (TMA producer, MMA, 4 softmax warps), 2 CTAs per SM,
+//          256 TMEM columns, 2+2-stage K/V rings -- every unit its own K/V stream;
+//  NQ = 2: 352 threads (producer, 2 MMA warps, 2 x 4 softmax warps), 1 CTA/SM, all
+//          512 TMEM columns, 4+5-stage rings -- the two q-tiles of a (request,
+//          kv head) share every K/V tile (loaded once for both), chosen when the
+//          trees span more than one 128-row q-tile (c4/c5 shapes).
+// TMEM columns of q-tile q: S at q*64, P (double) at NQ*64 + q*64 (+32),
+// O at NQ*128 + q*128.
+template <int NQ> struct TcCfg;
+template <> struct TcCfg<1> {
+    static constexpr int THREADS = 192, CTAS = 2, TMEM = 256, KST = 2, VST = 2;
+};
+template <> struct TcCfg<2> {
+    static constexpr int THREADS = 352, CTAS = 1, TMEM = 512, KST = 4, VST = 5;
+};
+constexpr int kCtasPerSm = 2;     // max over the shapes (workspace sizing)
 constexpr int kPtChunk = 256;     // page-table entries staged per refill
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 constexpr int kMaxRec = 64;       // pieces per CTA precomputed in the prologue
 constexpr int kTraceCtas = 512;   // per-CTA timeline records after the CTA-0 tile trace (debug)
 
-template <int D>
+template <int D, int NQ>
 struct TcSmem {
+    static constexpr int KST = TcCfg<NQ>::KST, VST = TcCfg<NQ>::VST;
     static constexpr int NCH = D / 64;                        // 128-byte swizzle chunks along d
-    static constexpr int Q_BYTES = NCH * kBM * 128;           // 16 KB per chunk
+    static constexpr int Q_BYTES = NCH * kBM * 128;           // 16 KB per chunk (one q-tile)
     static constexpr int KV_BYTES = NCH * kBN * 128;          // 8 KB per chunk
-    static constexpr int OFF_Q = 0;
-    static constexpr int OFF_K = OFF_Q + Q_BYTES;
-    static constexpr int OFF_V = OFF_K + kKStages * KV_BYTES;
-    static constexpr int OFF_PT = OFF_V + kVStages * KV_BYTES;     // [kPtChunk] staged page-table row
-    static constexpr int OFF_TP = OFF_PT + kPtChunk * 4;           // [2][AS_MAX_TREE] staged tree parents
-    static constexpr int OFF_REC = OFF_TP + 2 * AS_MAX_TREE * 4;  // [kMaxRec] this CTA's pieces
+    static constexpr int OFF_Q = 0;                           // [NQ] q-tiles
+    static constexpr int OFF_K = OFF_Q + NQ * Q_BYTES;
+    static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
+    static constexpr int OFF_PT = OFF_V + VST * KV_BYTES;     // [kPtChunk] staged page-table row
+    static constexpr int OFF_TP = OFF_PT + kPtChunk * 4;      // [NQ][2][AS_MAX_TREE] staged tree parents
+    static constexpr int OFF_REC = OFF_TP + NQ * 2 * AS_MAX_TREE * 4;  // [kMaxRec] this CTA's pieces
     static constexpr int OFF_BAR = OFF_REC + kMaxRec * 32;
-    static constexpr int N_BAR = 2 + 2 * kKStages + 2 * kVStages + 6 + 2;
+    // q_full q_empty, K/V rings, and per q-tile: s_full s_empty p_full[2] p_empty[2] o_full o_empty
+    static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + NQ * 8;
     static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
     static constexpr int BYTES = OFF_TMEM + 16;
     static constexpr int ALLOC = BYTES + 1024;  // alignment slack
     // stream-K plan scratch (long long per block) aliases the K+V rings before any TMA
-    static constexpr int PLAN_CAP = (kKStages + kVStages) * KV_BYTES / 8;
+    static constexpr int PLAN_CAP = (KST + VST) * KV_BYTES / 8;
     static constexpr int PLAN_HALF = PLAN_CAP / 2;  // [0,half) tile prefix, [half, cap) unit prefix
 };
 
@@ -76,13 +87,21 @@ struct TcSmem {
             p.trace[(size_t)(idx) * 8 + (e)] = clock64();                                      \
     } while (0)
 
+// Named barrier of one softmax warp group (128 threads; ids 1 and 2, constant
+// operands so the kernel claims only the barriers it uses).
+__device__ __forceinline__ void group_bar(int grp) {
+    if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
+    else asm volatile("bar.sync 2, 128;" ::: "memory");
+}
+
 struct Unit {
-    int i, g, mt, off, K, L, nt, n_prefix;
+    int i, g, mt, nq, off, K, L, nt, n_prefix;  // mt = first q-tile, nq = q-tiles in this unit
 };
 
-// Per-request geometry: MT q-tiles of 128 rows (rows = node*G + hh), nt KV tiles.
+// Per-request geometry: QT q-tiles of 128 rows (rows = node*G + hh) per kv head,
+// grouped p.nq at a time into MT units per head; nt KV tiles.
 struct Req {
-    int off, K, L, MT, nt, n_prefix;
+    int off, K, L, QT, MT, nt, n_prefix;
 };
 
 __device__ __forceinline__ void load_req(const TcParams& p, int i, Req& r) {
@@ -93,14 +112,16 @@ __device__ __forceinline__ void load_req(const TcParams& p, int i, Req& r) {
     if (r.L > p.max_pages * p.page_size) r.L = p.max_pages * p.page_size;
     r.n_prefix = (r.L + kBN - 1) / kBN;
     const bool ok = r.K > 0 && r.K <= AS_MAX_TREE && r.off + r.K <= p.n_tree_rows;
-    r.MT = ok ? (r.K * p.G + kBM - 1) / kBM : 0;
+    r.QT = ok ? (r.K * p.G + kBM - 1) / kBM : 0;
+    r.MT = (r.QT + p.nq - 1) / p.nq;
     r.nt = r.n_prefix + (r.K + kBN - 1) / kBN;
 }
 
-__device__ __forceinline__ void make_unit(const Req& r, int i, int j, Unit& u) {
+__device__ __forceinline__ void make_unit(const TcParams& p, const Req& r, int i, int j, Unit& u) {
     u.i = i;
     u.g = j / r.MT;
-    u.mt = j - u.g * r.MT;
+    u.mt = (j - u.g * r.MT) * p.nq;
+    u.nq = min(p.nq, r.QT - u.mt);
     u.off = r.off;
     u.K = r.K;
     u.L = r.L;
@@ -147,9 +168,10 @@ __device__ __forceinline__ bool rec_next(const TcParams& p, RecCursor& cur, Piec
     r.K = rc.K;
     r.L = rc.L;
     r.n_prefix = (r.L + kBN - 1) / kBN;
-    r.MT = (r.K * p.G + kBM - 1) / kBM;
+    r.QT = (r.K * p.G + kBM - 1) / kBM;
+    r.MT = (r.QT + p.nq - 1) / p.nq;
     r.nt = r.n_prefix + (r.K + kBN - 1) / kBN;
-    make_unit(r, rc.i, rc.j, pc.u);
+    make_unit(p, r, rc.i, rc.j, pc.u);
     pc.w = (rc.i * p.n_kv + pc.u.g) * p.mt_max + pc.u.mt;
     pc.tb = rc.tb;
     pc.te = rc.te;
@@ -176,7 +198,7 @@ __device__ __forceinline__ bool sched_next(const TcParams& p, Sched& sc, Piece& 
         }
         if (sc.i >= p.n_req) return false;
         const int j = (int)(sc.k - sc.ucum);
-        make_unit(sc.r, sc.i, j, pc.u);
+        make_unit(p, sc.r, sc.i, j, pc.u);
         pc.w = (sc.i * p.n_kv + pc.u.g) * p.mt_max + pc.u.mt;
         pc.tb = 0;
         pc.te = pc.u.nt;
@@ -192,7 +214,7 @@ __device__ __forceinline__ bool sched_next(const TcParams& p, Sched& sc, Piece& 
             sc.t = 0;
             continue;
         }
-        make_unit(sc.r, sc.i, sc.j, pc.u);
+        make_unit(p, sc.r, sc.i, sc.j, pc.u);
         pc.w = (sc.i * p.n_kv + pc.u.g) * p.mt_max + pc.u.mt;
         pc.tb = sc.t;
         const long long avail = pc.u.nt - sc.t;
@@ -220,13 +242,14 @@ __device__ __forceinline__ int sk_owner(long long T, int G, long long x) {
     return b;
 }
 
-template <int D>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+template <int D, int NQ>
+__global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
                         const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kt,
                         const __grid_constant__ CUtensorMap tm_vt, const TcParams p) {
-    using S = TcSmem<D>;
+    using S = TcSmem<D, NQ>;
     constexpr int NCH = S::NCH;
+    constexpr int kKStages = S::KST, kVStages = S::VST;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
@@ -236,12 +259,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     uint64_t* k_empty = k_full + kKStages;
     uint64_t* v_full = k_empty + kKStages;
     uint64_t* v_empty = v_full + kVStages;
-    uint64_t* s_full = v_empty + kVStages;
-    uint64_t* s_empty = s_full + 1;
-    uint64_t* p_full = s_empty + 1;   // [2] per P buffer
-    uint64_t* p_empty = p_full + 2;   // [2]
-    uint64_t* o_full = p_empty + 2;
-    uint64_t* o_empty = o_full + 1;
+    uint64_t* qbars = v_empty + kVStages;  // per q-tile q: 8 barriers at qbars + 8q
+    auto s_full = [&](int q) { return qbars + 8 * q + 0; };
+    auto s_empty = [&](int q) { return qbars + 8 * q + 1; };
+    auto p_full = [&](int q, int b) { return qbars + 8 * q + 2 + b; };   // per P buffer
+    auto p_empty = [&](int q, int b) { return qbars + 8 * q + 4 + b; };
+    auto o_full = [&](int q) { return qbars + 8 * q + 6; };
+    auto o_empty = [&](int q) { return qbars + 8 * q + 7; };
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + S::OFF_TMEM);
 
     const int warp = warp_id();
@@ -250,23 +274,25 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
     if (threadIdx.x == 0) {
         ptx::mbar_init(q_full, 1);
-        ptx::mbar_init(q_empty, 1);
+        ptx::mbar_init(q_empty, NQ);  // one commit per MMA warp
         for (int s = 0; s < kKStages; ++s) {
             ptx::mbar_init(k_full + s, 1);
-            ptx::mbar_init(k_empty + s, 1);
+            ptx::mbar_init(k_empty + s, NQ);
         }
         for (int s = 0; s < kVStages; ++s) {
             ptx::mbar_init(v_full + s, 1);
-            ptx::mbar_init(v_empty + s, 1);
+            ptx::mbar_init(v_empty + s, NQ);
         }
-        ptx::mbar_init(s_full, 1);
-        ptx::mbar_init(s_empty, 4);  // the 4 softmax warps
-        for (int b = 0; b < 2; ++b) {
-            ptx::mbar_init(p_full + b, 4);
-            ptx::mbar_init(p_empty + b, 1);
+        for (int q = 0; q < NQ; ++q) {
+            ptx::mbar_init(s_full(q), 1);
+            ptx::mbar_init(s_empty(q), 4);  // the q-tile's 4 softmax warps
+            for (int b = 0; b < 2; ++b) {
+                ptx::mbar_init(p_full(q, b), 4);
+                ptx::mbar_init(p_empty(q, b), 1);
+            }
+            ptx::mbar_init(o_full(q), 1);
+            ptx::mbar_init(o_empty(q), 4);
         }
-        ptx::mbar_init(o_full, 1);
-        ptx::mbar_init(o_empty, 4);
         ptx::fence_mbar_init();
         ptx::tma_prefetch(&tm_q);
         ptx::tma_prefetch(&tm_kc);
@@ -274,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         ptx::tma_prefetch(&tm_kt);
         ptx::tma_prefetch(&tm_vt);
     }
-    if (warp == 1) ptx::tmem_alloc(tmem_holder, kTmemCols);
+    if (warp == 1) ptx::tmem_alloc(tmem_holder, TcCfg<NQ>::TMEM);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -288,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     __shared__ int sk_cur[3];
     __shared__ int sk_stream;
     __shared__ long long scan_tmp[33];
-    __shared__ int red_tmp[3][8];
+    __shared__ int red_tmp[3][16];  // per warp (<= 10 warps)
     __shared__ int sk_last;
     RecCursor cur0;
     {
@@ -297,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         long long* pre = reinterpret_cast<long long*>(smem + S::OFF_K);
         long long* preu = pre + S::PLAN_HALF;
         const bool can_plan = n <= S::PLAN_HALF;
-        const bool can_stream = p.stream_k && can_plan;
+        const bool can_stream = NQ == 1 && p.stream_k && can_plan;  // paired q-tiles: static only
         int my_units = 0, my_maxnt = 0, my_minnt = 0x7fffffff;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             Req r;
@@ -484,9 +510,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             int chunk0 = -1;  // first page index currently staged
             if (lane == 0) {
                 ptx::mbar_wait(q_empty, (unit_it & 1) ^ 1);
-                ptx::mbar_arrive_expect_tx(q_full, S::Q_BYTES);
-                const int node0 = u.off + u.mt * (kBM / p.G);
-                ptx::tma_load_4d(smem + S::OFF_Q, &tm_q, q_full, 0, u.g * p.G, node0, 0);
+                ptx::mbar_arrive_expect_tx(q_full, (uint32_t)(u.nq * S::Q_BYTES));
+                for (int q = 0; q < u.nq; ++q) {
+                    const int node0 = u.off + (u.mt + q) * (kBM / p.G);
+                    ptx::tma_load_4d(smem + S::OFF_Q + q * S::Q_BYTES, &tm_q, q_full, 0, u.g * p.G, node0, 0);
+                }
             }
             const int n = pc.te - pc.tb;
             for (int j = 0; j < n + lead; ++j) {
@@ -553,56 +581,71 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             }
             ++unit_it;
         }
-    } else if (warp == 1) {
-        // ===================== MMA issuer =====================
+    } else if (warp <= NQ) {
+        // ===================== MMA issuers (warp 1 + q: q-tile q of each unit) =====================
         // Issue order per piece: QK0 | QK1 PV0 | QK2 PV1 | ...  QK_{t+1} waits for
-        // the softmax to have READ S_t (start of its tile), PV_t for P_t.
+        // the softmax to have READ S_t (start of its tile), PV_t for P_t.  Each
+        // q-tile has its own issuing warp, so the two q-tiles of a unit never wait
+        // on each other; a K/V slot is free once every MMA warp has released it
+        // (a warp whose q-tile the unit lacks releases it without an MMA).
+        const int q = warp - 1;
         constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(kBM, kBN, 0);
         constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(kBM, D, 1);
-        const uint32_t q_base = ptx::smem_u32(smem + S::OFF_Q);
+        const uint32_t q_base = ptx::smem_u32(smem + S::OFF_Q) + q * S::Q_BYTES;
         const uint32_t k_base = ptx::smem_u32(smem + S::OFF_K);
         const uint32_t v_base = ptx::smem_u32(smem + S::OFF_V);
-        uint32_t k_it = 0, v_it = 0, unit_it = 0, s_it = 0, p_it = 0;
+        const uint32_t s_col = tmem + q * 64, p_col = tmem + NQ * 64 + q * 64, o_col = tmem + NQ * 128 + q * 128;
+        uint32_t k_it = 0, v_it = 0, unit_it = 0, s_it = 0, p_it = 0, o_it = 0;
         RecCursor sc = cur0;
         Piece pc;
         while (rec_next(p, sc, pc)) {
             const Unit& u = pc.u;
+            const bool mine = q < u.nq;
             ptx::mbar_wait(q_full, unit_it & 1);
             auto do_qk = [&](int t) {
                 const int st = k_it % kKStages;
                 ptx::mbar_wait(k_full + st, (k_it / kKStages) & 1);
-                if (lane == 0) AS_TRACE(2, k_it);
-                ptx::mbar_wait(s_empty, (s_it & 1) ^ 1);
-                if (lane == 0) AS_TRACE(7, k_it);
-                ptx::tc_fence_after();
-                if (p.debug_mode >= 2) {
-                    if (lane == 0) {
+                if (lane == 0 && q == 0) AS_TRACE(2, k_it);
+                if (mine) {
+                    ptx::mbar_wait(s_empty(q), (s_it & 1) ^ 1);
+                    if (lane == 0 && q == 0) AS_TRACE(7, k_it);
+                    ptx::tc_fence_after();
+                }
+                if (lane == 0) {
+                    if (!mine || p.debug_mode >= 2) {
+                        if (mine) ptx::mbar_arrive(s_full(q));
                         ptx::mbar_arrive(k_empty + st);
-                        ptx::mbar_arrive(s_full);
                         if (t == pc.te - 1) ptx::mbar_arrive(q_empty);
-                    }
-                } else if (lane == 0) {
+                    } else {
 #pragma unroll
-                    for (int ks = 0; ks < D / 16; ++ks) {
-                        const int c = ks >> 2, kk = ks & 3;
-                        const uint64_t a = ptx::sw128_desc(q_base + c * kBM * 128 + kk * 32, 0, 1024);
-                        const uint64_t b = ptx::sw128_desc(k_base + st * S::KV_BYTES + c * kBN * 128 + kk * 32, 0, 1024);
-                        ptx::mma_bf16_ss(tmem + kScol, a, b, idesc_qk, ks > 0 ? 1u : 0u);
+                        for (int ks = 0; ks < D / 16; ++ks) {
+                            const int c = ks >> 2, kk = ks & 3;
+                            const uint64_t a = ptx::sw128_desc(q_base + c * kBM * 128 + kk * 32, 0, 1024);
+                            const uint64_t b = ptx::sw128_desc(k_base + st * S::KV_BYTES + c * kBN * 128 + kk * 32, 0, 1024);
+                            ptx::mma_bf16_ss(s_col, a, b, idesc_qk, ks > 0 ? 1u : 0u);
+                        }
+                        ptx::mma_commit(s_full(q));
+                        ptx::mma_commit(k_empty + st);
+                        if (t == pc.te - 1) ptx::mma_commit(q_empty);
                     }
-                    ptx::mma_commit(k_empty + st);
-                    ptx::mma_commit(s_full);
-                    if (t == pc.te - 1) ptx::mma_commit(q_empty);
                 }
                 __syncwarp();
                 ++k_it;
-                ++s_it;
+                if (mine) ++s_it;
             };
             auto do_pv = [&](int t) {
                 const int st = v_it % kVStages;
                 ptx::mbar_wait(v_full + st, (v_it / kVStages) & 1);
-                if (lane == 0) AS_TRACE(3, v_it);
+                if (lane == 0 && q == 0) AS_TRACE(3, v_it);
+                if (!mine) {
+                    if (lane == 0) ptx::mbar_arrive(v_empty + st);
+                    __syncwarp();
+                    ++v_it;
+                    return;
+                }
                 // zero V rows past the prefix end (stale/uninitialised smem or cache
-                // slots >= L may hold NaN; P is 0 there but 0 * NaN = NaN)
+                // slots >= L may hold NaN; P is 0 there but 0 * NaN = NaN); with two
+                // MMA warps both write the same zeros (benign)
                 if (t < u.n_prefix) {
                     const int valid = min(kBN, u.L - t * kBN);
                     if (valid < kBN) {
@@ -615,26 +658,25 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                     }
                 }
                 const uint32_t pbuf = p_it & 1;
-                ptx::mbar_wait(p_full + pbuf, (p_it >> 1) & 1);
-                if (lane == 0) AS_TRACE(4, v_it);
-                if (t == pc.tb) ptx::mbar_wait(o_empty, (unit_it & 1) ^ 1);  // O drained by the previous epilogue
+                ptx::mbar_wait(p_full(q, pbuf), (p_it >> 1) & 1);
+                if (lane == 0 && q == 0) AS_TRACE(4, v_it);
+                if (t == pc.tb) ptx::mbar_wait(o_empty(q), (o_it & 1) ^ 1);  // O drained by the last epilogue
                 ptx::tc_fence_after();
                 __syncwarp();
                 if (p.debug_mode >= 2) {
                     if (lane == 0) {
                         ptx::mbar_arrive(v_empty + st);
-                        ptx::mbar_arrive(p_empty + pbuf);
+                        ptx::mbar_arrive(p_empty(q, pbuf));
                     }
                 } else if (lane == 0) {
 #pragma unroll
                     for (int kk = 0; kk < kBN / 16; ++kk) {
-                        // A = P_t: bf16 pairs in TMEM columns [kPcol, kPcol + kBN/2)
+                        // A = P_t: bf16 pairs in the q-tile's TMEM P buffer
                         const uint64_t b = ptx::sw128_desc(v_base + st * S::KV_BYTES + kk * 16 * 128, kBN * 128, 1024);
-                        ptx::mma_bf16_ts(tmem + kOcol, tmem + kPcol + pbuf * 32 + kk * 8, b, idesc_pv,
-                                         (t > pc.tb || kk > 0) ? 1u : 0u);
+                        ptx::mma_bf16_ts(o_col, p_col + pbuf * 32 + kk * 8, b, idesc_pv, (t > pc.tb || kk > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(v_empty + st);
-                    ptx::mma_commit(p_empty + pbuf);
+                    ptx::mma_commit(p_empty(q, pbuf));
                 }
                 __syncwarp();
                 ++v_it;
@@ -645,21 +687,30 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 if (t + 1 < pc.te) do_qk(t + 1);
                 do_pv(t);
             }
-            if (lane == 0) {
-                if (p.debug_mode >= 2) ptx::mbar_arrive(o_full);
-                else ptx::mma_commit(o_full);
+            if (mine) {
+                if (lane == 0) {
+                    if (p.debug_mode >= 2) ptx::mbar_arrive(o_full(q));
+                    else ptx::mma_commit(o_full(q));
+                }
+                ++o_it;
             }
             __syncwarp();
             ++unit_it;
         }
     } else {
-        // ===================== softmax + epilogue (warps 2..5) =====================
-        const int quad = warp & 3;       // TMEM lane quadrant this warp may access
-        const int r = quad * 32 + lane;  // Q row in the tile == TMEM lane
+        // ============ softmax + epilogue (warps 1+NQ .. : 4 per q-tile) ============
+        const int grp = (warp - 1 - NQ) >> 2;  // q-tile of the unit this warp group handles
+        const int quad = warp & 3;        // TMEM lane quadrant this warp may access
+        const int r = quad * 32 + lane;   // Q row in the tile == TMEM lane
         const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-        const uint32_t s_addr = tmem + lane_addr + kScol;
-        const uint32_t p_addr = tmem + lane_addr + kPcol;
-        const uint32_t o_addr = tmem + lane_addr + kOcol;
+        const uint32_t s_addr = tmem + lane_addr + grp * 64;
+        const uint32_t p_addr = tmem + lane_addr + NQ * 64 + grp * 64;
+        const uint32_t o_addr = tmem + lane_addr + NQ * 128 + grp * 128;
+        uint64_t* const sf = s_full(grp);
+        uint64_t* const se = s_empty(grp);
+        uint64_t* const of = o_full(grp);
+        uint64_t* const oe = o_empty(grp);
+        const int gtid = (int)threadIdx.x - 32 * (1 + NQ) - 128 * grp;  // 0..127 within the group
         const float sl2 = p.scale_log2;
         uint32_t s_cnt = 0, unit_it = 0;
         int tbase = 0;  // CTA-local index of the piece's first tile (trace only)
@@ -667,15 +718,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         Piece pc;
         while (rec_next(p, sc, pc)) {
             const Unit& u = pc.u;
+            if (grp >= u.nq) continue;  // this unit has no q-tile for this group
             const int G = p.G;
-            const int rr = u.mt * kBM + r;
+            const int rr = (u.mt + grp) * kBM + r;
             const bool row_ok = rr < u.K * G;
             const int node = rr / G;
             const int hh = rr - node * G;
             // ancestor-or-self bitmask of this row's node (R15); parents staged in smem
-            int* tp_s = reinterpret_cast<int*>(smem + S::OFF_TP) + (unit_it & 1) * AS_MAX_TREE;
-            for (int j = (int)threadIdx.x - 64; j < u.K; j += 128) tp_s[j] = __ldg(p.tree_parent + u.off + j);
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            int* tp_s = reinterpret_cast<int*>(smem + S::OFF_TP) + (grp * 2 + (unit_it & 1)) * AS_MAX_TREE;
+            for (int j = gtid; j < u.K; j += 128) tp_s[j] = __ldg(p.tree_parent + u.off + j);
+            group_bar(grp);
             uint64_t anc0 = 0, anc1 = 0;
             if (row_ok) {
                 int v = node, steps = 0;
@@ -693,8 +745,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             float m_ref = -INFINITY, l_sum = 0.f;
             for (int t = pc.tb; t < pc.te; ++t, ++s_cnt) {
                 const uint32_t par = s_cnt & 1;
-                ptx::mbar_wait(s_full, par);
-                if (lane == 0 && quad == 0) AS_TRACE(5, tbase + t - pc.tb);
+                ptx::mbar_wait(sf, par);
+                if (lane == 0 && quad == 0 && grp == 0) AS_TRACE(5, tbase + t - pc.tb);
                 ptx::tc_fence_after();
                 uint32_t sr[kBN];
                 ptx::tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
@@ -702,11 +754,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 ptx::tmem_ld_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(s_empty);
+                if (lane == 0) ptx::mbar_arrive(se);
                 if (p.debug_mode >= 1) {  // timing experiment: no softmax math
-                    ptx::mbar_wait(p_empty + (s_cnt & 1), ((s_cnt >> 1) & 1) ^ 1);
+                    ptx::mbar_wait(p_empty(grp, s_cnt & 1), ((s_cnt >> 1) & 1) ^ 1);
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(p_full + (s_cnt & 1));
+                    if (lane == 0) ptx::mbar_arrive(p_full(grp, s_cnt & 1));
                     continue;
                 }
                 float* x = reinterpret_cast<float*>(sr);
@@ -722,23 +774,28 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                     for (int c = 0; c < kBN; ++c) x[c] = ((bits >> c) & 1ull) ? x[c] : -INFINITY;
                 }
                 // tree max of the raw scores (sm_scale > 0 commutes with max)
+                // 3-input max (FMNMX3): 32 instructions for the 64 scores instead of 63
                 float mx[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) mx[j] = fmaxf(fmaxf(x[j], x[j + 8]), fmaxf(x[j + 16], x[j + 24]));
+                for (int j = 0; j < 8; ++j) mx[j] = ptx::max3(x[j], x[j + 8], x[j + 16]);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) mx[j] = fmaxf(mx[j], fmaxf(fmaxf(x[j + 32], x[j + 40]), fmaxf(x[j + 48], x[j + 56])));
-                const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+                for (int j = 0; j < 8; ++j) mx[j] = ptx::max3(mx[j], x[j + 24], x[j + 32]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) mx[j] = ptx::max3(mx[j], x[j + 40], x[j + 48]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) mx[j] = fmaxf(mx[j], x[j + 56]);
+                const float tmax = ptx::max3(ptx::max3(mx[0], mx[1], mx[2]), ptx::max3(mx[3], mx[4], mx[5]),
+                                             fmaxf(mx[6], mx[7])) * sl2;
                 const float m_new = fmaxf(m_ref, tmax);
                 // P buffer s_cnt&1 is free once PV two tiles back completed (double buffer:
                 // the softmax of tile t+1 overlaps PV_t)
                 const uint32_t pb = s_cnt & 1;
-                ptx::mbar_wait(p_empty + pb, ((s_cnt >> 1) & 1) ^ 1);
+                ptx::mbar_wait(p_empty(grp, pb), ((s_cnt >> 1) & 1) ^ 1);
                 if (t > pc.tb) {
                     const bool need = m_new > m_ref + kRescaleThresh;
                     if (__any_sync(0xffffffffu, need)) {
                         // O must be stable: PV_{t-1} (other buffer, use (s_cnt-1)>>1) completed
-                        ptx::mbar_wait(p_empty + (pb ^ 1), ((s_cnt - 1) >> 1) & 1);
+                        ptx::mbar_wait(p_empty(grp, pb ^ 1), ((s_cnt - 1) >> 1) & 1);
                         ptx::tc_fence_after();
                         const float sc2 = need ? ptx::ex2(m_ref - m_new) : 1.f;
 #pragma unroll
@@ -776,11 +833,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(p_full + pb);
-                if (lane == 0 && quad == 0) AS_TRACE(6, tbase + t - pc.tb);
+                if (lane == 0) ptx::mbar_arrive(p_full(grp, pb));
+                if (lane == 0 && quad == 0 && grp == 0) AS_TRACE(6, tbase + t - pc.tb);
             }
             // ---- epilogue ----
-            ptx::mbar_wait(o_full, unit_it & 1);
+            ptx::mbar_wait(of, unit_it & 1);
             ptx::tc_fence_after();
             const bool full = (pc.tb == 0 && pc.te == u.nt);
             const float inv = full ? 1.f / l_sum : 1.f;  // partial piece: keep (O, m, l) unnormalised
@@ -821,18 +878,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(o_empty);
+            if (lane == 0) ptx::mbar_arrive(oe);
             if (!full) {
                 // stream-K fix-up: the CTA that completes the unit's last piece merges
                 // every piece's (O, m, l) (fp32, through L2) and writes the output.
                 __threadfence();
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+                group_bar(grp);
                 if (warp == 2 && lane == 0) {
                     const int n = pc.te - pc.tb;
                     const int old = atomicAdd(p.cnt + pc.w, n);
                     sk_last = (old + n == u.nt) ? 1 : 0;
                 }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+                group_bar(grp);
                 if (sk_last) {
                     __threadfence();
                     const long long T = sk_T;
@@ -896,7 +953,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem, kTmemCols);
+        ptx::tmem_dealloc(tmem, TcCfg<NQ>::TMEM);
     }
     if (p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceCtas) {
         // per-CTA timeline (debug): start/end globaltimer, after the CTA-0 tile trace
@@ -912,61 +969,55 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
-int tc_smem_bytes(int head_dim) {
-    return head_dim == 64 ? TcSmem<64>::ALLOC : TcSmem<128>::ALLOC;
-}
-int tc_ctas_per_sm() { return kCtasPerSm; }
-int launch_attn_tc_chunk(const CUtensorMap* maps, const TcParams& p, int head_dim, int grid_full, int smem,
-                         cudaStream_t stream);
-
-int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, int n_sms, cudaStream_t stream) {
-    const int smem = tc_smem_bytes(head_dim);
-    const int grid_full = n_sms * kCtasPerSm;
-    // Every CTA replays a list of at most kMaxRec pieces built in its prologue:
-    // batches with more units than kMaxRec * grid are verified in request chunks.
-    const int units_per_req = p0.n_kv * p0.mt_max;
-    const int chunk = units_per_req > 0 ? max(1, kMaxRec * grid_full / units_per_req) : p0.n_req;
-    for (int r0 = 0; r0 < p0.n_req; r0 += chunk) {
-        TcParams p = p0;
-        p.n_req = min(chunk, p0.n_req - r0);
-        p.page_table = p0.page_table + (size_t)r0 * p0.max_pages;
-        p.kv_len = p0.kv_len + r0;
-        p.tree_offsets = p0.tree_offsets + r0;
-        p.n_units = p.mt_max * p.n_req * p.n_kv;
-        if (launch_attn_tc_chunk(maps, p, head_dim, grid_full, smem, stream) != 0) return -1;
-    }
-    return 0;
-}
-
-int launch_attn_tc_chunk(const CUtensorMap* maps, const TcParams& p, int head_dim, int grid_full, int smem,
-                         cudaStream_t stream) {
-    int grid = grid_full;
-    if (!p.stream_k && p.n_units < grid) grid = p.n_units;
-    if (grid <= 0) return 0;
+template <int D, int NQ>
+static int launch_shape(const CUtensorMap* maps, const TcParams& p, int grid, cudaStream_t stream) {
+    const int smem = TcSmem<D, NQ>::ALLOC;
+    if (cudaFuncSetAttribute(tree_attn_tc_kernel<D, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+        return -1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(TcCfg<NQ>::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     cfg.attrs = attr;
     cfg.numAttrs = fill_launch_attrs(attr);
-    if (head_dim == 128) {
-        if (cudaFuncSetAttribute(tree_attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
-            return -1;
-        if (cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<128>, maps[0], maps[1], maps[2], maps[3], maps[4], p) !=
-            cudaSuccess)
-            return -1;
-    } else {
-        if (cudaFuncSetAttribute(tree_attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
-            return -1;
-        if (cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<64>, maps[0], maps[1], maps[2], maps[3], maps[4], p) !=
-            cudaSuccess)
-            return -1;
-    }
+    if (cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<D, NQ>, maps[0], maps[1], maps[2], maps[3], maps[4], p) !=
+        cudaSuccess)
+        return -1;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int tc_ctas_per_sm() { return kCtasPerSm; }
+
+// p0.nq selects the CTA shape (1: one q-tile per CTA, 2 CTAs/SM; 2: paired
+// q-tiles sharing K/V, 1 CTA/SM).  Every CTA replays a list of at most kMaxRec
+// pieces built in its prologue: batches with more units than kMaxRec * grid are
+// verified in request chunks.
+int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, int n_sms, cudaStream_t stream) {
+    const int nq = p0.nq == 2 ? 2 : 1;
+    const int grid_full = n_sms * (nq == 2 ? TcCfg<2>::CTAS : TcCfg<1>::CTAS);
+    const int units_per_req = p0.n_kv * ((p0.mt_max + nq - 1) / nq);
+    const int chunk = units_per_req > 0 ? max(1, kMaxRec * grid_full / units_per_req) : p0.n_req;
+    for (int r0 = 0; r0 < p0.n_req; r0 += chunk) {
+        TcParams p = p0;
+        p.nq = nq;
+        if (nq == 2) p.stream_k = 0;  // paired q-tiles: static schedule
+        p.n_req = min(chunk, p0.n_req - r0);
+        p.page_table = p0.page_table + (size_t)r0 * p0.max_pages;
+        p.kv_len = p0.kv_len + r0;
+        p.tree_offsets = p0.tree_offsets + r0;
+        p.n_units = units_per_req * p.n_req;
+        int grid = grid_full;
+        if (!p.stream_k && p.n_units < grid) grid = p.n_units;
+        if (grid <= 0) continue;
+        int rc;
+        if (head_dim == 128) rc = nq == 2 ? launch_shape<128, 2>(maps, p, grid, stream) : launch_shape<128, 1>(maps, p, grid, stream);
+        else rc = nq == 2 ? launch_shape<64, 2>(maps, p, grid, stream) : launch_shape<64, 1>(maps, p, grid, stream);
+        if (rc != 0) return -1;
+    }
+    return 0;
 }
 
 }  // namespace as

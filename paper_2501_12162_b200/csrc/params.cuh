@@ -62,6 +62,7 @@ struct TcParams {
     float* lse;
     void* ws;
     int n_units;
+    int nq;               // q-tiles per unit / CTA shape (1 or 2, chosen by the host)
     int mt_max;           // q-tiles per (request, kv head) upper bound (unit id stride)
     int stream_k;         // 1: stream-K tile ranges (needs cnt/partial), 0: static whole units
     int* cnt;             // [n_units] tiles completed per split unit (zeroed, self-resetting)

@@ -407,7 +407,12 @@ def test_attn_fp32(ada, ci):
 
 
 @pytest.mark.parametrize("ci", range(1, len(ATTN_CASES)))
-def test_attn_bf16(ada, ci):
+@pytest.mark.parametrize("nq", ["auto", "1", "2"])
+def test_attn_bf16(ada, ci, nq, monkeypatch):
+    """Both CTA shapes: one q-tile per CTA (NQ=1) and paired q-tiles sharing
+    every K/V tile (NQ=2; odd q-tile counts leave the second group idle)."""
+    if nq != "auto":
+        monkeypatch.setenv("AS_ATTN_NQ", nq)
     w = _attn_case(ATTN_CASES[ci], True, 400 + ci)
     scale = np.float32(1.0 / np.sqrt(w["q"].shape[2]))
     ref, ref_lse = oracle_attn(w, scale)
@@ -422,7 +427,9 @@ def test_attn_bf16(ada, ci):
     assert np.abs(lse.cpu().numpy() - ref_lse).max() <= BF16_TOL
 
 
-def test_attn_bf16_request_chunks(ada):
+@pytest.mark.parametrize("nq", ["1", "2"])
+def test_attn_bf16_request_chunks(ada, nq, monkeypatch):
+    monkeypatch.setenv("AS_ATTN_NQ", nq)
     """More units than the kernel's per-CTA piece lists hold (n_kv * q-tiles *
     n_req > 64 * 2 * SMs): the library verifies the batch in request chunks;
     every request, including those at chunk edges, must match the oracle."""
