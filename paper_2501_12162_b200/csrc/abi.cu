@@ -178,6 +178,9 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     if (!q || !k_tree || !v_tree || !out || !kv_len || !tree_offsets || !tree_parent) return AS_ERR_INVALID_ARG;
     if (num_pages > 0 && max_pages_per_req > 0 && (!k_cache || !v_cache || !page_table)) return AS_ERR_INVALID_ARG;
     const int G = n_q_heads / n_kv_heads;
+    if (!al16(q) || !al16(k_tree) || !al16(v_tree) || !al16(out) || (k_cache && !al16(k_cache)) ||
+        (v_cache && !al16(v_cache)))
+        return AS_ERR_INVALID_ARG;  // 16-byte vector / TMA access (both paths)
     if (dtype == AS_F32) {
         SimtParams p;
         p.n_req = n_req; p.n_tree_rows = n_tree_rows; p.n_q = n_q_heads; p.n_kv = n_kv_heads; p.G = G;
@@ -190,9 +193,6 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     }
     // bf16 tcgen05 path
     if ((G & (G - 1)) != 0 || G > 16) return AS_ERR_UNSUPPORTED;
-    if (!al16(q) || !al16(k_tree) || !al16(v_tree) || !al16(out) || (k_cache && !al16(k_cache)) ||
-        (v_cache && !al16(v_cache)))
-        return AS_ERR_INVALID_ARG;
     const uint64_t D = (uint64_t)head_dim;
     CUtensorMap maps[5];
     const uint64_t NCH = D / 64;
