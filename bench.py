@@ -529,8 +529,10 @@ def main():
     if not args.no_e2e and not args.profile:
         e2e = measure_e2e(W, step, args.steps, world)
     spec = None
+    logits_mode = None
     if rank == 0 and not args.profile and not args.no_spec:
         spec = measure_speculation(W, args.steps)
+        logits_mode = measure_accept_logits(W, args.steps)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         threads = os.cpu_count() or 1
@@ -555,7 +557,7 @@ def main():
                        else "1 GPU", "l2": ("inputs larger than L2: KV %.0f MiB/GPU" % (W["kv_bytes"] / 2**20))
                        if W["n_pools"] == 1 else f"{W['n_pools']} rotating KV pools (> 3x L2)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-            "clocks": clocks, "graph": use_graph, "speculation": spec, **({"ablation_skip": os.environ["AS_BENCH_SKIP"]}
+            "clocks": clocks, "graph": use_graph, "speculation": spec, "accept_logits": logits_mode, **({"ablation_skip": os.environ["AS_BENCH_SKIP"]}
                                                        if os.environ.get("AS_BENCH_SKIP") else {}),
             "breakdown_ms": {"select": round(t_sel, 4), "attention": round(t_attn_b, 4), "accept_commit": round(t_acc, 4),
                              "note": "separate instrumented replay (events around every call)"},
@@ -615,6 +617,50 @@ def measure_speculation(W, steps):
     return {"step": "beam layer (as_beam_step, layer 2)", "n_req": n, "width": w, "vocab": V,
             "draft_probs": "softmax(N(0, sigma^2)), sigma ~ U(1,4) per request, fp32",
             "layer_us": round(us, 2), "algorithmic_bytes": nbytes, "hbm_gbs": round(gbs, 1),
+            "hbm_frac": round(gbs / peak, 4), "launches": 2}
+
+
+def measure_accept_logits(W, steps):
+    """S8 logits mode: greedy targets from per-node target logits
+    [N_tree, |V| = 128 256] bf16 -- an HBM-bound argmax scan (lowest index on
+    ties) -- then the walk and commit, through as_accept_tokens.  Algorithmic
+    bytes = the logits read once."""
+    ada = W["ada"]
+    if W["dtype"] != torch.bfloat16:
+        return None
+    R, V = W["R"], synth.LLAMA3_VOCAB
+    gen = torch.Generator(device=W["device"]).manual_seed(synth.SEED_BASE + 7)
+    logits = torch.randn((R, V), generator=gen, device=W["device"], dtype=torch.float32).to(torch.bfloat16)
+    kc, vc = W["pools"][W["pool_idx"]]
+
+    def call():
+        ada.accept_tokens(ada.AS_ACCEPT_FUSED, W["sel"]["tree_offsets"], W["sel"]["tree_parent"],
+                          W["sel"]["tree_token"], target_logits=logits, max_path=W["max_path"], k_tree=W["k_tree"],
+                          v_tree=W["v_tree"], k_cache=kc, v_cache=vc, page_table=W["page_table"],
+                          kv_len=W["kv_len"], kv_len_out=W["kv_len_out"], accept_len=W["acc"]["accept_len"],
+                          accept_path=W["acc"]["accept_path"], bonus_token=W["acc"]["bonus_token"],
+                          n_tree_rows=R, workspace=W["ws_accept"])
+    for _ in range(3):
+        call()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(steps):
+            call()
+    g.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    us = s.elapsed_time(e) * 1e3 / steps
+    nbytes = int(W["tree_tokens_total"]) * V * 2
+    peak = float(_peaks()[0]["hbm_gbs"])
+    gbs = nbytes / (us * 1e-6) / 1e9
+    del logits
+    return {"step": "accept, logits mode (argmax scan + walk + commit)", "rows": int(W["tree_tokens_total"]),
+            "vocab": V, "us": round(us, 2), "algorithmic_bytes": nbytes, "hbm_gbs": round(gbs, 1),
             "hbm_frac": round(gbs / peak, 4), "launches": 2}
 
 

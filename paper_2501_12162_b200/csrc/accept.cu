@@ -49,8 +49,26 @@ __global__ void __launch_bounds__(512) argmax_rows_kernel(const T* __restrict__ 
     if (aligned) {
         const int nvec = vocab / kVec;
         const uint4* rv = reinterpret_cast<const uint4*>(r);
-        for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-            uint4 raw = __ldcs(rv + v);  // streamed once: evict-first
+        constexpr int U = 4;  // 16-byte loads in flight per thread
+        int v0 = threadIdx.x;
+        for (; v0 + (U - 1) * (int)blockDim.x < nvec; v0 += U * blockDim.x) {
+            uint4 raw[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) raw[u] = __ldcs(rv + v0 + u * blockDim.x);  // streamed once: evict-first
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const T* e = reinterpret_cast<const T*>(&raw[u]);
+                const int vb = (v0 + u * blockDim.x) * kVec;
+#pragma unroll
+                for (int q = 0; q < kVec; ++q) {
+                    float x = to_f<T>(e[q]);
+                    nan |= (x != x);
+                    better(bv, bi, x, vb + q);
+                }
+            }
+        }
+        for (int v = v0; v < nvec; v += blockDim.x) {
+            uint4 raw = __ldcs(rv + v);
             const T* e = reinterpret_cast<const T*>(&raw);
 #pragma unroll
             for (int q = 0; q < kVec; ++q) {
