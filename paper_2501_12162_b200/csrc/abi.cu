@@ -372,7 +372,7 @@ as_status as_selftest_umma(const void* a, const void* b, float* d, int32_t n, in
         uint32_t box[2] = {64, 128};
         if (!make_map(&ma, a, 2, dims, str, box)) return AS_ERR_CUDA;
     }
-    if (!b_mn_major) {
+    if (!(b_mn_major & 1)) {  // bit 0: B MN-major; bit 1: A staged in TMEM
         uint64_t dims[2] = {(uint64_t)k, (uint64_t)n};
         uint64_t str[1] = {(uint64_t)k * 2};
         uint32_t box[2] = {64, (uint32_t)n};
