@@ -7,14 +7,11 @@
 // keeps the w largest by (f-hat desc, parent asc, token asc) (R8).  The w x |V|
 // scan is HBM-bound (|V| = 128 256: 513 KB of fp32 per row):
 //
-//   beam_scan_kernel   one CTA per row: 16-byte streaming loads; each warp keeps
-//                      a shared-memory buffer of the 64-bit keys (f-hat bits
-//                      << 32 | ~(k*|V| + t)) -- the key order IS the tie order
-//                      and keys are unique -- that beat its threshold (the w-th
-//                      best so far), compacted to its top w when full; a
-//                      max-of-float4 prefilter on the raw probability keeps the
-//                      common path at a few instructions per element; the 8
-//                      warps' top-w merged into the row's slot.
+//   beam_scan_kernel   one CTA per row: 16-byte streaming loads, a warp-wide
+//                      top-w list of the 64-bit keys (f-hat bits << 32 |
+//                      ~(k*|V| + t)) -- the key order IS the tie order and keys
+//                      are unique -- behind a cheap max-of-float4 prefilter,
+//                      the 8 warp lists merged into the row's slot.
 //   beam_merge_kernel  one warp per request: top-w of its rows' lists; writes
 //                      the new layer's nodes into the candidate forest.
 #include "params.cuh"
@@ -98,33 +95,11 @@ __device__ __forceinline__ int first_cta(const BeamParams& p, long long row) {
 // warp top-w list behind a max-of-float4 prefilter, and merge the 8 lists into
 // the row's slot.  (Measured against a persistent TMA-ring variant with
 // CTA-shared filters: this simple form streams faster -- DESIGN.md §NEXT-1.)
-constexpr int kCandCap = 512;  // per-warp candidate buffer (keys above the warp's threshold)
-
-// The warp's buffered candidates cbuf[0..n) -> their top-w in cbuf[0..min(n,w))
-// (warp-distributed list insertion); returns the new count and sets thr to
-// the w-th key (0 while fewer than w).
-__device__ __forceinline__ int compact_cands(uint64_t* cbuf, int n, int w, uint64_t& thr) {
-    WarpList M;
-    wl_init(M);
-    const int lane = lane_id();
-    for (int x0 = 0; x0 < n; x0 += 32) {
-        const uint64_t k = x0 + lane < n ? cbuf[x0 + lane] : 0ull;
-        unsigned bb = __ballot_sync(0xffffffffu, k > M.thr);
-        while (bb) {
-            const int src = __ffs(bb) - 1;
-            bb &= bb - 1;
-            wl_insert(M, __shfl_sync(0xffffffffu, k, src), w);
-        }
-    }
-    __syncwarp();
-    if (lane < w) cbuf[lane] = M.v;
-    __syncwarp();
-    thr = M.thr;
-    return min(n, w);
-}
-
 __global__ void __launch_bounds__(256) beam_scan_kernel(BeamParams p) {
-    __shared__ uint64_t cbuf_all[8][kCandCap];
+    __shared__ uint64_t wls[8][kBeamW];
+    __shared__ unsigned long long s_bound;  // max over the 8 warps of their w-th key
+    if (threadIdx.x == 0) s_bound = 0ull;
+    __syncthreads();
     pdl_launch_dependents();
     pdl_wait();
     const long long row = blockIdx.x;
@@ -133,33 +108,24 @@ __global__ void __launch_bounds__(256) beam_scan_kernel(BeamParams p) {
     const float* r = p.probs + (size_t)row * p.vocab;
     const uint32_t ibase = (uint32_t)kpar * (uint32_t)p.vocab;
     const int w = p.w_out, warp = warp_id(), lane = lane_id();
-    uint64_t* cbuf = cbuf_all[warp];
-    int nc = 0;          // buffered candidates (warp-uniform)
-    uint64_t thr = 0ull;  // keys <= thr cannot be in the row's top w (warp-uniform)
-    // prefilter on the raw probability: fl32(fpar * e) > thr needs e >= f(thr) / fpar up to
-    // 2^-24 rounding; the 2^-18 margin keeps it conservative (exact keys decide)
-    const float inv_fpar = fpar > 0.f ? 1.f / fpar : 0.f;
-    float e_thr = 0.f;
-    auto set_thr = [&](uint64_t t) {
-        thr = t;
-        const float tf = __uint_as_float((uint32_t)(t >> 32));
-        e_thr = fpar > 0.f ? tf * inv_fpar * (1.f - 3.814697265625e-06f) : 0.f;
-    };
-    // push the elements of this lane that beat thr (warp-aggregated slots)
-    auto push = [&](bool ok, float f, uint32_t idx) {
-        const uint64_t key = beam_key(f, idx);
-        const bool c = ok && key > thr;
-        const unsigned bb = __ballot_sync(0xffffffffu, c);
-        if (c) cbuf[nc + __popc(bb & ((1u << lane) - 1u))] = key;
-        nc += __popc(bb);
-    };
+    WarpList L;
+    wl_init(L);
     float emin = 0.f;
     const int part = (((p.vocab + 7) / 8) + 3) & ~3;
     const int w0 = min(p.vocab, warp * part), w1 = min(p.vocab, w0 + part);
     const bool vec = ((reinterpret_cast<uintptr_t>(r) & 15u) == 0) && ((p.vocab & 3) == 0);
     if (vec) {
         constexpr int U = 8;
+        uint64_t published = 0ull;
         for (int base = w0; base < w1; base += 32 * 4 * U) {
+            // a key below any warp's w-th key is out of the row's top w: share the best bound
+            if (L.thr > published) {
+                if (lane == 0) atomicMax(&s_bound, (unsigned long long)L.thr);
+                published = L.thr;
+            }
+            uint64_t sb = 0ull;
+            if (lane == 0) sb = *reinterpret_cast<volatile unsigned long long*>(&s_bound);
+            wl_raise(L, __shfl_sync(0xffffffffu, sb, 0));
             float4 x[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -170,18 +136,15 @@ __global__ void __launch_bounds__(256) beam_scan_kernel(BeamParams p) {
             for (int u = 0; u < U; ++u) {
                 const int t = base + (u * 32 + lane) * 4;
                 const bool ok = t < w1;
-                const float mx = fmaxf(fmaxf(x[u].x, x[u].y), fmaxf(x[u].z, x[u].w));
+                const float f0 = __fmul_rn(fpar, x[u].x), f1 = __fmul_rn(fpar, x[u].y);
+                const float f2 = __fmul_rn(fpar, x[u].z), f3 = __fmul_rn(fpar, x[u].w);
                 emin = fminf(emin, fminf(fminf(x[u].x, x[u].y), fminf(x[u].z, x[u].w)));
-                if (__any_sync(0xffffffffu, ok && mx >= e_thr)) {  // rare once thr is established
-                    if (nc + 128 > kCandCap) {
-                        uint64_t t2;
-                        nc = compact_cands(cbuf, nc, w, t2);
-                        set_thr(t2);
-                    }
-                    push(ok, __fmul_rn(fpar, x[u].x), ibase + t);
-                    push(ok, __fmul_rn(fpar, x[u].y), ibase + t + 1);
-                    push(ok, __fmul_rn(fpar, x[u].z), ibase + t + 2);
-                    push(ok, __fmul_rn(fpar, x[u].w), ibase + t + 3);
+                const bool any = ok && fmaxf(fmaxf(f0, f1), fmaxf(f2, f3)) >= L.thr_f;
+                if (__any_sync(0xffffffffu, any)) {
+                    wl_offer(L, ok, f0, ibase + t, w);
+                    wl_offer(L, ok, f1, ibase + t + 1, w);
+                    wl_offer(L, ok, f2, ibase + t + 2, w);
+                    wl_offer(L, ok, f3, ibase + t + 3, w);
                 }
             }
         }
@@ -191,28 +154,17 @@ __global__ void __launch_bounds__(256) beam_scan_kernel(BeamParams p) {
             const bool ok = t < w1;
             const float ev = ok ? r[t] : 0.f;
             emin = fminf(emin, ev);
-            if (nc + 32 > kCandCap) {
-                uint64_t t2;
-                nc = compact_cands(cbuf, nc, w, t2);
-                set_thr(t2);
-            }
-            push(ok, __fmul_rn(fpar, ev), ibase + (uint32_t)t);
+            wl_offer(L, ok, __fmul_rn(fpar, ev), ibase + (uint32_t)t, w);
         }
     }
     if (emin < 0.f) set_dev_error(p.ws, AS_DEV_BAD_PROB, i);
-    __syncwarp();
-    {
-        uint64_t t2;
-        nc = compact_cands(cbuf, nc, w, t2);
-        if (lane < kBeamW && lane >= nc) cbuf[lane] = 0ull;  // fewer than w: empty keys
-    }
+    if (lane < kBeamW) wls[warp][lane] = L.v;
     __syncthreads();
     if (warp == 0) {
         WarpList M;
         wl_init(M);
         for (int x = lane; x < 8 * kBeamW; x += 32) {
-            const int wv = x / kBeamW, j = x % kBeamW;
-            const uint64_t k = j < w ? cbuf_all[wv][j] : 0ull;
+            const uint64_t k = wls[x / kBeamW][x % kBeamW];
             unsigned bb = __ballot_sync(0xffffffffu, k > M.thr);
             while (bb) {
                 const int src = __ffs(bb) - 1;
