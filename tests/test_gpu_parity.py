@@ -503,3 +503,43 @@ def test_attn_bf16_full_size_sampled(ada, cfg):
     rows, ref, _ = oracle_attn(w, np.float32(W["sm_scale"]), requests=reqs)
     got = out[torch.from_numpy(rows).cuda()].float().cpu().numpy()
     assert np.abs(got - ref).max() <= BF16_TOL
+
+
+# --------------------------------------------------------------------------- NEXT-2: iteration graph
+def test_iteration_graph_replay_equals_eager(ada):
+    """select -> attention -> accept captured once and replayed == the same
+    library calls made eagerly (bit-exact: same kernels, same inputs)."""
+    import bench
+    from paper_2501_12162_b200.iteration import IterationGraph, IterationShape
+    W = bench.make_workload("c2", "cuda", seed_salt=11)
+    c = W["c"]
+    N = int(W["cand_offsets"][-1])
+    kc, vc = W["pools"][0]
+    shape = IterationShape(W["n"], N, c["d"], c["n_max"], W["R"], W["n_q"], W["n_kv"], W["D"], kc.shape[0],
+                           W["page_size"], W["page_table"].shape[1], W["max_path"])
+    it = IterationGraph(shape, W["sm_scale"])
+    for k, src in (("cand_offsets", W["cand_offsets"]), ("cand_parent", W["cand_parent"]),
+                   ("cand_prob", W["cand_prob"]), ("cand_token", W["cand_token"]),
+                   ("slo_deficit", W["slo_deficit"]), ("q", W["q"]), ("k_tree", W["k_tree"]),
+                   ("v_tree", W["v_tree"]), ("target_tokens", W["target_tokens"]), ("k_cache", kc),
+                   ("v_cache", vc), ("page_table", W["page_table"]), ("kv_len", W["kv_len"])):
+        it.inputs[k].copy_(src)
+    it.capture()
+    it.inputs["k_cache"].copy_(kc)  # the capture's warm-up committed into the cache copy
+    it.inputs["v_cache"].copy_(vc)
+    out = it.replay()
+    torch.cuda.synchronize()
+    # eager reference through the bench's wrappers (same library calls)
+    W["pool_idx"] = 0
+    bench.run_select(W)
+    ref = bench.run_attention(W)
+    bench.run_accept(W)
+    torch.cuda.synchronize()
+    for k in ("tree_offsets", "tree_parent", "tree_src", "tree_token", "slo_count"):
+        n = out[k].numel()
+        assert torch.equal(out[k], W["sel"][k][:n]), k
+    used = int(out["tree_offsets"][-1])
+    assert torch.equal(out["out"][:used], ref[:used])
+    for k in ("accept_len", "accept_path", "bonus_token"):
+        assert torch.equal(out[k], W["acc"][k]), k
+    assert torch.equal(out["kv_len_out"], W["kv_len_out"])
