@@ -86,9 +86,6 @@ struct BeamParams {
     void* ws;
 };
 
-__device__ __forceinline__ int first_cta(const BeamParams& p, long long row) {
-    return (int)((row * p.vocab) / p.seg);
-}
 
 // Scan: one CTA per row (request, kept parent); 8 warps each stream a
 // contiguous 1/8 of the row with 8 float4 loads in flight per lane, keep a
@@ -102,7 +99,9 @@ __global__ void __launch_bounds__(256) beam_scan_kernel(BeamParams p) {
     __syncthreads();
     pdl_launch_dependents();
     pdl_wait();
-    const long long row = blockIdx.x;
+    const long long row = blockIdx.x / p.pieces;   // small batches: each row split into `pieces` CTAs
+    const int pc = (int)(blockIdx.x - row * p.pieces);
+    const int a = (int)min((long long)p.vocab, (long long)pc * p.seg), e = (int)min((long long)p.vocab, a + p.seg);
     const int i = (int)(row / p.w_in), kpar = (int)(row - (long long)i * p.w_in);
     const float fpar = p.cand_prob[(size_t)i * p.stride + p.base_prev + kpar];
     const float* r = p.probs + (size_t)row * p.vocab;
@@ -111,8 +110,8 @@ __global__ void __launch_bounds__(256) beam_scan_kernel(BeamParams p) {
     WarpList L;
     wl_init(L);
     float emin = 0.f;
-    const int part = (((p.vocab + 7) / 8) + 3) & ~3;
-    const int w0 = min(p.vocab, warp * part), w1 = min(p.vocab, w0 + part);
+    const int part = ((((e - a) + 7) / 8) + 3) & ~3;
+    const int w0 = min(e, a + warp * part), w1 = min(e, w0 + part);
     const bool vec = ((reinterpret_cast<uintptr_t>(r) & 15u) == 0) && ((p.vocab & 3) == 0);
     if (vec) {
         constexpr int U = 8;
@@ -172,7 +171,7 @@ __global__ void __launch_bounds__(256) beam_scan_kernel(BeamParams p) {
                 wl_insert(M, __shfl_sync(0xffffffffu, k, src), w);
             }
         }
-        if (lane < kBeamW) p.lists[(size_t)row * p.pieces * kBeamW + lane] = M.v;
+        if (lane < kBeamW) p.lists[((size_t)row * p.pieces + pc) * kBeamW + lane] = M.v;
     }
 }
 
@@ -188,7 +187,7 @@ __global__ void __launch_bounds__(128) beam_merge_kernel(BeamParams p) {
     constexpr int PF = 8;  // keys prefetched per lane (loads in flight before the serial inserts)
     for (int k = 0; k < p.w_in; ++k) {
         const long long row = (long long)i * p.w_in + k;
-        const int np = (int)((row * p.vocab + p.vocab - 1) / p.seg) - first_cta(p, row) + 1;
+        const int np = p.pieces;
         const uint64_t* K = p.lists + (size_t)row * p.pieces * kBeamW;
         const int nk = np * kBeamW;
         for (int x00 = 0; x00 < nk; x00 += 32 * PF) {
@@ -222,11 +221,21 @@ __global__ void __launch_bounds__(128) beam_merge_kernel(BeamParams p) {
     }
 }
 
+// One CTA per row; batches too small to fill the GPU (fewer rows than ~half the
+// resident CTA slots, 148 SMs x 4) split each row into `pieces` (>= 8192
+// elements each, 16-byte aligned), merged by the merge kernel.
 static void beam_geometry(int n_req, int w_in, int vocab, long long* total, long long* seg, int* grid, int* pieces) {
-    *total = (long long)n_req * w_in * vocab;
-    *seg = vocab;  // one row per CTA
-    *grid = n_req * w_in;
-    *pieces = 1;
+    const long long rows = (long long)n_req * w_in;
+    *total = rows * vocab;
+    int k = 1;
+    if (rows > 0 && rows < 296) k = (int)(592 / rows);
+    k = max(1, min(k, max(1, vocab / 8192)));
+    long long sg = (vocab + k - 1) / k;
+    sg = (sg + 3) / 4 * 4;
+    k = (int)((vocab + sg - 1) / sg);
+    *seg = sg;
+    *pieces = k;
+    *grid = (int)(rows * k);
 }
 
 size_t beam_ws_bytes(int n_req, int width, int vocab) {
