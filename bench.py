@@ -426,7 +426,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         from paper_2501_12162_b200.dist import ShardedAccept
         dist_ctx = ShardedAccept(rank, world)
-    W = make_workload(args.config, "cuda", rank=rank, world=world)
+    emu = int(os.environ.get("AS_BENCH_EMULATE_WORLD", "0"))  # analysis only: one rank's shard of an N-GPU run
+    W = make_workload(args.config, "cuda", rank=rank, world=emu if (emu > 1 and world == 1) else world)
     step = Step(W, dist_ctx)
     use_graph = not args.no_graph
     for _ in range(2):  # eager warm-up (attribute setup, NCCL communicator)
@@ -557,7 +558,8 @@ def main():
                        else "1 GPU", "l2": ("inputs larger than L2: KV %.0f MiB/GPU" % (W["kv_bytes"] / 2**20))
                        if W["n_pools"] == 1 else f"{W['n_pools']} rotating KV pools (> 3x L2)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-            "clocks": clocks, "graph": use_graph, "speculation": spec, "accept_logits": logits_mode, **({"ablation_skip": os.environ["AS_BENCH_SKIP"]}
+            "clocks": clocks, "graph": use_graph, "speculation": spec, "accept_logits": logits_mode,
+            **({"emulated_shard_of_world": emu} if (emu > 1 and world == 1) else {}), **({"ablation_skip": os.environ["AS_BENCH_SKIP"]}
                                                        if os.environ.get("AS_BENCH_SKIP") else {}),
             "breakdown_ms": {"select": round(t_sel, 4), "attention": round(t_attn_b, 4), "accept_commit": round(t_acc, 4),
                              "note": "separate instrumented replay (events around every call)"},

@@ -156,7 +156,7 @@ size_t as_attn_workspace_size(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     // for every GQA ratio) + 2 partial-state slots per SM
     const size_t units = (size_t)n_q_heads * (size_t)n_req;
     const size_t slot = ((size_t)128 * head_dim + 256) * 4;
-    return kWsHeaderBytes + kAttnTraceBytes + align_up(units * 4, 256) +
+    return kWsHeaderBytes + kAttnTraceBytes + align_up(2 * units * 4, 256) +
            2 * (size_t)sm_count() * (size_t)tc_ctas_per_sm() * slot;
 }
 
@@ -253,13 +253,14 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     {
         const int nsm = sm_count();
         const size_t slot = ((size_t)128 * head_dim + 256) * 4;
-        const size_t cnt_bytes = align_up((size_t)p.n_units * 4, 256);
+        const size_t cnt_bytes = align_up((size_t)p.n_units * 8, 256);  // tile counters + merge counters
         const size_t need = kWsHeaderBytes + kAttnTraceBytes + cnt_bytes + 2 * (size_t)nsm * tc_ctas_per_sm() * slot;
         unsigned char* base = reinterpret_cast<unsigned char*>(workspace) + kWsHeaderBytes + kAttnTraceBytes;
         const char* skenv = getenv("AS_ATTN_STREAMK");  // A/B switch (debug)
         // A/B: AS_ATTN_STREAMK=0 static only, =2 force stream-K
         p.stream_k = (workspace_bytes >= need && !(skenv && atoi(skenv) == 0)) ? ((skenv && atoi(skenv) == 2) ? 2 : 1) : 0;
         p.cnt = reinterpret_cast<int*>(base);
+        p.cnt2 = p.cnt + p.n_units;
         p.partial = reinterpret_cast<float*>(base + cnt_bytes);
         p.slot_floats = 128 * head_dim + 256;
     }

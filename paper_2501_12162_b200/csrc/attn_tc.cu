@@ -55,6 +55,7 @@ constexpr int kCtasPerSm = 2;     // max over the shapes (workspace sizing)
 constexpr int kPtChunk = 256;     // page-table entries staged per refill
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 constexpr int kMaxRec = 64;       // pieces per CTA precomputed in the prologue
+constexpr int kMaxSplit = 8;      // split-KV: pieces per unit when units are fewer than CTAs
 constexpr int kTraceCtas = 512;   // per-CTA timeline records after the CTA-0 tile trace (debug)
 
 template <int D, int NQ>
@@ -179,67 +180,76 @@ __device__ __forceinline__ bool rec_next(const TcParams& p, RecCursor& cur, Piec
     return true;
 }
 
-// Prologue-only walker of the stream-K tile range (builds the records).
-struct Sched {
-    int stream;
-    int i, j, t;         // cursor: request, unit within request (g*MT + mt), tile
-    long long rem, x;    // stream-K: tiles left for this CTA, global tile index of the cursor
-    long long k, ucum;   // static: next unit index, units before request i
-    Req r;               // geometry of request i
-};
-
-__device__ __forceinline__ bool sched_next(const TcParams& p, Sched& sc, Piece& pc) {
-    const int units_per_req = p.n_kv;  // times MT
-    if (!sc.stream) {
-        // advance the request cursor to the request holding unit k
-        while (sc.i < p.n_req && sc.k >= sc.ucum + (long long)units_per_req * sc.r.MT) {
-            sc.ucum += (long long)units_per_req * sc.r.MT;
-            if (++sc.i < p.n_req) load_req(p, sc.i, sc.r);
+// Split-KV merge of one row (DESIGN.md §5 "Schedule"): the unit's live pieces each left an
+// unnormalised fp32 (O, m, l) in their slot; this thread combines columns
+// [c_lo, c_hi) of row r (its share among the n_live pieces) into bf16 out_row,
+// out_row[c] = sum_s 2^(m_s - M) O_s[c] / sum_s 2^(m_s - M) l_s, M = max_s m_s.
+// Kept out of line so its registers do not count against the tile loop's.
+template <int D>
+__device__ __noinline__ void split_merge(const float* __restrict__ slot0, size_t slot_stride, int Sx, int nt, int r,
+                                         int my_rank, int n_live, __nv_bfloat16* out_row, float* lse_out) {
+    float mb[kMaxSplit], lb[kMaxSplit];
+    float M = -INFINITY;
+#pragma unroll
+    for (int s2 = 0; s2 < kMaxSplit; ++s2) {  // all (m, l) loads in flight at once
+        mb[s2] = -INFINITY;
+        lb[s2] = 0.f;
+        if (s2 < Sx && nt * (s2 + 1) / Sx > nt * s2 / Sx) {
+            mb[s2] = __ldcg(slot0 + s2 * slot_stride + 128 * D + r);
+            lb[s2] = __ldcg(slot0 + s2 * slot_stride + 128 * D + 128 + r);
         }
-        if (sc.i >= p.n_req) return false;
-        const int j = (int)(sc.k - sc.ucum);
-        make_unit(p, sc.r, sc.i, j, pc.u);
-        pc.w = (sc.i * p.n_kv + pc.u.g) * p.mt_max + pc.u.mt;
-        pc.tb = 0;
-        pc.te = pc.u.nt;
-        pc.x = -1;
-        sc.k += gridDim.x;
-        return true;
     }
-    while (sc.rem > 0 && sc.i < p.n_req) {
-        if (sc.j >= units_per_req * sc.r.MT) {  // next request (empty requests have no units)
-            if (++sc.i >= p.n_req) return false;
-            load_req(p, sc.i, sc.r);
-            sc.j = 0;
-            sc.t = 0;
-            continue;
-        }
-        make_unit(p, sc.r, sc.i, sc.j, pc.u);
-        pc.w = (sc.i * p.n_kv + pc.u.g) * p.mt_max + pc.u.mt;
-        pc.tb = sc.t;
-        const long long avail = pc.u.nt - sc.t;
-        pc.te = sc.t + (int)(avail < sc.rem ? avail : sc.rem);
-        pc.x = sc.x;
-        const int n = pc.te - pc.tb;
-        sc.rem -= n;
-        sc.x += n;
-        sc.t = pc.te;
-        if (sc.t >= pc.u.nt) {
-            sc.t = 0;
-            ++sc.j;
-        }
-        return true;
+#pragma unroll
+    for (int s2 = 0; s2 < kMaxSplit; ++s2) M = fmaxf(M, mb[s2]);
+    float Ltot = 0.f;
+#pragma unroll
+    for (int s2 = 0; s2 < kMaxSplit; ++s2) {
+        mb[s2] = mb[s2] == -INFINITY ? 0.f : ptx::ex2(mb[s2] - M);  // piece weight
+        Ltot += lb[s2] * mb[s2];
     }
-    return false;
-}
-
-__device__ __forceinline__ long long sk_start(long long T, int b, int G) { return T * (long long)b / G; }
-__device__ __forceinline__ int sk_owner(long long T, int G, long long x) {
-    int b = (int)((x * G) / (T > 0 ? T : 1));
-    if (b >= G) b = G - 1;
-    while (b + 1 < G && sk_start(T, b + 1, G) <= x) ++b;
-    while (b > 0 && sk_start(T, b, G) > x) --b;
-    return b;
+    const float invL = 1.f / Ltot;
+#pragma unroll
+    for (int s2 = 0; s2 < kMaxSplit; ++s2) mb[s2] *= invL;
+    if (out_row != nullptr) {
+        // this piece's columns: a multiple of 8 (16-byte bf16 stores)
+        const int c_lo = my_rank * (D / 8) / n_live * 8, c_hi = (my_rank + 1) * (D / 8) / n_live * 8;
+#pragma unroll 2
+        for (int c0 = c_lo; c0 < c_hi; c0 += 8) {
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+            float4 qa[kMaxSplit], qb[kMaxSplit];
+#pragma unroll
+            for (int s2 = 0; s2 < kMaxSplit; ++s2) {  // every piece's 8 columns in flight
+                qa[s2] = qb[s2] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (s2 < Sx && mb[s2] != 0.f) {
+                    const float4* src = reinterpret_cast<const float4*>(slot0 + s2 * slot_stride) + (c0 / 4) * 128 + r;
+                    qa[s2] = __ldcg(src);
+                    qb[s2] = __ldcg(src + 128);
+                }
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < kMaxSplit; ++s2) {
+                const float fb = mb[s2];
+                acc[0] = fmaf(qa[s2].x, fb, acc[0]);
+                acc[1] = fmaf(qa[s2].y, fb, acc[1]);
+                acc[2] = fmaf(qa[s2].z, fb, acc[2]);
+                acc[3] = fmaf(qa[s2].w, fb, acc[3]);
+                acc[4] = fmaf(qb[s2].x, fb, acc[4]);
+                acc[5] = fmaf(qb[s2].y, fb, acc[5]);
+                acc[6] = fmaf(qb[s2].z, fb, acc[6]);
+                acc[7] = fmaf(qb[s2].w, fb, acc[7]);
+            }
+            uint32_t pkk[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
+                pkk[j] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            *reinterpret_cast<uint4*>(out_row + c0) = make_uint4(pkk[0], pkk[1], pkk[2], pkk[3]);
+        }
+    }
+    if (lse_out != nullptr) *lse_out = (M + __log2f(Ltot)) * 0.6931471805599453f;
 }
 
 template <int D, int NQ>
@@ -310,12 +320,9 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     if (p.trace != nullptr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
     // ---------------- schedule plan (all threads; K/V rings used as scratch) ----------------
-    __shared__ long long sk_T, sk_x0, sk_rem;
-    __shared__ int sk_cur[3];
-    __shared__ int sk_stream;
+    __shared__ int sk_split;  // split-KV pieces per unit (0: whole units)
     __shared__ long long scan_tmp[33];
     __shared__ int red_tmp[3][16];  // per warp (<= 10 warps)
-    __shared__ int sk_last;
     RecCursor cur0;
     {
         const int n = p.n_req;
@@ -323,7 +330,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         long long* pre = reinterpret_cast<long long*>(smem + S::OFF_K);
         long long* preu = pre + S::PLAN_HALF;
         const bool can_plan = n <= S::PLAN_HALF;
-        const bool can_stream = NQ == 1 && p.stream_k && can_plan;  // paired q-tiles: static only
+        const bool can_split = p.stream_k && can_plan;
         int my_units = 0, my_maxnt = 0, my_minnt = 0x7fffffff;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             Req r;
@@ -401,71 +408,34 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         PieceRec* recs = reinterpret_cast<PieceRec*>(smem + S::OFF_REC);
         __shared__ int s_nrec;
         if (threadIdx.x == 0) {
-            // makespan model (tiles): static = ceil(U/G) whole units of <= maxnt tiles;
-            // stream-K = T/G plus ~30% for the split fix-ups (measured on c2).
-            const long long static_ms = (long long)((U + G - 1) / G) * maxnt;
-            // every CTA's tile range must fit kMaxRec pieces: <= ceil(T/G)/min_nt + 2 of them
-            const bool fits = minnt > 0 && ((T + G - 1) / G) / minnt + 2 <= kMaxRec;
-            const bool stream = can_stream && fits && T > 0 &&
-                                (p.stream_k == 2 || (T * 13 / 10) / G + 1 < static_ms);
-            sk_stream = stream ? 1 : 0;
-            sk_T = T;
-            sk_x0 = 0;
-            sk_rem = 0;
-            int i0 = 0, j0 = 0, t0 = 0;
-            if (stream) {
-                const long long x0 = sk_start(T, blockIdx.x, G), x1 = sk_start(T, blockIdx.x + 1, G);
-                sk_x0 = x0;
-                sk_rem = x1 - x0;
-                if (x1 > x0) {
-                    int lo_b = 0, hi_b = n - 1;  // last i with pre[i] <= x0
+            // Split-KV when units are at most half the CTAs: unit k's tiles are cut into
+            // S = min(kMaxSplit, G / U) contiguous pieces, piece s on CTA k*S + s (one
+            // piece per CTA); the CTA finishing a unit's last piece merges the fp32
+            // partials (O, m, l).  Otherwise whole units, unit k on CTA k mod G.
+            const int Sx = (can_split && U > 0) ? min(kMaxSplit, G / U) : 1;
+            sk_split = Sx >= 2 ? Sx : 0;
+            s_nrec = -1;
+            if (sk_split) {
+                s_nrec = 0;
+                const int k = (int)blockIdx.x / Sx, sidx = (int)blockIdx.x - k * Sx;
+                if (k < U) {
+                    int lo_b = 0, hi_b = n - 1;  // last i with preu[i] <= k
                     while (lo_b < hi_b) {
                         const int mid = (lo_b + hi_b + 1) >> 1;
-                        if (pre[mid] <= x0) lo_b = mid; else hi_b = mid - 1;
+                        if (preu[mid] <= k) lo_b = mid; else hi_b = mid - 1;
                     }
-                    i0 = lo_b;
                     Req r;
-                    load_req(p, i0, r);
-                    const long long off = x0 - pre[i0];
-                    j0 = (int)(off / r.nt);
-                    t0 = (int)(off - (long long)j0 * r.nt);
-                }
-            }
-            sk_cur[0] = i0;
-            sk_cur[1] = j0;
-            sk_cur[2] = t0;
-            // static pieces are built in parallel below; stream-K ones here (falling
-            // back to static when this CTA's range would need more than kMaxRec pieces)
-            s_nrec = -1;
-            if (stream) {
-                Sched w;
-                w.stream = 1;
-                w.i = i0; w.j = j0; w.t = t0;
-                w.rem = sk_rem; w.x = sk_x0;
-                w.k = 0; w.ucum = 0;
-                if (n > 0) load_req(p, i0, w.r);
-                else w.r.MT = 0;
-                Piece pc;
-                int q = 0;
-                while (q <= kMaxRec && sched_next(p, w, pc)) {
-                    if (q < kMaxRec) {
-                        const int MT = (pc.u.K * p.G + kBM - 1) / kBM;
-                        recs[q] = PieceRec{pc.u.i, pc.u.g * MT + pc.u.mt, pc.tb, pc.te, pc.u.off, pc.u.K, pc.u.L,
-                                           (int)pc.x};
+                    load_req(p, lo_b, r);
+                    const int tb = r.nt * sidx / Sx, te = r.nt * (sidx + 1) / Sx;
+                    if (te > tb) {
+                        recs[0] = PieceRec{lo_b, (int)(k - preu[lo_b]), tb, te, r.off, r.K, r.L, sidx};
+                        s_nrec = 1;
                     }
-                    ++q;
                 }
-                s_nrec = q <= kMaxRec ? q : -1;
             }
         }
         __syncthreads();
-        if (sk_stream && s_nrec < 0) {  // some CTA may take this branch alone: static for it is wrong,
-            // so every CTA computes the same bound -- the host keeps U <= kMaxRec * G -- and we
-            // flag the (unreachable) overflow instead of mixing schedules.
-            if (threadIdx.x == 0) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, -2);
-            s_nrec = 0;
-        }
-        if (!sk_stream) {
+        if (!sk_split) {
             const int cnt = U > (int)blockIdx.x ? (U - 1 - (int)blockIdx.x) / G + 1 : 0;
             if (cnt > kMaxRec || !can_plan) {
                 if (threadIdx.x == 0) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, -2);
@@ -474,7 +444,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             if (threadIdx.x == 0) s_nrec = (cnt <= kMaxRec && can_plan) ? cnt : 0;
             __syncthreads();
         }
-        const int nrec_static = (!sk_stream && s_nrec >= 0) ? s_nrec : 0;
+        const int nrec_static = (!sk_split && s_nrec >= 0) ? s_nrec : 0;
         for (int q = threadIdx.x; q < nrec_static; q += blockDim.x) {
             const long long k = (long long)blockIdx.x + (long long)q * G;
             int lo_b = 0, hi_b = n - 1;  // last i with preu[i] <= k
@@ -490,6 +460,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         cur0.q = 0;
         cur0.rec = recs;
         __syncthreads();  // plan scratch (K/V rings) is free again; records are visible
+    }
+    if (p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceCtas) {
+        unsigned long long tn;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+        p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 2] = tn;  // plan done
     }
 
     if (warp == 0) {
@@ -747,6 +722,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 const uint32_t par = s_cnt & 1;
                 ptx::mbar_wait(sf, par);
                 if (lane == 0 && quad == 0 && grp == 0) AS_TRACE(5, tbase + t - pc.tb);
+                if (t == pc.tb && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
+                    unsigned long long tn;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+                    p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 6] = tn;  // first S tile seen
+                }
                 ptx::tc_fence_after();
                 uint32_t sr[kBN];
                 ptx::tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
@@ -839,11 +819,16 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             // ---- epilogue ----
             ptx::mbar_wait(of, unit_it & 1);
             ptx::tc_fence_after();
+            if (p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
+                unsigned long long tn;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+                p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 7] = tn;  // O of the (last) piece ready
+            }
             const bool full = (pc.tb == 0 && pc.te == u.nt);
             const float inv = full ? 1.f / l_sum : 1.f;  // partial piece: keep (O, m, l) unnormalised
             const size_t orow = (size_t)(u.off + node) * p.n_q + (size_t)u.g * G + hh;
-            const int slot = 2 * blockIdx.x + (pc.x == sk_x0 ? 0 : 1);
-            float* part = p.partial + (size_t)slot * p.slot_floats;  // [128][D] O, then m[128], l[128]
+            const int slot = 2 * blockIdx.x + grp;  // split-KV: one piece per CTA, one slot per q-tile
+            float* part = p.partial + (size_t)slot * p.slot_floats;  // O as [D/4][128] float4, then m[128], l[128]
 #pragma unroll
             for (int c0 = 0; c0 < D; c0 += 32) {
                 uint32_t oa[32];
@@ -864,10 +849,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                             dst[j] = make_uint4(pkk[4 * j], pkk[4 * j + 1], pkk[4 * j + 2], pkk[4 * j + 3]);
                     }
                 } else {
-                    float4* dst = reinterpret_cast<float4*>(part + (size_t)r * D + c0);
+                    // column-quad-major [D/4][128] float4: a warp's store is 512 contiguous bytes
+                    float4* dst = reinterpret_cast<float4*>(part) + (c0 / 4) * 128 + r;
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        dst[j] = make_float4(__uint_as_float(oa[4 * j]), __uint_as_float(oa[4 * j + 1]),
+                        dst[j * 128] = make_float4(__uint_as_float(oa[4 * j]), __uint_as_float(oa[4 * j + 1]),
                                              __uint_as_float(oa[4 * j + 2]), __uint_as_float(oa[4 * j + 3]));
                 }
             }
@@ -879,70 +865,57 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(oe);
+            if (!full && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
+                unsigned long long tn;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+                p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 5] = tn;  // partial written
+            }
             if (!full) {
-                // stream-K fix-up: the CTA that completes the unit's last piece merges
-                // every piece's (O, m, l) (fp32, through L2) and writes the output.
+                // split-KV merge, shared by the unit's pieces: once every piece has
+                // published its fp32 (O, m, l), piece CTA s merges its share of the
+                // columns for all rows (all pieces of a unit are co-resident: one piece
+                // per CTA of a persistent grid), so no CTA merges a whole unit alone.
+                const int lead_warp = 1 + NQ + 4 * grp;  // first softmax warp of this group
+                const int wq = pc.w + grp;               // counters of this q-tile
+                const int Sx = sk_split;
+                const int sidx = (int)blockIdx.x % Sx;
+                const int b0 = (int)blockIdx.x - sidx;
+                auto live = [&](int s2) { return u.nt * (s2 + 1) / Sx > u.nt * s2 / Sx; };
+                int n_live = 0, my_rank = 0;
+                for (int s2 = 0; s2 < Sx; ++s2)
+                    if (live(s2)) {
+                        if (s2 < sidx) ++my_rank;
+                        ++n_live;
+                    }
                 __threadfence();
                 group_bar(grp);
-                if (warp == 2 && lane == 0) {
-                    const int n = pc.te - pc.tb;
-                    const int old = atomicAdd(p.cnt + pc.w, n);
-                    sk_last = (old + n == u.nt) ? 1 : 0;
+                if (warp == lead_warp && lane == 0) {
+                    atomicAdd(p.cnt + wq, pc.te - pc.tb);
+                    while (*reinterpret_cast<volatile int*>(p.cnt + wq) < u.nt) __nanosleep(64);
                 }
                 group_bar(grp);
-                if (sk_last) {
-                    __threadfence();
-                    const long long T = sk_T;
-                    const int Gd = gridDim.x;
-                    const long long U0 = pc.x - pc.tb;
-                    const int b_first = sk_owner(T, Gd, U0), b_last = sk_owner(T, Gd, U0 + u.nt - 1);
-                    auto slot_of = [&](int b) {
-                        return p.partial + (size_t)(2 * b + (sk_start(T, b, Gd) < U0 ? 1 : 0)) * p.slot_floats;
-                    };
-                    float M = -INFINITY;
-                    for (int b = b_first; b <= b_last; ++b) M = fmaxf(M, __ldcg(slot_of(b) + 128 * D + r));
-                    float Ltot = 0.f;
-                    for (int b = b_first; b <= b_last; ++b) {
-                        const float* pb = slot_of(b);
-                        const float mb = __ldcg(pb + 128 * D + r);
-                        if (mb != -INFINITY) Ltot += __ldcg(pb + 128 * D + 128 + r) * ptx::ex2(mb - M);
+                __threadfence();
+                if (p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
+                    unsigned long long tn;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+                    p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 3] = tn;  // all pieces published
+                }
+                split_merge<D>(p.partial + (size_t)(2 * b0 + grp) * p.slot_floats, 2 * p.slot_floats, Sx, u.nt, r,
+                               my_rank, n_live, row_ok ? p.out + orow * D : nullptr,
+                               (my_rank == 0 && row_ok && p.lse != nullptr) ? p.lse + orow : nullptr);
+                if (p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
+                    unsigned long long tn;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+                    p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 4] = tn;  // merge done
+                }
+                // the last piece done reading the partials resets the counters (reusable workspace)
+                group_bar(grp);
+                if (warp == lead_warp && lane == 0) {
+                    if (atomicAdd(p.cnt2 + wq, 1) == n_live - 1) {
+                        p.cnt[wq] = 0;
+                        p.cnt2[wq] = 0;
+                        __threadfence();
                     }
-                    const float invL = 1.f / Ltot;
-#pragma unroll 1
-                    for (int c0 = 0; c0 < D; c0 += 32) {
-                        float acc[32];
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-                        for (int b = b_first; b <= b_last; ++b) {
-                            const float* pb = slot_of(b);
-                            const float mb = __ldcg(pb + 128 * D + r);
-                            if (mb == -INFINITY) continue;
-                            const float fb = ptx::ex2(mb - M) * invL;
-                            const float4* src = reinterpret_cast<const float4*>(pb + (size_t)r * D + c0);
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                const float4 q4 = __ldcg(src + j);
-                                acc[4 * j] = fmaf(q4.x, fb, acc[4 * j]);
-                                acc[4 * j + 1] = fmaf(q4.y, fb, acc[4 * j + 1]);
-                                acc[4 * j + 2] = fmaf(q4.z, fb, acc[4 * j + 2]);
-                                acc[4 * j + 3] = fmaf(q4.w, fb, acc[4 * j + 3]);
-                            }
-                        }
-                        if (row_ok) {
-                            uint32_t pkk[16];
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                __nv_bfloat162 h2 = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
-                                pkk[j] = *reinterpret_cast<uint32_t*>(&h2);
-                            }
-                            uint4* dst = reinterpret_cast<uint4*>(p.out + orow * D + c0);
-#pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                dst[j] = make_uint4(pkk[4 * j], pkk[4 * j + 1], pkk[4 * j + 2], pkk[4 * j + 3]);
-                        }
-                    }
-                    if (row_ok && p.lse) p.lse[orow] = (M + __log2f(Ltot)) * 0.6931471805599453f;
-                    if (warp == 2 && lane == 0) atomicExch(p.cnt + pc.w, 0);  // reusable workspace
                 }
             }
             ++unit_it;
@@ -962,7 +935,6 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         unsigned long long* rec = p.trace + (size_t)(p.trace_cap + blockIdx.x) * 8;
         rec[0] = t_start;
         rec[1] = t_end;
-        rec[2] = sk_stream;
     }
 }
 
@@ -1003,7 +975,6 @@ int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, in
     for (int r0 = 0; r0 < p0.n_req; r0 += chunk) {
         TcParams p = p0;
         p.nq = nq;
-        if (nq == 2) p.stream_k = 0;  // paired q-tiles: static schedule
         p.n_req = min(chunk, p0.n_req - r0);
         p.page_table = p0.page_table + (size_t)r0 * p0.max_pages;
         p.kv_len = p0.kv_len + r0;

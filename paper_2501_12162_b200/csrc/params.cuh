@@ -66,6 +66,7 @@ struct TcParams {
     int mt_max;           // q-tiles per (request, kv head) upper bound (unit id stride)
     int stream_k;         // 1: stream-K tile ranges (needs cnt/partial), 0: static whole units
     int* cnt;             // [n_units] tiles completed per split unit (zeroed, self-resetting)
+    int* cnt2;            // [n_units] pieces that finished merging (zeroed, self-resetting)
     float* partial;       // [2 * gridDim.x][slot_floats] partial (O, m, l) of split units
     int slot_floats;      // 128 * D + 256
     int prefetch_tiles;

@@ -36,7 +36,7 @@ _e.record()
 torch.cuda.synchronize()
 print(f"calibration: torch copy {2 * _a.numel() * 2 * 5 / (_s.elapsed_time(_e) / 1e3) / 1e9:.0f} GB/s")
 del _a, _b
-W = bench.make_workload(args.config, "cuda")
+W = bench.make_workload(args.config, "cuda", world=int(os.environ.get("AS_BENCH_EMULATE_WORLD", "1")))
 for _ in range(3):
     bench.run_attention(W)
 torch.cuda.synchronize()
@@ -55,12 +55,24 @@ if len(cta):
     t0c = cta[:, 0].min()
     st = (cta[:, 0] - t0c) / 1e3
     en = (cta[:, 1] - t0c) / 1e3
-    print(f"per-CTA timeline ({len(cta)} CTAs, us from first start, stream-K={int(cta[0, 2])}):")
+    print(f"per-CTA timeline ({len(cta)} CTAs, us from first start):")
+    print(f"  plan done median {np.median((cta[:, 2] - t0c) / 1e3):.2f}  max {((cta[:, 2] - t0c) / 1e3).max():.2f}")
     print(f"  start  median {np.median(st):.2f}  max {st.max():.2f}")
     print(f"  end    min {en.min():.2f}  p10 {np.percentile(en, 10):.2f}  median {np.median(en):.2f}  "
           f"p90 {np.percentile(en, 90):.2f}  max {en.max():.2f}")
     print(f"  busy fraction (sum of CTA spans / (CTAs x makespan)) {((en - st).sum() / (len(cta) * en.max())):.3f}")
     print("  end-time histogram (us):", np.histogram(en, bins=10)[0].tolist(), np.round(np.histogram(en, bins=10)[1], 1).tolist())
+    sp = cta[cta[:, 6] != 0]
+    if len(sp):
+        pw = (sp[:, 5] - t0c) / 1e3
+        pub = (sp[:, 3] - t0c) / 1e3
+        mg = (sp[:, 4] - t0c) / 1e3
+        f6 = (sp[:, 6] - t0c) / 1e3
+        o7 = (sp[:, 7] - t0c) / 1e3
+        print(f"  split pieces: first S tile median {np.median(f6):.2f}; O ready median {np.median(o7):.2f}")
+        if (sp[:, 5] != 0).any():
+            print(f"  split pieces: partial written median {np.median(pw):.2f} max {pw.max():.2f}; all published median "
+              f"{np.median(pub):.2f}; merge done median {np.median(mg):.2f} max {mg.max():.2f} (us)")
 n = int((tr[:, 0] != 0).sum())
 tr = tr[:n].astype(np.float64)
 t0 = tr[0, 0]
@@ -80,4 +92,5 @@ np.set_printoptions(linewidth=200, suppress=True)
 print("QK issue -> softmax start      ", ns(tr[:, 5] - tr[:, 7]))
 print("QK issue interval             ", ns(np.diff(tr[:, 7])))
 print("cols: Kiss Viss Kland Vland PViss Sstart Send QKiss ; rows = tiles 20..36 (ns rel. to tile 20 K issue)")
-print(np.round(tr[20:37, :8] - tr[20, 0]))
+if n > 20:
+    print(np.round(tr[20:37, :8] - tr[20, 0]))
