@@ -13,7 +13,7 @@ import os
 
 import torch
 
-__all__ = ["lib", "select_trees", "tree_verify_attn", "accept_tokens", "Workspace", "check_device_error",
+__all__ = ["lib", "select_trees", "select_global_greedy", "tree_verify_attn", "accept_tokens", "Workspace", "check_device_error",
            "selftest_umma", "AS_ACCEPT_FUSED", "AS_ACCEPT_WALK_ONLY", "AS_ACCEPT_COMMIT_ONLY",
            "AS_ACCEPT_WALK_RECORDS", "AS_ACCEPT_COMMIT_RECORDS", "beam_step", "beam_workspace_size", "AdaServeError",
            "select_workspace_size", "attn_workspace_size", "accept_workspace_size", "DEVICE_ERRORS"]
@@ -192,6 +192,18 @@ def select_trees(cand_offsets, cand_parent, cand_prob, slo_deficit, depth_d, n_m
     out["workspace"] = ws
     return out
 
+
+
+def select_global_greedy(cand_offsets, cand_parent, cand_prob, budget, cand_token=None, out=None, workspace=None):
+    """GlobalGreedy (the paper's ablation) as a
+    parameterisation of as_select_trees: with every A(r) <= 1 the SLO stage
+    takes nothing (1 + sum f-hat < A_cap never holds), so after the roots the
+    whole budget goes to the global top-(B - n) candidates by (f-hat desc,
+    request asc, index asc).  Same kernel, same launch."""
+    n = cand_offsets.numel() - 1
+    zeros = torch.zeros(max(n, 1), dtype=torch.float64, device=cand_prob.device)[:n]
+    return select_trees(cand_offsets, cand_parent, cand_prob, zeros, 0, 0, budget, cand_token=cand_token, out=out,
+                        workspace=workspace)
 
 def tree_verify_attn(q, k_tree, v_tree, k_cache, v_cache, page_table, kv_len, tree_offsets, tree_parent, sm_scale,
                      want_lse=False, out=None, lse=None, workspace=None):

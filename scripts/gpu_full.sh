@@ -25,3 +25,7 @@ echo "ncu beam rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"select_trees|walk_commit" -s 4 -c 2 \
    -o gpurun_out/prof_small_${TAG}_c2 -f python bench.py --profile --steps 2 --warmup 3 --no-graph > gpurun_out/ncu_small_${TAG}.log 2>&1
 echo "ncu small rc=$?"
+for W in 8; do for C in c2 c4 c5; do
+  AS_BENCH_EMULATE_WORLD=$W timeout 300 python bench.py --config $C --no-cpu-baseline --no-spec > gpurun_out/bench_${TAG}_${C}_w$W.json 2>/dev/null
+  echo "emulated w$W $C rc=$?"
+done; done

@@ -192,6 +192,36 @@ def test_select_fuzz(ada, seed):
         _assert_select_equal(F, A, d, n_max, B, got)
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_select_global_greedy_is_lexsort_topk(ada, seed):
+    """NEXT-4 GlobalGreedy through select_global_greedy: every root,
+    then the global top-(B - n) non-root candidates by (f-hat desc, request asc,
+    index asc) -- computed here with np.lexsort, not by the oracle's Alg. 2.
+    The set is ancestor-closed because f-hat never grows down a path and a
+    parent's index precedes its child's (P-sel-4, R8)."""
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(1, [5, 60, 400, 2000][seed]))
+    F = synth.random_forest(rng, n, [20, 60, 120, 9][seed], tie_prob=[0.0, 0.5, 0.2, 0.7][seed])
+    co, cp, cf = F["cand_offsets"], F["cand_parent"], F["cand_prob"]
+    N = int(co[-1])
+    B = n + int(rng.integers(0, N - n + 1))
+    out = ada.select_global_greedy(dev(co), dev(cp), dev(cf), B)
+    assert ada.check_device_error(out["workspace"])[0] == 0
+    req = np.repeat(np.arange(n), np.diff(co))
+    loc = np.arange(N) - co[req]
+    nonroot = np.nonzero(loc > 0)[0]
+    order = nonroot[np.lexsort((loc[nonroot], req[nonroot], -cf[nonroot].astype(np.float64)))]
+    chosen = np.zeros(N, bool)
+    chosen[co[:-1]] = True
+    chosen[order[:B - n]] = True
+    to = out["tree_offsets"].cpu().numpy()
+    src = out["tree_src"].cpu().numpy()
+    np.testing.assert_array_equal(np.diff(to), np.bincount(req[chosen], minlength=n))
+    for i in range(n):
+        np.testing.assert_array_equal(src[to[i]:to[i + 1]], loc[chosen & (req == i)])
+    np.testing.assert_array_equal(out["slo_count"].cpu().numpy()[:n], 0)
+
+
 def test_select_exact_sum_guards(ada):
     """Both desired_i paths of the kernel: the warp fp64 scan is used only when
     every f-hat >= 2^-24 and 1 + sum < 64 (R9); chains of f-hat = 1.0 (sums past
