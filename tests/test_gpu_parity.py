@@ -479,6 +479,35 @@ def test_attn_bf16_request_chunks(ada, nq, monkeypatch):
     assert np.abs(out.float().cpu().numpy() - ref).max() <= BF16_TOL
 
 
+@pytest.mark.parametrize("sk", ["0", "1", "2"])
+def test_attn_bf16_tail_stream_k(ada, sk, monkeypatch):
+    """More units than CTAs (64 requests x 8 kv heads = 512 > 296): with
+    AS_ATTN_STREAMK unset/1 the makespan model picks tail stream-K (whole-unit
+    wave, then the remaining units' tiles spread over every CTA, units cut
+    between CTAs merged by the last one), =2 forces it, =0 keeps whole units.
+    Ragged kv lengths put the cuts at every offset within a unit."""
+    monkeypatch.setenv("AS_ATTN_STREAMK", sk)
+    monkeypatch.setenv("AS_ATTN_NQ", "1")
+    rng = np.random.default_rng(57)
+    n = 64
+    sizes = rng.integers(20, 33, n)
+    kv = rng.integers(500, 1200, n)
+    kv[::9] = 0  # prefix-free requests among them
+    w = synth.tree_workload(rng, sizes, kv, 32, 8, 128, 64, bf16=True)
+    scale = np.float32(1.0 / np.sqrt(128))
+    ref, ref_lse = oracle_attn(w, scale)
+    g = workload_to_device(w, torch.bfloat16)
+    ws = ada.Workspace(256)
+    for rep in range(2):  # the second launch reuses the (self-resetting) counters
+        out, lse = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"],
+                                        g["page_table"], g["kv_len"], g["tree_offsets"], g["tree_parent"], scale,
+                                        want_lse=True, workspace=ws)
+        assert ada.check_device_error(ws)[0] == 0
+        err = np.abs(out.float().cpu().numpy() - ref).max()
+        assert err <= BF16_TOL, (rep, err)
+        assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-2
+
+
 def test_attn_bf16_nan_in_unused_cache_slots(ada):
     """Cache slots past kv_len may hold garbage (NaN): outputs must not see them."""
     w = _attn_case(([6, 9], [70, 33], 8, 2, 128, 64, "random", 1.0), True, 77)
