@@ -55,8 +55,6 @@ constexpr int kCtasPerSm = 2;     // max over the shapes (workspace sizing)
 constexpr int kPtChunk = 256;     // page-table entries staged per refill
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 constexpr int kMaxRec = 64;       // pieces per CTA precomputed in the prologue
-constexpr int kSkOverhead = 3;     // tail stream-K: per-CTA cost of partials + merge, in tiles (model)
-constexpr int kSkMinTiles = 4;     // tail stream-K only when every CTA gets >= this many tail tiles
 constexpr int kMaxSplit = 8;      // split-KV: pieces per unit when units are fewer than CTAs
 constexpr int kTraceCtas = 512;   // per-CTA timeline records after the CTA-0 tile trace (debug)
 
@@ -81,7 +79,6 @@ struct TcSmem {
     // stream-K plan scratch (long long per block) aliases the K+V rings before any TMA
     static constexpr int PLAN_CAP = (KST + VST) * KV_BYTES / 8;
     static constexpr int PLAN_HALF = PLAN_CAP / 2;  // [0,half) tile prefix, [half, cap) unit prefix
-    static constexpr int RQ_CAP = NQ * Q_BYTES / 16;  // request cache {off, K, L} (int4) in the Q region
 };
 
 // CTA-0 pipeline trace (debug): event e of CTA-local tile index idx.
@@ -114,19 +111,6 @@ __device__ __forceinline__ void load_req(const TcParams& p, int i, Req& r) {
     r.L = __ldg(p.kv_len + i);
     if (r.L < 0) r.L = 0;
     if (r.L > p.max_pages * p.page_size) r.L = p.max_pages * p.page_size;
-    r.n_prefix = (r.L + kBN - 1) / kBN;
-    const bool ok = r.K > 0 && r.K <= AS_MAX_TREE && r.off + r.K <= p.n_tree_rows;
-    r.QT = ok ? (r.K * p.G + kBM - 1) / kBM : 0;
-    r.MT = (r.QT + p.nq - 1) / p.nq;
-    r.nt = r.n_prefix + (r.K + kBN - 1) / kBN;
-}
-
-// Request geometry as load_req computes it, from a shared-memory copy {off, K, L}
-// written by the prologue (no global round trip while building pieces).
-__device__ __forceinline__ void req_from(const TcParams& p, int4 c, Req& r) {
-    r.off = c.x;
-    r.K = c.y;
-    r.L = c.z;
     r.n_prefix = (r.L + kBN - 1) / kBN;
     const bool ok = r.K > 0 && r.K <= AS_MAX_TREE && r.off + r.K <= p.n_tree_rows;
     r.QT = ok ? (r.K * p.G + kBM - 1) / kBM : 0;
@@ -194,96 +178,6 @@ __device__ __forceinline__ bool rec_next(const TcParams& p, RecCursor& cur, Piec
     pc.te = rc.te;
     pc.x = rc.x;
     return true;
-}
-
-// Tail stream-K merge of one row: the unit's tiles [xu, xu + nt) were cut
-// between CTAs b_first..b_last (CTA b owns tail tiles [x0 + tt*b/G, x0 + tt*(b+1)/G));
-// each left an unnormalised fp32 (O, m, l) in slot 2b (the piece continuing a unit
-// begun before b's range) or 2b + 1 (b's last piece).  All D columns of row r.
-template <int D>
-__device__ __noinline__ void sk_merge(const float* __restrict__ partial, int slot_floats, long long x0, long long tt,
-                                      int G, long long xu, int nt, int r, __nv_bfloat16* out_row, float* lse_out) {
-    auto start = [&](int b) { return x0 + tt * (long long)b / G; };
-    auto owner = [&](long long x) {
-        int b = (int)(((x - x0) * G) / tt);
-        b = min(max(b, 0), G - 1);
-        while (b > 0 && start(b) > x) --b;
-        while (b + 1 < G && start(b + 1) <= x) ++b;
-        return b;
-    };
-    const int b_first = owner(xu), b_last = owner(xu + nt - 1);
-    auto slot = [&](int b) { return partial + (size_t)(2 * b + (start(b) > xu ? 0 : 1)) * slot_floats; };
-    // pass 1: M and sum_b 2^(m_b - M) l_b, 4 pieces' (m, l) in flight at a time
-    float M = -INFINITY, Ltot = 0.f;
-    for (int b0 = b_first; b0 <= b_last; b0 += 4) {
-        float m4[4], l4[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            m4[j] = -INFINITY;
-            l4[j] = 0.f;
-            if (b0 + j <= b_last) {
-                m4[j] = __ldcg(slot(b0 + j) + 128 * D + r);
-                l4[j] = __ldcg(slot(b0 + j) + 128 * D + 128 + r);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (m4[j] == -INFINITY) continue;
-            const float Mn = fmaxf(M, m4[j]);
-            Ltot = Ltot * ptx::ex2(M - Mn) + l4[j] * ptx::ex2(m4[j] - Mn);
-            M = Mn;
-        }
-    }
-    const float invL = 1.f / Ltot;
-    // pass 2: 32 columns at a time, two pieces' 8 float4 each in flight
-#pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 32) {
-        float4 acc[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int b0 = b_first; b0 <= b_last; b0 += 2) {
-            float4 q4[2][8];
-            float fb[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                fb[h] = 0.f;
-                if (b0 + h <= b_last) {
-                    const float* pb = slot(b0 + h);
-                    const float mb = __ldcg(pb + 128 * D + r);
-                    fb[h] = mb == -INFINITY ? 0.f : ptx::ex2(mb - M) * invL;
-                    const float4* src = reinterpret_cast<const float4*>(pb) + (c0 / 4) * 128 + r;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) q4[h][j] = __ldcg(src + j * 128);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) q4[h][j] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    acc[j].x = fmaf(q4[h][j].x, fb[h], acc[j].x);
-                    acc[j].y = fmaf(q4[h][j].y, fb[h], acc[j].y);
-                    acc[j].z = fmaf(q4[h][j].z, fb[h], acc[j].z);
-                    acc[j].w = fmaf(q4[h][j].w, fb[h], acc[j].w);
-                }
-        }
-        if (out_row != nullptr) {
-            uint32_t pkk[16];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                __nv_bfloat162 h0 = __floats2bfloat162_rn(acc[j].x, acc[j].y);
-                __nv_bfloat162 h1 = __floats2bfloat162_rn(acc[j].z, acc[j].w);
-                pkk[2 * j] = *reinterpret_cast<uint32_t*>(&h0);
-                pkk[2 * j + 1] = *reinterpret_cast<uint32_t*>(&h1);
-            }
-            uint4* dst = reinterpret_cast<uint4*>(out_row + c0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pkk[4 * j], pkk[4 * j + 1], pkk[4 * j + 2], pkk[4 * j + 3]);
-        }
-    }
-    if (lse_out != nullptr) *lse_out = (M + __log2f(Ltot)) * 0.6931471805599453f;
 }
 
 // Split-KV merge of one row (DESIGN.md §5 "Schedule"): the unit's live pieces each left an
@@ -427,8 +321,6 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
 
     // ---------------- schedule plan (all threads; K/V rings used as scratch) ----------------
     __shared__ int sk_split;  // split-KV pieces per unit (0: whole units)
-    __shared__ long long sk_x0, sk_tt;  // tail stream-K: first tail tile, tail tiles (0: off)
-    __shared__ int sk_last[2];         // tail stream-K: this group completed the unit
     __shared__ long long scan_tmp[33];
     __shared__ int red_tmp[3][16];  // per warp (<= 10 warps)
     RecCursor cur0;
@@ -440,12 +332,9 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         const bool can_plan = n <= S::PLAN_HALF;
         const bool can_split = p.stream_k && can_plan;
         int my_units = 0, my_maxnt = 0, my_minnt = 0x7fffffff;
-        int4* rq = reinterpret_cast<int4*>(smem + S::OFF_Q);  // request cache (Q region is free until the first Q load)
-        const bool use_rq = n <= S::RQ_CAP;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             Req r;
             load_req(p, i, r);
-            if (use_rq) rq[i] = make_int4(r.off, r.K, r.L, 0);
             if (r.MT == 0 && r.K > AS_MAX_TREE) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, i);
             if (r.MT > 0 && __ldg(p.kv_len + i) > p.max_pages * p.page_size) set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, i);
             my_units += p.n_kv * r.MT;
@@ -536,7 +425,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         if (preu[mid] <= k) lo_b = mid; else hi_b = mid - 1;
                     }
                     Req r;
-                    if (use_rq) req_from(p, rq[lo_b], r); else load_req(p, lo_b, r);
+                    load_req(p, lo_b, r);
                     const int tb = r.nt * sidx / Sx, te = r.nt * (sidx + 1) / Sx;
                     if (te > tb) {
                         recs[0] = PieceRec{lo_b, (int)(k - preu[lo_b]), tb, te, r.off, r.K, r.L, sidx};
@@ -544,40 +433,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     }
                 }
             }
-            // Tail stream-K (one q-tile per CTA only): the first wv = floor(U / G)
-            // waves of whole units stay static; the remaining units' tiles are
-            // concatenated and CTA b takes tail tiles [Tt*b/G, Tt*(b+1)/G) after its
-            // static units.  A unit cut between CTAs is merged by the CTA that
-            // completes its last piece (atomic tile count, no waiting).  Chosen by a
-            // makespan model in tiles (+ kSkOverhead per CTA for partials/merge).
-            sk_tt = 0;
-            sk_x0 = 0;
-            const int wv = G > 0 ? U / G : 0;
-            if (!sk_split && can_plan && p.stream_k && p.nq == 1 && wv >= 1 && U - wv * G > 0 && T < (1ll << 30)) {
-                const long long k0 = (long long)wv * G;
-                int lo_b = 0, hi_b = n - 1;  // request of unit k0
-                while (lo_b < hi_b) {
-                    const int mid = (lo_b + hi_b + 1) >> 1;
-                    if (preu[mid] <= k0) lo_b = mid; else hi_b = mid - 1;
-                }
-                Req r;
-                if (use_rq) req_from(p, rq[lo_b], r); else load_req(p, lo_b, r);
-                const long long X0 = pre[lo_b] + (k0 - preu[lo_b]) * r.nt;
-                const long long Tt = T - X0;
-                const long long per = Tt / G;
-                const long long static_ms = (long long)(wv + 1) * maxnt;
-                const long long hybrid_ms = (long long)wv * maxnt + per + 1 + kSkOverhead;
-                const bool fits = minnt > 0 && wv + (per + 1) / minnt + 3 <= kMaxRec && per >= kSkMinTiles;
-                if (fits && (p.stream_k == 2 || hybrid_ms * 100 < static_ms * 95)) {
-                    sk_tt = Tt;
-                    sk_x0 = X0;
-                }
-            }
         }
         __syncthreads();
         if (!sk_split) {
-            const int cnt_all = U > (int)blockIdx.x ? (U - 1 - (int)blockIdx.x) / G + 1 : 0;
-            const int cnt = sk_tt > 0 ? U / G : cnt_all;
+            const int cnt = U > (int)blockIdx.x ? (U - 1 - (int)blockIdx.x) / G + 1 : 0;
             if (cnt > kMaxRec || !can_plan) {
                 if (threadIdx.x == 0) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, -2);
             }
@@ -594,33 +453,9 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 if (preu[mid] <= k) lo_b = mid; else hi_b = mid - 1;
             }
             Req r;
-            if (use_rq) req_from(p, rq[lo_b], r); else load_req(p, lo_b, r);
+            load_req(p, lo_b, r);
             recs[q] = PieceRec{lo_b, (int)(k - preu[lo_b]), 0, r.nt, r.off, r.K, r.L, -1};
         }
-        if (sk_tt > 0 && threadIdx.x == 0) {
-            const int G = gridDim.x;
-            long long x = sk_x0 + sk_tt * (long long)blockIdx.x / G;
-            const long long xe = sk_x0 + sk_tt * ((long long)blockIdx.x + 1) / G;
-            int q = nrec_static;
-            while (x < xe && q < kMaxRec) {
-                int lo_b = 0, hi_b = n - 1;  // last i with pre[i] <= x
-                while (lo_b < hi_b) {
-                    const int mid = (lo_b + hi_b + 1) >> 1;
-                    if (pre[mid] <= x) lo_b = mid; else hi_b = mid - 1;
-                }
-                Req r;
-                if (use_rq) req_from(p, rq[lo_b], r); else load_req(p, lo_b, r);
-                const long long rel = x - pre[lo_b];
-                const int j = (int)(rel / r.nt);
-                const int tb = (int)(rel - (long long)j * r.nt);
-                const int te = (int)min((long long)r.nt, tb + (xe - x));
-                recs[q++] = PieceRec{lo_b, j, tb, te, r.off, r.K, r.L, (int)x};
-                x += te - tb;
-            }
-            if (x < xe) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, -2);  // unreachable (fits check)
-            s_nrec = q;
-        }
-        if (sk_tt > 0) __syncthreads();  // s_nrec (block-uniform branch)
         cur0.nrec = s_nrec;
         cur0.q = 0;
         cur0.rec = recs;
@@ -993,11 +828,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             const bool full = (pc.tb == 0 && pc.te == u.nt);
             const float inv = full ? 1.f / l_sum : 1.f;  // partial piece: keep (O, m, l) unnormalised
             const size_t orow = (size_t)(u.off + node) * p.n_q + (size_t)u.g * G + hh;
-            // split-KV: one piece per CTA, one slot per q-tile; tail stream-K (one q-tile):
-            // slot 0 = the piece continuing a unit begun before this CTA's range, 1 = the last
-            const int slot = 2 * blockIdx.x +
-                             (sk_tt > 0 ? (sk_x0 + sk_tt * (long long)blockIdx.x / gridDim.x > pc.x - pc.tb ? 0 : 1)
-                                        : grp);
+            const int slot = 2 * blockIdx.x + grp;  // split-KV: one piece per CTA, one slot per q-tile
             float* part = p.partial + (size_t)slot * p.slot_floats;  // O as [D/4][128] float4, then m[128], l[128]
 #pragma unroll
             for (int c0 = 0; c0 < D; c0 += 32) {
@@ -1040,24 +871,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
                 p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 5] = tn;  // partial written
             }
-            if (!full && sk_tt > 0) {
-                // tail stream-K: the CTA completing the unit's last piece merges all of them
-                const int lead_warp = 1 + NQ + 4 * grp;
-                __threadfence();
-                group_bar(grp);
-                if (warp == lead_warp && lane == 0) {
-                    const int nn = pc.te - pc.tb;
-                    sk_last[grp] = (atomicAdd(p.cnt + pc.w, nn) + nn == u.nt) ? 1 : 0;
-                }
-                group_bar(grp);
-                if (sk_last[grp]) {
-                    __threadfence();
-                    sk_merge<D>(p.partial, p.slot_floats, sk_x0, sk_tt, (int)gridDim.x, pc.x - pc.tb, u.nt, r,
-                                row_ok ? p.out + orow * D : nullptr,
-                                (row_ok && p.lse != nullptr) ? p.lse + orow : nullptr);
-                    if (warp == lead_warp && lane == 0) p.cnt[pc.w] = 0;  // all pieces counted: reusable
-                }
-            } else if (!full) {
+            if (!full) {
                 // split-KV merge, shared by the unit's pieces: once every piece has
                 // published its fp32 (O, m, l), piece CTA s merges its share of the
                 // columns for all rows (all pieces of a unit are co-resident: one piece
