@@ -184,28 +184,26 @@ __global__ void __launch_bounds__(128) beam_merge_kernel(BeamParams p) {
     const int w = p.w_out;
     WarpList M;
     wl_init(M);
-    constexpr int PF = 8;  // keys prefetched per lane (loads in flight before the serial inserts)
-    for (int k = 0; k < p.w_in; ++k) {
-        const long long row = (long long)i * p.w_in + k;
-        const int np = p.pieces;
-        const uint64_t* K = p.lists + (size_t)row * p.pieces * kBeamW;
-        const int nk = np * kBeamW;
-        for (int x00 = 0; x00 < nk; x00 += 32 * PF) {
-            uint64_t kk[PF];
+    // the request's rows' lists are contiguous ([w_in][pieces][kBeamW] keys):
+    // one pass, PF keys per lane in flight before the serial inserts
+    constexpr int PF = 8;
+    const int nk = p.w_in * p.pieces * kBeamW;
+    const uint64_t* K = p.lists + (size_t)i * nk;
+    for (int x00 = 0; x00 < nk; x00 += 32 * PF) {
+        uint64_t kk[PF];
 #pragma unroll
-            for (int u = 0; u < PF; ++u) {
-                const int x = x00 + u * 32 + lane;
-                kk[u] = x < nk ? __ldcg(K + x) : 0ull;
-            }
+        for (int u = 0; u < PF; ++u) {
+            const int x = x00 + u * 32 + lane;
+            kk[u] = x < nk ? __ldcg(K + x) : 0ull;
+        }
 #pragma unroll
-            for (int u = 0; u < PF; ++u) {
-                const uint64_t key = kk[u];
-                unsigned b = __ballot_sync(0xffffffffu, key > M.thr);
-                while (b) {
-                    const int src = __ffs(b) - 1;
-                    b &= b - 1;
-                    wl_insert(M, __shfl_sync(0xffffffffu, key, src), w);
-                }
+        for (int u = 0; u < PF; ++u) {
+            const uint64_t key = kk[u];
+            unsigned b = __ballot_sync(0xffffffffu, key > M.thr);
+            while (b) {
+                const int src = __ffs(b) - 1;
+                b &= b - 1;
+                wl_insert(M, __shfl_sync(0xffffffffu, key, src), w);
             }
         }
     }
