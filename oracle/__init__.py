@@ -25,6 +25,11 @@ Contents
   (P:L691-694), ties (parent asc, token asc) (R8); pinned by exhaustive
   enumeration, the complete-tree case and Thm. 2 containment.
 
+* ``sampling.sample_rows`` -- NEXT-3(a): per-node target samples by
+  Gumbel-max with a counter-based generator and a fixed fp32 logarithm
+  (reading R23), pinned by the Philox known-answer vectors, the fp64 log and a
+  chi-squared test of the Gumbel-max theorem (``tests/test_oracle_sampling.py``).
+
 Parity unpinned: none (see DESIGN.md §Oracle pins).
 """
 from __future__ import annotations
