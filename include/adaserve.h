@@ -257,6 +257,29 @@ as_status as_accept_tokens(as_accept_phase phase, int32_t n_req, int32_t req_beg
                            void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------- */
+/* Target samples for the stochastic walk: Gumbel-max (NEXT-3(a), reading R23) */
+/* ------------------------------------------------------------------------- */
+/*
+ * out_tokens[r] = argmax_t fl32(fl32(logits[r, t] * inv_temperature) + g(r, t)),
+ * lowest t on ties, for r in [0, n_rows): one sample of softmax(logits / T)
+ * per tree node (T = 1 / inv_temperature), the per-node target samples R13's
+ * lossless stochastic walk takes as target_tokens of as_accept_tokens
+ * (E[accept_len] = sum_v f(v), Thm. 1).  g(r, t) is R23's
+ * Gumbel draw: Philox4x32-10 with key (seed lo, seed hi) and counter
+ * (t / 4, r, offset lo, offset hi), word t % 4 -> x; u = fl32((x >> 9)*2 + 1)
+ * * 2^-24; g = -ln(-ln u) with R23's fp32 logarithm, so the
+ * result is bit-identical to oracle/sampling.py.  A new (seed, offset) pair per
+ * iteration gives fresh samples.
+ * Inputs (device): logits [n_rows, vocab] of logits_dtype (AS_F32 or AS_BF16),
+ *   finite (NaN sets AS_DEV_NAN_LOGIT; +-inf rows follow IEEE arithmetic).
+ * Output (device): out_tokens [n_rows] int32.
+ * Workspace: >= 256 bytes (device error word), 256-byte aligned.
+ */
+as_status as_sample_tokens(int32_t n_rows, int32_t vocab, const void* logits, as_dtype logits_dtype,
+                           float inv_temperature, unsigned long long seed, unsigned long long offset,
+                           int32_t* out_tokens, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------- */
 /* Utilities                                                                 */
 /* ------------------------------------------------------------------------- */
 const char* as_status_string(as_status s);

@@ -13,7 +13,7 @@ import os
 
 import torch
 
-__all__ = ["lib", "select_trees", "select_global_greedy", "tree_verify_attn", "accept_tokens", "Workspace", "check_device_error",
+__all__ = ["lib", "select_trees", "select_global_greedy", "sample_tokens", "tree_verify_attn", "accept_tokens", "Workspace", "check_device_error",
            "selftest_umma", "AS_ACCEPT_FUSED", "AS_ACCEPT_WALK_ONLY", "AS_ACCEPT_COMMIT_ONLY",
            "AS_ACCEPT_WALK_RECORDS", "AS_ACCEPT_COMMIT_RECORDS", "beam_step", "beam_workspace_size", "AdaServeError",
            "select_workspace_size", "attn_workspace_size", "accept_workspace_size", "DEVICE_ERRORS"]
@@ -50,6 +50,8 @@ def lib():
         L.as_beam_workspace_size.argtypes = [_c_i32, _c_i32, _c_i32]
         L.as_beam_step.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _vp, _c_i32, _vp, _vp, _vp, _vp, _c_sz, _vp]
         L.as_select_workspace_size.argtypes = [_c_i32, _c_i32]
+        L.as_sample_tokens.argtypes = [_c_i32, _c_i32, _vp, _c_i32, _f32, ctypes.c_ulonglong, ctypes.c_ulonglong, _vp,
+                                       _vp, _c_sz, _vp]
         L.as_attn_workspace_size.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32]
         L.as_accept_workspace_size.argtypes = [_c_i32]
         L.as_select_trees.argtypes = [_c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32,
@@ -119,6 +121,23 @@ def beam_step(layer, width, draft_probs, cand_parent, cand_prob, cand_token, can
     _check(lib().as_beam_step(n, layer, width, vocab, _ptr(draft_probs), cand_stride, _ptr(cand_parent),
                               _ptr(cand_prob), _ptr(cand_token), ws.ptr, ws.nbytes, _stream()), "as_beam_step")
     return ws
+
+
+def sample_tokens(logits, inv_temperature, seed, offset=0, out=None, workspace=None):
+    """as_sample_tokens (NEXT-3(a), reading R23): one Gumbel-max sample of
+    softmax(logits * inv_temperature) per row of logits [rows, vocab] (fp32 or
+    bf16, device); returns int32 [rows] -- the per-node target samples of the
+    stochastic walk (pass them as accept_tokens' target_tokens)."""
+    if logits.dtype not in (torch.float32, torch.bfloat16) or logits.dim() != 2 or not logits.is_contiguous():
+        raise AdaServeError("logits must be a contiguous [rows, vocab] fp32/bf16 tensor")
+    rows, vocab = logits.shape
+    if out is None:
+        out = torch.empty(rows, dtype=torch.int32, device=logits.device)
+    ws = workspace if workspace is not None else Workspace(256, logits.device)
+    _check(lib().as_sample_tokens(rows, vocab, _ptr(logits), 1 if logits.dtype == torch.bfloat16 else 0,
+                                  float(inv_temperature), int(seed) & (2**64 - 1), int(offset) & (2**64 - 1),
+                                  _ptr(out), ws.ptr, ws.nbytes, _stream()), "as_sample_tokens")
+    return out, ws
 
 
 def select_workspace_size(n_req, n_cand_total):

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libadaserve.so")
-SOURCES = ["abi.cu", "beam.cu", "select.cu", "accept.cu", "attn_simt.cu", "attn_tc.cu", "selftest.cu", "membench.cu"]
+SOURCES = ["abi.cu", "beam.cu", "sample.cu", "select.cu", "accept.cu", "attn_simt.cu", "attn_tc.cu", "selftest.cu", "membench.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -119,6 +119,20 @@ as_status as_beam_step(int32_t n_req, int32_t layer, int32_t width, int32_t voca
                        workspace, S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
 }
 
+// ----------------------------------------------------------------- sample (NEXT-3a)
+as_status as_sample_tokens(int32_t n_rows, int32_t vocab, const void* logits, as_dtype logits_dtype,
+                           float inv_temperature, unsigned long long seed, unsigned long long offset,
+                           int32_t* out_tokens, void* workspace, size_t workspace_bytes, void* stream) {
+    if (n_rows < 0 || vocab < 1) return AS_ERR_INVALID_ARG;
+    if (logits_dtype != AS_F32 && logits_dtype != AS_BF16) return AS_ERR_UNSUPPORTED;
+    if (!(inv_temperature >= 0.f) || isinf(inv_temperature)) return AS_ERR_INVALID_ARG;
+    if (n_rows == 0) return AS_OK;
+    if (!logits || !out_tokens) return AS_ERR_INVALID_ARG;
+    if (!workspace || !al256(workspace) || workspace_bytes < kWsHeaderBytes) return AS_ERR_WORKSPACE;
+    return launch_sample(logits, logits_dtype == AS_BF16, n_rows, vocab, inv_temperature, seed, offset, out_tokens,
+                         workspace, S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
+}
+
 // ----------------------------------------------------------------- select
 size_t as_select_workspace_size(int32_t n_req, int32_t n_cand_total) {
     if (n_req < 0 || n_cand_total < 0) return 0;

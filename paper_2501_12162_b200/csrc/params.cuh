@@ -83,6 +83,8 @@ int launch_select(int, int, const int32_t*, const int32_t*, const float*, const 
 int launch_accept(const AcceptParams& p, const void* target_logits, int logits_bf16, int vocab, int32_t* argmax_buf,
                   cudaStream_t stream);
 int launch_attn_simt(const SimtParams& p, int head_dim, cudaStream_t stream);
+int launch_sample(const void* logits, int logits_bf16, int n_rows, int vocab, float inv_t, unsigned long long seed,
+                  unsigned long long offset, int32_t* out, void* ws, cudaStream_t stream);
 int launch_attn_tc(const CUtensorMap* maps, const TcParams& p, int head_dim, int n_sms, cudaStream_t stream);
 int tc_ctas_per_sm();
 size_t beam_ws_bytes(int n_req, int width, int vocab);

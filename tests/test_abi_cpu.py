@@ -80,3 +80,16 @@ def test_product_path_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src and "liboracle" not in src, f
                 assert "adaserve_ref" not in src, f
+
+
+def test_sample_tokens_host_checks(L):
+    """as_sample_tokens rejects bad host arguments before any launch."""
+    f = L.as_sample_tokens
+    f.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_float,
+                  ctypes.c_ulonglong, ctypes.c_ulonglong, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                  ctypes.c_void_p]
+    assert f(0, 10, None, 0, 1.0, 1, 0, None, None, 0, None) == 0          # nothing to do
+    assert f(-1, 10, None, 0, 1.0, 1, 0, None, None, 0, None) != 0         # negative rows
+    assert f(2, 10, None, 0, 1.0, 1, 0, None, None, 0, None) != 0          # null logits
+    assert f(2, 10, 256, 0, -1.0, 1, 0, 512, 768, 256, None) != 0          # negative inv_temperature
+    assert f(2, 10, 256, 5, 1.0, 1, 0, 512, 768, 256, None) != 0           # unknown dtype

@@ -602,3 +602,51 @@ def test_iteration_graph_replay_equals_eager(ada):
     for k in ("accept_len", "accept_path", "bonus_token"):
         assert torch.equal(out[k], W["acc"][k]), k
     assert torch.equal(out["kv_len_out"], W["kv_len_out"])
+
+
+# --------------------------------------------------------------------------- NEXT-3(a) sampling
+@pytest.mark.parametrize("rows,vocab,dtype,inv_t", [(37, 1000, "f32", 1.0), (19, 4099, "bf16", 0.7),
+                                                    (5, 7, "f32", 2.0), (300, 64, "bf16", 0.0),
+                                                    (4, 128256, "bf16", 1.0), (3, 128256, "f32", 0.6)])
+def test_sample_tokens_bit_exact(ada, rows, vocab, dtype, inv_t):
+    """as_sample_tokens == oracle.sampling.sample_rows token for token (R23
+    fixes every fp32 operation); ragged vocabularies take the scalar path."""
+    from oracle import sampling
+    rng = np.random.default_rng(rows * 7 + vocab)
+    lg = rng.normal(0.0, 3.0, (rows, vocab)).astype(np.float32)
+    lg[0, : min(vocab, 5)] = 4.0  # exact ties in the logits
+    t = torch.from_numpy(lg)
+    if dtype == "bf16":
+        t = t.to(torch.bfloat16)
+        lg = t.float().numpy()
+    seed, offset = 0x1234_5678_9ABC + rows, vocab * 3
+    got, ws = ada.sample_tokens(t.cuda(), np.float32(inv_t), seed, offset)
+    assert ada.check_device_error(ws)[0] == 0
+    want = sampling.sample_rows(lg, np.float32(inv_t), seed, offset)
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+
+
+def test_stochastic_walk_with_sampled_targets(ada):
+    """The stochastic walk (R13) end to end on the GPU: per-node target samples
+    from as_sample_tokens feed as_accept_tokens; equals the oracle walk driven by
+    the oracle's samples."""
+    from oracle import sampling
+    rng = np.random.default_rng(8)
+    n, V = 12, 50
+    sizes = rng.integers(1, 20, n)
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    par = np.concatenate([[0] + [int(rng.integers(0, j)) for j in range(1, k)] for k in sizes]).astype(np.int32)
+    tok = rng.integers(0, 4, offs[-1]).astype(np.int32)  # tiny alphabet: many matches
+    lg = rng.normal(0.0, 1.0, (offs[-1], V)).astype(np.float32)
+    lg[:, :4] += 3.0
+    samp, _ = ada.sample_tokens(torch.from_numpy(lg).cuda(), 1.0, 77, 0)
+    want_samp = sampling.sample_rows(lg, np.float32(1.0), 77, 0)
+    np.testing.assert_array_equal(samp.cpu().numpy(), want_samp)
+    max_path = int(sizes.max()) + 1
+    out = ada.accept_tokens(ada.AS_ACCEPT_WALK_ONLY, dev(offs), dev(par), dev(tok), target_tokens=samp,
+                            max_path=max_path, n_tree_rows=int(offs[-1]))
+    ref = oracle.accept_walk(offs, par, tok, target_tokens=want_samp, max_path=max_path)
+    assert ref["status"] == 0
+    np.testing.assert_array_equal(out["accept_path"].cpu().numpy(), ref["accept_path"])
+    np.testing.assert_array_equal(out["accept_len"].cpu().numpy(), ref["accept_len"])
+    np.testing.assert_array_equal(out["bonus_token"].cpu().numpy(), ref["bonus_token"])
