@@ -531,9 +531,11 @@ def main():
         e2e = measure_e2e(W, step, args.steps, world)
     spec = None
     logits_mode = None
+    sampling = None
     if rank == 0 and not args.profile and not args.no_spec:
         spec = measure_speculation(W, args.steps)
         logits_mode = measure_accept_logits(W, args.steps)
+        sampling = measure_sampling(W, args.steps)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         threads = os.cpu_count() or 1
@@ -559,6 +561,7 @@ def main():
                        if W["n_pools"] == 1 else f"{W['n_pools']} rotating KV pools (> 3x L2)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks, "graph": use_graph, "speculation": spec, "accept_logits": logits_mode,
+            "sampling": sampling,
             **({"emulated_shard_of_world": emu} if (emu > 1 and world == 1) else {}), **({"ablation_skip": os.environ["AS_BENCH_SKIP"]}
                                                        if os.environ.get("AS_BENCH_SKIP") else {}),
             "breakdown_ms": {"select": round(t_sel, 4), "attention": round(t_attn_b, 4), "accept_commit": round(t_acc, 4),
@@ -664,6 +667,53 @@ def measure_accept_logits(W, steps):
     return {"step": "accept, logits mode (argmax scan + walk + commit)", "rows": int(W["tree_tokens_total"]),
             "vocab": V, "us": round(us, 2), "algorithmic_bytes": nbytes, "hbm_gbs": round(gbs, 1),
             "hbm_frac": round(gbs / peak, 4), "launches": 2}
+
+
+def measure_sampling(W, steps):
+    """NEXT-3(a): per-node target samples by Gumbel-max (as_sample_tokens) over
+    the same [N_tree, 128 256] bf16 target logits.  ALU-bound (10 Philox rounds
+    per 4 tokens, two R23 logarithms per token): reported as scored tokens/s
+    against DESIGN.md's FP32-lane peak, plus the HBM fraction for context."""
+    ada = W["ada"]
+    if W["dtype"] != torch.bfloat16:
+        return None
+    R, V = W["R"], synth.LLAMA3_VOCAB
+    gen = torch.Generator(device=W["device"]).manual_seed(synth.SEED_BASE + 8)
+    logits = torch.randn((R, V), generator=gen, device=W["device"], dtype=torch.float32).to(torch.bfloat16)
+    out = torch.empty(R, dtype=torch.int32, device=W["device"])
+    ws = ada.Workspace(256, W["device"])
+    for _ in range(3):
+        ada.sample_tokens(logits, 1.0, 1234, 0, out=out, workspace=ws)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for k in range(steps):
+            ada.sample_tokens(logits, 1.0, 1234, k, out=out, workspace=ws)
+    g.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    us = s.elapsed_time(e) * 1e3 / steps
+    toks = R * V
+    nbytes = toks * 2
+    peak = float(_peaks()[0]["hbm_gbs"])
+    gbs = nbytes / (us * 1e-6) / 1e9
+    del logits
+    # issue-bound: warp instructions per scored token from the ncu capture
+    # (profiles/r01/ncu_sample_c2_r01i.md: 857.45e6 / (2048 * 128256)); peak =
+    # 148 SMs x 4 schedulers x 1 warp instruction per clock at the max SM clock
+    winst = 857452936 / (2048 * 128256)
+    clk = float((_peaks()[0].get("sm_max_mhz") or 1965)) * 1e6
+    issue_peak = 148 * 4 * clk
+    achieved = toks / (us * 1e-6) * winst
+    return {"step": "per-node target samples, Gumbel-max (as_sample_tokens)", "rows": R, "vocab": V,
+            "us": round(us, 2), "scored_tokens_per_s": round(toks / (us * 1e-6), 1), "bound": "alu",
+            "alu": {"achieved_warp_inst_per_s": round(achieved, 1), "peak_warp_inst_per_s": issue_peak,
+                    "frac": round(achieved / issue_peak, 4), "warp_inst_per_token": round(winst, 4)},
+            "algorithmic_bytes": nbytes, "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4), "launches": 1}
 
 
 def measure_e2e(W, step, steps, world):
