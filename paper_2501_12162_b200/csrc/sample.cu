@@ -11,8 +11,9 @@
 // sample_rows_kernel: one CTA per row; each thread owns 4-token groups (one
 // Philox call each), reads the group's logits with one 16-byte (fp32) or 8-byte
 // (bf16) load, and keeps its best (score, index); warp then CTA reduction.
-// ALU-bound: ~70 instructions per token (10 Philox rounds per 4 tokens, two
-// logarithms with a division each) against 4 or 2 bytes of logits.
+// ALU-bound: 10 Philox rounds per 4 tokens, and two logarithms with a division
+// each for every token that can still win -- the rest are pruned exactly
+// against the row's best score so far (below), which the threads share.
 #include "params.cuh"
 
 namespace as {
@@ -97,12 +98,29 @@ __device__ __forceinline__ void load4<__nv_bfloat16>(const __nv_bfloat16* r, int
     }
 }
 
+// Exact pruning: a token whose score cannot reach the row's best score so far
+// need not have its logarithms evaluated.  For draws in the tier v = x >> 9 <
+// kTierV (u <= 1 - 2^-10), g <= g_tier = g(top of the tier) + 1e-3 (the margin
+// covers R23's last-ulp non-monotonicity); fl32 addition is monotone, so
+// score = fl(s + g) <= fl(s + g_tier), and fl(s + g_tier) < B (a score some
+// token of this row already achieved) proves the token is not the argmax.
+constexpr uint32_t kTierV = (1u << 23) - (1u << 13);
+
+__device__ __forceinline__ int ord_of(float f) {  // order-preserving float -> int
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float float_of_ord(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+
 template <typename T>
-__global__ void __launch_bounds__(512) sample_rows_kernel(const T* __restrict__ logits, int n_rows, int vocab,
+__global__ void __launch_bounds__(512, 3) sample_rows_kernel(const T* __restrict__ logits, int n_rows, int vocab,
                                                           float inv_t, uint32_t k0, uint32_t k1, uint32_t o0,
                                                           uint32_t o1, int32_t* __restrict__ out, void* ws) {
     __shared__ float sv[16];
     __shared__ int si[16];
+    __shared__ int s_best;  // ord_of(best score seen by any thread of this row)
+    if (threadIdx.x == 0) s_best = ord_of(-INFINITY);
+    __syncthreads();
     pdl_launch_dependents();
     pdl_wait();
     const int row = blockIdx.x;
@@ -112,19 +130,28 @@ __global__ void __launch_bounds__(512) sample_rows_kernel(const T* __restrict__ 
     float bv = -INFINITY;
     int bi = 0x7fffffff;
     bool nan = false;
+    const float g_tier = __fadd_rn(gumbel_r23((kTierV - 1u) << 9 | 0x1FFu), 1e-3f);
     const int nblk = (vocab + 3) / 4;
+    int published = ord_of(-INFINITY);
     for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
         const int t0 = 4 * b;
         float x[4];
         load4<T>(r, t0, vocab, vec, x);
         uint32_t c[4] = {(uint32_t)b, (uint32_t)row, o0, o1};
         philox4x32_10(c, k0, k1);
+        const float B = fmaxf(bv, float_of_ord(*reinterpret_cast<volatile int*>(&s_best)));
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (t0 + j >= vocab) break;
             nan |= (x[j] != x[j]);
-            const float sc = __fadd_rn(__fmul_rn(x[j], inv_t), gumbel_r23(c[j]));
+            const float sj = __fmul_rn(x[j], inv_t);
+            if ((c[j] >> 9) < kTierV && __fadd_rn(sj, g_tier) < B) continue;  // provably below the best
+            const float sc = __fadd_rn(sj, gumbel_r23(c[j]));
             better_s(bv, bi, sc, t0 + j);
+        }
+        if (ord_of(bv) > published) {  // share the bound with the row's other threads
+            published = ord_of(bv);
+            atomicMax(&s_best, published);
         }
     }
     if (nan) set_dev_error(ws, AS_DEV_NAN_LOGIT, row);
