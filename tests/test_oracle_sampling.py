@@ -72,3 +72,29 @@ def test_ties_lowest_index_and_rows_independent():
     b = S.sample_rows(lg[:50], 1.0, seed=9, offset=1)
     np.testing.assert_array_equal(a, tok[:50])
     assert (a != b).any()
+
+
+def test_stochastic_walk_matches_theorem1():
+    """Thm. 1 for the sampler + walk pair: with per-node target
+    samples from sample_rows and f(v) the product of target conditionals of the
+    tokens on v's path, E[accept_len] = sum_v f(v).  Monte Carlo over 40 000
+    independent trials (different rows of the Philox stream) of one tree."""
+    import oracle
+    rng = np.random.default_rng(21)
+    V = 4
+    parent = np.array([0, 0, 0, 1, 1, 2, 3, 3, 5], np.int32)  # topological, root 0
+    token = np.array([0, 0, 1, 2, 3, 1, 0, 2, 3], np.int32)  # siblings distinct
+    K = len(parent)
+    logits = rng.normal(0.0, 1.2, (K, V)).astype(np.float32)
+    p = np.exp(logits.astype(np.float64))
+    p /= p.sum(axis=1, keepdims=True)
+    f = np.ones(K)
+    for c in range(1, K):
+        f[c] = f[parent[c]] * p[parent[c], token[c]]
+    trials = 40000
+    tgt = S.sample_rows(np.tile(logits, (trials, 1)), 1.0, seed=2024)
+    offs = np.arange(0, (trials + 1) * K, K, dtype=np.int32)
+    w = oracle.accept_walk(offs, np.tile(parent, trials), np.tile(token, trials), target_tokens=tgt, max_path=K + 1)
+    al = w["accept_len"].astype(np.float64)
+    se = al.std() / np.sqrt(trials)
+    assert abs(al.mean() - f.sum()) < 4 * se, (al.mean(), f.sum(), se)
