@@ -703,10 +703,10 @@ def measure_sampling(W, steps):
     gbs = nbytes / (us * 1e-6) / 1e9
     del logits
     # issue-bound: warp instructions per scored token from the ncu capture of the
-    # pruned kernel (profiles/r01/ncu_sample_c2_r01j.md: 354.2e6 / (2048 * 128256)
+    # pruned kernel (profiles/r01/ncu_sample_c2_r01j.md: 323.9e6 / (2048 * 128256)
     # on these c2 logits -- data-dependent); peak = 148 SMs x 4 schedulers x 1 warp
     # instruction per clock at the max SM clock
-    winst = 354209400 / (2048 * 128256)
+    winst = 323894291 / (2048 * 128256)
     clk = float((_peaks()[0].get("sm_max_mhz") or 1965)) * 1e6
     issue_peak = 148 * 4 * clk
     achieved = toks / (us * 1e-6) * winst

@@ -18,18 +18,23 @@
 
 namespace as {
 
-__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+// The ten round keys (k0 + r*W0, k1 + r*W1) are computed on the host and passed
+// as kernel parameters: the XORs read them from the constant bank, no key
+// schedule arithmetic in the per-token loop.
+struct PhiloxKeys {
+    uint32_t k[20];
+};
+
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], const PhiloxKeys& ks) {
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
         const uint32_t lo0 = 0xD2511F53u * c[0], hi0 = __umulhi(0xD2511F53u, c[0]);
         const uint32_t lo1 = 0xCD9E8D57u * c[2], hi1 = __umulhi(0xCD9E8D57u, c[2]);
-        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        const uint32_t n0 = hi1 ^ c[1] ^ ks.k[2 * r], n2 = hi0 ^ c[3] ^ ks.k[2 * r + 1];
         c[0] = n0;
         c[1] = lo1;
         c[2] = n2;
         c[3] = lo0;
-        k0 += 0x9E3779B9u;
-        k1 += 0xBB67AE85u;
     }
 }
 
@@ -114,7 +119,7 @@ __device__ __forceinline__ float float_of_ord(int i) { return __int_as_float(i >
 
 template <typename T>
 __global__ void __launch_bounds__(512, 3) sample_rows_kernel(const T* __restrict__ logits, int n_rows, int vocab,
-                                                          float inv_t, uint32_t k0, uint32_t k1, uint32_t o0,
+                                                          float inv_t, const PhiloxKeys ks, uint32_t o0,
                                                           uint32_t o1, int32_t* __restrict__ out, void* ws) {
     __shared__ float sv[16];
     __shared__ int si[16];
@@ -138,7 +143,7 @@ __global__ void __launch_bounds__(512, 3) sample_rows_kernel(const T* __restrict
         float x[4];
         load4<T>(r, t0, vocab, vec, x);
         uint32_t c[4] = {(uint32_t)b, (uint32_t)row, o0, o1};
-        philox4x32_10(c, k0, k1);
+        philox4x32_10(c, ks);
         const float B = fmaxf(bv, float_of_ord(*reinterpret_cast<volatile int*>(&s_best)));
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -182,15 +187,19 @@ int launch_sample(const void* logits, int logits_bf16, int n_rows, int vocab, fl
     cudaLaunchAttribute attr[1];
     cfg.attrs = attr;
     cfg.numAttrs = fill_launch_attrs(attr);
-    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    PhiloxKeys ks;
+    for (int r = 0; r < 10; ++r) {
+        ks.k[2 * r] = (uint32_t)seed + (uint32_t)r * 0x9E3779B9u;
+        ks.k[2 * r + 1] = (uint32_t)(seed >> 32) + (uint32_t)r * 0xBB67AE85u;
+    }
     const uint32_t o0 = (uint32_t)offset, o1 = (uint32_t)(offset >> 32);
     cudaError_t e;
     if (logits_bf16)
         e = cudaLaunchKernelEx(&cfg, sample_rows_kernel<__nv_bfloat16>, reinterpret_cast<const __nv_bfloat16*>(logits),
-                               n_rows, vocab, inv_t, k0, k1, o0, o1, out, ws);
+                               n_rows, vocab, inv_t, ks, o0, o1, out, ws);
     else
         e = cudaLaunchKernelEx(&cfg, sample_rows_kernel<float>, reinterpret_cast<const float*>(logits), n_rows, vocab,
-                               inv_t, k0, k1, o0, o1, out, ws);
+                               inv_t, ks, o0, o1, out, ws);
     if (e != cudaSuccess) return -1;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
