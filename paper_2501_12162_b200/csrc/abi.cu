@@ -166,8 +166,8 @@ size_t as_attn_workspace_size(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
                               int32_t head_dim, int32_t max_kv_len) {
     (void)dtype; (void)n_tree_rows; (void)max_kv_len;
     if (n_req < 0 || n_q_heads < 0 || head_dim <= 0) return 0;
-    // header + debug trace + stream-K counters (one per unit: n_units = n_q * n_req
-    // for every GQA ratio) + 2 partial-state slots per SM
+    // header + debug trace + split-KV counters (two per unit: n_units = n_q * n_req
+    // for every GQA ratio) + 2 partial-state slots per resident CTA
     const size_t units = (size_t)n_q_heads * (size_t)n_req;
     const size_t slot = ((size_t)128 * head_dim + 256) * 4;
     return kWsHeaderBytes + kAttnTraceBytes + align_up(2 * units * 4, 256) +
@@ -271,7 +271,7 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
         const size_t need = kWsHeaderBytes + kAttnTraceBytes + cnt_bytes + 2 * (size_t)nsm * tc_ctas_per_sm() * slot;
         unsigned char* base = reinterpret_cast<unsigned char*>(workspace) + kWsHeaderBytes + kAttnTraceBytes;
         const char* skenv = getenv("AS_ATTN_STREAMK");  // A/B switch (debug)
-        // A/B: AS_ATTN_STREAMK=0 static only, =2 force stream-K
+        // A/B: AS_ATTN_STREAMK=0 whole units only (no split-KV)
         p.stream_k = (workspace_bytes >= need && !(skenv && atoi(skenv) == 0)) ? ((skenv && atoi(skenv) == 2) ? 2 : 1) : 0;
         p.cnt = reinterpret_cast<int*>(base);
         p.cnt2 = p.cnt + p.n_units;

@@ -8,7 +8,7 @@
 //
 // Structure: persistent, TWO 192-thread CTAs per SM (measured: one CTA's TMA
 // stream tops out near 4.7 TB/s chip-wide with 16 KB operations, two CTAs per
-// SM reach 6.5-6.9 TB/s -- DESIGN.md §5), stream-K tile schedule.
+// SM reach 6.5-6.9 TB/s -- DESIGN.md §5); static or split-KV schedule.
 //   warp 0      TMA producer: Q tile (4-D map, box 64 x G x 128/G x 2 chunks,
 //               SW128) and 64-key K/V tiles (5-D map over [page][head][row]
 //               [chunk][64] -> one 16 KB box per tile, coordinates from the
@@ -26,8 +26,8 @@
 //               (only when the running max grows by > 8, i.e. 256x) ->
 //               P (bf16 pairs) tcgen05.st to TMEM -> PV.  Epilogue:
 //               tcgen05.ld O, * 1/l, bf16 store, optional natural-log LSE; or,
-//               for a unit split across CTAs, the fp32 partial (O, m, l) and
-//               the stream-K fix-up by the CTA that completes the unit.
+//               for a unit split across CTAs (split-KV), the fp32 partial
+//               (O, m, l), then a share of the unit's cooperative merge.
 #include "params.cuh"
 #include "tc_ptx.cuh"
 
@@ -76,7 +76,7 @@ struct TcSmem {
     static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
     static constexpr int BYTES = OFF_TMEM + 16;
     static constexpr int ALLOC = BYTES + 1024;  // alignment slack
-    // stream-K plan scratch (long long per block) aliases the K+V rings before any TMA
+    // schedule-plan scratch (long long per request) aliases the K+V rings before any TMA
     static constexpr int PLAN_CAP = (KST + VST) * KV_BYTES / 8;
     static constexpr int PLAN_HALF = PLAN_CAP / 2;  // [0,half) tile prefix, [half, cap) unit prefix
 };
@@ -136,23 +136,22 @@ __device__ __forceinline__ void make_unit(const TcParams& p, const Req& r, int i
 // read that head's KV from L2 the second time.  A "piece" is a contiguous tile
 // range [tb, te) of one unit.
 //  static mode: non-empty unit k goes to CTA k mod G (whole units);
-//  stream-K mode: the units' tiles are concatenated and CTA b processes global
-//   tiles [T*b/G, T*(b+1)/G); a unit cut between CTAs is finished by the last
-//   CTA to complete a piece of it (partial (O, m, l) merged in fp32 through
-//   the workspace).  Chosen per launch by a makespan model (prologue).
+//  split-KV mode (units <= CTAs / 2): unit k's tiles are cut into S pieces,
+//   piece s on CTA k*S + s; the co-resident pieces publish fp32 (O, m, l),
+//   wait for each other and each merges 1/S of the columns.
 // ---------------------------------------------------------------------------
 struct Piece {
     Unit u;
     int w;         // unit id (i, g, mt) -> counter index
     int tb, te;    // tile range of this piece
-    long long x;   // global tile index of (u, tb) in stream-K mode
+    long long x;   // split-KV: piece index within the unit (else -1)
 };
 
 // A piece precomputed in the prologue (shared memory): no global load and no
 // request walk at a unit boundary.
 struct PieceRec {
     int i, j, tb, te;  // request, unit within request (g*MT + mt), tile range
-    int off, K, L, x;  // request geometry, global tile index of (unit, tb) (stream-K)
+    int off, K, L, x;  // request geometry, split-KV piece index (-1: whole unit)
 };
 
 // The roles (producer, MMA, softmax) only replay the CTA's records.

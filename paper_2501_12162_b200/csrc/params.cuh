@@ -64,7 +64,7 @@ struct TcParams {
     int n_units;
     int nq;               // q-tiles per unit / CTA shape (1 or 2, chosen by the host)
     int mt_max;           // q-tiles per (request, kv head) upper bound (unit id stride)
-    int stream_k;         // 1: stream-K tile ranges (needs cnt/partial), 0: static whole units
+    int stream_k;         // 1: split-KV allowed (needs cnt/cnt2/partial in the workspace), 0: whole units only
     int* cnt;             // [n_units] tiles completed per split unit (zeroed, self-resetting)
     int* cnt2;            // [n_units] pieces that finished merging (zeroed, self-resetting)
     float* partial;       // [2 * gridDim.x][slot_floats] partial (O, m, l) of split units
