@@ -568,7 +568,7 @@ def main():
                              "note": "separate instrumented replay (events around every call)"},
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_ctx is not None:
         torch.distributed.destroy_process_group()
 
 
