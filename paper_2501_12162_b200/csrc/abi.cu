@@ -280,8 +280,6 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     }
     const char* dbg = getenv("AS_ATTN_DEBUG_MODE");  // timing experiments only (wrong outputs)
     p.debug_mode = dbg ? atoi(dbg) : 0;
-    const char* pf = getenv("AS_ATTN_PREFETCH");  // tuning override of the L2 prefetch distance
-    p.prefetch_tiles = pf ? atoi(pf) : 0;
     const char* ef = getenv("AS_ATTN_EVICT_FIRST");  // A/B: L2 evict-first hint on KV loads
     p.evict_first = ef ? atoi(ef) : 1;
     const char* kl = getenv("AS_ATTN_KLEAD");  // tuning: K stream lead over V (tiles)

@@ -69,7 +69,6 @@ struct TcParams {
     int* cnt2;            // [n_units] pieces that finished merging (zeroed, self-resetting)
     float* partial;       // [2 * gridDim.x][slot_floats] partial (O, m, l) of split units
     int slot_floats;      // 128 * D + 256
-    int prefetch_tiles;
     int evict_first;
     int k_lead;           // tiles by which the K stream leads the V stream in the producer      // L2 evict-first policy on the KV tile loads  // L2 prefetch distance of the TMA producers (tiles)
     int debug_mode;  // 0 = normal; 1 = skip softmax math; 2 = also skip MMAs (timing experiments only)
