@@ -122,7 +122,8 @@ def make_workload(cfg_name, device="cuda", seed_salt=0, rank=0, world=1, engine=
     W["k_tree"] = rnd(R, n_kv, D)
     W["v_tree"] = rnd(R, n_kv, D)
     W["out"] = torch.empty_like(W["q"])
-    W["sample_requests"] = sorted(set([0, n // 3, n - 1]))
+    # parity sample of the full-size test: 16 requests spread over the batch
+    W["sample_requests"] = sorted(set(np.linspace(0, n - 1, min(n, 16)).round().astype(int).tolist()))
     W["max_path"] = c["d"] + 1
     if engine == "oracle":
         import oracle  # reference arm only
@@ -192,15 +193,14 @@ def run_accept(W, phase=None, req_range=None):
                       bonus_token=W["acc"]["bonus_token"], n_tree_rows=W["R"], workspace=W["ws_accept"])
 
 
-def run_accept_records(W, phase, records, req_range=None):
-    """Multi-GPU form: walk / commit through the contiguous record rows."""
-    ada = W["ada"]
+def run_accept_dist(W, sharded):
+    """N>1: the library's multi-GPU acceptance (paper_2501_12162_b200.dist):
+    WALK_RECORDS on this rank's request shard -> in-place NCCL all-gather ->
+    COMMIT_RECORDS for this rank's kv heads."""
     kc, vc = W["pools"][W["pool_idx"]]
-    ada.accept_tokens(phase, W["sel"]["tree_offsets"], W["sel"]["tree_parent"], W["sel"]["tree_token"],
-                      target_tokens=W["target_tokens"], max_path=W["max_path"], k_tree=W["k_tree"],
-                      v_tree=W["v_tree"], k_cache=kc, v_cache=vc, page_table=W["page_table"], kv_len=W["kv_len"],
-                      kv_len_out=W["kv_len_out"], req_range=req_range, accept_path=records, n_tree_rows=W["R"],
-                      workspace=W["ws_accept"])
+    sharded(W["sel"]["tree_offsets"], W["sel"]["tree_parent"], W["sel"]["tree_token"], W["k_tree"], W["v_tree"],
+            kc, vc, W["page_table"], W["kv_len"], max_path=W["max_path"], target_tokens=W["target_tokens"],
+            kv_len_out=W["kv_len_out"], n_tree_rows=W["R"], workspace=W["ws_accept"])
 
 
 def attn_algorithmic_bytes(W):
@@ -285,7 +285,7 @@ class Step:
         elif self.dist is None:
             run_accept(W)
         else:
-            self.dist.accept_and_commit(W)
+            run_accept_dist(W, self.dist)
         if eb:
             _record(eb[3], external)
         return events
@@ -425,7 +425,7 @@ def main():
             os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         from paper_2501_12162_b200.dist import ShardedAccept
-        dist_ctx = ShardedAccept(rank, world)
+        dist_ctx = ShardedAccept()  # default process group
     emu = int(os.environ.get("AS_BENCH_EMULATE_WORLD", "0"))  # analysis only: one rank's shard of an N-GPU run
     W = make_workload(args.config, "cuda", rank=rank, world=emu if (emu > 1 and world == 1) else world)
     step = Step(W, dist_ctx)

@@ -298,15 +298,6 @@ as_status as_reset_workspace(void* workspace, size_t workspace_bytes, void* stre
 as_status as_selftest_umma(const void* a, const void* b, float* d, int32_t n, int32_t k,
                            int32_t b_mn_major, void* stream);
 
-/* Debug / tuning only: every CTA of `grid` streams chunks (chunk_bytes each, in
- * the order given by `order` [n_chunks] chunk indices) of the device buffer
- * `src` through a shared-memory ring of `stages` slots.  mode 0: one thread
- * issues bulk copies (TMA engine); 1: two issuing threads; 2: 16-byte vector
- * loads by 256 threads.  `sink` [grid] receives a dummy value.  Time it with
- * events to measure achievable HBM streaming bandwidth. */
-as_status as_debug_stream_bw(const void* src, const int32_t* order, int32_t n_chunks, int32_t chunk_bytes,
-                             int32_t stages, int32_t mode, unsigned long long* sink, int32_t grid, void* stream);
-
 #ifdef __cplusplus
 }
 #endif

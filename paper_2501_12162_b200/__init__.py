@@ -19,7 +19,9 @@ __all__ = ["lib", "select_trees", "select_global_greedy", "sample_tokens", "tree
            "select_workspace_size", "attn_workspace_size", "accept_workspace_size", "DEVICE_ERRORS"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libadaserve.so")
+# AS_DEBUG_LIB=1 loads the debug build (experiment switches + tuning instruments,
+# include/adaserve_debug.h) -- tuning scripts only; the product path never sets it
+LIB_PATH = os.path.join(_PKG, "libadaserve_debug.so" if os.environ.get("AS_DEBUG_LIB") == "1" else "libadaserve.so")
 
 AS_F32, AS_BF16 = 0, 1
 AS_ACCEPT_FUSED, AS_ACCEPT_WALK_ONLY, AS_ACCEPT_COMMIT_ONLY = 0, 1, 2

@@ -8,6 +8,9 @@
 #include <mutex>
 
 #include "params.cuh"
+#ifdef AS_DEBUG
+#include "../../include/adaserve_debug.h"
+#endif
 
 
 using namespace as;
@@ -278,21 +281,26 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
         p.partial = reinterpret_cast<float*>(base + cnt_bytes);
         p.slot_floats = 128 * head_dim + 256;
     }
-    const char* dbg = getenv("AS_ATTN_DEBUG_MODE");  // timing experiments only (wrong outputs)
-    p.debug_mode = dbg ? atoi(dbg) : 0;
-    const char* ef = getenv("AS_ATTN_EVICT_FIRST");  // A/B: L2 evict-first hint on KV loads
-    p.evict_first = ef ? atoi(ef) : 1;
-    const char* kl = getenv("AS_ATTN_KLEAD");  // tuning: K stream lead over V (tiles)
-    p.k_lead = kl ? atoi(kl) : 1;
-    if (p.k_lead < 0) p.k_lead = 0;
-    if (p.k_lead > kMaxKLead) p.k_lead = kMaxKLead;
-    const char* tr = getenv("AS_ATTN_TRACE");  // CTA-0 pipeline timestamps into the workspace (debug)
+    p.req_base = 0;
+    p.debug_mode = 0;
+    p.evict_first = 1;
+    p.k_lead = 1;
     p.trace = nullptr;
     p.trace_cap = 0;
+#ifdef AS_DEBUG
+    // Experiment switches, compiled only into the debug build (AS_DEBUG=1 build.py):
+    // the product library reads no environment variable on this path.
+    if (const char* dbg = getenv("AS_ATTN_DEBUG_MODE")) p.debug_mode = atoi(dbg);  // timing only (wrong outputs)
+    if (const char* ef = getenv("AS_ATTN_EVICT_FIRST")) p.evict_first = atoi(ef);  // L2 evict-first hint A/B
+    if (const char* kl = getenv("AS_ATTN_KLEAD")) p.k_lead = atoi(kl);             // K stream lead over V
+    if (p.k_lead < 0) p.k_lead = 0;
+    if (p.k_lead > kMaxKLead) p.k_lead = kMaxKLead;
+    const char* tr = getenv("AS_ATTN_TRACE");  // CTA-0 pipeline timestamps into the workspace
     if (tr && atoi(tr) && workspace_bytes >= kWsHeaderBytes + kAttnTraceBytes) {
         p.trace = reinterpret_cast<unsigned long long*>(reinterpret_cast<unsigned char*>(workspace) + kWsHeaderBytes);
         p.trace_cap = (int)(kAttnTraceBytes / 64) - 512;  // last 512 records: per-CTA timeline
     }
+#endif
     return launch_attn_tc(maps, p, head_dim, sm_count(), S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
 }
 
@@ -353,6 +361,7 @@ as_status as_accept_tokens(as_accept_phase phase, int32_t n_req, int32_t req_beg
                                                                                                       : AS_ERR_CUDA;
 }
 
+#ifdef AS_DEBUG
 // ----------------------------------------------------------------- debug
 as_status as_debug_stream_bw(const void* src, const int32_t* order, int32_t n_chunks, int32_t chunk_bytes,
                              int32_t stages, int32_t mode, unsigned long long* sink, int32_t grid, void* stream) {
@@ -372,6 +381,8 @@ as_status as_debug_stream_bw(const void* src, const int32_t* order, int32_t n_ch
                ? AS_OK
                : AS_ERR_CUDA;
 }
+
+#endif  // AS_DEBUG
 
 // ----------------------------------------------------------------- selftest
 as_status as_selftest_umma(const void* a, const void* b, float* d, int32_t n, int32_t k, int32_t b_mn_major,

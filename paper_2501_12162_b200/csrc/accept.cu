@@ -34,11 +34,16 @@ __device__ __forceinline__ void better(float& bv, int& bi, float v, int i) {
 template <typename T>
 __global__ void __launch_bounds__(512) argmax_rows_kernel(const T* __restrict__ logits, int vocab,
                                                           const int32_t* tree_offsets, int req_begin,
-                                                          int req_end, int32_t* __restrict__ out, void* ws) {
+                                                          int req_end, int n_tree_rows, int32_t* __restrict__ out,
+                                                          void* ws) {
     const int row_lo = tree_offsets[req_begin];
-    const int row_hi = tree_offsets[req_end];
+    int row_hi = tree_offsets[req_end];
+    if (row_lo < 0 || row_hi > n_tree_rows) {  // rows past the logits tensor / the argmax buffer: flag, clamp
+        if (blockIdx.x == 0 && threadIdx.x == 0) set_dev_error(ws, AS_DEV_ROWS_OVERFLOW, req_end - 1);
+        row_hi = min(row_hi, n_tree_rows);
+    }
     const int row = row_lo + blockIdx.x;
-    if (row >= row_hi) return;
+    if (row_lo < 0 || row >= row_hi) return;
     const T* r = logits + (size_t)row * vocab;
     float bv = -INFINITY;
     int bi = 0x7fffffff;
@@ -344,11 +349,11 @@ int launch_accept(const AcceptParams& p, const void* target_logits, int logits_b
             if (logits_bf16)
                 argmax_rows_kernel<__nv_bfloat16><<<rows, 512, 0, stream>>>(
                     reinterpret_cast<const __nv_bfloat16*>(target_logits), vocab, q.tree_offsets, q.req_begin,
-                    q.req_end, argmax_buf, q.ws);
+                    q.req_end, rows, argmax_buf, q.ws);
             else
                 argmax_rows_kernel<float><<<rows, 512, 0, stream>>>(reinterpret_cast<const float*>(target_logits),
                                                                    vocab, q.tree_offsets, q.req_begin, q.req_end,
-                                                                   argmax_buf, q.ws);
+                                                                   rows, argmax_buf, q.ws);
             if (cudaGetLastError() != cudaSuccess) return -1;
         }
         q.target_tokens = argmax_buf;

@@ -61,7 +61,13 @@ __global__ void __launch_bounds__(256) tree_attn_simt_kernel(SimtParams p) {
         if (threadIdx.x == 0 && rb == 0 && g == 0) set_dev_error(p.ws, AS_DEV_ROWS_OVERFLOW, i);
         return;
     }
-    const int L = p.kv_len[i];
+    // kv_len outside [0, max_pages * page_size] would read another request's
+    // page-table row (or past the table): flag it and clamp, as the tcgen05 path does
+    int L = p.kv_len[i];
+    if (L < 0 || L > p.max_pages * p.page_size) {
+        if (threadIdx.x == 0 && rb == 0 && g == 0) set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, i);
+        L = min(max(L, 0), p.max_pages * p.page_size);
+    }
     const int lane = lane_id();
     const int warp = warp_id();
 

@@ -334,8 +334,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             Req r;
             load_req(p, i, r);
-            if (r.MT == 0 && r.K > AS_MAX_TREE) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, i);
-            if (r.MT > 0 && __ldg(p.kv_len + i) > p.max_pages * p.page_size) set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, i);
+            // device errors carry the caller's request index (chunked launches add req_base)
+            if (r.MT == 0 && r.K > AS_MAX_TREE) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, p.req_base + i);
+            else if (r.MT == 0 && r.K > 0) set_dev_error(p.ws, AS_DEV_ROWS_OVERFLOW, p.req_base + i);
+            if (r.MT > 0 && __ldg(p.kv_len + i) > p.max_pages * p.page_size)
+                set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, p.req_base + i);
             my_units += p.n_kv * r.MT;
             if (r.MT > 0) {
                 my_maxnt = max(my_maxnt, r.nt);
@@ -531,7 +534,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                             const int page = pt_s[kp / p.page_size - chunk0];
                             const int slot = kp % p.page_size;
                             // out-of-range pages read as zeros (TMA bounds check); flag them
-                            if (is_k && (page < 0 || page >= p.num_pages)) set_dev_error(p.ws, AS_DEV_BAD_PAGE, u.i);
+                            if (is_k && (page < 0 || page >= p.num_pages)) set_dev_error(p.ws, AS_DEV_BAD_PAGE, p.req_base + u.i);
                             if (p.kv_split_d) {
                                 ptx::tma_load_5d_hint(dst, tm_c, full, 0, slot, 0, u.g, page, pol);
                             } else {
@@ -618,11 +621,14 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     ++v_it;
                     return;
                 }
-                // zero V rows past the prefix end (stale/uninitialised smem or cache
-                // slots >= L may hold NaN; P is 0 there but 0 * NaN = NaN); with two
-                // MMA warps both write the same zeros (benign)
-                if (t < u.n_prefix) {
-                    const int valid = min(kBN, u.L - t * kBN);
+                // zero V rows past the prefix end, and in a tree tile the rows past
+                // the request's last node (cache slots >= L, the next request's tree
+                // rows or the caller's padding rows may hold NaN; P is 0 there but
+                // 0 * NaN = NaN: verification must not depend on them);
+                // with two MMA warps both write the same zeros (benign)
+                {
+                    const int valid = t < u.n_prefix ? min(kBN, u.L - t * kBN)
+                                                     : min(kBN, u.K - (t - u.n_prefix) * kBN);
                     if (valid < kBN) {
                         unsigned char* vs = smem + S::OFF_V + st * S::KV_BYTES;
                         const int nvec = (kBN - valid) * 8;  // 16-byte vectors per chunk
@@ -711,7 +717,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     if (v == 0) break;
                     const int pv = tp_s[v];
                     if (pv < 0 || pv >= v || ++steps > u.K) {
-                        set_dev_error(p.ws, AS_DEV_BAD_PARENT, u.i);
+                        set_dev_error(p.ws, AS_DEV_BAD_PARENT, p.req_base + u.i);
                         break;
                     }
                     v = pv;
@@ -971,7 +977,11 @@ int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, in
     const int nq = p0.nq == 2 ? 2 : 1;
     const int grid_full = n_sms * (nq == 2 ? TcCfg<2>::CTAS : TcCfg<1>::CTAS);
     const int units_per_req = p0.n_kv * ((p0.mt_max + nq - 1) / nq);
-    const int chunk = units_per_req > 0 ? max(1, kMaxRec * grid_full / units_per_req) : p0.n_req;
+    int chunk = units_per_req > 0 ? max(1, kMaxRec * grid_full / units_per_req) : p0.n_req;
+    // the prologue's schedule plan holds at most PLAN_HALF requests (per-request prefix sums)
+    const int plan_half = head_dim == 128 ? (nq == 2 ? TcSmem<128, 2>::PLAN_HALF : TcSmem<128, 1>::PLAN_HALF)
+                                          : (nq == 2 ? TcSmem<64, 2>::PLAN_HALF : TcSmem<64, 1>::PLAN_HALF);
+    chunk = min(chunk, plan_half);
     for (int r0 = 0; r0 < p0.n_req; r0 += chunk) {
         TcParams p = p0;
         p.nq = nq;
@@ -979,6 +989,7 @@ int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, in
         p.page_table = p0.page_table + (size_t)r0 * p0.max_pages;
         p.kv_len = p0.kv_len + r0;
         p.tree_offsets = p0.tree_offsets + r0;
+        p.req_base = p0.req_base + r0;
         p.n_units = units_per_req * p.n_req;
         int grid = grid_full;
         if (!p.stream_k && p.n_units < grid) grid = p.n_units;

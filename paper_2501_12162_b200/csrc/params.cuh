@@ -62,6 +62,7 @@ struct TcParams {
     float* lse;
     void* ws;
     int n_units;
+    int req_base;         // caller's index of request 0 of this launch (device-error reports)
     int nq;               // q-tiles per unit / CTA shape (1 or 2, chosen by the host)
     int mt_max;           // q-tiles per (request, kv head) upper bound (unit id stride)
     int stream_k;         // 1: split-KV allowed (needs cnt/cnt2/partial in the workspace), 0: whole units only
@@ -70,7 +71,7 @@ struct TcParams {
     float* partial;       // [2 * gridDim.x][slot_floats] partial (O, m, l) of split units
     int slot_floats;      // 128 * D + 256
     int evict_first;
-    int k_lead;           // tiles by which the K stream leads the V stream in the producer      // L2 evict-first policy on the KV tile loads  // L2 prefetch distance of the TMA producers (tiles)
+    int k_lead;           // tiles by which the K stream leads the V stream in the producer
     int debug_mode;  // 0 = normal; 1 = skip softmax math; 2 = also skip MMAs (timing experiments only)
     unsigned long long* trace;  // CTA-0 pipeline timestamps [trace_cap][8] (clock64) or NULL
     int trace_cap;
@@ -89,8 +90,10 @@ int tc_ctas_per_sm();
 size_t beam_ws_bytes(int n_req, int width, int vocab);
 int launch_beam(int n_req, int layer, int width, int vocab, const float* probs, int stride, int32_t* cand_parent,
                 float* cand_prob, int32_t* cand_token, void* ws, cudaStream_t stream);
+#ifdef AS_DEBUG
 int launch_stream_bw(const void* src, const int* order, int n_chunks, int chunk_bytes, int stages, int mode,
                      unsigned long long* sink, int grid, const CUtensorMap* tmap, cudaStream_t stream);
+#endif
 int launch_umma_selftest(const CUtensorMap* ma, const CUtensorMap* mb, float* d, int N, int K, int b_mn,
                          const void* a_g, int a_tmem, cudaStream_t stream);
 

@@ -39,6 +39,7 @@
 // workspace instead (same code path, generic pointers).
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -827,14 +828,21 @@ int launch_select(int n_req, int n_cand_total, const int32_t* cand_offsets, cons
     p.slo_count = slo_count;
     p.ws = ws;
     p.skey_g = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(ws) + kWsHeaderBytes);
-    static bool attrs_set = false;
-    if (!attrs_set) {
-        if (cudaFuncSetAttribute(select_trees_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSelSmemLimit + 16 * 1024) != cudaSuccess ||
-            cudaFuncSetAttribute(select_trees_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-                cudaSuccess)
-            return -1;
-        attrs_set = true;
+    // kernel attributes are per device: set once per device, under a mutex (re-entrant ABI)
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return -1;
+        static std::mutex mu;
+        static bool attrs_set[64] = {false};
+        std::lock_guard<std::mutex> lk(mu);
+        if (!attrs_set[dev]) {
+            if (cudaFuncSetAttribute(select_trees_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kSelSmemLimit + 16 * 1024) != cudaSuccess ||
+                cudaFuncSetAttribute(select_trees_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                    cudaSuccess)
+                return -1;
+            attrs_set[dev] = true;
+        }
     }
     int cs = cluster_size_for(n_req);
     for (;;) {
@@ -845,10 +853,14 @@ int launch_select(int n_req, int n_cand_total, const int32_t* cand_offsets, cons
         cs = fit;
     }
     const size_t smem = SelLayout(n_req, p.rpc, p.cand_cap).bytes;
-    static const int dbg_stop = [] {
+#ifdef AS_DEBUG
+    static const int dbg_stop = [] {  // phase-latency experiments only (early exit, wrong outputs)
         const char* e = getenv("AS_SEL_STOP");
         return e ? atoi(e) : 99;
     }();
+#else
+    constexpr int dbg_stop = 99;
+#endif
     p.dbg_stop = dbg_stop;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);

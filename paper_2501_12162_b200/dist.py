@@ -1,5 +1,5 @@
 """Multi-GPU glue: KV-head sharding of verification attention and the single
-NCCL exchange of the hot path (BASELINE north_star, DESIGN.md §Multi-GPU).
+NCCL exchange of the hot path (BASELINE north_star, SURVEY §8(e), DESIGN.md §7).
 
 * select is replicated (deterministic, bit-exact on every rank, no traffic);
 * attention is sharded by KV head: rank p owns kv heads
@@ -13,8 +13,12 @@ NCCL exchange of the hot path (BASELINE north_star).
   the records (AS_ACCEPT_COMMIT_RECORDS): 2 kernels + 1 collective, no packing.
 Nothing else crosses NVLink: no KV, no activations, no logits.
 
-The packing helpers are plain torch ops (device-agnostic) so the protocol is
-tested with the gloo backend on CPU (tests/test_dist_gloo.py).
+`accept_and_commit(pg, ...)` is the library call (SURVEY §8(b) "Python
+surface"); `ShardedAccept` keeps the record buffer static across calls (CUDA
+graph capture) and re-sizes it whenever the request shard size changes.  The
+record kernels are reached through `accept_fn` (default: the library's
+`accept_tokens`), so the host protocol runs unchanged under gloo on CPU with a
+stand-in (tests/test_dist_gloo.py).
 """
 from __future__ import annotations
 
@@ -31,7 +35,7 @@ def head_range(n_kv: int, rank: int, world: int):
 
 
 def request_range(n: int, rank: int, world: int):
-    """Requests walked by `rank`: [b, e) with shard size ceil(n/world)."""
+    """Requests walked by `rank`: [b, e) with shard size s = ceil(n/world)."""
     s = (n + world - 1) // world
     b = min(n, rank * s)
     return b, min(n, b + s), s
@@ -68,29 +72,79 @@ def record_shard(records, rank, s):
     return records[rank * s:(rank + 1) * s]
 
 
-def all_gather_in_place(records, rank, world, group=None):
-    """Fill every rank's rows of `records` from the owner rank (in place)."""
-    s = records.shape[0] // world
-    dist.all_gather_into_tensor(records, record_shard(records, rank, s), group=group)
+def all_gather_in_place(records, rank, world, group=None, s=None):
+    """Fill every rank's rows of `records` from the owner rank (in place).  The
+    shard size `s` defaults to the buffer's rows / world; pass it explicitly
+    when the buffer may be larger than world * ceil(n / world)."""
+    if s is None:
+        s = records.shape[0] // world
+    view = records[:world * s]
+    dist.all_gather_into_tensor(view, record_shard(records, rank, s), group=group)
+    return records
+
+
+def record_buffer(n: int, world: int, max_path: int, device) -> torch.Tensor:
+    """The [world * ceil(n/world), 2 + max_path] int32 record buffer of one step."""
+    s = (n + world - 1) // world
+    return torch.zeros((max(world * s, 1), 2 + max_path), dtype=torch.int32, device=device)
+
+
+def accept_and_commit(pg, tree_offsets, tree_parent, tree_tokens, k_tree, v_tree, k_cache, v_cache, page_table,
+                      kv_len, *, max_path, target_tokens=None, target_logits=None, kv_len_out=None, records=None,
+                      n_tree_rows=None, workspace=None, accept_fn=None):
+    """One multi-GPU acceptance step: this rank walks its
+    request shard into its rows of `records` (WALK_RECORDS), one in-place
+    all_gather_into_tensor on `pg` completes the records on every rank, and
+    every rank commits every request's accepted path into ITS kv-head shard of
+    the paged cache (COMMIT_RECORDS; `k_tree/v_tree/k_cache/v_cache` are this
+    rank's head slices; kv_len += accept_len, out of place into kv_len_out when
+    given).  Returns the [world*s, 2 + max_path] records {len, bonus, path}.
+
+    `records` (optional) must have exactly world * ceil(n / world) rows (a
+    static buffer for graph capture; see ShardedAccept).  `accept_fn` defaults
+    to the library's accept_tokens (the CUDA record kernels)."""
+    if accept_fn is None:
+        from . import accept_tokens as accept_fn
+        from . import AS_ACCEPT_COMMIT_RECORDS, AS_ACCEPT_WALK_RECORDS
+    else:
+        AS_ACCEPT_WALK_RECORDS, AS_ACCEPT_COMMIT_RECORDS = 3, 4
+    world = dist.get_world_size(pg)
+    rank = dist.get_rank(pg)
+    n = tree_offsets.numel() - 1
+    b, e, s = request_range(n, rank, world)
+    if records is None:
+        records = record_buffer(n, world, max_path, tree_offsets.device)
+    if records.shape != (max(world * s, 1), 2 + max_path) or records.dtype != torch.int32:
+        raise ValueError(f"records must be int32 [{world * s}, {2 + max_path}] for n={n}, world={world}; "
+                         f"got {tuple(records.shape)} {records.dtype}")
+    common = dict(max_path=max_path, k_tree=k_tree, v_tree=v_tree, k_cache=k_cache, v_cache=v_cache,
+                  page_table=page_table, kv_len=kv_len, kv_len_out=kv_len_out, accept_path=records,
+                  n_tree_rows=n_tree_rows, workspace=workspace)
+    accept_fn(AS_ACCEPT_WALK_RECORDS, tree_offsets, tree_parent, tree_tokens, target_tokens=target_tokens,
+              target_logits=target_logits, req_range=(b, e), **common)
+    if world > 1:
+        all_gather_in_place(records, rank, world, group=pg, s=s)
+    accept_fn(AS_ACCEPT_COMMIT_RECORDS, tree_offsets, tree_parent, tree_tokens, **common)
     return records
 
 
 class ShardedAccept:
-    """WALK_RECORDS on this rank's request shard -> in-place all-gather ->
-    COMMIT_RECORDS (every rank, its own kv heads)."""
+    """accept_and_commit with a static record buffer (captured into CUDA graphs),
+    re-allocated whenever ceil(n / world) or max_path changes."""
 
-    def __init__(self, rank: int, world: int, group=None):
-        self.rank, self.world, self.group = rank, world, group
+    def __init__(self, pg=None, accept_fn=None):
+        self.pg = pg
+        self.accept_fn = accept_fn
         self.records = None
 
-    def accept_and_commit(self, W):
-        import paper_2501_12162_b200 as ada
-        from bench import run_accept_records  # the bench's call wrapper (same arguments)
-        n = W["n"]
-        b, e, s = request_range(n, self.rank, self.world)
-        if self.records is None:
-            self.records = torch.zeros((self.world * s, 2 + W["max_path"]), dtype=torch.int32,
-                                       device=W["kv_len"].device)
-        run_accept_records(W, ada.AS_ACCEPT_WALK_RECORDS, self.records, req_range=(b, e))
-        all_gather_in_place(self.records, self.rank, self.world, self.group)
-        run_accept_records(W, ada.AS_ACCEPT_COMMIT_RECORDS, self.records)
+    def __call__(self, tree_offsets, tree_parent, tree_tokens, k_tree, v_tree, k_cache, v_cache, page_table, kv_len,
+                 *, max_path, **kw):
+        world = dist.get_world_size(self.pg)
+        n = tree_offsets.numel() - 1
+        s = (n + world - 1) // world
+        want = (max(world * s, 1), 2 + max_path)
+        if self.records is None or tuple(self.records.shape) != want:
+            self.records = record_buffer(n, world, max_path, tree_offsets.device)
+        return accept_and_commit(self.pg, tree_offsets, tree_parent, tree_tokens, k_tree, v_tree, k_cache, v_cache,
+                                 page_table, kv_len, max_path=max_path, records=self.records,
+                                 accept_fn=self.accept_fn, **kw)

@@ -109,13 +109,23 @@ class IterationGraph:
                           accept_len=O["accept_len"], accept_path=O["accept_path"], bonus_token=O["bonus_token"],
                           n_tree_rows=s.budget, workspace=self.ws["accept"])
 
+    def _reset_workspaces(self):
+        # the warm-up runs on whatever the static inputs hold (zeros before the
+        # caller fills them) and may leave sticky device-error words: clear them
+        # so as_check_device_error reports only what real iterations cause
+        for ws in self.ws.values():
+            ws.view.zero_()
+
     def capture(self):
         """Warm up eagerly (first-use attribute setup), then capture."""
         self._run()
         torch.cuda.synchronize()
+        self._reset_workspaces()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self._run()
+        torch.cuda.synchronize()
+        self._reset_workspaces()
         return self
 
     def replay(self):

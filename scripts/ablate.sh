@@ -1,6 +1,7 @@
 #!/bin/bash
 # Incremental in-step cost of each kernel: step time with one call skipped (ablation, debug only).
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
+export AS_DEBUG=1 AS_DEBUG_LIB=1  # debug build (experiment switches)
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 for C in ${CFGS:-c2}; do
   for SK in none select accept attention "select,accept"; do

@@ -1,6 +1,7 @@
 #!/bin/bash
 # A/B matrix for the bf16 attention kernel on one box (with a TMA streaming calibration).
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
+export AS_DEBUG=1 AS_DEBUG_LIB=1  # debug build (experiment switches)
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 python - <<'PY'
 import ctypes, torch, sys

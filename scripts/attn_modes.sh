@@ -1,6 +1,7 @@
 #!/bin/bash
 # Timing experiments for the bf16 attention kernel (debug modes produce wrong outputs).
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
+export AS_DEBUG=1 AS_DEBUG_LIB=1  # debug build (experiment switches)
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 one() {

@@ -10,6 +10,7 @@ Events per CTA-local tile (clock64 cycles):
 """
 import argparse
 import os
+os.environ.setdefault("AS_DEBUG_LIB", "1")  # debug build: experiment switches / instruments
 import sys
 
 import numpy as np

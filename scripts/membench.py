@@ -1,6 +1,7 @@
 """HBM streaming micro-benchmark (as_debug_stream_bw) -- sizing the attention load path."""
 import ctypes
 import os
+os.environ.setdefault("AS_DEBUG_LIB", "1")  # debug build: experiment switches / instruments
 import sys
 
 import torch

@@ -1,5 +1,6 @@
 """Per-SM TMA concurrency: 1 vs 2 vs 4 CTAs per SM (debug)."""
 import ctypes, os, sys
+os.environ.setdefault("AS_DEBUG_LIB", "1")  # debug build: experiment switches / instruments
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2501_12162_b200 as ada  # noqa: E402

@@ -1,5 +1,6 @@
 """TMA streaming rate vs CTAs/SM, ring depth and issuing threads (debug)."""
 import ctypes, os, sys
+os.environ.setdefault("AS_DEBUG_LIB", "1")  # debug build: experiment switches / instruments
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2501_12162_b200 as ada  # noqa: E402

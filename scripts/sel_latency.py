@@ -2,6 +2,7 @@
 back-to-back launches, for each AS_SEL_STOP value (the kernel returns after
 phase k; debug only).  Usage: python scripts/sel_latency.py c2"""
 import os
+os.environ.setdefault("AS_DEBUG_LIB", "1")  # debug build: experiment switches / instruments
 import subprocess
 import sys
 

@@ -12,8 +12,8 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from paper_2501_12162_b200.dist import (all_gather_in_place, all_gather_records, head_range, pack_records,
-                                        record_shard, request_range, unpack_records)
+from paper_2501_12162_b200.dist import (ShardedAccept, accept_and_commit, all_gather_in_place, all_gather_records,
+                                        head_range, pack_records, record_shard, request_range, unpack_records)
 
 
 def _free_port():
@@ -109,6 +109,98 @@ def _worker_records(rank, world, port, n, q):
     ok = ok and np.array_equal(kl_me, kl_all)
     q.put((rank, bool(ok)))
     dist.destroy_process_group()
+
+
+def _cpu_record_kernels(phase, tree_offsets, tree_parent=None, tree_tokens=None, target_tokens=None,
+                        target_logits=None, max_path=16, k_tree=None, v_tree=None, k_cache=None, v_cache=None,
+                        page_table=None, kv_len=None, kv_len_out=None, accept_path=None, req_range=None,
+                        n_tree_rows=None, workspace=None):
+    """CPU stand-in for the two record kernels of as_accept_tokens (test
+    infrastructure: the oracle's walk and commit, same arguments and record
+    layout as the library call), injected into dist.accept_and_commit."""
+    to = tree_offsets.numpy()
+    n = len(to) - 1
+    rec = accept_path
+    if phase == 3:  # AS_ACCEPT_WALK_RECORDS: rows [b, e) of this rank's requests
+        b, e = req_range
+        if e > b:
+            sub_to = (to[b:e + 1] - to[b]).astype(np.int32)
+            rows = slice(int(to[b]), int(to[e]))
+            r = oracle.accept_walk(sub_to, tree_parent.numpy()[rows], tree_tokens.numpy()[rows],
+                                   target_tokens=target_tokens.numpy()[rows], max_path=max_path)
+            rec[b:e, 0] = torch.from_numpy(r["accept_len"])
+            rec[b:e, 1] = torch.from_numpy(r["bonus_token"])
+            rec[b:e, 2:] = torch.from_numpy(r["accept_path"])
+    elif phase == 4:  # AS_ACCEPT_COMMIT_RECORDS: every request, this rank's heads
+        kc, vc, kl = k_cache.numpy(), v_cache.numpy(), kv_len.numpy().copy()
+        oracle.commit(to, rec[:n, 0].numpy().copy(), rec[:n, 2:].numpy().copy(), k_tree.numpy(), v_tree.numpy(),
+                      kc, vc, page_table.numpy(), kl)
+        (kv_len_out if kv_len_out is not None else kv_len).copy_(torch.from_numpy(kl))
+    else:
+        raise AssertionError(phase)
+
+
+def _worker_library(rank, world, port, q):
+    """dist.accept_and_commit / ShardedAccept -- the library's multi-GPU call --
+    over gloo with the CPU record kernels: two batches of different sizes
+    through one ShardedAccept (the record buffer is re-sized when ceil(n/world)
+    changes), each equal to the single-process walk + commit of this rank's heads."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sharded = ShardedAccept(accept_fn=_cpu_record_kernels)
+    ok = True
+    for n, seed in ((9, 21), (30, 22), (3, 23), (30, 24)):
+        to, par, toks, tgt = _walk_inputs(seed, n)
+        mpth = 20
+        rng = np.random.default_rng(seed)
+        R = int(to[-1])
+        n_kv, d, ps = 2 * world, 8, 4
+        kv_len = rng.integers(0, 9, n).astype(np.int32)
+        table, n_pages = synth.paged_kv(rng, kv_len, ps, extra_slots=mpth + 2)
+        kt = rng.standard_normal((R, n_kv, d)).astype(np.float32)
+        vt = rng.standard_normal((R, n_kv, d)).astype(np.float32)
+        kc = rng.standard_normal((n_pages, n_kv, ps, d)).astype(np.float32)
+        vc = rng.standard_normal((n_pages, n_kv, ps, d)).astype(np.float32)
+        full = oracle.accept_walk(to, par, toks, target_tokens=tgt, max_path=mpth)
+        kc_all, vc_all, kl_all = kc.copy(), vc.copy(), kv_len.copy()
+        oracle.commit(to, full["accept_len"], full["accept_path"], kt, vt, kc_all, vc_all, table, kl_all)
+        h0, h1 = head_range(n_kv, rank, world)
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a))
+        kc_me, vc_me = T(kc[:, h0:h1]), T(vc[:, h0:h1])
+        kl_in, kl_out = T(kv_len), torch.full((n,), -1, dtype=torch.int32)
+        rec = sharded(T(to), T(par), T(toks), T(kt[:, h0:h1]), T(vt[:, h0:h1]), kc_me, vc_me, T(table), kl_in,
+                      max_path=mpth, target_tokens=T(tgt), kv_len_out=kl_out)
+        s = (n + world - 1) // world
+        ok = ok and tuple(rec.shape) == (world * s, 2 + mpth)
+        ok = ok and np.array_equal(rec[:n, 0].numpy(), full["accept_len"])
+        ok = ok and np.array_equal(rec[:n, 1].numpy(), full["bonus_token"])
+        ok = ok and np.array_equal(rec[:n, 2:].numpy(), full["accept_path"])
+        ok = ok and np.array_equal(kc_me.numpy(), kc_all[:, h0:h1]) and np.array_equal(vc_me.numpy(), vc_all[:, h0:h1])
+        ok = ok and np.array_equal(kl_out.numpy(), kl_all) and np.array_equal(kl_in.numpy(), kv_len)
+    # a mis-sized static buffer is refused, not silently misaligned
+    to, par, toks, tgt = _walk_inputs(1, 5)
+    try:
+        accept_and_commit(None, torch.from_numpy(to), None, None, None, None, None, None, None, None, max_path=4,
+                          records=torch.zeros((1, 6), dtype=torch.int32), accept_fn=_cpu_record_kernels)
+        ok = False
+    except ValueError:
+        pass
+    q.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_library_accept_and_commit_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_library, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
 
 
 @pytest.mark.parametrize("n,world", [(7, 2), (64, 2), (1, 2), (10, 4)])

@@ -528,6 +528,125 @@ def test_attn_bf16_nan_in_unused_cache_slots(ada):
     assert np.abs(o - ref).max() <= BF16_TOL
 
 
+@pytest.mark.parametrize("nq", ["1", "2"])
+@pytest.mark.parametrize("pad", ["nan", "inf"])
+def test_attn_bf16_nan_in_tree_padding(ada, nq, pad, monkeypatch):
+    """Tree tiles are loaded 64 rows at a time from the request's first row: the
+    rows past K_i belong to the next request or to the caller's padding past
+    tree_offsets[n] (e.g. a budget-sized torch.empty buffer).  NaN/Inf there
+    must not reach any output (P is 0 there, but 0 * NaN = NaN in the PV MMA).
+    K_i around the 64-row tile edges: 63, 64, 65, 127, 128."""
+    monkeypatch.setenv("AS_ATTN_NQ", nq)
+    sizes = [63, 64, 65, 127, 128, 1]
+    w = _attn_case((sizes, [70, 0, 129, 64, 5, 33], 8, 2, 128, 64, "random", 1.0), True, 91)
+    scale = np.float32(1.0 / np.sqrt(128))
+    ref, ref_lse = oracle_attn(w, scale)
+    R = int(w["tree_offsets"][-1])
+    bad = np.float32(np.nan if pad == "nan" else np.inf)
+    extra = 200  # budget-sized buffers: padding rows past tree_offsets[n]
+    g = workload_to_device(w, torch.bfloat16)
+    for k in ("q", "k_tree", "v_tree"):
+        t = g[k]
+        big = torch.full((R + extra,) + tuple(t.shape[1:]), float(bad), dtype=t.dtype, device=t.device)
+        big[:R] = t
+        g[k] = big
+    par = torch.zeros(R + extra, dtype=torch.int32, device="cuda")
+    par[:R] = g["tree_parent"]
+    ws = ada.Workspace(256)
+    out, lse = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"], g["page_table"],
+                                    g["kv_len"], g["tree_offsets"], par, scale, want_lse=True, workspace=ws)
+    assert ada.check_device_error(ws)[0] == 0
+    o = out[:R].float().cpu().numpy()
+    assert np.isfinite(o).all()
+    assert np.abs(o - ref).max() <= BF16_TOL
+    assert np.abs(lse[:R].cpu().numpy() - ref_lse).max() <= BF16_TOL
+
+
+def test_accept_records_vs_oracle(ada):
+    """The multi-GPU record phases compared with the oracle directly (not with
+    the fused GPU path): WALK_RECORDS over request shards == oracle.accept_walk
+    row by row, COMMIT_RECORDS == oracle.commit byte for byte."""
+    rng = np.random.default_rng(17)
+    for n, world in ((45, 4), (8, 3), (1, 2)):
+        X = _accept_inputs(rng, n, 40, dtype="bf16")
+        mp = 24
+        s = (n + world - 1) // world
+        rec = torch.full((world * s, 2 + mp), -9, dtype=torch.int32, device="cuda")
+        for r in range(world):
+            b, e = min(n, r * s), min(n, r * s + s)
+            ada.accept_tokens(ada.AS_ACCEPT_WALK_RECORDS, dev(X["to"]), dev(X["par"]), dev(X["toks"]),
+                              target_tokens=dev(X["tgt"]), max_path=mp, req_range=(b, e), accept_path=rec)
+        ref = oracle.accept_walk(X["to"], X["par"], X["toks"], target_tokens=X["tgt"], max_path=mp)
+        got = rec.cpu().numpy()
+        np.testing.assert_array_equal(got[:n, 0], ref["accept_len"])
+        np.testing.assert_array_equal(got[:n, 1], ref["bonus_token"])
+        np.testing.assert_array_equal(got[:n, 2:], ref["accept_path"])
+        kc_g, vc_g, kl_g = dev(X["kc"], torch.bfloat16), dev(X["vc"], torch.bfloat16), dev(X["kv_len"])
+        kl_out = torch.full_like(kl_g, -1)
+        res = ada.accept_tokens(ada.AS_ACCEPT_COMMIT_RECORDS, dev(X["to"]), max_path=mp, accept_path=rec,
+                                k_tree=dev(X["kt"], torch.bfloat16), v_tree=dev(X["vt"], torch.bfloat16),
+                                k_cache=kc_g, v_cache=vc_g, page_table=dev(X["table"]), kv_len=kl_g,
+                                kv_len_out=kl_out, n_tree_rows=int(X["to"][-1]))
+        assert ada.check_device_error(res["workspace"])[0] == 0
+        to_bits = lambda a: bf16_bits(torch.from_numpy(a).to(torch.bfloat16))
+        kc, vc, kt, vt = (to_bits(X[k]) for k in ("kc", "vc", "kt", "vt"))
+        kl = X["kv_len"].copy()
+        assert oracle.commit(X["to"], ref["accept_len"], ref["accept_path"], kt, vt, kc, vc, X["table"], kl) == 0
+        np.testing.assert_array_equal(kl_out.cpu().numpy(), kl)
+        np.testing.assert_array_equal(bf16_bits(kc_g).view(np.uint8), kc.view(np.uint8))
+        np.testing.assert_array_equal(bf16_bits(vc_g).view(np.uint8), vc.view(np.uint8))
+
+
+def test_dist_accept_and_commit_single_rank_nccl(ada):
+    """paper_2501_12162_b200.dist.accept_and_commit on a single-rank NCCL group,
+    eagerly and replayed from a captured CUDA graph (the static record buffer of
+    ShardedAccept): equals FUSED and the oracle."""
+    import torch.distributed as tdist
+    from paper_2501_12162_b200.dist import ShardedAccept, accept_and_commit
+    created = False
+    if not tdist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        created = True
+    try:
+        rng = np.random.default_rng(19)
+        n = 33
+        X = _accept_inputs(rng, n, 30, dtype="bf16")
+        kt, vt = dev(X["kt"], torch.bfloat16), dev(X["vt"], torch.bfloat16)
+        args = lambda kc, vc: (dev(X["to"]), dev(X["par"]), dev(X["toks"]), kt, vt, kc, vc, dev(X["table"]),
+                               dev(X["kv_len"]))
+        ref = oracle.accept_walk(X["to"], X["par"], X["toks"], target_tokens=X["tgt"], max_path=24)
+        kc1, vc1 = dev(X["kc"], torch.bfloat16), dev(X["vc"], torch.bfloat16)
+        rec = accept_and_commit(None, *args(kc1, vc1), max_path=24, target_tokens=dev(X["tgt"]))
+        np.testing.assert_array_equal(rec[:n, 0].cpu().numpy(), ref["accept_len"])
+        np.testing.assert_array_equal(rec[:n, 2:].cpu().numpy(), ref["accept_path"])
+        kc0, vc0, kl0 = dev(X["kc"], torch.bfloat16), dev(X["vc"], torch.bfloat16), dev(X["kv_len"])
+        ada.accept_tokens(ada.AS_ACCEPT_FUSED, dev(X["to"]), dev(X["par"]), dev(X["toks"]),
+                          target_tokens=dev(X["tgt"]), max_path=24, k_tree=kt, v_tree=vt, k_cache=kc0, v_cache=vc0,
+                          page_table=dev(X["table"]), kv_len=kl0)
+        assert torch.equal(kc1, kc0) and torch.equal(vc1, vc0)
+        # captured: static inputs, static record buffer, replayed
+        sh = ShardedAccept()
+        a = args(dev(X["kc"], torch.bfloat16), dev(X["vc"], torch.bfloat16))
+        tgt = dev(X["tgt"])
+        klo = torch.empty_like(a[8])
+        sh(*a, max_path=24, target_tokens=tgt, kv_len_out=klo)  # warm-up (NCCL communicator, attributes)
+        torch.cuda.synchronize()
+        kc2, vc2 = dev(X["kc"], torch.bfloat16), dev(X["vc"], torch.bfloat16)
+        a = a[:5] + (kc2, vc2) + a[7:]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            sh(*a, max_path=24, target_tokens=tgt, kv_len_out=klo)
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(kc2, kc0) and torch.equal(vc2, vc0) and torch.equal(klo, kl0)
+        np.testing.assert_array_equal(sh.records[:n, 1].cpu().numpy(), ref["bonus_token"])
+    finally:
+        if created:
+            tdist.destroy_process_group()
+
+
 @pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
 def test_attn_bf16_full_size_sampled(ada, cfg):
     """BASELINE full sizes in the launch bench.py times; the oracle checks sampled
@@ -544,8 +663,9 @@ def test_attn_bf16_full_size_sampled(ada, cfg):
     used = int(ref_sel["tree_offsets"][-1])
     np.testing.assert_array_equal(W["sel"]["tree_offsets"].cpu().numpy(), ref_sel["tree_offsets"])
     np.testing.assert_array_equal(W["sel"]["tree_parent"].cpu().numpy()[:used], ref_sel["tree_parent"])
-    reqs = W["sample_requests"]
     to = ref_sel["tree_offsets"]
+    # 16 spread requests plus the largest tree and the longest prefix
+    reqs = sorted(set(W["sample_requests"]) | {int(np.argmax(np.diff(to))), int(np.argmax(W["kv_len_host"]))})
     kc, vc = W["pools"][W["pool_idx"]]
     w = dict(q=W["q"].float().cpu().numpy(), k_tree=W["k_tree"].float().cpu().numpy(),
              v_tree=W["v_tree"].float().cpu().numpy(), tree_offsets=to,
