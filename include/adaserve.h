@@ -69,7 +69,7 @@ enum {
     AS_DEV_BAD_PAGE = 9        /* page id outside [0, num_pages)                          */
 };
 
-#define AS_MAX_TREE 128 /* nodes per tree (incl. root) accepted by as_tree_verify_attn */
+#define AS_MAX_TREE 256 /* nodes per tree (incl. root) accepted by as_tree_verify_attn */
 #define AS_MAX_CAND 256 /* non-root candidates per request accepted by as_select_trees */
 #define AS_MAX_BEAM 16  /* beam width accepted by as_beam_step */
 

@@ -171,7 +171,8 @@ size_t as_attn_workspace_size(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     if (n_req < 0 || n_q_heads < 0 || head_dim <= 0) return 0;
     // header + debug trace + split-KV counters (two per unit: n_units = n_q * n_req
     // for every GQA ratio) + 2 partial-state slots per resident CTA
-    const size_t units = (size_t)n_q_heads * (size_t)n_req;
+    // mt_max * n_kv = ceil(AS_MAX_TREE * G / 128) * n_kv = n_q * AS_MAX_TREE / 128 (G >= 1)
+    const size_t units = (size_t)n_q_heads * (size_t)n_req * (AS_MAX_TREE / 128);
     const size_t slot = ((size_t)128 * head_dim + 256) * 4;
     return kWsHeaderBytes + kAttnTraceBytes + align_up(2 * units * 4, 256) +
            2 * (size_t)sm_count() * (size_t)tc_ctas_per_sm() * slot;

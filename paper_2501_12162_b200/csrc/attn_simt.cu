@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) tree_attn_simt_kernel(SimtParams p) {
     float* sv = sk + KC * DP;                    // [KC][D]
     float* sq = sv + KC * D;                     // [kSimtRows][D]
     float* sp = sq + kSimtRows * D;              // [kSimtRows][KC] probabilities of the chunk
-    __shared__ unsigned long long anc[AS_MAX_TREE][2];
+    __shared__ unsigned long long anc[AS_MAX_TREE][AS_MAX_TREE / 64];
     __shared__ int spar[AS_MAX_TREE];
     __shared__ int spage[KC];
     pdl_launch_dependents();
@@ -75,19 +75,17 @@ __global__ void __launch_bounds__(256) tree_attn_simt_kernel(SimtParams p) {
     for (int j = threadIdx.x; j < K; j += blockDim.x) spar[j] = p.tree_parent[off + j];
     __syncthreads();
     for (int j = threadIdx.x; j < K; j += blockDim.x) {
-        unsigned long long a0 = 0, a1 = 0;
+        for (int w = 0; w < AS_MAX_TREE / 64; ++w) anc[j][w] = 0;
         int u = j, steps = 0;
         bool bad = false;
         for (;;) {
-            if (u < 64) a0 |= 1ull << u; else a1 |= 1ull << (u - 64);
+            anc[j][u >> 6] |= 1ull << (u & 63);
             if (u == 0) break;
             int pu = spar[u];
             if (pu < 0 || pu >= u || ++steps > K) { bad = true; break; }
             u = pu;
         }
         if (bad && g == 0 && rb == 0) set_dev_error(p.ws, AS_DEV_BAD_PARENT, i);
-        anc[j][0] = a0;
-        anc[j][1] = a1;
     }
     // this block's query rows
     for (int x = threadIdx.x; x < kSimtRows * D; x += blockDim.x) {

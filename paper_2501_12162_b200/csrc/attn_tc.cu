@@ -13,18 +13,21 @@
 //               SW128) and 64-key K/V tiles (5-D map over [page][head][row]
 //               [chunk][64] -> one 16 KB box per tile, coordinates from the
 //               page-table row staged in shared memory; k_tree/v_tree for the
-//               tree tile).  K_{t+1} and V_t are issued by two lanes of the
-//               same instructions (consumption order).  2+2-stage rings.
+//               tree tiles).  K_{t+1} and V_t are issued by two lanes of the
+//               same instructions (consumption order).
 //   warp 1      TMEM owner + single-thread tcgen05.mma issuer:
 //               S_t = Q K_t^T (M=128, N=64, K=d; SS, both K-major SW128) into
-//               TMEM; O += P_t V_t (M=128, N=d, K=64; A = P from TMEM, V
-//               MN-major SW128).  QK_{t+1} is issued as soon as the softmax has
-//               read S_t, PV_t as soon as P_t is written.
+//               TMEM S buffer t&1; O += P_t V_t (M=128, N=d, K=64; A = P_t read
+//               from TMEM where the softmax wrote it over S_t, V MN-major SW128).
+//               Issue order QK_0 QK_1 PV_0 QK_2 PV_1 ...: S is double-buffered,
+//               so S_{t+1} is computed while the softmax works on S_t, and
+//               QK_{t+2} may overwrite buffer t&1 right after PV_t is issued
+//               (tcgen05.mma of one thread execute in issue order).
 //   warps 2-5   softmax + epilogue, one TMEM lane (= Q row) per thread:
-//               tcgen05.ld S -> mask (prefix length / ancestor bitmask) ->
+//               tcgen05.ld S -> mask (prefix length / ancestor bit words) ->
 //               online softmax in the log2 domain with lazy O rescaling
 //               (only when the running max grows by > 8, i.e. 256x) ->
-//               P (bf16 pairs) tcgen05.st to TMEM -> PV.  Epilogue:
+//               P (bf16 pairs) tcgen05.st over S_t -> PV.  Epilogue:
 //               tcgen05.ld O, * 1/l, bf16 store, optional natural-log LSE; or,
 //               for a unit split across CTAs (split-KV), the fp32 partial
 //               (O, m, l), then a share of the unit's cooperative merge.
@@ -39,17 +42,18 @@ constexpr int kBN = 64;           // keys per tile
 //  NQ = 1: 192 threads (TMA producer, MMA, 4 softmax warps), 2 CTAs per SM,
 //          256 TMEM columns, 2+2-stage K/V rings -- every unit its own K/V stream;
 //  NQ = 2: 352 threads (producer, 2 MMA warps, 2 x 4 softmax warps), 1 CTA/SM, all
-//          512 TMEM columns, 4+5-stage rings -- the two q-tiles of a (request,
+//          512 TMEM columns, 4+4-stage rings -- the two q-tiles of a (request,
 //          kv head) share every K/V tile (loaded once for both), chosen when the
 //          trees span more than one 128-row q-tile (c4/c5 shapes).
-// TMEM columns of q-tile q: S at q*64, P (double) at NQ*64 + q*64 (+32),
-// O at NQ*128 + q*128.
+// TMEM columns of q-tile q (base q * (128 + D)): S/P buffers b = 0, 1 at
+// base + 64 b (S_t fp32 in 64 columns; P_t bf16 pairs over its first 32), O at
+// base + 128.
 template <int NQ> struct TcCfg;
 template <> struct TcCfg<1> {
     static constexpr int THREADS = 192, CTAS = 2, TMEM = 256, KST = 2, VST = 2;
 };
 template <> struct TcCfg<2> {
-    static constexpr int THREADS = 352, CTAS = 1, TMEM = 512, KST = 4, VST = 5;
+    static constexpr int THREADS = 352, CTAS = 1, TMEM = 512, KST = 4, VST = 4;
 };
 constexpr int kCtasPerSm = 2;     // max over the shapes (workspace sizing)
 constexpr int kPtChunk = 256;     // page-table entries staged per refill
@@ -57,6 +61,12 @@ constexpr float kRescaleThresh = 8.0f;  // log2 units
 constexpr int kMaxRec = 64;       // pieces per CTA precomputed in the prologue
 constexpr int kMaxSplit = 8;      // split-KV: pieces per unit when units are fewer than CTAs
 constexpr int kTraceCtas = 512;   // per-CTA timeline records after the CTA-0 tile trace (debug)
+constexpr int kAncWords = AS_MAX_TREE / 64;  // 64-bit ancestor words per row (one per tree tile)
+#ifdef AS_DEBUG
+constexpr bool kDebug = true;     // timing-experiment switches (p.debug_mode, trace) compiled in
+#else
+constexpr bool kDebug = false;
+#endif
 
 template <int D, int NQ>
 struct TcSmem {
@@ -68,10 +78,11 @@ struct TcSmem {
     static constexpr int OFF_K = OFF_Q + NQ * Q_BYTES;
     static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
     static constexpr int OFF_PT = OFF_V + VST * KV_BYTES;     // [kPtChunk] staged page-table row
-    static constexpr int OFF_TP = OFF_PT + kPtChunk * 4;      // [NQ][2][AS_MAX_TREE] staged tree parents
+    static constexpr int OFF_ANC = OFF_PT + kPtChunk * 4;     // [NQ][kAncWords][128] ancestor words per row
+    static constexpr int OFF_TP = OFF_ANC + NQ * kAncWords * kBM * 8;  // [NQ][2][AS_MAX_TREE] staged tree parents
     static constexpr int OFF_REC = OFF_TP + NQ * 2 * AS_MAX_TREE * 4;  // [kMaxRec] this CTA's pieces
     static constexpr int OFF_BAR = OFF_REC + kMaxRec * 32;
-    // q_full q_empty, K/V rings, and per q-tile: s_full s_empty p_full[2] p_empty[2] o_full o_empty
+    // q_full q_empty, K/V rings, and per q-tile: s_full[2] p_full[2] pv_done[2] o_full o_empty
     static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + NQ * 8;
     static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
     static constexpr int BYTES = OFF_TMEM + 16;
@@ -79,12 +90,15 @@ struct TcSmem {
     // schedule-plan scratch (long long per request) aliases the K+V rings before any TMA
     static constexpr int PLAN_CAP = (KST + VST) * KV_BYTES / 8;
     static constexpr int PLAN_HALF = PLAN_CAP / 2;  // [0,half) tile prefix, [half, cap) unit prefix
+    static constexpr int TM_QT = 128 + D;           // TMEM columns per q-tile (2 S/P buffers + O)
+    static_assert(NQ * TM_QT <= TcCfg<NQ>::TMEM, "TMEM columns");
+    static_assert(TcCfg<NQ>::CTAS * (ALLOC + 1024) <= 233472, "shared memory per SM");
 };
 
 // CTA-0 pipeline trace (debug): event e of CTA-local tile index idx.
 #define AS_TRACE(e, idx)                                                                       \
     do {                                                                                       \
-        if (p.trace != nullptr && blockIdx.x == 0 && (int)(idx) < p.trace_cap)                 \
+        if (kDebug && p.trace != nullptr && blockIdx.x == 0 && (int)(idx) < p.trace_cap)      \
             p.trace[(size_t)(idx) * 8 + (e)] = clock64();                                      \
     } while (0)
 
@@ -269,10 +283,9 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     uint64_t* v_full = k_empty + kKStages;
     uint64_t* v_empty = v_full + kVStages;
     uint64_t* qbars = v_empty + kVStages;  // per q-tile q: 8 barriers at qbars + 8q
-    auto s_full = [&](int q) { return qbars + 8 * q + 0; };
-    auto s_empty = [&](int q) { return qbars + 8 * q + 1; };
-    auto p_full = [&](int q, int b) { return qbars + 8 * q + 2 + b; };   // per P buffer
-    auto p_empty = [&](int q, int b) { return qbars + 8 * q + 4 + b; };
+    auto s_full = [&](int q, int b) { return qbars + 8 * q + 0 + b; };   // QK into S buffer b done
+    auto p_full = [&](int q, int b) { return qbars + 8 * q + 2 + b; };   // softmax wrote P over S buffer b
+    auto pv_done = [&](int q, int b) { return qbars + 8 * q + 4 + b; };  // PV reading buffer b done
     auto o_full = [&](int q) { return qbars + 8 * q + 6; };
     auto o_empty = [&](int q) { return qbars + 8 * q + 7; };
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + S::OFF_TMEM);
@@ -293,11 +306,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             ptx::mbar_init(v_empty + s, NQ);
         }
         for (int q = 0; q < NQ; ++q) {
-            ptx::mbar_init(s_full(q), 1);
-            ptx::mbar_init(s_empty(q), 4);  // the q-tile's 4 softmax warps
             for (int b = 0; b < 2; ++b) {
-                ptx::mbar_init(p_full(q, b), 4);
-                ptx::mbar_init(p_empty(q, b), 1);
+                ptx::mbar_init(s_full(q, b), 1);
+                ptx::mbar_init(p_full(q, b), 4);  // the q-tile's 4 softmax warps
+                ptx::mbar_init(pv_done(q, b), 1);
             }
             ptx::mbar_init(o_full(q), 1);
             ptx::mbar_init(o_empty(q), 4);
@@ -316,7 +328,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     const uint32_t tmem = *tmem_holder;
     pdl_wait();  // the trees come from the select kernel launched just before
     unsigned long long t_start = 0;
-    if (p.trace != nullptr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    if (kDebug && p.trace != nullptr && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
     // ---------------- schedule plan (all threads; K/V rings used as scratch) ----------------
     __shared__ int sk_split;  // split-KV pieces per unit (0: whole units)
@@ -464,7 +476,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         ptx::fence_proxy_async_smem();  // plan scratch (generic writes) is reused by TMA next
         __syncthreads();  // plan scratch (K/V rings) is free again; records are visible
     }
-    if (p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceCtas) {
+    if (kDebug && p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceCtas) {
         unsigned long long tn;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
         p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 2] = tn;  // plan done
@@ -561,18 +573,21 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         }
     } else if (warp <= NQ) {
         // ===================== MMA issuers (warp 1 + q: q-tile q of each unit) =====================
-        // Issue order per piece: QK0 | QK1 PV0 | QK2 PV1 | ...  QK_{t+1} waits for
-        // the softmax to have READ S_t (start of its tile), PV_t for P_t.  Each
-        // q-tile has its own issuing warp, so the two q-tiles of a unit never wait
-        // on each other; a K/V slot is free once every MMA warp has released it
-        // (a warp whose q-tile the unit lacks releases it without an MMA).
+        // Issue order per piece: QK_tb | QK_tb+1 PV_tb | QK_tb+2 PV_tb+1 | ... PV_te-1.
+        // S/P buffers alternate with the q-tile's global tile count, so QK_{t+1}
+        // overwrites the buffer PV_{t-1} read -- issued after it by this thread,
+        // hence executed after it -- and never waits for the softmax; PV_t waits
+        // for P_t.  Each q-tile has its own issuing warp, so the two q-tiles of a
+        // unit never wait on each other; a K/V slot is free once every MMA warp
+        // has released it (a warp whose q-tile the unit lacks releases it at once).
         const int q = warp - 1;
         constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(kBM, kBN, 0);
         constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(kBM, D, 1);
         const uint32_t q_base = ptx::smem_u32(smem + S::OFF_Q) + q * S::Q_BYTES;
         const uint32_t k_base = ptx::smem_u32(smem + S::OFF_K);
         const uint32_t v_base = ptx::smem_u32(smem + S::OFF_V);
-        const uint32_t s_col = tmem + q * 64, p_col = tmem + NQ * 64 + q * 64, o_col = tmem + NQ * 128 + q * 128;
+        const uint32_t tq = tmem + q * S::TM_QT;  // S/P buffers at tq + 64 b, O at tq + 128
+        const uint32_t o_col = tq + 128;
         uint32_t k_it = 0, v_it = 0, unit_it = 0, s_it = 0, p_it = 0, o_it = 0;
         RecCursor sc = cur0;
         Piece pc;
@@ -584,17 +599,14 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 const int st = k_it % kKStages;
                 ptx::mbar_wait(k_full + st, (k_it / kKStages) & 1);
                 if (lane == 0 && q == 0) AS_TRACE(2, k_it);
-                if (mine) {
-                    ptx::mbar_wait(s_empty(q), (s_it & 1) ^ 1);
-                    if (lane == 0 && q == 0) AS_TRACE(7, k_it);
-                    ptx::tc_fence_after();
-                }
+                ptx::tc_fence_after();
                 if (lane == 0) {
-                    if (!mine || p.debug_mode >= 2) {
-                        if (mine) ptx::mbar_arrive(s_full(q));
+                    if (!mine || (kDebug && p.debug_mode >= 2)) {
+                        if (mine) ptx::mbar_arrive(s_full(q, s_it & 1));
                         ptx::mbar_arrive(k_empty + st);
                         if (t == pc.te - 1) ptx::mbar_arrive(q_empty);
                     } else {
+                        const uint32_t s_col = tq + (s_it & 1) * 64;
 #pragma unroll
                         for (int ks = 0; ks < D / 16; ++ks) {
                             const int c = ks >> 2, kk = ks & 3;
@@ -602,7 +614,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                             const uint64_t b = ptx::sw128_desc(k_base + st * S::KV_BYTES + c * kBN * 128 + kk * 32, 0, 1024);
                             ptx::mma_bf16_ss(s_col, a, b, idesc_qk, ks > 0 ? 1u : 0u);
                         }
-                        ptx::mma_commit(s_full(q));
+                        ptx::mma_commit(s_full(q, s_it & 1));
                         ptx::mma_commit(k_empty + st);
                         if (t == pc.te - 1) ptx::mma_commit(q_empty);
                     }
@@ -644,33 +656,33 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 if (t == pc.tb) ptx::mbar_wait(o_empty(q), (o_it & 1) ^ 1);  // O drained by the last epilogue
                 ptx::tc_fence_after();
                 __syncwarp();
-                if (p.debug_mode >= 2) {
+                if (kDebug && p.debug_mode >= 2) {
                     if (lane == 0) {
                         ptx::mbar_arrive(v_empty + st);
-                        ptx::mbar_arrive(p_empty(q, pbuf));
+                        ptx::mbar_arrive(pv_done(q, pbuf));
                     }
                 } else if (lane == 0) {
 #pragma unroll
                     for (int kk = 0; kk < kBN / 16; ++kk) {
-                        // A = P_t: bf16 pairs in the q-tile's TMEM P buffer
+                        // A = P_t: bf16 pairs over the first 32 columns of S buffer pbuf
                         const uint64_t b = ptx::sw128_desc(v_base + st * S::KV_BYTES + kk * 16 * 128, kBN * 128, 1024);
-                        ptx::mma_bf16_ts(o_col, p_col + pbuf * 32 + kk * 8, b, idesc_pv, (t > pc.tb || kk > 0) ? 1u : 0u);
+                        ptx::mma_bf16_ts(o_col, tq + pbuf * 64 + kk * 8, b, idesc_pv, (t > pc.tb || kk > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(v_empty + st);
-                    ptx::mma_commit(p_empty(q, pbuf));
+                    ptx::mma_commit(pv_done(q, pbuf));
                 }
                 __syncwarp();
                 ++v_it;
                 ++p_it;
             };
-            do_qk(pc.tb);
             for (int t = pc.tb; t < pc.te; ++t) {
-                if (t + 1 < pc.te) do_qk(t + 1);
-                do_pv(t);
+                do_qk(t);
+                if (t > pc.tb) do_pv(t - 1);
             }
+            do_pv(pc.te - 1);
             if (mine) {
                 if (lane == 0) {
-                    if (p.debug_mode >= 2) ptx::mbar_arrive(o_full(q));
+                    if (kDebug && p.debug_mode >= 2) ptx::mbar_arrive(o_full(q));
                     else ptx::mma_commit(o_full(q));
                 }
                 ++o_it;
@@ -684,15 +696,14 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         const int quad = warp & 3;        // TMEM lane quadrant this warp may access
         const int r = quad * 32 + lane;   // Q row in the tile == TMEM lane
         const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-        const uint32_t s_addr = tmem + lane_addr + grp * 64;
-        const uint32_t p_addr = tmem + lane_addr + NQ * 64 + grp * 64;
-        const uint32_t o_addr = tmem + lane_addr + NQ * 128 + grp * 128;
-        uint64_t* const sf = s_full(grp);
-        uint64_t* const se = s_empty(grp);
+        const uint32_t sp_addr = tmem + lane_addr + grp * S::TM_QT;  // S/P buffer b at sp_addr + 64 b
+        const uint32_t o_addr = sp_addr + 128;
         uint64_t* const of = o_full(grp);
         uint64_t* const oe = o_empty(grp);
         const int gtid = (int)threadIdx.x - 32 * (1 + NQ) - 128 * grp;  // 0..127 within the group
         const float sl2 = p.scale_log2;
+        // this row's ancestor-or-self bit words, one per 64-node tree tile ([word][row]: conflict-free)
+        uint64_t* const anc_s = reinterpret_cast<uint64_t*>(smem + S::OFF_ANC) + grp * kAncWords * kBM + r;
         uint32_t s_cnt = 0, unit_it = 0;
         int tbase = 0;  // CTA-local index of the piece's first tile (trace only)
         RecCursor sc = cur0;
@@ -705,30 +716,43 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             const bool row_ok = rr < u.K * G;
             const int node = rr / G;
             const int hh = rr - node * G;
-            // ancestor-or-self bitmask of this row's node (R15); parents staged in smem
+            // ancestor-or-self bit words of this row's node (R15); parents staged in smem
             int* tp_s = reinterpret_cast<int*>(smem + S::OFF_TP) + (grp * 2 + (unit_it & 1)) * AS_MAX_TREE;
             for (int j = gtid; j < u.K; j += 128) tp_s[j] = __ldg(p.tree_parent + u.off + j);
             group_bar(grp);
-            uint64_t anc0 = 0, anc1 = 0;
-            if (row_ok) {
-                int v = node, steps = 0;
-                for (;;) {
-                    if (v < 64) anc0 |= 1ull << v; else anc1 |= 1ull << (v - 64);
-                    if (v == 0) break;
-                    const int pv = tp_s[v];
-                    if (pv < 0 || pv >= v || ++steps > u.K) {
-                        set_dev_error(p.ws, AS_DEV_BAD_PARENT, p.req_base + u.i);
-                        break;
+            {
+                static_assert(kAncWords == 4, "ancestor words: four named registers below");
+                uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;  // named, not an array: stays in registers
+                if (row_ok) {
+                    int v = node, steps = 0;
+                    for (;;) {
+                        const uint64_t bit = 1ull << (v & 63);
+                        const int wv = v >> 6;
+                        a0 |= wv == 0 ? bit : 0ull;
+                        a1 |= wv == 1 ? bit : 0ull;
+                        a2 |= wv == 2 ? bit : 0ull;
+                        a3 |= wv == 3 ? bit : 0ull;
+                        if (v == 0) break;
+                        const int pv = tp_s[v];
+                        if (pv < 0 || pv >= v || ++steps > u.K) {
+                            set_dev_error(p.ws, AS_DEV_BAD_PARENT, p.req_base + u.i);
+                            break;
+                        }
+                        v = pv;
                     }
-                    v = pv;
                 }
+                anc_s[0 * kBM] = a0;
+                anc_s[1 * kBM] = a1;
+                anc_s[2 * kBM] = a2;
+                anc_s[3 * kBM] = a3;
             }
             float m_ref = -INFINITY, l_sum = 0.f;
             for (int t = pc.tb; t < pc.te; ++t, ++s_cnt) {
-                const uint32_t par = s_cnt & 1;
-                ptx::mbar_wait(sf, par);
+                const uint32_t b = s_cnt & 1;
+                const uint32_t s_addr = sp_addr + b * 64;
+                ptx::mbar_wait(s_full(grp, b), (s_cnt >> 1) & 1);
                 if (lane == 0 && quad == 0 && grp == 0) AS_TRACE(5, tbase + t - pc.tb);
-                if (t == pc.tb && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
+                if (kDebug && t == pc.tb && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
                     unsigned long long tn;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
                     p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 6] = tn;  // first S tile seen
@@ -738,13 +762,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 ptx::tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
                 ptx::tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
                 ptx::tmem_ld_wait();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(se);
-                if (p.debug_mode >= 1) {  // timing experiment: no softmax math
-                    ptx::mbar_wait(p_empty(grp, s_cnt & 1), ((s_cnt >> 1) & 1) ^ 1);
+                if (kDebug && p.debug_mode >= 1) {  // timing experiment: no softmax math
+                    ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(p_full(grp, s_cnt & 1));
+                    if (lane == 0) ptx::mbar_arrive(p_full(grp, b));
                     continue;
                 }
                 float* x = reinterpret_cast<float*>(sr);
@@ -755,7 +776,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         for (int c = 0; c < kBN; ++c) x[c] = (c < valid) ? x[c] : -INFINITY;
                     }
                 } else {
-                    const uint64_t bits = (t - u.n_prefix) == 0 ? anc0 : anc1;
+                    const uint64_t bits = anc_s[(t - u.n_prefix) * kBM];
 #pragma unroll
                     for (int c = 0; c < kBN; ++c) x[c] = ((bits >> c) & 1ull) ? x[c] : -INFINITY;
                 }
@@ -773,15 +794,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 const float tmax = ptx::max3(ptx::max3(mx[0], mx[1], mx[2]), ptx::max3(mx[3], mx[4], mx[5]),
                                              fmaxf(mx[6], mx[7])) * sl2;
                 const float m_new = fmaxf(m_ref, tmax);
-                // P buffer s_cnt&1 is free once PV two tiles back completed (double buffer:
-                // the softmax of tile t+1 overlaps PV_t)
-                const uint32_t pb = s_cnt & 1;
-                ptx::mbar_wait(p_empty(grp, pb), ((s_cnt >> 1) & 1) ^ 1);
                 if (t > pc.tb) {
                     const bool need = m_new > m_ref + kRescaleThresh;
                     if (__any_sync(0xffffffffu, need)) {
-                        // O must be stable: PV_{t-1} (other buffer, use (s_cnt-1)>>1) completed
-                        ptx::mbar_wait(p_empty(grp, pb ^ 1), ((s_cnt - 1) >> 1) & 1);
+                        // O must be stable: PV_{t-1} (read the other buffer) completed
+                        ptx::mbar_wait(pv_done(grp, b ^ 1), ((s_cnt - 1) >> 1) & 1);
                         ptx::tc_fence_after();
                         const float sc2 = need ? ptx::ex2(m_ref - m_new) : 1.f;
 #pragma unroll
@@ -794,7 +811,6 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                             ptx::tmem_st32(o_addr + c0, o);
                         }
                         ptx::tmem_st_wait();
-                        ptx::tc_fence_before();
                         if (need) {
                             l_sum *= sc2;
                             m_ref = m_new;
@@ -815,17 +831,18 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     pk[c >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                 }
                 l_sum += (rs[0] + rs[1]) + (rs[2] + rs[3]);
-                ptx::tmem_st32(p_addr + pb * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+                // P_t over the first 32 columns of S_t's buffer (S_t already in registers)
+                ptx::tmem_st32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(p_full(grp, pb));
+                if (lane == 0) ptx::mbar_arrive(p_full(grp, b));
                 if (lane == 0 && quad == 0 && grp == 0) AS_TRACE(6, tbase + t - pc.tb);
             }
             // ---- epilogue ----
             ptx::mbar_wait(of, unit_it & 1);
             ptx::tc_fence_after();
-            if (p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
+            if (kDebug && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
                 unsigned long long tn;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
                 p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 7] = tn;  // O of the (last) piece ready
@@ -871,7 +888,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(oe);
-            if (!full && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
+            if (kDebug && !full && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
                 unsigned long long tn;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
                 p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 5] = tn;  // partial written
@@ -901,7 +918,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 }
                 group_bar(grp);
                 __threadfence();
-                if (p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
+                if (kDebug && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
                     unsigned long long tn;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
                     p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 3] = tn;  // all pieces published
@@ -909,7 +926,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 split_merge<D>(p.partial + (size_t)(2 * b0 + grp) * p.slot_floats, 2 * p.slot_floats, Sx, u.nt, r,
                                my_rank, n_live, row_ok ? p.out + orow * D : nullptr,
                                (my_rank == 0 && row_ok && p.lse != nullptr) ? p.lse + orow : nullptr);
-                if (p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
+                if (kDebug && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
                     unsigned long long tn;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
                     p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 4] = tn;  // merge done
@@ -934,7 +951,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, TcCfg<NQ>::TMEM);
     }
-    if (p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceCtas) {
+    if (kDebug && p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceCtas) {
         // per-CTA timeline (debug): start/end globaltimer, after the CTA-0 tile trace
         unsigned long long t_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));

@@ -411,6 +411,10 @@ ATTN_CASES = [
     ([64, 3, 128], [200, 5, 77], 4, 1, 128, 64, "random", 4.0),    # multi m-tile, K=128, peaky
     ([128], [96], 16, 1, 128, 16, "chain", 1.0),                   # G=16, 16 m-tiles, deep chain
     ([9, 31, 2, 64, 15], [1000, 33, 0, 511, 2049], 32, 8, 128, 64, "random", 1.0),  # Llama-3-8B heads
+    # NEXT-4: trees past 128 nodes (3-4 tree tiles, up to 8 q-tiles per head)
+    ([256, 129, 192, 3], [300, 64, 0, 1000], 8, 2, 128, 64, "random", 1.0),
+    ([255, 200], [130, 17], 4, 4, 64, 32, "chain", 2.0),           # deep chains, d=64
+    ([257 - 1, 130], [64, 700], 32, 8, 128, 64, "star", 1.0),       # 8B heads, G=4: 8 q-tiles
 ]
 
 
@@ -508,6 +512,23 @@ def test_attn_bf16_many_units(ada, sk, monkeypatch):
         assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-2
 
 
+def test_attn_tree_too_big_is_flagged(ada):
+    """K_i > AS_MAX_TREE (256): the request is skipped and AS_DEV_TREE_TOO_BIG
+    reported with its index; the other requests are still verified."""
+    w = _attn_case(([5, 257, 9], [40, 10, 70], 8, 2, 128, 64, "random", 1.0), True, 93)
+    scale = np.float32(1.0 / np.sqrt(128))
+    g = workload_to_device(w, torch.bfloat16)
+    ws = ada.Workspace(256)
+    out, _ = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"], g["page_table"],
+                                  g["kv_len"], g["tree_offsets"], g["tree_parent"], scale, workspace=ws)
+    assert ada.check_device_error(ws) == (4, 1)
+    to = w["tree_offsets"]
+    keep = [0, 2]
+    rows, ref, _ = oracle_attn(w, scale, requests=keep)
+    got = out[torch.from_numpy(rows).cuda()].float().cpu().numpy()
+    assert np.abs(got - ref).max() <= BF16_TOL
+
+
 def test_attn_bf16_nan_in_unused_cache_slots(ada):
     """Cache slots past kv_len may hold garbage (NaN): outputs must not see them."""
     w = _attn_case(([6, 9], [70, 33], 8, 2, 128, 64, "random", 1.0), True, 77)
@@ -537,8 +558,8 @@ def test_attn_bf16_nan_in_tree_padding(ada, nq, pad, monkeypatch):
     must not reach any output (P is 0 there, but 0 * NaN = NaN in the PV MMA).
     K_i around the 64-row tile edges: 63, 64, 65, 127, 128."""
     monkeypatch.setenv("AS_ATTN_NQ", nq)
-    sizes = [63, 64, 65, 127, 128, 1]
-    w = _attn_case((sizes, [70, 0, 129, 64, 5, 33], 8, 2, 128, 64, "random", 1.0), True, 91)
+    sizes = [63, 64, 65, 127, 128, 1, 191, 256]
+    w = _attn_case((sizes, [70, 0, 129, 64, 5, 33, 64, 1], 8, 2, 128, 64, "random", 1.0), True, 91)
     scale = np.float32(1.0 / np.sqrt(128))
     ref, ref_lse = oracle_attn(w, scale)
     R = int(w["tree_offsets"][-1])
