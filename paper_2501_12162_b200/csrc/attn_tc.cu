@@ -68,6 +68,14 @@ constexpr bool kDebug = true;     // timing-experiment switches (p.debug_mode, t
 constexpr bool kDebug = false;
 #endif
 
+// A piece precomputed in the prologue (shared memory): no global load and no
+// request walk at a unit boundary.
+struct PieceRec {
+    int i, j, tb, te;  // request, unit within request (g*MT + mt), tile range
+    int off, K, L, x;  // request geometry, piece kind (Piece::x)
+    int x0, tr;        // tail pieces only (Piece::x0, Piece::tr)
+};
+
 template <int D, int NQ>
 struct TcSmem {
     static constexpr int KST = TcCfg<NQ>::KST, VST = TcCfg<NQ>::VST;
@@ -81,7 +89,7 @@ struct TcSmem {
     static constexpr int OFF_ANC = OFF_PT + kPtChunk * 4;     // [NQ][kAncWords][128] ancestor words per row
     static constexpr int OFF_TP = OFF_ANC + NQ * kAncWords * kBM * 8;  // [NQ][2][AS_MAX_TREE] staged tree parents
     static constexpr int OFF_REC = OFF_TP + NQ * 2 * AS_MAX_TREE * 4;  // [kMaxRec] this CTA's pieces
-    static constexpr int OFF_BAR = OFF_REC + kMaxRec * 32;
+    static constexpr int OFF_BAR = OFF_REC + kMaxRec * (int)sizeof(PieceRec);
     // q_full q_empty, K/V rings, and per q-tile: s_full[2] p_full[2] pv_done[2] o_full o_empty
     static constexpr int N_BAR = 2 + 2 * KST + 2 * VST + NQ * 8;
     static constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
@@ -158,14 +166,9 @@ struct Piece {
     Unit u;
     int w;         // unit id (i, g, mt) -> counter index
     int tb, te;    // tile range of this piece
-    long long x;   // split-KV: piece index within the unit (else -1)
-};
-
-// A piece precomputed in the prologue (shared memory): no global load and no
-// request walk at a unit boundary.
-struct PieceRec {
-    int i, j, tb, te;  // request, unit within request (g*MT + mt), tile range
-    int off, K, L, x;  // request geometry, split-KV piece index (-1: whole unit)
+    int x;         // >= 0: co-resident split-KV piece index; -1: whole unit; -2 - e: tail piece (e = 0
+                   // the CTA's first tail piece, 1 its last), merged by the last finisher
+    int x0, tr;    // tail pieces: the unit's first tile in the remainder stream, the stream's length
 };
 
 // The roles (producer, MMA, softmax) only replay the CTA's records.
@@ -190,6 +193,8 @@ __device__ __forceinline__ bool rec_next(const TcParams& p, RecCursor& cur, Piec
     pc.tb = rc.tb;
     pc.te = rc.te;
     pc.x = rc.x;
+    pc.x0 = rc.x0;
+    pc.tr = rc.tr;
     return true;
 }
 
@@ -263,6 +268,81 @@ __device__ __noinline__ void split_merge(const float* __restrict__ slot0, size_t
         }
     }
     if (lse_out != nullptr) *lse_out = (M + __log2f(Ltot)) * 0.6931471805599453f;
+}
+
+// Tail stream-K merge (DESIGN.md §5 "Schedule"): the last of a unit's pieces to
+// finish combines its own unnormalised (O in TMEM, m, l) with the n_oth other
+// pieces' fp32 partials (slots s0..s2) for row r:
+// out_row[c] = sum_k 2^(m_k - M) O_k[c] / sum_k 2^(m_k - M) l_k, M = max_k m_k.
+template <int D>
+__device__ __noinline__ void tail_merge(uint32_t o_addr, float m_own, float l_own, const float* __restrict__ part0,
+                                        size_t slot_floats, int n_oth, int s0, int s1, int s2, int r,
+                                        __nv_bfloat16* out_row, float* lse_out) {
+    const int sl[3] = {s0, s1, s2};
+    const float* src[3];
+    float mo[3], wo[3], lo[3];
+    float M = m_own;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        src[k] = part0 + (size_t)sl[k] * slot_floats;
+        mo[k] = -INFINITY;
+        lo[k] = 0.f;
+        if (k < n_oth) {
+            mo[k] = __ldcg(src[k] + 128 * D + r);
+            lo[k] = __ldcg(src[k] + 128 * D + 128 + r);
+        }
+        M = fmaxf(M, mo[k]);
+    }
+    const float w_own = m_own == -INFINITY ? 0.f : ptx::ex2(m_own - M);
+    float Ltot = l_own * w_own;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        wo[k] = mo[k] == -INFINITY ? 0.f : ptx::ex2(mo[k] - M);
+        Ltot += lo[k] * wo[k];
+    }
+    const float inv = 1.f / Ltot;
+#pragma unroll 1
+    for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t oa[32];
+        ptx::tmem_ld32(o_addr + c0, oa);
+        float4 q[3][8];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                q[k][j] = (k < n_oth) ? __ldcg(reinterpret_cast<const float4*>(src[k]) + (c0 / 4 + j) * 128 + r)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        ptx::tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float a[4] = {__uint_as_float(oa[4 * j]) * w_own, __uint_as_float(oa[4 * j + 1]) * w_own,
+                          __uint_as_float(oa[4 * j + 2]) * w_own, __uint_as_float(oa[4 * j + 3]) * w_own};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                a[0] = fmaf(q[k][j].x, wo[k], a[0]);
+                a[1] = fmaf(q[k][j].y, wo[k], a[1]);
+                a[2] = fmaf(q[k][j].z, wo[k], a[2]);
+                a[3] = fmaf(q[k][j].w, wo[k], a[3]);
+            }
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(a[0] * inv, a[1] * inv);
+            __nv_bfloat162 h1 = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
+            pk[2 * j] = *reinterpret_cast<uint32_t*>(&h0);
+            pk[2 * j + 1] = *reinterpret_cast<uint32_t*>(&h1);
+        }
+        if (out_row != nullptr) {
+            uint4* dst = reinterpret_cast<uint4*>(out_row + c0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        }
+    }
+    if (lse_out != nullptr) *lse_out = (M + __log2f(Ltot)) * 0.6931471805599453f;
+}
+
+// Partial-result slot of a tail piece: e = 0 for a CTA's first tail piece, 1 for its last.
+template <int NQ>
+__device__ __forceinline__ int tail_slot(int cta, int e, int grp) {
+    return NQ == 1 ? 2 * cta + e : 4 * cta + 2 * e + grp;
 }
 
 template <int D, int NQ>
@@ -442,23 +522,70 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     load_req(p, lo_b, r);
                     const int tb = r.nt * sidx / Sx, te = r.nt * (sidx + 1) / Sx;
                     if (te > tb) {
-                        recs[0] = PieceRec{lo_b, (int)(k - preu[lo_b]), tb, te, r.off, r.K, r.L, sidx};
+                        recs[0] = PieceRec{lo_b, (int)(k - preu[lo_b]), tb, te, r.off, r.K, r.L, sidx, 0, 0};
                         s_nrec = 1;
                     }
                 }
             }
         }
         __syncthreads();
+        __shared__ int s_ntail;
         if (!sk_split) {
-            const int cnt = U > (int)blockIdx.x ? (U - 1 - (int)blockIdx.x) / G + 1 : 0;
-            if (cnt > kMaxRec || !can_plan) {
-                if (threadIdx.x == 0) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, -2);
+            // Whole units, unit k on CTA k mod G.  Tail stream-K (units > CTAs and the
+            // last partial wave more than half full): the W1 = U / G full waves stay
+            // whole; the tiles of the R remainder units are cut evenly over all G CTAs
+            // (each unit then spans at most 3 CTAs).  Every CTA runs its tail pieces
+            // FIRST -- the pieces of a unit finish at about the same time, early, and
+            // the last to finish merges them from its TMEM while the other CTAs
+            // continue with their whole units (DESIGN.md §5 "Schedule").
+            const int W1 = U / G, R = U - W1 * G;
+            if (threadIdx.x == 0) {
+                int nt_rec = 0;
+                bool tail = p.stream_k && can_plan && W1 >= 1 && 2 * R > G && W1 + 2 <= kMaxRec;
+                bool ok = can_plan;
+                if (tail) {
+                    const long long k0 = (long long)W1 * G;  // first remainder unit
+                    int lo_b = 0, hi_b = n - 1;              // last i with preu[i] <= k0
+                    while (lo_b < hi_b) {
+                        const int mid = (lo_b + hi_b + 1) >> 1;
+                        if (preu[mid] <= k0) lo_b = mid; else hi_b = mid - 1;
+                    }
+                    Req r0;
+                    load_req(p, lo_b, r0);
+                    const long long S0 = pre[lo_b] + (k0 - preu[lo_b]) * r0.nt;  // remainder stream start
+                    const long long TR = T - S0;
+                    // every unit must span at most 3 CTAs (the merger reads at most 2 partials)
+                    if ((long long)maxnt * G > 2 * TR) tail = false;
+                    const long long a = S0 + TR * blockIdx.x / G, b = S0 + TR * (blockIdx.x + 1) / G;
+                    long long pos = tail ? a : b;
+                    while (pos < b) {
+                        if (nt_rec + W1 >= kMaxRec) { ok = false; break; }
+                        int lb = 0, hb = n - 1;  // last i with pre[i] <= pos
+                        while (lb < hb) {
+                            const int mid = (lb + hb + 1) >> 1;
+                            if (pre[mid] <= pos) lb = mid; else hb = mid - 1;
+                        }
+                        Req r;
+                        load_req(p, lb, r);
+                        const long long j = (pos - pre[lb]) / r.nt;
+                        const long long ustart = pre[lb] + j * r.nt;
+                        const int tb = (int)(pos - ustart);
+                        const int te = (int)min((long long)r.nt, b - ustart);
+                        const int x = (tb == 0 && te == r.nt) ? -1 : (pos == a ? -2 : -3);
+                        recs[nt_rec++] = PieceRec{lb, (int)j, tb, te, r.off, r.K, r.L, x, (int)(ustart - S0), (int)TR};
+                        pos = ustart + te;
+                    }
+                }
+                const int n_whole = tail ? W1 : (U > (int)blockIdx.x ? (U - 1 - (int)blockIdx.x) / G + 1 : 0);
+                ok = ok && n_whole <= kMaxRec;
+                if (!ok) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, -2);
+                s_ntail = ok ? nt_rec : 0;
+                s_nrec = ok ? nt_rec + n_whole : 0;
             }
             __syncthreads();
-            if (threadIdx.x == 0) s_nrec = (cnt <= kMaxRec && can_plan) ? cnt : 0;
-            __syncthreads();
         }
-        const int nrec_static = (!sk_split && s_nrec >= 0) ? s_nrec : 0;
+        const int nrec_static = (!sk_split && s_nrec > 0) ? s_nrec - s_ntail : 0;
+        const int rec_base = (!sk_split && s_nrec > 0) ? s_ntail : 0;
         for (int q = threadIdx.x; q < nrec_static; q += blockDim.x) {
             const long long k = (long long)blockIdx.x + (long long)q * G;
             int lo_b = 0, hi_b = n - 1;  // last i with preu[i] <= k
@@ -468,7 +595,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             }
             Req r;
             load_req(p, lo_b, r);
-            recs[q] = PieceRec{lo_b, (int)(k - preu[lo_b]), 0, r.nt, r.off, r.K, r.L, -1};
+            recs[rec_base + q] = PieceRec{lo_b, (int)(k - preu[lo_b]), 0, r.nt, r.off, r.K, r.L, -1, 0, 0};
         }
         cur0.nrec = s_nrec;
         cur0.q = 0;
@@ -607,6 +734,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         if (t == pc.te - 1) ptx::mbar_arrive(q_empty);
                     } else {
                         const uint32_t s_col = tq + (s_it & 1) * 64;
+                        if (q == 0) AS_TRACE(7, k_it);
 #pragma unroll
                         for (int ks = 0; ks < D / 16; ++ks) {
                             const int c = ks >> 2, kk = ks & 3;
@@ -848,42 +976,93 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 7] = tn;  // O of the (last) piece ready
             }
             const bool full = (pc.tb == 0 && pc.te == u.nt);
-            const float inv = full ? 1.f / l_sum : 1.f;  // partial piece: keep (O, m, l) unnormalised
+            const bool tailp = !full && pc.x <= -2;  // tail stream-K piece (else co-resident split-KV)
+            const int lead_warp = 1 + NQ + 4 * grp;  // first softmax warp of this group
+            const int wq = pc.w + grp;               // counters of this q-tile
             const size_t orow = (size_t)(u.off + node) * p.n_q + (size_t)u.g * G + hh;
-            const int slot = 2 * blockIdx.x + grp;  // split-KV: one piece per CTA, one slot per q-tile
-            float* part = p.partial + (size_t)slot * p.slot_floats;  // O as [D/4][128] float4, then m[128], l[128]
+            __shared__ int s_merge[NQ];
+            bool merge_now = false;
+            if (tailp) {
+                // every other piece already published (their counts are in): merge straight
+                // from this piece's TMEM and publish nothing
+                if (warp == lead_warp && lane == 0)
+                    s_merge[grp] = *reinterpret_cast<volatile int*>(p.cnt + wq) + (pc.te - pc.tb) == u.nt;
+                group_bar(grp);
+                merge_now = s_merge[grp] != 0;
+                group_bar(grp);
+            }
+            if (!merge_now) {
+                const float inv = full ? 1.f / l_sum : 1.f;  // partial piece: keep (O, m, l) unnormalised
+                // co-resident split-KV: one piece per CTA, one slot per q-tile; tail: tail_slot()
+                const int slot = tailp ? tail_slot<NQ>((int)blockIdx.x, -2 - pc.x, grp) : 2 * (int)blockIdx.x + grp;
+                float* part = p.partial + (size_t)slot * p.slot_floats;  // O as [D/4][128] float4, then m[128], l[128]
 #pragma unroll
-            for (int c0 = 0; c0 < D; c0 += 32) {
-                uint32_t oa[32];
-                ptx::tmem_ld32(o_addr + c0, oa);
-                ptx::tmem_ld_wait();
-                if (full) {
-                    if (row_ok) {
-                        uint32_t pkk[16];
+                for (int c0 = 0; c0 < D; c0 += 32) {
+                    uint32_t oa[32];
+                    ptx::tmem_ld32(o_addr + c0, oa);
+                    ptx::tmem_ld_wait();
+                    if (full) {
+                        if (row_ok) {
+                            uint32_t pkk[16];
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(oa[2 * j]) * inv,
-                                                                      __uint_as_float(oa[2 * j + 1]) * inv);
-                            pkk[j] = *reinterpret_cast<uint32_t*>(&h2);
+                            for (int j = 0; j < 16; ++j) {
+                                __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(oa[2 * j]) * inv,
+                                                                          __uint_as_float(oa[2 * j + 1]) * inv);
+                                pkk[j] = *reinterpret_cast<uint32_t*>(&h2);
+                            }
+                            uint4* dst = reinterpret_cast<uint4*>(p.out + orow * D + c0);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                dst[j] = make_uint4(pkk[4 * j], pkk[4 * j + 1], pkk[4 * j + 2], pkk[4 * j + 3]);
                         }
-                        uint4* dst = reinterpret_cast<uint4*>(p.out + orow * D + c0);
+                    } else {
+                        // column-quad-major [D/4][128] float4: a warp's store is 512 contiguous bytes
+                        float4* dst = reinterpret_cast<float4*>(part) + (c0 / 4) * 128 + r;
 #pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            dst[j] = make_uint4(pkk[4 * j], pkk[4 * j + 1], pkk[4 * j + 2], pkk[4 * j + 3]);
+                        for (int j = 0; j < 8; ++j)
+                            dst[j * 128] = make_float4(__uint_as_float(oa[4 * j]), __uint_as_float(oa[4 * j + 1]),
+                                                       __uint_as_float(oa[4 * j + 2]), __uint_as_float(oa[4 * j + 3]));
                     }
-                } else {
-                    // column-quad-major [D/4][128] float4: a warp's store is 512 contiguous bytes
-                    float4* dst = reinterpret_cast<float4*>(part) + (c0 / 4) * 128 + r;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        dst[j * 128] = make_float4(__uint_as_float(oa[4 * j]), __uint_as_float(oa[4 * j + 1]),
-                                             __uint_as_float(oa[4 * j + 2]), __uint_as_float(oa[4 * j + 3]));
+                }
+                if (full && row_ok && p.lse) p.lse[orow] = (m_ref + __log2f(l_sum)) * 0.6931471805599453f;
+                if (!full) {
+                    part[128 * D + r] = m_ref;
+                    part[128 * D + 128 + r] = l_sum;
+                }
+                if (tailp) {
+                    // publish, then count this piece's tiles in; the piece completing the count merges
+                    __threadfence();
+                    group_bar(grp);
+                    if (warp == lead_warp && lane == 0)
+                        s_merge[grp] = atomicAdd(p.cnt + wq, pc.te - pc.tb) + (pc.te - pc.tb) == u.nt;
+                    group_bar(grp);
+                    merge_now = s_merge[grp] != 0;
+                    group_bar(grp);
                 }
             }
-            if (full && row_ok && p.lse) p.lse[orow] = (m_ref + __log2f(l_sum)) * 0.6931471805599453f;
-            if (!full) {
-                part[128 * D + r] = m_ref;
-                part[128 * D + 128 + r] = l_sum;
+            if (merge_now) {
+                __threadfence();  // the other pieces' partials, published before their counts
+                // the unit's pieces: the CTAs whose remainder-stream ranges [tr*c/G, tr*(c+1)/G)
+                // meet [x0, x0 + nt); a CTA's piece is its first (e = 0) unless the unit starts
+                // strictly inside that CTA's range (then it is its last, e = 1)
+                const long long Gd = gridDim.x, tr = pc.tr;
+                auto start = [&](long long c) { return tr * c / Gd; };
+                auto cta_of = [&](long long x) {
+                    long long c = x * Gd / (tr > 0 ? tr : 1);
+                    while (c + 1 < Gd && start(c + 1) <= x) ++c;
+                    while (c > 0 && start(c) > x) --c;
+                    return c;
+                };
+                const long long cA = cta_of(pc.x0), cB = cta_of((long long)pc.x0 + u.nt - 1);
+                int oth[3] = {0, 0, 0}, n_oth = 0;
+                for (long long c = cA; c <= cB && n_oth < 3; ++c) {
+                    if (c == (long long)blockIdx.x) continue;
+                    const int e = (c > cA || start(cA) == pc.x0) ? 0 : 1;
+                    oth[n_oth++] = tail_slot<NQ>((int)c, e, grp);
+                }
+                tail_merge<D>(o_addr, m_ref, l_sum, p.partial, p.slot_floats, n_oth, oth[0], oth[1], oth[2], r,
+                              row_ok ? p.out + orow * D : nullptr, (row_ok && p.lse != nullptr) ? p.lse + orow : nullptr);
+                if (warp == lead_warp && lane == 0) p.cnt[wq] = 0;  // last user of the counter this launch
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -893,13 +1072,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
                 p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 5] = tn;  // partial written
             }
-            if (!full) {
+            if (!full && !tailp) {
                 // split-KV merge, shared by the unit's pieces: once every piece has
                 // published its fp32 (O, m, l), piece CTA s merges its share of the
                 // columns for all rows (all pieces of a unit are co-resident: one piece
                 // per CTA of a persistent grid), so no CTA merges a whole unit alone.
-                const int lead_warp = 1 + NQ + 4 * grp;  // first softmax warp of this group
-                const int wq = pc.w + grp;               // counters of this q-tile
                 const int Sx = sk_split;
                 const int sidx = (int)blockIdx.x % Sx;
                 const int b0 = (int)blockIdx.x - sidx;
