@@ -96,8 +96,8 @@ struct TcSmem {
     static constexpr int BYTES = OFF_TMEM + 16;
     static constexpr int ALLOC = BYTES + 1024;  // alignment slack
     // schedule-plan scratch (long long per request) aliases the K+V rings before any TMA
-    static constexpr int PLAN_CAP = (KST + VST) * KV_BYTES / 8;
-    static constexpr int PLAN_HALF = PLAN_CAP / 2;  // [0,half) tile prefix, [half, cap) unit prefix
+    // per request: tile prefix (8 B), unit prefix (8 B), geometry {off, K, L} (16 B)
+    static constexpr int PLAN_N = (KST + VST) * KV_BYTES / 32;
     static constexpr int TM_QT = 128 + D;           // TMEM columns per q-tile (2 S/P buffers + O)
     static_assert(NQ * TM_QT <= TcCfg<NQ>::TMEM, "TMEM columns");
     static_assert(TcCfg<NQ>::CTAS * (ALLOC + 1024) <= 233472, "shared memory per SM");
@@ -127,10 +127,12 @@ struct Req {
     int off, K, L, QT, MT, nt, n_prefix;
 };
 
-__device__ __forceinline__ void load_req(const TcParams& p, int i, Req& r) {
-    r.off = __ldg(p.tree_offsets + i);
-    r.K = __ldg(p.tree_offsets + i + 1) - r.off;
-    r.L = __ldg(p.kv_len + i);
+// Request geometry from {tree offset, tree size, kv_len} (the plan caches the
+// triple in shared memory: the prologue's later steps make no global loads).
+__device__ __forceinline__ void req_from(const TcParams& p, int off, int K, int L, Req& r) {
+    r.off = off;
+    r.K = K;
+    r.L = L;
     if (r.L < 0) r.L = 0;
     if (r.L > p.max_pages * p.page_size) r.L = p.max_pages * p.page_size;
     r.n_prefix = (r.L + kBN - 1) / kBN;
@@ -138,6 +140,11 @@ __device__ __forceinline__ void load_req(const TcParams& p, int i, Req& r) {
     r.QT = ok ? (r.K * p.G + kBM - 1) / kBM : 0;
     r.MT = (r.QT + p.nq - 1) / p.nq;
     r.nt = r.n_prefix + (r.K + kBN - 1) / kBN;
+}
+
+__device__ __forceinline__ void req_geo(const TcParams& p, const int4* geo, int i, Req& r) {
+    const int4 g = geo[i];
+    req_from(p, g.x, g.y, g.z, r);
 }
 
 __device__ __forceinline__ void make_unit(const TcParams& p, const Req& r, int i, int j, Unit& u) {
@@ -417,19 +424,23 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     RecCursor cur0;
     {
         const int n = p.n_req;
-        // per-request prefixes (K/V rings as scratch): tiles [0, half), units [half, 2 half)
+        // per-request prefixes and geometry (K/V rings as scratch)
         long long* pre = reinterpret_cast<long long*>(smem + S::OFF_K);
-        long long* preu = pre + S::PLAN_HALF;
-        const bool can_plan = n <= S::PLAN_HALF;
+        long long* preu = pre + S::PLAN_N;
+        int4* geo = reinterpret_cast<int4*>(preu + S::PLAN_N);
+        const bool can_plan = n <= S::PLAN_N;
         const bool can_split = p.stream_k && can_plan;
         int my_units = 0, my_maxnt = 0, my_minnt = 0x7fffffff;
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             Req r;
-            load_req(p, i, r);
+            const int off = __ldg(p.tree_offsets + i);
+            const int4 g = make_int4(off, __ldg(p.tree_offsets + i + 1) - off, __ldg(p.kv_len + i), 0);
+            req_from(p, g.x, g.y, g.z, r);
+            if (can_plan) geo[i] = g;
             // device errors carry the caller's request index (chunked launches add req_base)
             if (r.MT == 0 && r.K > AS_MAX_TREE) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, p.req_base + i);
             else if (r.MT == 0 && r.K > 0) set_dev_error(p.ws, AS_DEV_ROWS_OVERFLOW, p.req_base + i);
-            if (r.MT > 0 && __ldg(p.kv_len + i) > p.max_pages * p.page_size)
+            if (r.MT > 0 && g.z > p.max_pages * p.page_size)
                 set_dev_error(p.ws, AS_DEV_PAGE_OVERFLOW, p.req_base + i);
             my_units += p.n_kv * r.MT;
             if (r.MT > 0) {
@@ -519,7 +530,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         if (preu[mid] <= k) lo_b = mid; else hi_b = mid - 1;
                     }
                     Req r;
-                    load_req(p, lo_b, r);
+                    req_geo(p, geo, lo_b, r);
                     const int tb = r.nt * sidx / Sx, te = r.nt * (sidx + 1) / Sx;
                     if (te > tb) {
                         recs[0] = PieceRec{lo_b, (int)(k - preu[lo_b]), tb, te, r.off, r.K, r.L, sidx, 0, 0};
@@ -551,7 +562,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         if (preu[mid] <= k0) lo_b = mid; else hi_b = mid - 1;
                     }
                     Req r0;
-                    load_req(p, lo_b, r0);
+                    req_geo(p, geo, lo_b, r0);
                     const long long S0 = pre[lo_b] + (k0 - preu[lo_b]) * r0.nt;  // remainder stream start
                     const long long TR = T - S0;
                     // every unit must span at most 3 CTAs (the merger reads at most 2 partials)
@@ -566,7 +577,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                             if (pre[mid] <= pos) lb = mid; else hb = mid - 1;
                         }
                         Req r;
-                        load_req(p, lb, r);
+                        req_geo(p, geo, lb, r);
                         const long long j = (pos - pre[lb]) / r.nt;
                         const long long ustart = pre[lb] + j * r.nt;
                         const int tb = (int)(pos - ustart);
@@ -594,7 +605,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 if (preu[mid] <= k) lo_b = mid; else hi_b = mid - 1;
             }
             Req r;
-            load_req(p, lo_b, r);
+            req_geo(p, geo, lo_b, r);
             recs[rec_base + q] = PieceRec{lo_b, (int)(k - preu[lo_b]), 0, r.nt, r.off, r.K, r.L, -1, 0, 0};
         }
         cur0.nrec = s_nrec;
@@ -1063,6 +1074,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 tail_merge<D>(o_addr, m_ref, l_sum, p.partial, p.slot_floats, n_oth, oth[0], oth[1], oth[2], r,
                               row_ok ? p.out + orow * D : nullptr, (row_ok && p.lse != nullptr) ? p.lse + orow : nullptr);
                 if (warp == lead_warp && lane == 0) p.cnt[wq] = 0;  // last user of the counter this launch
+                if (kDebug && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
+                    unsigned long long tn;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+                    p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 4] = tn;  // tail merge done
+                }
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -1172,9 +1188,9 @@ int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, in
     const int grid_full = n_sms * (nq == 2 ? TcCfg<2>::CTAS : TcCfg<1>::CTAS);
     const int units_per_req = p0.n_kv * ((p0.mt_max + nq - 1) / nq);
     int chunk = units_per_req > 0 ? max(1, kMaxRec * grid_full / units_per_req) : p0.n_req;
-    // the prologue's schedule plan holds at most PLAN_HALF requests (per-request prefix sums)
-    const int plan_half = head_dim == 128 ? (nq == 2 ? TcSmem<128, 2>::PLAN_HALF : TcSmem<128, 1>::PLAN_HALF)
-                                          : (nq == 2 ? TcSmem<64, 2>::PLAN_HALF : TcSmem<64, 1>::PLAN_HALF);
+    // the prologue's schedule plan holds at most PLAN_N requests (prefix sums, geometry)
+    const int plan_half = head_dim == 128 ? (nq == 2 ? TcSmem<128, 2>::PLAN_N : TcSmem<128, 1>::PLAN_N)
+                                          : (nq == 2 ? TcSmem<64, 2>::PLAN_N : TcSmem<64, 1>::PLAN_N);
     chunk = min(chunk, plan_half);
     for (int r0 = 0; r0 < p0.n_req; r0 += chunk) {
         TcParams p = p0;

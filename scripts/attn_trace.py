@@ -63,6 +63,11 @@ if len(cta):
           f"p90 {np.percentile(en, 90):.2f}  max {en.max():.2f}")
     print(f"  busy fraction (sum of CTA spans / (CTAs x makespan)) {((en - st).sum() / (len(cta) * en.max())):.3f}")
     print("  end-time histogram (us):", np.histogram(en, bins=10)[0].tolist(), np.round(np.histogram(en, bins=10)[1], 1).tolist())
+    for col, nm in ((5, "partial written"), (4, "merge done")):
+        sel = cta[cta[:, col] != 0]
+        if len(sel):
+            v = (sel[:, col] - t0c) / 1e3
+            print(f"  {nm}: {len(sel)} CTAs, median {np.median(v):.2f} max {v.max():.2f} (us)")
     sp = cta[cta[:, 6] != 0]
     if len(sp):
         pw = (sp[:, 5] - t0c) / 1e3

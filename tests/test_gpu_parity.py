@@ -483,6 +483,26 @@ def test_attn_bf16_request_chunks(ada, nq, monkeypatch):
     assert np.abs(out.float().cpu().numpy() - ref).max() <= BF16_TOL
 
 
+def test_attn_bf16_plan_capacity_chunks(ada):
+    """More requests than one launch's schedule plan holds (head_dim 64, G = 1:
+    few units per request, so the plan's per-request capacity binds before the
+    per-CTA piece lists do): the library launches request chunks sized by both
+    limits; every request matches the oracle and no device error is raised."""
+    rng = np.random.default_rng(41)
+    n = 2600
+    sizes = rng.integers(1, 4, n)
+    kv = rng.integers(0, 40, n)
+    w = synth.tree_workload(rng, sizes, kv, 2, 2, 64, 16, bf16=True)
+    scale = np.float32(1.0 / 8.0)
+    ref, _ = oracle_attn(w, scale)
+    g = workload_to_device(w, torch.bfloat16)
+    ws = ada.Workspace(256)
+    out, _ = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"], g["page_table"],
+                                  g["kv_len"], g["tree_offsets"], g["tree_parent"], scale, workspace=ws)
+    assert ada.check_device_error(ws)[0] == 0
+    assert np.abs(out.float().cpu().numpy() - ref).max() <= BF16_TOL
+
+
 @pytest.mark.parametrize("sk", ["0", "1", "2"])
 def test_attn_bf16_many_units(ada, sk, monkeypatch):
     """More units than CTAs (64 requests x 8 kv heads = 512 > 296 one-q-tile
