@@ -260,13 +260,23 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     const int mt_max = (AS_MAX_TREE * G + 127) / 128;
     p.n_units = mt_max * n_req * n_kv_heads;
     p.mt_max = mt_max;
-    // CTA shape: pair the q-tiles of a (request, kv head) -- each K/V tile loaded
-    // once for both -- when the trees on average span more than one 128-row
-    // q-tile (n_tree_rows / n_req: the caller's row allocation per request).
+    // CTA shape, from the trees' q-tiles per (request, kv head) -- n_tree_rows / n_req
+    // is the caller's row allocation per request: one q-tile -> one-q-tile CTAs, two
+    // per SM; more -> the q-tiles of a head share every K/V tile fetch (NQ = 2: two
+    // q-tiles in one CTA; cs: a cluster of one-q-tile CTAs with multicast).
+    // AS_ATTN_NQ / AS_ATTN_CS override the choice (schedule A/B; results identical).
     {
-        const char* nqe = getenv("AS_ATTN_NQ");  // A/B override: 1 or 2
         const long long rows_per_req = n_req > 0 ? (long long)n_tree_rows / n_req : 0;
-        p.nq = (nqe && (atoi(nqe) == 1 || atoi(nqe) == 2)) ? atoi(nqe) : (G * rows_per_req > 128 ? 2 : 1);
+        const long long qt = (G * rows_per_req + 127) / 128;
+        p.nq = qt > 1 ? 2 : 1;
+        p.cs = 1;
+        const char* nqe = getenv("AS_ATTN_NQ");
+        if (nqe && (atoi(nqe) == 1 || atoi(nqe) == 2)) p.nq = atoi(nqe);
+        const char* cse = getenv("AS_ATTN_CS");
+        if (cse && (atoi(cse) == 1 || atoi(cse) == 2 || atoi(cse) == 4)) {
+            p.cs = atoi(cse);
+            if (p.cs > 1) p.nq = 1;
+        }
     }
     {
         const int nsm = sm_count();

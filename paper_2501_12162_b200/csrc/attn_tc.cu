@@ -31,6 +31,8 @@
 //               tcgen05.ld O, * 1/l, bf16 store, optional natural-log LSE; or,
 //               for a unit split across CTAs (split-KV), the fp32 partial
 //               (O, m, l), then a share of the unit's cooperative merge.
+#include <mutex>
+
 #include "params.cuh"
 #include "tc_ptx.cuh"
 
@@ -352,14 +354,26 @@ __device__ __forceinline__ int tail_slot(int cta, int e, int grp) {
     return NQ == 1 ? 2 * cta + e : 4 * cta + 2 * e + grp;
 }
 
-template <int D, int NQ>
+// CS = thread-block cluster size (NQ = 1 only): the CS CTAs of a cluster take the
+// CS q-tiles of one (request, kv head) unit and share its K/V stream -- each K or
+// V tile is fetched by ONE of them (round robin over the tile's two operands) and
+// multicast into all CS shared memories; every CTA releases a ring slot in all
+// CS CTAs (DESIGN.md §5 "Clusters").
+template <int D, int NQ, int CS>
 __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
                         const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kt,
                         const __grid_constant__ CUtensorMap tm_vt, const TcParams p) {
+    static_assert(CS == 1 || CS == 2 || CS == 4, "cluster size");
+    static_assert(NQ == 1 || CS == 1, "clusters pair one-q-tile CTAs");
     using S = TcSmem<D, NQ>;
     constexpr int NCH = S::NCH;
     constexpr int kKStages = S::KST, kVStages = S::VST;
+    constexpr uint16_t kMask = (uint16_t)((1u << CS) - 1);  // every CTA of the cluster
+    // cluster coordinates (CS = 1: the CTA itself); the schedule is per cluster
+    const int crank = CS > 1 ? (int)ptx::cluster_ctarank() : 0;
+    const int cl = (int)blockIdx.x / CS;   // cluster index
+    const int ncl = (int)gridDim.x / CS;   // clusters in the grid
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
@@ -384,13 +398,14 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     if (threadIdx.x == 0) {
         ptx::mbar_init(q_full, 1);
         ptx::mbar_init(q_empty, NQ);  // one commit per MMA warp
+        // a ring slot is free once every MMA warp of every CTA of the cluster released it
         for (int s = 0; s < kKStages; ++s) {
             ptx::mbar_init(k_full + s, 1);
-            ptx::mbar_init(k_empty + s, NQ);
+            ptx::mbar_init(k_empty + s, NQ * CS);
         }
         for (int s = 0; s < kVStages; ++s) {
             ptx::mbar_init(v_full + s, 1);
-            ptx::mbar_init(v_empty + s, NQ);
+            ptx::mbar_init(v_empty + s, NQ * CS);
         }
         for (int q = 0; q < NQ; ++q) {
             for (int b = 0; b < 2; ++b) {
@@ -411,6 +426,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     if (warp == 1) ptx::tmem_alloc(tmem_holder, TcCfg<NQ>::TMEM);
     ptx::tc_fence_before();
     __syncthreads();
+    if (CS > 1) ptx::cluster_sync();  // peers' barriers initialised before any multicast or remote arrive
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
     pdl_wait();  // the trees come from the select kernel launched just before
@@ -472,7 +488,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             maxnt = max(maxnt, red_tmp[1][k]);
             minnt = min(minnt, red_tmp[2][k]);
         }
-        const int G = gridDim.x;
+        const int G = ncl;  // schedule slots = clusters
         long long T = 0;
         if (can_plan) {
             // exclusive scans of pre[] and preu[]: per-thread chunks, then warp and block totals
@@ -522,7 +538,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             s_nrec = -1;
             if (sk_split) {
                 s_nrec = 0;
-                const int k = (int)blockIdx.x / Sx, sidx = (int)blockIdx.x - k * Sx;
+                const int k = cl / Sx, sidx = cl - k * Sx;
                 if (k < U) {
                     int lo_b = 0, hi_b = n - 1;  // last i with preu[i] <= k
                     while (lo_b < hi_b) {
@@ -567,7 +583,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     const long long TR = T - S0;
                     // every unit must span at most 3 CTAs (the merger reads at most 2 partials)
                     if ((long long)maxnt * G > 2 * TR) tail = false;
-                    const long long a = S0 + TR * blockIdx.x / G, b = S0 + TR * (blockIdx.x + 1) / G;
+                    const long long a = S0 + TR * cl / G, b = S0 + TR * (cl + 1) / G;
                     long long pos = tail ? a : b;
                     while (pos < b) {
                         if (nt_rec + W1 >= kMaxRec) { ok = false; break; }
@@ -587,7 +603,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         pos = ustart + te;
                     }
                 }
-                const int n_whole = tail ? W1 : (U > (int)blockIdx.x ? (U - 1 - (int)blockIdx.x) / G + 1 : 0);
+                const int n_whole = tail ? W1 : (U > cl ? (U - 1 - cl) / G + 1 : 0);
                 ok = ok && n_whole <= kMaxRec;
                 if (!ok) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, -2);
                 s_ntail = ok ? nt_rec : 0;
@@ -598,7 +614,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         const int nrec_static = (!sk_split && s_nrec > 0) ? s_nrec - s_ntail : 0;
         const int rec_base = (!sk_split && s_nrec > 0) ? s_ntail : 0;
         for (int q = threadIdx.x; q < nrec_static; q += blockDim.x) {
-            const long long k = (long long)blockIdx.x + (long long)q * G;
+            const long long k = (long long)cl + (long long)q * G;
             int lo_b = 0, hi_b = n - 1;  // last i with preu[i] <= k
             while (lo_b < hi_b) {
                 const int mid = (lo_b + hi_b + 1) >> 1;
@@ -637,10 +653,13 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             const int n_pages_u = (u.L + p.page_size - 1) / p.page_size;
             int chunk0 = -1;  // first page index currently staged
             if (lane == 0) {
+                // this CTA's q-tiles of the unit: crank*NQ + q (a CTA past the unit's
+                // last q-tile only streams and releases K/V for its cluster)
+                const int nq_loc = max(0, min(NQ, u.nq - crank * NQ));
                 ptx::mbar_wait(q_empty, (unit_it & 1) ^ 1);
-                ptx::mbar_arrive_expect_tx(q_full, (uint32_t)(u.nq * S::Q_BYTES));
-                for (int q = 0; q < u.nq; ++q) {
-                    const int node0 = u.off + (u.mt + q) * (kBM / p.G);
+                ptx::mbar_arrive_expect_tx(q_full, (uint32_t)(nq_loc * S::Q_BYTES));
+                for (int q = 0; q < nq_loc; ++q) {
+                    const int node0 = u.off + (u.mt + crank * NQ + q) * (kBM / p.G);
                     ptx::tma_load_4d(smem + S::OFF_Q + q * S::Q_BYTES, &tm_q, q_full, 0, u.g * p.G, node0, 0);
                 }
             }
@@ -670,6 +689,9 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     uint64_t* full = (is_k ? k_full : v_full) + st;
                     uint64_t* empty = (is_k ? k_empty : v_empty) + st;
                     unsigned char* dst = smem + (is_k ? S::OFF_K : S::OFF_V) + st * S::KV_BYTES;
+                    // cluster: operand 2t (K) / 2t+1 (V) is fetched by CTA (2t + !is_k) % CS and
+                    // multicast; every CTA posts the bytes it will receive on its own barrier
+                    const bool owner = CS == 1 || (2 * t + (is_k ? 0 : 1)) % CS == crank;
                     if (t < u.n_prefix) {
                         const CUtensorMap* tm_c = is_k ? &tm_kc : &tm_vc;
                         const int key0 = t * kBN;
@@ -679,19 +701,22 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         ptx::mbar_wait(empty, ph ^ 1);
                         AS_TRACE(is_k ? 0 : 1, myit);
                         ptx::mbar_arrive_expect_tx(full, bytes);
-                        for (int b = 0; b < nbox; ++b) {
+                        for (int b = 0; owner && b < nbox; ++b) {
                             const int kp = key0 + b * p.box_rows;
                             const int page = pt_s[kp / p.page_size - chunk0];
                             const int slot = kp % p.page_size;
                             // out-of-range pages read as zeros (TMA bounds check); flag them
-                            if (is_k && (page < 0 || page >= p.num_pages)) set_dev_error(p.ws, AS_DEV_BAD_PAGE, p.req_base + u.i);
+                            if (page < 0 || page >= p.num_pages) set_dev_error(p.ws, AS_DEV_BAD_PAGE, p.req_base + u.i);
                             if (p.kv_split_d) {
-                                ptx::tma_load_5d_hint(dst, tm_c, full, 0, slot, 0, u.g, page, pol);
+                                if (CS == 1) ptx::tma_load_5d_hint(dst, tm_c, full, 0, slot, 0, u.g, page, pol);
+                                else ptx::tma_load_5d_mc(dst, tm_c, full, 0, slot, 0, u.g, page, kMask, pol);
                             } else {
 #pragma unroll
-                                for (int c = 0; c < NCH; ++c)
-                                    ptx::tma_load_4d_hint(dst + c * kBN * 128 + b * p.box_rows * 128, tm_c, full,
-                                                          c * 64, slot, u.g, page, pol);
+                                for (int c = 0; c < NCH; ++c) {
+                                    unsigned char* dc = dst + c * kBN * 128 + b * p.box_rows * 128;
+                                    if (CS == 1) ptx::tma_load_4d_hint(dc, tm_c, full, c * 64, slot, u.g, page, pol);
+                                    else ptx::tma_load_4d_mc(dc, tm_c, full, c * 64, slot, u.g, page, kMask, pol);
+                                }
                             }
                         }
                     } else {
@@ -700,7 +725,8 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         ptx::mbar_wait(empty, ph ^ 1);
                         AS_TRACE(is_k ? 0 : 1, myit);
                         ptx::mbar_arrive_expect_tx(full, (uint32_t)(NCH * kBN * 128));
-                        ptx::tma_load_4d(dst, tm_t, full, 0, row0, 0, u.g);
+                        if (CS == 1) ptx::tma_load_4d(dst, tm_t, full, 0, row0, 0, u.g);
+                        else if (owner) ptx::tma_load_4d_mc(dst, tm_t, full, 0, row0, 0, u.g, kMask, pol);
                     }
                 }
                 __syncwarp();
@@ -708,6 +734,18 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 if (tv >= pc.tb && tv < pc.te) ++itv;
             }
             ++unit_it;
+        }
+        if (CS > 1 && lane < 2) {
+            // drain: every CTA of the cluster released every slot's last use, so no
+            // remote arrive or multicast write is still in flight to this CTA at exit
+            const bool is_k = lane == 0;
+            const uint32_t its = is_k ? itk : itv;
+            const int n_st = is_k ? kKStages : kVStages;
+            for (int st = 0; st < n_st; ++st)
+                if (its > (uint32_t)st) {
+                    const uint32_t last_use = (its - 1 - st) / n_st;
+                    ptx::mbar_wait((is_k ? k_empty : v_empty) + st, last_use & 1);
+                }
         }
     } else if (warp <= NQ) {
         // ===================== MMA issuers (warp 1 + q: q-tile q of each unit) =====================
@@ -729,9 +767,21 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         uint32_t k_it = 0, v_it = 0, unit_it = 0, s_it = 0, p_it = 0, o_it = 0;
         RecCursor sc = cur0;
         Piece pc;
+        // release of a K/V ring slot: in every CTA of the cluster (each counts all releases)
+        auto release = [&](uint64_t* bar, bool after_mma) {
+            if (CS == 1) {
+                if (after_mma) ptx::mma_commit(bar);
+                else ptx::mbar_arrive(bar);
+            } else if (after_mma) {
+                ptx::mma_commit_mc(bar, kMask);
+            } else {
+#pragma unroll
+                for (int r2 = 0; r2 < CS; ++r2) ptx::mbar_arrive_remote(bar, (uint32_t)r2);
+            }
+        };
         while (rec_next(p, sc, pc)) {
             const Unit& u = pc.u;
-            const bool mine = q < u.nq;
+            const bool mine = crank * NQ + q < u.nq;
             ptx::mbar_wait(q_full, unit_it & 1);
             auto do_qk = [&](int t) {
                 const int st = k_it % kKStages;
@@ -741,7 +791,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 if (lane == 0) {
                     if (!mine || (kDebug && p.debug_mode >= 2)) {
                         if (mine) ptx::mbar_arrive(s_full(q, s_it & 1));
-                        ptx::mbar_arrive(k_empty + st);
+                        release(k_empty + st, false);
                         if (t == pc.te - 1) ptx::mbar_arrive(q_empty);
                     } else {
                         const uint32_t s_col = tq + (s_it & 1) * 64;
@@ -754,7 +804,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                             ptx::mma_bf16_ss(s_col, a, b, idesc_qk, ks > 0 ? 1u : 0u);
                         }
                         ptx::mma_commit(s_full(q, s_it & 1));
-                        ptx::mma_commit(k_empty + st);
+                        release(k_empty + st, true);
                         if (t == pc.te - 1) ptx::mma_commit(q_empty);
                     }
                 }
@@ -767,7 +817,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 ptx::mbar_wait(v_full + st, (v_it / kVStages) & 1);
                 if (lane == 0 && q == 0) AS_TRACE(3, v_it);
                 if (!mine) {
-                    if (lane == 0) ptx::mbar_arrive(v_empty + st);
+                    if (lane == 0) release(v_empty + st, false);
                     __syncwarp();
                     ++v_it;
                     return;
@@ -797,7 +847,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 __syncwarp();
                 if (kDebug && p.debug_mode >= 2) {
                     if (lane == 0) {
-                        ptx::mbar_arrive(v_empty + st);
+                        release(v_empty + st, false);
                         ptx::mbar_arrive(pv_done(q, pbuf));
                     }
                 } else if (lane == 0) {
@@ -807,7 +857,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         const uint64_t b = ptx::sw128_desc(v_base + st * S::KV_BYTES + kk * 16 * 128, kBN * 128, 1024);
                         ptx::mma_bf16_ts(o_col, tq + pbuf * 64 + kk * 8, b, idesc_pv, (t > pc.tb || kk > 0) ? 1u : 0u);
                     }
-                    ptx::mma_commit(v_empty + st);
+                    release(v_empty + st, true);
                     ptx::mma_commit(pv_done(q, pbuf));
                 }
                 __syncwarp();
@@ -849,9 +899,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         Piece pc;
         while (rec_next(p, sc, pc)) {
             const Unit& u = pc.u;
-            if (grp >= u.nq) continue;  // this unit has no q-tile for this group
+            const int qi = crank * NQ + grp;  // this group's q-tile within the unit
+            if (qi >= u.nq) continue;          // the unit has no q-tile for this group
             const int G = p.G;
-            const int rr = (u.mt + grp) * kBM + r;
+            const int rr = (u.mt + qi) * kBM + r;
             const bool row_ok = rr < u.K * G;
             const int node = rr / G;
             const int hh = rr - node * G;
@@ -989,7 +1040,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             const bool full = (pc.tb == 0 && pc.te == u.nt);
             const bool tailp = !full && pc.x <= -2;  // tail stream-K piece (else co-resident split-KV)
             const int lead_warp = 1 + NQ + 4 * grp;  // first softmax warp of this group
-            const int wq = pc.w + grp;               // counters of this q-tile
+            const int wq = pc.w + qi;                // counters of this q-tile
             const size_t orow = (size_t)(u.off + node) * p.n_q + (size_t)u.g * G + hh;
             __shared__ int s_merge[NQ];
             bool merge_now = false;
@@ -1056,7 +1107,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 // the unit's pieces: the CTAs whose remainder-stream ranges [tr*c/G, tr*(c+1)/G)
                 // meet [x0, x0 + nt); a CTA's piece is its first (e = 0) unless the unit starts
                 // strictly inside that CTA's range (then it is its last, e = 1)
-                const long long Gd = gridDim.x, tr = pc.tr;
+                const long long Gd = ncl, tr = pc.tr;  // the partition is over clusters
                 auto start = [&](long long c) { return tr * c / Gd; };
                 auto cta_of = [&](long long x) {
                     long long c = x * Gd / (tr > 0 ? tr : 1);
@@ -1067,9 +1118,9 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 const long long cA = cta_of(pc.x0), cB = cta_of((long long)pc.x0 + u.nt - 1);
                 int oth[3] = {0, 0, 0}, n_oth = 0;
                 for (long long c = cA; c <= cB && n_oth < 3; ++c) {
-                    if (c == (long long)blockIdx.x) continue;
+                    if (c == (long long)cl) continue;
                     const int e = (c > cA || start(cA) == pc.x0) ? 0 : 1;
-                    oth[n_oth++] = tail_slot<NQ>((int)c, e, grp);
+                    oth[n_oth++] = tail_slot<NQ>((int)c * CS + crank, e, grp);  // same rank in cluster c
                 }
                 tail_merge<D>(o_addr, m_ref, l_sum, p.partial, p.slot_floats, n_oth, oth[0], oth[1], oth[2], r,
                               row_ok ? p.out + orow * D : nullptr, (row_ok && p.lse != nullptr) ? p.lse + orow : nullptr);
@@ -1094,8 +1145,8 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 // columns for all rows (all pieces of a unit are co-resident: one piece
                 // per CTA of a persistent grid), so no CTA merges a whole unit alone.
                 const int Sx = sk_split;
-                const int sidx = (int)blockIdx.x % Sx;
-                const int b0 = (int)blockIdx.x - sidx;
+                const int sidx = cl % Sx;
+                const int b0 = cl - sidx;  // cluster of the unit's piece 0; piece s2 on cluster b0 + s2
                 auto live = [&](int s2) { return u.nt * (s2 + 1) / Sx > u.nt * s2 / Sx; };
                 int n_live = 0, my_rank = 0;
                 for (int s2 = 0; s2 < Sx; ++s2)
@@ -1116,7 +1167,8 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
                     p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 3] = tn;  // all pieces published
                 }
-                split_merge<D>(p.partial + (size_t)(2 * b0 + grp) * p.slot_floats, 2 * p.slot_floats, Sx, u.nt, r,
+                split_merge<D>(p.partial + (size_t)(2 * (b0 * CS + crank) + grp) * p.slot_floats,
+                               (size_t)2 * CS * p.slot_floats, Sx, u.nt, r,
                                my_rank, n_live, row_ok ? p.out + orow * D : nullptr,
                                (my_rank == 0 && row_ok && p.lse != nullptr) ? p.lse + orow : nullptr);
                 if (kDebug && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
@@ -1140,6 +1192,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if (CS > 1) ptx::cluster_sync();  // no peer still multicasts into, or arrives on, this CTA
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, TcCfg<NQ>::TMEM);
@@ -1157,10 +1210,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
-template <int D, int NQ>
+template <int D, int NQ, int CS>
 static int launch_shape(const CUtensorMap* maps, const TcParams& p, int grid, cudaStream_t stream) {
     const int smem = TcSmem<D, NQ>::ALLOC;
-    if (cudaFuncSetAttribute(tree_attn_tc_kernel<D, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+    if (cudaFuncSetAttribute(tree_attn_tc_kernel<D, NQ, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
         cudaSuccess)
         return -1;
     cudaLaunchConfig_t cfg = {};
@@ -1168,33 +1221,89 @@ static int launch_shape(const CUtensorMap* maps, const TcParams& p, int grid, cu
     cfg.blockDim = dim3(TcCfg<NQ>::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     cfg.attrs = attr;
-    cfg.numAttrs = fill_launch_attrs(attr);
-    if (cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<D, NQ>, maps[0], maps[1], maps[2], maps[3], maps[4], p) !=
+    int na = 0;
+    if (CS > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = CS;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    na += fill_launch_attrs(attr + na);
+    cfg.numAttrs = na;
+    if (cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<D, NQ, CS>, maps[0], maps[1], maps[2], maps[3], maps[4], p) !=
         cudaSuccess)
         return -1;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+// CTAs of a cluster shape that can be resident at once (the persistent grid and the
+// co-resident split-KV pieces need every CTA resident): per device, cached.
+template <int D, int CS>
+static int resident_ctas(int n_sms) {
+    const int want = n_sms * TcCfg<1>::CTAS;
+    if (CS == 1) return want;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+    static std::mutex mu;
+    static int cache[64] = {0};
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache[dev] == 0) {
+        const int smem = TcSmem<D, 1>::ALLOC;
+        if (cudaFuncSetAttribute(tree_attn_tc_kernel<D, 1, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
+            return 0;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(want);
+        cfg.blockDim = dim3(TcCfg<1>::THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, tree_attn_tc_kernel<D, 1, CS>, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        cache[dev] = min(want, nc * CS);
+    }
+    return cache[dev];
+}
+
 int tc_ctas_per_sm() { return kCtasPerSm; }
 
-// p0.nq selects the CTA shape (1: one q-tile per CTA, 2 CTAs/SM; 2: paired
-// q-tiles sharing K/V, 1 CTA/SM).  Every CTA replays a list of at most kMaxRec
-// pieces built in its prologue: batches with more units than kMaxRec * grid are
-// verified in request chunks.
+// p0.nq selects the CTA shape: 1 (one q-tile per CTA, 2 CTAs/SM), 2 (paired q-tiles
+// sharing K/V in one CTA, 1 CTA/SM); p0.cs > 1 (with nq 1): clusters of cs one-q-tile
+// CTAs sharing each K/V tile fetch by multicast.  Every CTA replays a list of at most
+// kMaxRec pieces built in its prologue: batches with more units than kMaxRec * grid
+// are verified in request chunks.
 int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, int n_sms, cudaStream_t stream) {
     const int nq = p0.nq == 2 ? 2 : 1;
-    const int grid_full = n_sms * (nq == 2 ? TcCfg<2>::CTAS : TcCfg<1>::CTAS);
-    const int units_per_req = p0.n_kv * ((p0.mt_max + nq - 1) / nq);
-    int chunk = units_per_req > 0 ? max(1, kMaxRec * grid_full / units_per_req) : p0.n_req;
+    const int cs = (nq == 1 && (p0.cs == 2 || p0.cs == 4)) ? p0.cs : 1;
+    int grid_full = n_sms * (nq == 2 ? TcCfg<2>::CTAS : TcCfg<1>::CTAS);
+    if (cs > 1) {
+        const int res = head_dim == 128 ? (cs == 2 ? resident_ctas<128, 2>(n_sms) : resident_ctas<128, 4>(n_sms))
+                                        : (cs == 2 ? resident_ctas<64, 2>(n_sms) : resident_ctas<64, 4>(n_sms));
+        if (res < cs) return -1;
+        grid_full = res / cs * cs;
+    }
+    const int qpu = nq * cs;  // q-tiles per unit
+    const int units_per_req = p0.n_kv * ((p0.mt_max + qpu - 1) / qpu);
+    int chunk = units_per_req > 0 ? max(1, kMaxRec * (grid_full / cs) / units_per_req) : p0.n_req;
     // the prologue's schedule plan holds at most PLAN_N requests (prefix sums, geometry)
     const int plan_half = head_dim == 128 ? (nq == 2 ? TcSmem<128, 2>::PLAN_N : TcSmem<128, 1>::PLAN_N)
                                           : (nq == 2 ? TcSmem<64, 2>::PLAN_N : TcSmem<64, 1>::PLAN_N);
     chunk = min(chunk, plan_half);
     for (int r0 = 0; r0 < p0.n_req; r0 += chunk) {
         TcParams p = p0;
-        p.nq = nq;
+        p.nq = qpu;
+        p.cs = cs;
         p.n_req = min(chunk, p0.n_req - r0);
         p.page_table = p0.page_table + (size_t)r0 * p0.max_pages;
         p.kv_len = p0.kv_len + r0;
@@ -1202,11 +1311,20 @@ int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, in
         p.req_base = p0.req_base + r0;
         p.n_units = units_per_req * p.n_req;
         int grid = grid_full;
-        if (!p.stream_k && p.n_units < grid) grid = p.n_units;
+        if (!p.stream_k && p.n_units * cs < grid) grid = p.n_units * cs;
         if (grid <= 0) continue;
         int rc;
-        if (head_dim == 128) rc = nq == 2 ? launch_shape<128, 2>(maps, p, grid, stream) : launch_shape<128, 1>(maps, p, grid, stream);
-        else rc = nq == 2 ? launch_shape<64, 2>(maps, p, grid, stream) : launch_shape<64, 1>(maps, p, grid, stream);
+        if (head_dim == 128) {
+            rc = nq == 2 ? launch_shape<128, 2, 1>(maps, p, grid, stream)
+                 : cs == 2 ? launch_shape<128, 1, 2>(maps, p, grid, stream)
+                 : cs == 4 ? launch_shape<128, 1, 4>(maps, p, grid, stream)
+                           : launch_shape<128, 1, 1>(maps, p, grid, stream);
+        } else {
+            rc = nq == 2 ? launch_shape<64, 2, 1>(maps, p, grid, stream)
+                 : cs == 2 ? launch_shape<64, 1, 2>(maps, p, grid, stream)
+                 : cs == 4 ? launch_shape<64, 1, 4>(maps, p, grid, stream)
+                           : launch_shape<64, 1, 1>(maps, p, grid, stream);
+        }
         if (rc != 0) return -1;
     }
     return 0;

@@ -63,7 +63,8 @@ struct TcParams {
     void* ws;
     int n_units;
     int req_base;         // caller's index of request 0 of this launch (device-error reports)
-    int nq;               // q-tiles per unit / CTA shape (1 or 2, chosen by the host)
+    int nq;               // host in: CTA shape (1 or 2 q-tiles per CTA); kernel: q-tiles per unit (nq * cs)
+    int cs;               // thread-block cluster size (1, 2, 4; one-q-tile CTAs sharing K/V by multicast)
     int mt_max;           // q-tiles per (request, kv head) upper bound (unit id stride)
     int stream_k;         // 1: split-KV allowed (needs cnt/cnt2/partial in the workspace), 0: whole units only
     int* cnt;             // [n_units] tiles completed per split unit (zeroed, self-resetting)

@@ -440,13 +440,23 @@ def test_attn_fp32(ada, ci):
     assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-4
 
 
+def _shape_env(monkeypatch, shape):
+    """Schedule overrides: "1"/"2" = AS_ATTN_NQ (q-tiles per CTA), "cs2"/"cs4" =
+    AS_ATTN_CS (clusters of one-q-tile CTAs sharing K/V by multicast)."""
+    if shape.startswith("cs"):
+        monkeypatch.setenv("AS_ATTN_CS", shape[2:])
+    elif shape != "auto":
+        monkeypatch.setenv("AS_ATTN_NQ", shape)
+
+
 @pytest.mark.parametrize("ci", range(1, len(ATTN_CASES)))
-@pytest.mark.parametrize("nq", ["auto", "1", "2"])
+@pytest.mark.parametrize("nq", ["auto", "1", "2", "cs2", "cs4"])
 def test_attn_bf16(ada, ci, nq, monkeypatch):
-    """Both CTA shapes: one q-tile per CTA (NQ=1) and paired q-tiles sharing
-    every K/V tile (NQ=2; odd q-tile counts leave the second group idle)."""
-    if nq != "auto":
-        monkeypatch.setenv("AS_ATTN_NQ", nq)
+    """Every CTA shape: one q-tile per CTA (NQ=1), paired q-tiles sharing every
+    K/V tile (NQ=2; odd q-tile counts leave the second group idle), and clusters
+    of 2 / 4 one-q-tile CTAs fetching each K/V tile once and multicasting it
+    (CTAs past a head's last q-tile only stream and release)."""
+    _shape_env(monkeypatch, nq)
     w = _attn_case(ATTN_CASES[ci], True, 400 + ci)
     scale = np.float32(1.0 / np.sqrt(w["q"].shape[2]))
     ref, ref_lse = oracle_attn(w, scale)
@@ -461,9 +471,9 @@ def test_attn_bf16(ada, ci, nq, monkeypatch):
     assert np.abs(lse.cpu().numpy() - ref_lse).max() <= BF16_TOL
 
 
-@pytest.mark.parametrize("nq", ["1", "2"])
+@pytest.mark.parametrize("nq", ["1", "2", "cs2"])
 def test_attn_bf16_request_chunks(ada, nq, monkeypatch):
-    monkeypatch.setenv("AS_ATTN_NQ", nq)
+    _shape_env(monkeypatch, nq)
     """More units than the kernel's per-CTA piece lists hold (n_kv * q-tiles *
     n_req > 64 * 2 * SMs): the library verifies the batch in request chunks;
     every request, including those at chunk edges, must match the oracle."""
@@ -504,14 +514,15 @@ def test_attn_bf16_plan_capacity_chunks(ada):
 
 
 @pytest.mark.parametrize("sk", ["0", "1", "2"])
-def test_attn_bf16_many_units(ada, sk, monkeypatch):
+@pytest.mark.parametrize("shape", ["1", "cs2"])
+def test_attn_bf16_many_units(ada, sk, shape, monkeypatch):
     """More units than CTAs (64 requests x 8 kv heads = 512 > 296 one-q-tile
     CTAs), ragged kv lengths, under every AS_ATTN_STREAMK setting (0: never
     split; 1/2: split-KV allowed -- not taken here, units outnumber CTAs), two
     launches on one workspace.  (A tail stream-K schedule for this regime was
     tried in commit 2530b31 and measured slower.)"""
     monkeypatch.setenv("AS_ATTN_STREAMK", sk)
-    monkeypatch.setenv("AS_ATTN_NQ", "1")
+    _shape_env(monkeypatch, shape)
     rng = np.random.default_rng(57)
     n = 64
     sizes = rng.integers(20, 33, n)
@@ -569,7 +580,7 @@ def test_attn_bf16_nan_in_unused_cache_slots(ada):
     assert np.abs(o - ref).max() <= BF16_TOL
 
 
-@pytest.mark.parametrize("nq", ["1", "2"])
+@pytest.mark.parametrize("nq", ["1", "2", "cs2", "cs4"])
 @pytest.mark.parametrize("pad", ["nan", "inf"])
 def test_attn_bf16_nan_in_tree_padding(ada, nq, pad, monkeypatch):
     """Tree tiles are loaded 64 rows at a time from the request's first row: the
@@ -577,7 +588,7 @@ def test_attn_bf16_nan_in_tree_padding(ada, nq, pad, monkeypatch):
     tree_offsets[n] (e.g. a budget-sized torch.empty buffer).  NaN/Inf there
     must not reach any output (P is 0 there, but 0 * NaN = NaN in the PV MMA).
     K_i around the 64-row tile edges: 63, 64, 65, 127, 128."""
-    monkeypatch.setenv("AS_ATTN_NQ", nq)
+    _shape_env(monkeypatch, nq)
     sizes = [63, 64, 65, 127, 128, 1, 191, 256]
     w = _attn_case((sizes, [70, 0, 129, 64, 5, 33, 64, 1], 8, 2, 128, 64, "random", 1.0), True, 91)
     scale = np.float32(1.0 / np.sqrt(128))
@@ -688,8 +699,9 @@ def test_dist_accept_and_commit_single_rank_nccl(ada):
             tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cfg", ["c2", "c3", "c4", "c5"])
-def test_attn_bf16_full_size_sampled(ada, cfg):
+@pytest.mark.parametrize("cfg,shape", [("c2", "auto"), ("c3", "auto"), ("c4", "auto"), ("c5", "auto"),
+                                       ("c4", "cs4"), ("c4", "2"), ("c5", "cs2"), ("c3", "cs2")])
+def test_attn_bf16_full_size_sampled(ada, cfg, shape, monkeypatch):
     """BASELINE full sizes in the launch bench.py times; the oracle checks sampled
     requests (all their heads).  The oracle's trees come from the oracle's own
     select on the same forest (asserted bit-identical to the GPU's)."""
