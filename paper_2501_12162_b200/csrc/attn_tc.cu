@@ -44,7 +44,7 @@ constexpr int kBN = 64;           // keys per tile
 //  NQ = 1: 192 threads (TMA producer, MMA, 4 softmax warps), 2 CTAs per SM,
 //          256 TMEM columns, 2+2-stage K/V rings -- every unit its own K/V stream;
 //  NQ = 2: 352 threads (producer, 2 MMA warps, 2 x 4 softmax warps), 1 CTA/SM, all
-//          512 TMEM columns, 4+4-stage rings -- the two q-tiles of a (request,
+//          512 TMEM columns, 4+5-stage rings -- the two q-tiles of a (request,
 //          kv head) share every K/V tile (loaded once for both), chosen when the
 //          trees span more than one 128-row q-tile (c4/c5 shapes).
 // TMEM columns of q-tile q (base q * (128 + D)): S/P buffers b = 0, 1 at
@@ -55,7 +55,7 @@ template <> struct TcCfg<1> {
     static constexpr int THREADS = 192, CTAS = 2, TMEM = 256, KST = 2, VST = 2;
 };
 template <> struct TcCfg<2> {
-    static constexpr int THREADS = 352, CTAS = 1, TMEM = 512, KST = 4, VST = 4;
+    static constexpr int THREADS = 352, CTAS = 1, TMEM = 512, KST = 4, VST = 5;
 };
 constexpr int kCtasPerSm = 2;     // max over the shapes (workspace sizing)
 constexpr int kPtChunk = 256;     // page-table entries staged per refill
