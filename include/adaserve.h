@@ -154,6 +154,28 @@ as_status as_select_trees(int32_t n_req, int32_t n_cand_total, const int32_t* ca
                           int32_t* tree_token, int32_t* slo_count, void* workspace,
                           size_t workspace_bytes, void* stream);
 
+/*
+ * Selection variants without SLO awareness (NEXT-4; reading R24 in DESIGN.md):
+ * request i keeps its root plus its best m_i candidates, chosen greedily by
+ * (f-hat desc, lower local index) (R8) -- the first m_i entries of pi_i, an
+ * ancestor-closed set (App. B) -- with
+ *   m_i = min(m_base + (i < m_extra ? 1 : 0), C_i - 1).
+ *   EqualGreedy (dead-text ablation "evenly distributes the budget among
+ *   requests and greedily selects tokens ... for each request"): budget B split
+ *   evenly, m_base = floor(B / n) - 1, m_extra = B mod n (a share a request
+ *   cannot fill stays unused); Eagle-2 top-m: m_base = m, m_extra = 0.
+ * Same inputs/outputs as as_select_trees (no slo_deficit, depth_d or budget;
+ * tree_parent / tree_src / tree_depth / tree_token need sum_i (1 + m_i) rows);
+ * kept [n_req] (or NULL) receives m_i.  Requires 0 <= m_extra <= n_req,
+ * m_base >= 0.  Same kernel, device preconditions and workspace as
+ * as_select_trees; bit-identical to the per-request greedy loop (the oracle).
+ */
+as_status as_select_topm(int32_t n_req, int32_t n_cand_total, const int32_t* cand_offsets,
+                         const int32_t* cand_parent, const float* cand_prob, const int32_t* cand_token,
+                         int32_t m_base, int32_t m_extra, int32_t* tree_offsets, int32_t* tree_parent,
+                         int32_t* tree_src, int32_t* tree_depth, int32_t* tree_token, int32_t* kept,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------------- */
 /* Verify: tree-masked attention over the paged KV cache */
 /* ------------------------------------------------------------------------- */

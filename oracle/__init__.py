@@ -13,6 +13,10 @@ Contents
 * ``select_closed_form`` -- O2: the data-parallel restatement of Alg. 2
   (per-request sorted prefixes, clamped scan in A order, global top-R).  Pinned
   to ``select_literal`` by fuzzing (proof sketch in DESIGN.md §Select).
+* ``select_per_request_greedy`` / ``equal_greedy_caps`` -- NEXT-4 selection
+  variants without SLO awareness: EqualGreedy and Eagle-2 top-m
+  (P:L1218), per-request GetTop loops (reading R24); pinned by np.lexsort
+  per-request top-k and by the n = 1 identity with GlobalGreedy.
 * ``alg1_optimal`` / ``brute_force_optimal`` -- Alg. 1 (P:L638-679) and an
   exhaustive enumerator; pins App. C optimality on tiny forests.
 * ``tree_attn`` -- explicit-mask attention per tree node in fp64 (C).
@@ -157,6 +161,63 @@ def select_closed_form(cand_offsets, cand_parent, cand_prob, slo_deficit, depth_
         m[i] += 1
     chosen = [set(pis[i][: s[i] + m[i]].tolist()) | {0} for i in range(n)]
     return chosen, s, m
+
+
+def select_per_request_greedy(cand_offsets, cand_parent, cand_prob, caps):
+    """Selection without SLO awareness (NEXT-4, reading R24): request i keeps
+    its root and then, caps[i] times or until its candidates run out, GetTop of
+    its own remaining candidates -- the linear-scan argmax of (f-hat, -index)
+    (R8), as Alg. 2's GetTop restricted to one request.  EqualGreedy
+    ("evenly distributes the budget among requests and greedily selects
+    tokens from the candidate token tree for each request") uses
+    caps = equal_greedy_caps(n, B); Eagle-2's top-m uses caps = m.
+    Emitted like select_literal: ascending local index, compact parents, depth;
+    'kept' = the non-root nodes taken per request."""
+    co = [int(x) for x in cand_offsets]
+    n = len(co) - 1
+    par = np.asarray(cand_parent, np.int64)
+    f = np.asarray(cand_prob, np.float32)
+    to = [0]
+    tp, ts, td, kept = [], [], [], []
+    for i in range(n):
+        C = co[i + 1] - co[i]
+        chosen = {0}
+        for _ in range(int(caps[i])):
+            best = None
+            for j in range(1, C):  # GetTop: largest f-hat, lowest index on ties
+                if j in chosen:
+                    continue
+                if best is None or f[co[i] + j] > f[co[i] + best]:
+                    best = j
+            if best is None:
+                break
+            chosen.add(best)
+        nodes = sorted(chosen)
+        remap = {v: k for k, v in enumerate(nodes)}
+        for v in nodes:
+            pv = int(par[co[i] + v]) if v > 0 else 0
+            if pv not in remap:
+                raise ValueError("selection not ancestor-closed")
+            d, u = 0, v
+            while u != 0:
+                u = int(par[co[i] + u])
+                d += 1
+            ts.append(v)
+            tp.append(remap[pv])
+            td.append(d)
+        kept.append(len(nodes) - 1)
+        to.append(to[-1] + len(nodes))
+    return dict(tree_offsets=np.array(to, np.int32), tree_parent=np.array(tp, np.int32),
+                tree_src=np.array(ts, np.int32), tree_depth=np.array(td, np.int32), kept=np.array(kept, np.int32))
+
+
+def equal_greedy_caps(n, budget):
+    """EqualGreedy's even split of the budget B (roots included, R1): floor(B/n)
+    nodes per request and one more for the first B mod n requests (R24), i.e.
+    share - 1 non-root candidates each."""
+    if budget < n:
+        raise ValueError("budget < n_req (R10)")
+    return np.array([budget // n + (1 if i < budget % n else 0) - 1 for i in range(n)], np.int64)
 
 
 def trees_from_result(res, n):

@@ -13,7 +13,7 @@ import os
 
 import torch
 
-__all__ = ["lib", "select_trees", "select_global_greedy", "sample_tokens", "tree_verify_attn", "accept_tokens", "Workspace", "check_device_error",
+__all__ = ["lib", "select_trees", "select_global_greedy", "select_topm", "select_equal_greedy", "sample_tokens", "tree_verify_attn", "accept_tokens", "Workspace", "check_device_error",
            "selftest_umma", "AS_ACCEPT_FUSED", "AS_ACCEPT_WALK_ONLY", "AS_ACCEPT_COMMIT_ONLY",
            "AS_ACCEPT_WALK_RECORDS", "AS_ACCEPT_COMMIT_RECORDS", "beam_step", "beam_workspace_size", "AdaServeError",
            "select_workspace_size", "attn_workspace_size", "accept_workspace_size", "DEVICE_ERRORS"]
@@ -58,6 +58,8 @@ def lib():
         L.as_accept_workspace_size.argtypes = [_c_i32]
         L.as_select_trees.argtypes = [_c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32,
                                       _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_sz, _vp]
+        L.as_select_topm.argtypes = [_c_i32, _c_i32, _vp, _vp, _vp, _vp, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp,
+                                     _vp, _vp, _c_sz, _vp]
         L.as_tree_verify_attn.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp,
                                           _c_i32, _c_i32, _vp, _c_i32, _vp, _vp, _vp, _f32, _vp, _vp, _vp, _c_sz,
                                           _vp]
@@ -225,6 +227,50 @@ def select_global_greedy(cand_offsets, cand_parent, cand_prob, budget, cand_toke
     zeros = torch.zeros(max(n, 1), dtype=torch.float64, device=cand_prob.device)[:n]
     return select_trees(cand_offsets, cand_parent, cand_prob, zeros, 0, 0, budget, cand_token=cand_token, out=out,
                         workspace=workspace)
+
+def select_topm(cand_offsets, cand_parent, cand_prob, m_base, m_extra=0, cand_token=None, out=None,
+                workspace=None):
+    """as_select_topm (NEXT-4, reading R24): request i keeps its root and its
+    best min(m_base + (i < m_extra), C_i - 1) candidates by (f-hat desc, index
+    asc).  Eagle-2 top-m: select_topm(..., m); EqualGreedy: select_equal_greedy.
+    Returns the same dict as select_trees ('kept' instead of 'slo_count')."""
+    n = cand_offsets.numel() - 1
+    _need(cand_offsets, torch.int32, "cand_offsets")
+    _need(cand_parent, torch.int32, "cand_parent")
+    _need(cand_prob, torch.float32, "cand_prob")
+    N = cand_prob.numel()
+    dev = cand_prob.device
+    if out is None:
+        cap = max(1, n + n * int(m_base) + int(m_extra))
+        cap = min(cap, max(N, 1))
+        out = dict(tree_offsets=torch.empty(n + 1, dtype=torch.int32, device=dev),
+                   tree_parent=torch.empty(cap, dtype=torch.int32, device=dev),
+                   tree_src=torch.empty(cap, dtype=torch.int32, device=dev),
+                   tree_depth=torch.empty(cap, dtype=torch.int32, device=dev),
+                   tree_token=torch.empty(cap, dtype=torch.int32, device=dev) if cand_token is not None else None,
+                   kept=torch.empty(max(n, 1), dtype=torch.int32, device=dev))
+    ws = workspace if workspace is not None else Workspace(select_workspace_size(n, N), dev)
+    ws.ensure(select_workspace_size(n, N))
+    st = lib().as_select_topm(n, N, _ptr(cand_offsets), _ptr(cand_parent), _ptr(cand_prob), _ptr(cand_token),
+                              int(m_base), int(m_extra), _ptr(out["tree_offsets"]), _ptr(out["tree_parent"]),
+                              _ptr(out["tree_src"]), _ptr(out.get("tree_depth")), _ptr(out.get("tree_token")),
+                              _ptr(out.get("kept")), ws.ptr, ws.nbytes, _stream())
+    _check(st, "as_select_topm")
+    out["workspace"] = ws
+    return out
+
+
+def select_equal_greedy(cand_offsets, cand_parent, cand_prob, budget, cand_token=None, out=None, workspace=None):
+    """EqualGreedy (reading R24): the budget B (roots included, R1)
+    split evenly -- floor(B/n) nodes per request, one more for the first B mod n
+    requests -- each request filling its share greedily by f-hat."""
+    n = cand_offsets.numel() - 1
+    if budget < n:
+        raise AdaServeError("budget smaller than the number of requests (R10)")
+    if n == 0:
+        return select_topm(cand_offsets, cand_parent, cand_prob, 0, 0, cand_token, out, workspace)
+    return select_topm(cand_offsets, cand_parent, cand_prob, budget // n - 1, budget % n, cand_token, out, workspace)
+
 
 def tree_verify_attn(q, k_tree, v_tree, k_cache, v_cache, page_table, kv_len, tree_offsets, tree_parent, sm_scale,
                      want_lse=False, out=None, lse=None, workspace=None):

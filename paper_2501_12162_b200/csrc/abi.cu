@@ -164,6 +164,26 @@ as_status as_select_trees(int32_t n_req, int32_t n_cand_total, const int32_t* ca
     return rc == 0 ? AS_OK : AS_ERR_CUDA;
 }
 
+as_status as_select_topm(int32_t n_req, int32_t n_cand_total, const int32_t* cand_offsets, const int32_t* cand_parent,
+                         const float* cand_prob, const int32_t* cand_token, int32_t m_base, int32_t m_extra,
+                         int32_t* tree_offsets, int32_t* tree_parent, int32_t* tree_src, int32_t* tree_depth,
+                         int32_t* tree_token, int32_t* kept, void* workspace, size_t workspace_bytes, void* stream) {
+    if (n_req < 0 || n_cand_total < n_req || m_base < 0 || m_extra < 0 || m_extra > n_req || !tree_offsets)
+        return AS_ERR_INVALID_ARG;
+    if (n_req > 4096) return AS_ERR_UNSUPPORTED;
+    if (n_req == 0) {
+        return cudaMemsetAsync(tree_offsets, 0, sizeof(int32_t), S(stream)) == cudaSuccess ? AS_OK : AS_ERR_CUDA;
+    }
+    if (!cand_offsets || !cand_parent || !cand_prob || !tree_parent || !tree_src) return AS_ERR_INVALID_ARG;
+    if (tree_token && !cand_token) return AS_ERR_INVALID_ARG;
+    if (!workspace || !al256(workspace) || workspace_bytes < select_ws_bytes(n_req, n_cand_total))
+        return AS_ERR_WORKSPACE;
+    int rc = launch_select(n_req, n_cand_total, cand_offsets, cand_parent, cand_prob, cand_token, nullptr, 0, m_base,
+                           0, tree_offsets, tree_parent, tree_src, tree_depth, tree_token, kept, workspace, S(stream),
+                           1, m_extra);
+    return rc == 0 ? AS_OK : AS_ERR_CUDA;
+}
+
 // ----------------------------------------------------------------- attention
 size_t as_attn_workspace_size(as_dtype dtype, int32_t n_req, int32_t n_tree_rows, int32_t n_q_heads,
                               int32_t head_dim, int32_t max_kv_len) {

@@ -80,7 +80,8 @@ struct TcParams {
 
 size_t select_ws_bytes(int n_req, int n_cand_total);
 int launch_select(int, int, const int32_t*, const int32_t*, const float*, const int32_t*, const double*, int, int,
-                  int, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, void*, cudaStream_t);
+                  int, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, void*, cudaStream_t,
+                  int topm = 0, int n_max_extra = 0);
 int launch_accept(const AcceptParams& p, const void* target_logits, int logits_bf16, int vocab, int32_t* argmax_buf,
                   cudaStream_t stream);
 int launch_attn_simt(const SimtParams& p, int head_dim, cudaStream_t stream);

@@ -72,6 +72,9 @@ struct SelectParams {
     void* ws;
     uint64_t* skey_g;   // [N - n] workspace pi keys (used when a CTA's candidates do not fit smem)
     int cand_cap;       // candidates a CTA can stage in shared memory
+    int topm;           // 1: per-request greedy caps (as_select_topm): request i keeps
+                        //    min(n_max + (i < n_max_extra), C_i - 1) best candidates, no budget
+    int n_max_extra;
     int dbg_stop;       // latency profiling only (AS_SEL_STOP): return after phase k (wrong outputs)
 };
 
@@ -212,6 +215,7 @@ __device__ __forceinline__ int sort_request(const SelectParams& p, int i, const 
         const int s = e * 32 + lane;
         fv[e] = (s < nr) ? __uint_as_float((uint32_t)(key_out[s] >> 32)) : 0.f;
     }
+    if (p.topm) return min(p.n_max + (i < p.n_max_extra ? 1 : 0), nr);  // per-request greedy cap
     // SLO stage threshold with unlimited budget: the loop adds
     // f-hat in pi order in fp64 starting from n_acc = 1.0 (R9) and stops at the
     // first k with n_acc >= A_cap, or at lim = min(n_max, nr).
@@ -407,7 +411,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
     if (p.dbg_stop == 0) return;
     // ---- stage: own offsets, every A(r); then f-hat, parents (and tokens) ----
     for (int k = tid; k <= nown; k += kSelThreads) off_s[k] = p.cand_offsets[r0 + k];
-    for (int k = tid; k < n; k += kSelThreads) A_s[k] = p.A[k];
+    if (!p.topm)
+        for (int k = tid; k < n; k += kSelThreads) A_s[k] = p.A[k];
     __syncthreads();
     const int cbase = off_s[0];
     const int ncand = off_s[nown] - cbase;
@@ -486,10 +491,13 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
             __syncthreads();
             // (1d) desired_i (warp 0 of the group) and the A-order rank (warp 1, or 0)
             if (active && wg == 0) {
-                const int des = slo_prefix_len(p, i, keyc + (off - i), nr);
+                const int des = p.topm ? min(p.n_max + (i < p.n_max_extra ? 1 : 0), nr)
+                                       : slo_prefix_len(p, i, keyc + (off - i), nr);
                 if (lane == 0) desired_s[k] = des;
             }
-            if (active && wg == (W > 1 ? 1 : 0)) {
+            if (active && p.topm) {
+                if (wg == 0 && lane == 0) arank_s[k] = i;  // no A ordering: the caps never compete
+            } else if (active && wg == (W > 1 ? 1 : 0)) {
                 const double a = A_s[i];
                 int rk = 0;
                 for (int j = lane; j < n; j += 32) {
@@ -512,13 +520,16 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
             else if (nr <= 64) des = sort_request<2>(p, i, probc + off, parc + off, nr, ko);
             else if (nr <= 128) des = sort_request<4>(p, i, probc + off, parc + off, nr, ko);
             else des = sort_request<8>(p, i, probc + off, parc + off, nr, ko);
-            const double a = A_s[i];
-            int rk = 0;
-            for (int j = lane; j < n; j += 32) {
-                const double b = A_s[j];
-                rk += (b > a) || (b == a && j < i);
+            int rk = i;
+            if (!p.topm) {
+                const double a = A_s[i];
+                rk = 0;
+                for (int j = lane; j < n; j += 32) {
+                    const double b = A_s[j];
+                    rk += (b > a) || (b == a && j < i);
+                }
+                rk = warp_sum(rk);
             }
-            rk = warp_sum(rk);
             if (lane == 0) {
                 desired_s[k] = des;
                 arank_s[k] = rk;
@@ -544,7 +555,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
 
     if (p.dbg_stop == 3) return;
     // ---- (3) budget sequencing, redundant in every CTA (warp 0) ----
-    const int B0 = p.budget - n;
+    const int B0 = p.topm ? 0x3fffffff : p.budget - n;  // topm: the caps alone bound the trees
     if (warp == 0) {
         warp_exclusive_scan(des_all, exc_all, n);
         __syncwarp();
@@ -561,7 +572,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
     __syncthreads();
     const int sum_s = s_bcast[4];
     const int sum_tail = s_bcast[5] - sum_s;
-    const int R = min(B0 - sum_s, sum_tail);
+    const int R = p.topm ? 0 : min(B0 - sum_s, sum_tail);  // topm: no throughput stage
     for (int k = tid; k < nown; k += kSelThreads) {
         const int sv = max(0, min(B0 - exc_all[arank_s[k]], desired_s[k]));
         s_s[k] = sv;
@@ -576,7 +587,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
     // then every CTA picks the same digit.  hsum is double-buffered by pass.
     int sh = 64;
     uint64_t prefix = 0;
-    const bool select_all = (R >= sum_tail);
+    const bool select_all = (R >= sum_tail) && R > 0;
     const bool select_none = (R <= 0);
     if (!select_all && !select_none) {
         int need = R;
@@ -808,9 +819,11 @@ int launch_select(int n_req, int n_cand_total, const int32_t* cand_offsets, cons
                   const float* cand_prob, const int32_t* cand_token, const double* A, int depth_d,
                   int n_max, int budget, int32_t* tree_offsets, int32_t* tree_parent, int32_t* tree_src,
                   int32_t* tree_depth, int32_t* tree_token, int32_t* slo_count, void* ws,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, int topm, int n_max_extra) {
     if (n_req > kSelMaxReq) return -1;
     SelectParams p;
+    p.topm = topm;
+    p.n_max_extra = n_max_extra;
     p.n_req = n_req;
     p.cand_offsets = cand_offsets;
     p.cand_parent = cand_parent;

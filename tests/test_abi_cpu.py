@@ -50,6 +50,12 @@ def test_host_checks_return_without_launch(L):
     st = L.as_select_trees(4, 8, dummy, dummy, dummy, None, dummy, 3, 3, 3, dummy, dummy, dummy, None, None, None,
                            dummy, 1 << 20, None)
     assert st == 2
+    # as_select_topm: m_extra outside [0, n_req] / negative m_base -> AS_ERR_INVALID_ARG
+    f = L.as_select_topm
+    f.argtypes = [ctypes.c_int32, ctypes.c_int32] + [vp] * 4 + [ctypes.c_int32] * 2 + [vp] * 7 + [ctypes.c_size_t, vp]
+    assert f(4, 8, dummy, dummy, dummy, None, 1, 5, dummy, dummy, dummy, None, None, None, dummy, 1 << 20, None) == 1
+    assert f(4, 8, dummy, dummy, dummy, None, -1, 0, dummy, dummy, dummy, None, None, None, dummy, 1 << 20, None) == 1
+    assert f(4, 8, dummy, dummy, dummy, None, 1, 0, dummy, dummy, dummy, None, None, None, None, 0, None) == 4
     # unsupported head_dim -> AS_ERR_UNSUPPORTED
     st = L.as_tree_verify_attn(1, 1, 8, 4, 4, 96, dummy, dummy, dummy, dummy, dummy, 4, 16, dummy, 4, dummy,
                                dummy, dummy, ctypes.c_float(0.1), dummy, None, vp(256 * 64), 256, None)

@@ -222,6 +222,40 @@ def test_select_global_greedy_is_lexsort_topk(ada, seed):
     np.testing.assert_array_equal(out["slo_count"].cpu().numpy()[:n], 0)
 
 
+@pytest.mark.parametrize("seed", range(5))
+def test_select_topm_and_equal_greedy_bit_exact(ada, seed):
+    """NEXT-4 variants (reading R24) through as_select_topm: Eagle-2 top-m and
+    EqualGreedy(B) == the oracle's per-request GetTop loop, bit for bit (src,
+    compact parents, depth, tokens, kept), incl. exact f-hat ties, caps larger
+    than the candidate count, and a batch past the shared staging area."""
+    rng = np.random.default_rng(1300 + seed)
+    n, maxn = [(5, 20), (60, 70), (300, 66), (2500, 100), (1, 257)][seed]
+    F = synth.random_forest(rng, n, maxn, tie_prob=0.4, min_nodes=1)
+    N = int(F["cand_offsets"][-1])
+    tok = rng.integers(0, 128256, N).astype(np.int32)
+    co, cp, cf = dev(F["cand_offsets"]), dev(F["cand_parent"]), dev(F["cand_prob"])
+    for mode in ("topm", "equal"):
+        if mode == "topm":
+            m = int(rng.integers(0, maxn + 3))
+            caps = np.full(n, m)
+            out = ada.select_topm(co, cp, cf, m, cand_token=dev(tok))
+        else:
+            B = n + int(rng.integers(0, max(1, N - n + 1)))
+            caps = oracle.equal_greedy_caps(n, B)
+            out = ada.select_equal_greedy(co, cp, cf, B, cand_token=dev(tok))
+        assert ada.check_device_error(out["workspace"])[0] == 0
+        ref = oracle.select_per_request_greedy(F["cand_offsets"], F["cand_parent"], F["cand_prob"], caps)
+        used = int(ref["tree_offsets"][-1])
+        np.testing.assert_array_equal(out["tree_offsets"].cpu().numpy(), ref["tree_offsets"])
+        np.testing.assert_array_equal(out["tree_src"].cpu().numpy()[:used], ref["tree_src"])
+        np.testing.assert_array_equal(out["tree_parent"].cpu().numpy()[:used], ref["tree_parent"])
+        np.testing.assert_array_equal(out["tree_depth"].cpu().numpy()[:used], ref["tree_depth"])
+        np.testing.assert_array_equal(out["kept"].cpu().numpy()[:n], ref["kept"])
+        req = np.repeat(np.arange(n), np.diff(ref["tree_offsets"]))
+        np.testing.assert_array_equal(out["tree_token"].cpu().numpy()[:used],
+                                      tok[F["cand_offsets"][req] + ref["tree_src"]])
+
+
 def test_select_exact_sum_guards(ada):
     """Both desired_i paths of the kernel: the warp fp64 scan is used only when
     every f-hat >= 2^-24 and 1 + sum < 64 (R9); chains of f-hat = 1.0 (sums past

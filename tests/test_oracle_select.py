@@ -211,3 +211,55 @@ def test_beam_forest_c3_sizes():
     K = np.diff(res["tree_offsets"])
     assert K.sum() <= 1024 and K.min() >= 1 and K.max() <= 65
     _check_invariants(F["cand_offsets"], F["cand_parent"], F["cand_prob"], A, 8, 63, 1024, res)
+
+
+# --------------------------------------------------------------------------- NEXT-4 variants (R24)
+def _lexsort_topk_sets(F, caps):
+    """Independent reference: per request, np.lexsort by (-f, index) over the
+    non-root candidates, first caps[i] -- no loop of the oracle's."""
+    co, cf = F["cand_offsets"], F["cand_prob"]
+    out = []
+    for i in range(len(co) - 1):
+        idx = np.arange(1, co[i + 1] - co[i])
+        f = cf[co[i] + idx].astype(np.float64)
+        order = idx[np.lexsort((idx, -f))]
+        out.append({0} | set(order[: max(0, int(caps[i]))].tolist()))
+    return out
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_per_request_greedy_is_lexsort_topk(seed):
+    rng = np.random.default_rng(500 + seed)
+    n = int(rng.integers(1, 30))
+    F = synth.random_forest(rng, n, int(rng.integers(2, 40)), tie_prob=float(rng.choice([0.0, 0.6])))
+    caps = rng.integers(0, 45, n)
+    res = oracle.select_per_request_greedy(F["cand_offsets"], F["cand_parent"], F["cand_prob"], caps)
+    got = oracle.trees_from_result(res, n)
+    assert got == _lexsort_topk_sets(F, caps)
+    # ancestor-closed, topological emission, compact parents point backwards
+    to = res["tree_offsets"]
+    for i in range(n):
+        seg = slice(to[i], to[i + 1])
+        assert (res["tree_parent"][seg][1:] < np.arange(1, to[i + 1] - to[i])).all()
+        assert (np.diff(res["tree_src"][seg]) > 0).all()
+    np.testing.assert_array_equal(res["kept"], np.diff(to) - 1)
+
+
+def test_equal_greedy_caps_and_single_request_identity():
+    """EqualGreedy splits B evenly (sum of shares = B); with one request it is
+    GlobalGreedy (every A <= 1: Alg. 2's SLO stage is inert, P-sel-4)."""
+    for n, B in ((7, 30), (3, 3), (5, 64), (1, 9)):
+        caps = oracle.equal_greedy_caps(n, B)
+        assert int((caps + 1).sum()) == B and caps.max() - caps.min() <= 1
+    rng = np.random.default_rng(77)
+    for _ in range(20):
+        F = synth.random_forest(rng, 1, 30, tie_prob=0.3)
+        N = int(F["cand_offsets"][-1])
+        B = int(rng.integers(1, N + 3))
+        eg = oracle.select_per_request_greedy(F["cand_offsets"], F["cand_parent"], F["cand_prob"],
+                                              oracle.equal_greedy_caps(1, B))
+        gg = oracle.select_literal(F["cand_offsets"], F["cand_parent"], F["cand_prob"], [0.5], 3, 0, B)
+        np.testing.assert_array_equal(eg["tree_src"], gg["tree_src"])
+        np.testing.assert_array_equal(eg["tree_parent"], gg["tree_parent"])
+    with pytest.raises(ValueError):
+        oracle.equal_greedy_caps(4, 3)
