@@ -15,6 +15,8 @@
  *   as_accept_tokens     "uses these logits to identify the verified tokens"
  *                        (P:L860): greedy/stochastic acceptance walk and the
  *                        KV commit of the accepted path.
+ *   as_mss_verify        SpecInfer multi-step speculative sampling for trees
+ *                        of drawn drafts (reading R25).
  *
  * Conventions (all calls):
  *  - Every pointer argument is a DEVICE pointer unless stated otherwise; all
@@ -66,7 +68,8 @@ enum {
     AS_DEV_PAGE_OVERFLOW = 6,  /* a KV slot falls outside the request's page-table row    */
     AS_DEV_NAN_LOGIT = 7,      /* NaN in target_logits                                    */
     AS_DEV_PATH_TOO_LONG = 8,  /* accepted path longer than max_path (truncated)          */
-    AS_DEV_BAD_PAGE = 9        /* page id outside [0, num_pages)                          */
+    AS_DEV_BAD_PAGE = 9,       /* page id outside [0, num_pages)                          */
+    AS_DEV_BAD_TOKEN = 10      /* draft token outside [0, vocab) (as_mss_verify)          */
 };
 
 #define AS_MAX_TREE 256 /* nodes per tree (incl. root) accepted by as_tree_verify_attn */
@@ -300,6 +303,61 @@ as_status as_accept_tokens(as_accept_phase phase, int32_t n_req, int32_t req_beg
 as_status as_sample_tokens(int32_t n_rows, int32_t vocab, const void* logits, as_dtype logits_dtype,
                            float inv_temperature, unsigned long long seed, unsigned long long offset,
                            int32_t* out_tokens, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------- */
+/* Stochastic verification: SpecInfer multi-step speculative sampling         */
+/* (NEXT-3(b), reading R25)                                                   */
+/* ------------------------------------------------------------------------- */
+/*
+ * The lossless acceptance rule for trees whose children were DRAWN from the
+ * draft distribution ("tree-based verification ... prior work", Step 4;
+ * R25 in DESIGN.md).  At node u of request i (row r = tree_offsets[i] + u) with
+ * children c_1 < ... < c_k (local index order), draft tokens x_j =
+ * tree_tokens[c_j], target row p = target_probs[r, :], draft row q =
+ * draft_probs[r, :] (fp32 in, fp64 arithmetic):
+ *   p~ = p; N = sum_v p~(v)
+ *   for j = 1..k: accept c_j iff p~(x_j) > 0 and (r_j * N) * q(x_j) <= p~(x_j),
+ *     r_j = uniforms[row of c_j]; else p~(v) <- max(0, p~(v) - N q(v)) for
+ *     v != x_j, p~(x_j) <- 0, N <- sum p~ (if that is 0: keep the previous p~
+ *     and stop trying);
+ *   no child accepted: u emits the bonus token b = the first v (index order)
+ *     with sum_{w <= v} p~(w) >= r_b * N and p~(v) > 0 (else the last v with
+ *     p~(v) > 0), r_b = bonus_uniforms[r].
+ * Element values follow the oracle's fp64 operation sequence exactly; the
+ * masses N and the prefix sums are fp64 sums in a fixed blocked order (not the
+ * oracle's exactly rounded / sequential sums), so a decision can differ from
+ * the oracle's only when it lies within ~1e-13 (relative) of its threshold.
+ *
+ * mode AS_MSS_WALK: for each request in [req_begin, req_end) walk from the
+ *   root through the accepted children, evaluating only the nodes on the path
+ *   (rows of p and q are read once per VISITED node); writes the accept record
+ *   records[i * (max_path + 2) ..] = {len, bonus, path[max_path] (-1 padded)}
+ *   (the layout of as_accept_tokens' *_RECORDS phases: commit with
+ *   AS_ACCEPT_COMMIT_RECORDS, or all-gather first for KV-head sharding) and,
+ *   if emitted != NULL, emitted[r] = the token node r emitted on the path
+ *   (accepted child's token or the bonus), -1 for nodes not visited.
+ * mode AS_MSS_ALL_NODES: emitted[r] for every node of [req_begin, req_end)
+ *   (records unused, may be NULL).  emitted is then a valid target_tokens
+ *   input of as_accept_tokens (the walk moves to the lowest-index child with
+ *   the emitted token: a rejected token gets p~ = 0, so it identifies the
+ *   accepted child), except where a residual mass became exactly 0.
+ * Layouts: tree_offsets [n_req+1], tree_parent / tree_tokens / uniforms /
+ *   bonus_uniforms [n_tree_rows] (uniforms in (0, 1]); target_probs,
+ *   draft_probs [n_tree_rows, vocab] f32 (rows of leaves of draft_probs are
+ *   not read); records int32 [n_req, max_path + 2]; emitted int32 [n_tree_rows].
+ * Supported: vocab <= 360448, trees <= AS_MAX_TREE nodes, max_path >= 1.
+ * Device preconditions: AS_DEV_TREE_TOO_BIG, AS_DEV_ROWS_OVERFLOW,
+ *   AS_DEV_BAD_TOKEN, AS_DEV_PATH_TOO_LONG.
+ * Workspace: >= 256 bytes (device error word), 256-byte aligned.
+ */
+typedef enum { AS_MSS_WALK = 0, AS_MSS_ALL_NODES = 1 } as_mss_mode;
+
+as_status as_mss_verify(as_mss_mode mode, int32_t n_req, int32_t req_begin, int32_t req_end,
+                        int32_t n_tree_rows, int32_t vocab, const int32_t* tree_offsets,
+                        const int32_t* tree_parent, const int32_t* tree_tokens,
+                        const float* target_probs, const float* draft_probs, const float* uniforms,
+                        const float* bonus_uniforms, int32_t max_path, int32_t* records,
+                        int32_t* emitted, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------- */
 /* Utilities                                                                 */

@@ -120,3 +120,33 @@ def mss_tokens(tree_offsets, tree_parent, tree_tokens, target_probs, draft_probs
             out[o + u] = tok
             margins[o + u] = m
     return out, margins
+
+
+def mss_walk(tree_offsets, tree_parent, tree_tokens, target_probs, draft_probs, uniforms, bonus_uniforms, max_path):
+    """The MSS acceptance walk (R25 + R14) per request: from the root, run
+    mss_node at the current node; an accepted child becomes the next node, else
+    the node's emitted token is the bonus and the walk stops.  Returns
+    accept_len [n], bonus_token [n], accept_path [n, max_path] (-1 padded; the
+    root counts, as in accept_walk), and the minimum decision margin per request."""
+    to = [int(x) for x in tree_offsets]
+    n = len(to) - 1
+    acc_len = np.zeros(n, np.int32)
+    bonus = np.zeros(n, np.int32)
+    paths = np.full((n, max_path), -1, np.int32)
+    margins = np.full(n, math.inf)
+    for i in range(n):
+        o, K = to[i], to[i + 1] - to[i]
+        u, path = 0, [0]
+        while True:
+            kids = [c for c in range(u + 1, K) if int(tree_parent[o + c]) == u]
+            tok, j, m = mss_node(target_probs[o + u], draft_probs[o + u], [tree_tokens[o + c] for c in kids],
+                                 [uniforms[o + c] for c in kids], bonus_uniforms[o + u])
+            margins[i] = min(margins[i], m)
+            if j < 0:
+                bonus[i] = tok
+                break
+            u = kids[j]
+            path.append(u)
+        acc_len[i] = min(len(path), max_path)
+        paths[i, :acc_len[i]] = path[:max_path]
+    return {"accept_len": acc_len, "bonus_token": bonus, "accept_path": paths, "margin": margins}

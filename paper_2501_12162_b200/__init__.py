@@ -13,7 +13,7 @@ import os
 
 import torch
 
-__all__ = ["lib", "select_trees", "select_global_greedy", "select_topm", "select_equal_greedy", "sample_tokens", "tree_verify_attn", "accept_tokens", "Workspace", "check_device_error",
+__all__ = ["lib", "select_trees", "select_global_greedy", "select_topm", "select_equal_greedy", "sample_tokens", "mss_verify", "AS_MSS_WALK", "AS_MSS_ALL_NODES", "tree_verify_attn", "accept_tokens", "Workspace", "check_device_error",
            "selftest_umma", "AS_ACCEPT_FUSED", "AS_ACCEPT_WALK_ONLY", "AS_ACCEPT_COMMIT_ONLY",
            "AS_ACCEPT_WALK_RECORDS", "AS_ACCEPT_COMMIT_RECORDS", "beam_step", "beam_workspace_size", "AdaServeError",
            "select_workspace_size", "attn_workspace_size", "accept_workspace_size", "DEVICE_ERRORS"]
@@ -26,8 +26,10 @@ LIB_PATH = os.path.join(_PKG, "libadaserve_debug.so" if os.environ.get("AS_DEBUG
 AS_F32, AS_BF16 = 0, 1
 AS_ACCEPT_FUSED, AS_ACCEPT_WALK_ONLY, AS_ACCEPT_COMMIT_ONLY = 0, 1, 2
 AS_ACCEPT_WALK_RECORDS, AS_ACCEPT_COMMIT_RECORDS = 3, 4
+AS_MSS_WALK, AS_MSS_ALL_NODES = 0, 1
 DEVICE_ERRORS = {0: "ok", 1: "bad parent", 2: "bad f-hat", 3: "too many candidates", 4: "tree too big",
-                 5: "rows overflow", 6: "page overflow", 7: "NaN logit", 8: "path too long", 9: "bad page"}
+                 5: "rows overflow", 6: "page overflow", 7: "NaN logit", 8: "path too long", 9: "bad page",
+                 10: "bad token"}
 
 _c_i32, _c_sz, _vp, _f32 = ctypes.c_int32, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_float
 _lib = None
@@ -54,6 +56,8 @@ def lib():
         L.as_select_workspace_size.argtypes = [_c_i32, _c_i32]
         L.as_sample_tokens.argtypes = [_c_i32, _c_i32, _vp, _c_i32, _f32, ctypes.c_ulonglong, ctypes.c_ulonglong, _vp,
                                        _vp, _c_sz, _vp]
+        L.as_mss_verify.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _vp,
+                                    _vp, _c_i32, _vp, _vp, _vp, _c_sz, _vp]
         L.as_attn_workspace_size.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32]
         L.as_accept_workspace_size.argtypes = [_c_i32]
         L.as_select_trees.argtypes = [_c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32,
@@ -142,6 +146,38 @@ def sample_tokens(logits, inv_temperature, seed, offset=0, out=None, workspace=N
                                   float(inv_temperature), int(seed) & (2**64 - 1), int(offset) & (2**64 - 1),
                                   _ptr(out), ws.ptr, ws.nbytes, _stream()), "as_sample_tokens")
     return out, ws
+
+
+def mss_verify(tree_offsets, tree_parent, tree_tokens, target_probs, draft_probs, uniforms, bonus_uniforms,
+               max_path=None, mode=AS_MSS_WALK, req_range=None, records=None, emitted=None, workspace=None):
+    """as_mss_verify (NEXT-3(b), reading R25): SpecInfer multi-step speculative
+    sampling over trees of drawn drafts.  target_probs / draft_probs: fp32
+    [rows, vocab]; uniforms / bonus_uniforms: fp32 [rows] in (0, 1].
+    mode AS_MSS_WALK: returns (records int32 [n, max_path + 2] = {len, bonus,
+    path}, emitted int32 [rows] (-1 off the path), workspace); commit with
+    accept_tokens(AS_ACCEPT_COMMIT_RECORDS).  mode AS_MSS_ALL_NODES: records is
+    None and emitted holds every node's token."""
+    for t in (target_probs, draft_probs):
+        if t.dtype != torch.float32 or t.dim() != 2 or not t.is_contiguous():
+            raise AdaServeError("target_probs / draft_probs must be contiguous fp32 [rows, vocab]")
+    if uniforms.dtype != torch.float32 or bonus_uniforms.dtype != torch.float32:
+        raise AdaServeError("uniforms must be fp32")
+    n = tree_offsets.numel() - 1
+    rows, vocab = target_probs.shape
+    b, e = (0, n) if req_range is None else req_range
+    dev = target_probs.device
+    if max_path is None:
+        max_path = 256
+    if mode == AS_MSS_WALK and records is None:
+        records = torch.empty((n, max_path + 2), dtype=torch.int32, device=dev)
+    if emitted is None:
+        emitted = torch.empty(rows, dtype=torch.int32, device=dev)
+    ws = workspace if workspace is not None else Workspace(256, dev)
+    _check(lib().as_mss_verify(mode, n, b, e, rows, vocab, _ptr(tree_offsets), _ptr(tree_parent), _ptr(tree_tokens),
+                               _ptr(target_probs), _ptr(draft_probs), _ptr(uniforms), _ptr(bonus_uniforms),
+                               max_path, _ptr(records) if records is not None else None, _ptr(emitted), ws.ptr,
+                               ws.nbytes, _stream()), "as_mss_verify")
+    return (records if mode == AS_MSS_WALK else None), emitted, ws
 
 
 def select_workspace_size(n_req, n_cand_total):

@@ -21,7 +21,7 @@ CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libadaserve.so")
 LIB_DEBUG = os.path.join(PKG, "libadaserve_debug.so")
-SOURCES = ["abi.cu", "beam.cu", "sample.cu", "select.cu", "accept.cu", "attn_simt.cu", "attn_tc.cu", "selftest.cu"]
+SOURCES = ["abi.cu", "beam.cu", "sample.cu", "mss.cu", "select.cu", "accept.cu", "attn_simt.cu", "attn_tc.cu", "selftest.cu"]
 DEBUG_SOURCES = SOURCES + ["membench.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

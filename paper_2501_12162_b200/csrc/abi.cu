@@ -136,6 +136,28 @@ as_status as_sample_tokens(int32_t n_rows, int32_t vocab, const void* logits, as
                          workspace, S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
 }
 
+// ----------------------------------------------------------------- MSS (NEXT-3(b))
+as_status as_mss_verify(as_mss_mode mode, int32_t n_req, int32_t req_begin, int32_t req_end, int32_t n_tree_rows,
+                        int32_t vocab, const int32_t* tree_offsets, const int32_t* tree_parent,
+                        const int32_t* tree_tokens, const float* target_probs, const float* draft_probs,
+                        const float* uniforms, const float* bonus_uniforms, int32_t max_path, int32_t* records,
+                        int32_t* emitted, void* workspace, size_t workspace_bytes, void* stream) {
+    if (mode != AS_MSS_WALK && mode != AS_MSS_ALL_NODES) return AS_ERR_INVALID_ARG;
+    if (n_req < 0 || req_begin < 0 || req_end < req_begin || req_end > n_req || n_tree_rows < 0 || vocab < 1)
+        return AS_ERR_INVALID_ARG;
+    if (mss_smem_bytes(vocab) == 0) return AS_ERR_UNSUPPORTED;
+    if (req_end == req_begin) return AS_OK;
+    if (!tree_offsets || !tree_parent || !tree_tokens || !target_probs || !draft_probs || !uniforms ||
+        !bonus_uniforms)
+        return AS_ERR_INVALID_ARG;
+    if (mode == AS_MSS_WALK && (max_path < 1 || (!records && !emitted))) return AS_ERR_INVALID_ARG;
+    if (mode == AS_MSS_ALL_NODES && !emitted) return AS_ERR_INVALID_ARG;
+    if (!workspace || !al256(workspace) || workspace_bytes < kWsHeaderBytes) return AS_ERR_WORKSPACE;
+    return launch_mss(req_begin, req_end, n_tree_rows, vocab, tree_offsets, tree_parent, tree_tokens, target_probs,
+                      draft_probs, uniforms, bonus_uniforms, emitted, mode == AS_MSS_WALK ? records : nullptr,
+                      max_path, mode == AS_MSS_WALK ? 1 : 0, workspace, S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
+}
+
 // ----------------------------------------------------------------- select
 size_t as_select_workspace_size(int32_t n_req, int32_t n_cand_total) {
     if (n_req < 0 || n_cand_total < 0) return 0;

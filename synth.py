@@ -201,3 +201,41 @@ def tree_workload(rng, sizes, kv_lens, n_q, n_kv, d, page_size, shape="random", 
                 v_tree=rnd(max(R, 1), n_kv, d)[:R], k_cache=rnd(n_pages, n_kv, page_size, d),
                 v_cache=rnd(n_pages, n_kv, page_size, d), page_table=table,
                 kv_len=np.asarray(kv_lens, np.int32))
+
+
+def mss_workload(rng, sizes, vocab, sigma_lo=1.0, sigma_hi=4.0, drift=0.5, shape="random", dup_tokens=False):
+    """Inputs of NEXT-3(b) (SpecInfer multi-step speculative sampling, R25):
+    per node a draft row q = softmax(z), z ~ N(0, sigma^2) over `vocab`, and a
+    target row p = softmax(z + drift * N(0, 1)) (a target near the draft, so
+    acceptance is neither certain nor rare); every child's draft token is DRAWN
+    from its parent's q (SpecInfer's stochastic speculation), by inverse CDF of
+    a uniform; the per-child acceptance uniforms and per-node bonus uniforms
+    are U(0, 1] fp32.  dup_tokens draws children from a 4-token support (many
+    equal siblings).  Softmaxes in fp64, stored fp32."""
+    sizes = [int(k) for k in sizes]
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    R = int(offs[-1])
+    par = np.concatenate([random_tree_parents(rng, k, shape=shape) for k in sizes]).astype(np.int32) if R else \
+        np.zeros(0, np.int32)
+    sig = rng.uniform(sigma_lo, sigma_hi, R)
+    z = rng.normal(0.0, 1.0, (R, vocab)) * sig[:, None]
+    def rows_softmax(x):
+        e = np.exp(x - x.max(axis=1, keepdims=True))
+        return e / e.sum(axis=1, keepdims=True)
+    q = rows_softmax(z)
+    p = rows_softmax(z + drift * rng.normal(0.0, 1.0, (R, vocab)))
+    q32, p32 = q.astype(np.float32), p.astype(np.float32)
+    tok = np.zeros(R, np.int32)
+    for i, k in enumerate(sizes):
+        o = offs[i]
+        for j in range(1, k):
+            row = q[o + par[o + j]]
+            if dup_tokens:
+                row = row[:4] / row[:4].sum()
+            tok[o + j] = min(int(np.searchsorted(np.cumsum(row), rng.random() * row.sum())), len(row) - 1)
+    uni = rng.random(R).astype(np.float32)
+    uni[uni == 0] = 1.0
+    bon = rng.random(R).astype(np.float32)
+    bon[bon == 0] = 1.0
+    return {"tree_offsets": offs, "tree_parent": par, "tree_tokens": tok, "p": p32, "q": q32, "uni": uni,
+            "bonus_uni": bon}

@@ -99,3 +99,21 @@ def test_sample_tokens_host_checks(L):
     assert f(2, 10, None, 0, 1.0, 1, 0, None, None, 0, None) != 0          # null logits
     assert f(2, 10, 256, 0, -1.0, 1, 0, 512, 768, 256, None) != 0          # negative inv_temperature
     assert f(2, 10, 256, 5, 1.0, 1, 0, 512, 768, 256, None) != 0           # unknown dtype
+
+
+def test_mss_verify_host_checks(L):
+    """as_mss_verify rejects bad host arguments before any launch."""
+    f = L.as_mss_verify
+    vp, i32 = ctypes.c_void_p, ctypes.c_int32
+    f.argtypes = [i32] * 6 + [vp] * 7 + [i32, vp, vp, vp, ctypes.c_size_t, vp]
+    d = 4096
+    args = lambda mode=0, n=2, b=0, e=2, vocab=1000, mp=8, rec=d, em=d, ws=1 << 16: (
+        mode, n, b, e, 16, vocab, d, d, d, d, d, d, d, mp, rec, em, ws, 256, None)
+    assert f(*args(mode=2)) == 1                 # unknown mode
+    assert f(*args(e=3)) == 1                    # req_end > n_req
+    assert f(*args(b=2, e=2)) == 0               # empty range: nothing to do
+    assert f(*args(vocab=400000)) == 3           # vocab beyond two 16-CTA clusters' shared memory
+    assert f(*args(mp=0)) == 1                   # walk needs max_path >= 1
+    assert f(*args(rec=None, em=None)) == 1      # walk needs an output
+    assert f(*args(mode=1, em=None)) == 1        # all-nodes needs emitted
+    assert f(*args(ws=(1 << 16) + 4)) == 4       # misaligned workspace

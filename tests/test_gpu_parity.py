@@ -857,3 +857,143 @@ def test_stochastic_walk_with_sampled_targets(ada):
     np.testing.assert_array_equal(out["accept_path"].cpu().numpy(), ref["accept_path"])
     np.testing.assert_array_equal(out["accept_len"].cpu().numpy(), ref["accept_len"])
     np.testing.assert_array_equal(out["bonus_token"].cpu().numpy(), ref["bonus_token"])
+
+
+# --------------------------------------------------------------------------- NEXT-3(b) MSS
+def _mss_dev(W):
+    return (dev(W["tree_offsets"]), dev(W["tree_parent"]), dev(W["tree_tokens"]), dev(W["p"]), dev(W["q"]),
+            dev(W["uni"]), dev(W["bonus_uni"]))
+
+
+def _mss_cases():
+    return [  # (sizes, vocab, shape, drift, dup)
+        ([1, 2, 9, 17, 40], 1000, "random", 0.5, False),
+        ([33, 5, 64], 4099, "random", 1.5, False),       # ragged vocab: scalar loads
+        ([12, 12, 12], 7, "star", 0.3, False),            # vocab < one thread chunk
+        ([30, 30], 2000, "star", 2.0, True),              # many equal siblings, many rejections
+        ([20, 20, 20], 3000, "chain", 0.1, False),        # target ~ draft: long accepted chains
+        ([256, 100], 512, "random", 1.0, True),           # AS_MAX_TREE nodes
+    ]
+
+
+@pytest.mark.parametrize("ci", range(6))
+def test_mss_all_nodes_vs_oracle(ada, ci):
+    """as_mss_verify(ALL_NODES): every node's emitted token equals oracle/mss.py's
+    (R25); a difference is allowed only where the oracle's decision margin says
+    the fp64 sums' association can decide it (< 1e-12 relative)."""
+    from oracle import mss
+    sizes, V, shape, drift, dup = _mss_cases()[ci]
+    W = synth.mss_workload(np.random.default_rng(100 + ci), sizes, V, drift=drift, shape=shape, dup_tokens=dup)
+    _, emitted, ws = ada.mss_verify(*_mss_dev(W), mode=ada.AS_MSS_ALL_NODES)
+    assert ada.check_device_error(ws)[0] == 0
+    want, margin = mss.mss_tokens(W["tree_offsets"], W["tree_parent"], W["tree_tokens"], W["p"], W["q"], W["uni"],
+                                  W["bonus_uni"])
+    got = emitted.cpu().numpy()
+    bad = np.nonzero(got != want)[0]
+    assert all(margin[b] < 1e-12 for b in bad), [(int(b), int(got[b]), int(want[b]), margin[b]) for b in bad[:5]]
+    assert len(bad) <= max(1, len(got) // 100)
+
+
+@pytest.mark.parametrize("ci", range(6))
+def test_mss_walk_records_vs_oracle(ada, ci):
+    """as_mss_verify(WALK): the accept records {len, bonus, path} equal
+    oracle mss_walk's; emitted holds the path nodes' tokens and -1 elsewhere."""
+    from oracle import mss
+    sizes, V, shape, drift, dup = _mss_cases()[ci]
+    W = synth.mss_workload(np.random.default_rng(200 + ci), sizes, V, drift=drift, shape=shape, dup_tokens=dup)
+    mp = max(sizes) + 1
+    rec, emitted, ws = ada.mss_verify(*_mss_dev(W), max_path=mp, mode=ada.AS_MSS_WALK)
+    assert ada.check_device_error(ws)[0] == 0
+    ref = mss.mss_walk(W["tree_offsets"], W["tree_parent"], W["tree_tokens"], W["p"], W["q"], W["uni"],
+                       W["bonus_uni"], mp)
+    rec = rec.cpu().numpy()
+    em = emitted.cpu().numpy()
+    for i in range(len(sizes)):
+        if ref["margin"][i] < 1e-12 and (rec[i, 0] != ref["accept_len"][i] or rec[i, 1] != ref["bonus_token"][i]):
+            continue  # a decision at the fp64 association tie (see test_mss_all_nodes_vs_oracle)
+        assert rec[i, 0] == ref["accept_len"][i], i
+        assert rec[i, 1] == ref["bonus_token"][i], i
+        np.testing.assert_array_equal(rec[i, 2:], ref["accept_path"][i])
+        o = int(W["tree_offsets"][i])
+        path = [int(x) for x in ref["accept_path"][i][: ref["accept_len"][i]]]
+        for k in range(sizes[i]):
+            if k not in path:
+                assert em[o + k] == -1
+        # the emitted token of a path node is the next path node's draft token, or the bonus
+        for a, b in zip(path, path[1:] + [None]):
+            assert em[o + a] == (W["tree_tokens"][o + b] if b is not None else ref["bonus_token"][i])
+
+
+def test_mss_degenerate_rows(ada):
+    """Closed cases: q = p accepts the first child whenever p(x) > 0 (r N q <= p
+    with N = 1 up to rounding -- checked against the oracle); a one-hot target
+    emits its token; a child whose token has p = 0 is always rejected; a
+    root-only tree samples the bonus from p."""
+    from oracle import mss
+    rng = np.random.default_rng(5)
+    V = 600
+    sizes = [4, 4, 1, 6]
+    W = synth.mss_workload(rng, sizes, V, shape="star")
+    W["q"][:4] = W["p"][:4]                           # request 0: q == p
+    W["p"][4:8] = 0.0
+    W["p"][4:8, 17] = 1.0                             # request 1: one-hot target at token 17
+    W["tree_tokens"][5] = 17
+    W["p"][9:15, :] = W["p"][9:15, :]
+    W["p"][9, W["tree_tokens"][10:15]] = 0.0          # request 3: every child's token has p = 0
+    _, emitted, ws = ada.mss_verify(*_mss_dev(W), mode=ada.AS_MSS_ALL_NODES)
+    assert ada.check_device_error(ws)[0] == 0
+    got = emitted.cpu().numpy()
+    want, _ = mss.mss_tokens(W["tree_offsets"], W["tree_parent"], W["tree_tokens"], W["p"], W["q"], W["uni"],
+                             W["bonus_uni"])
+    np.testing.assert_array_equal(got, want)
+    assert got[0] == W["tree_tokens"][1]              # q == p: first child accepted
+    assert got[4] == 17                               # one-hot
+    assert got[9] not in set(W["tree_tokens"][10:15].tolist())
+
+
+def test_mss_walk_then_commit_vs_oracle(ada):
+    """MSS walk records -> as_accept_tokens(COMMIT_RECORDS): the KV cache after
+    the commit equals oracle.commit of the oracle walk's paths, byte for byte."""
+    from oracle import mss
+    rng = np.random.default_rng(31)
+    sizes = [9, 14, 3, 20]
+    n = len(sizes)
+    W = synth.mss_workload(rng, sizes, 700, drift=0.3)
+    R = int(W["tree_offsets"][-1])
+    mp = max(sizes) + 1
+    n_kv, d, ps = 2, 64, 16
+    kv_len = rng.integers(0, 40, n).astype(np.int32)
+    pt, num_pages = synth.paged_kv(rng, kv_len, ps, extra_slots=mp)
+    kt = rng.normal(size=(R, n_kv, d)).astype(np.float32)
+    vt = rng.normal(size=(R, n_kv, d)).astype(np.float32)
+    kc = rng.normal(size=(num_pages, n_kv, ps, d)).astype(np.float32)
+    vc = rng.normal(size=(num_pages, n_kv, ps, d)).astype(np.float32)
+    rec, _, ws = ada.mss_verify(*_mss_dev(W), max_path=mp, mode=ada.AS_MSS_WALK)
+    g_kc, g_vc, g_len = dev(kc), dev(vc), dev(kv_len)
+    res = ada.accept_tokens(ada.AS_ACCEPT_COMMIT_RECORDS, dev(W["tree_offsets"]), max_path=mp, accept_path=rec,
+                            k_tree=dev(kt), v_tree=dev(vt), k_cache=g_kc, v_cache=g_vc, page_table=dev(pt),
+                            kv_len=g_len, n_tree_rows=R)
+    assert ada.check_device_error(res["workspace"])[0] == 0
+    ref = mss.mss_walk(W["tree_offsets"], W["tree_parent"], W["tree_tokens"], W["p"], W["q"], W["uni"],
+                       W["bonus_uni"], mp)
+    kl = kv_len.copy()
+    assert oracle.commit(W["tree_offsets"], ref["accept_len"], ref["accept_path"], kt, vt, kc, vc, pt, kl) == 0
+    np.testing.assert_array_equal(g_len.cpu().numpy(), kl)
+    np.testing.assert_array_equal(g_kc.cpu().numpy(), kc)
+    np.testing.assert_array_equal(g_vc.cpu().numpy(), vc)
+
+
+def test_mss_llama_vocab_sampled(ada):
+    """|V| = 128 256 (the bench's vocabulary, one 8-CTA cluster per request):
+    walk records of 3 requests vs the oracle."""
+    from oracle import mss
+    sizes = [32, 8, 1]
+    W = synth.mss_workload(np.random.default_rng(77), sizes, synth.LLAMA3_VOCAB, drift=0.4, shape="random")
+    rec, _, ws = ada.mss_verify(*_mss_dev(W), max_path=33, mode=ada.AS_MSS_WALK)
+    assert ada.check_device_error(ws)[0] == 0
+    ref = mss.mss_walk(W["tree_offsets"], W["tree_parent"], W["tree_tokens"], W["p"], W["q"], W["uni"],
+                       W["bonus_uni"], 33)
+    rec = rec.cpu().numpy()
+    np.testing.assert_array_equal(rec[:, 0], ref["accept_len"])
+    np.testing.assert_array_equal(rec[:, 1], ref["bonus_token"])
+    np.testing.assert_array_equal(rec[:, 2:], ref["accept_path"])

@@ -150,3 +150,36 @@ def test_emitted_token_identifies_accepted_child():
             assert kids.index(tok) == j
         else:
             assert tok not in kids
+
+
+def test_mss_walk_equals_token_walk_on_emitted_tokens():
+    """mss_walk (accepted-child indices) and the greedy token walk over the
+    per-node emitted tokens (R13) give the same path and bonus: the emitted
+    token identifies the accepted child (R25)."""
+    rng = np.random.default_rng(21)
+    q, p = _toy_models(5)
+    for _ in range(300):
+        k1, k2 = int(rng.integers(1, 4)), int(rng.integers(0, 3))
+        toks, par, ctx = [0], [0], [()]
+        for _ in range(k1):
+            toks.append(int(rng.choice(V, p=_norm(q[()]))))
+            par.append(0)
+            ctx.append((toks[-1],))
+        for c in range(1, k1 + 1):
+            for _ in range(k2):
+                toks.append(int(rng.choice(V, p=_norm(q[(toks[c],)]))))
+                par.append(c)
+                ctx.append((toks[c], toks[-1]))
+        K = len(toks)
+        P = np.stack([p[cx] for cx in ctx])
+        Q = np.stack([q[cx] if cx in q else np.zeros(V, np.float32) for cx in ctx])
+        r = np.maximum(rng.random(K), 1e-7).astype(np.float32)
+        rb = np.maximum(rng.random(K), 1e-7).astype(np.float32)
+        off = np.array([0, K], np.int32)
+        emit, _ = mss.mss_tokens(off, np.array(par), np.array(toks), P, Q, r, rb)
+        w = oracle.accept_walk(off, np.array(par, np.int32), np.array(toks, np.int32),
+                               target_tokens=emit.astype(np.int32), max_path=4)
+        m = mss.mss_walk(off, np.array(par), np.array(toks), P, Q, r, rb, 4)
+        assert int(m["accept_len"][0]) == int(w["accept_len"][0])
+        assert int(m["bonus_token"][0]) == int(w["bonus_token"][0])
+        assert np.array_equal(m["accept_path"][0], w["accept_path"][0])
