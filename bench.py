@@ -532,10 +532,12 @@ def main():
     spec = None
     logits_mode = None
     sampling = None
+    mss = None
     if rank == 0 and not args.profile and not args.no_spec:
         spec = measure_speculation(W, args.steps)
         logits_mode = measure_accept_logits(W, args.steps)
         sampling = measure_sampling(W, args.steps)
+        mss = measure_mss(W, args.steps)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         threads = os.cpu_count() or 1
@@ -561,7 +563,7 @@ def main():
                        if W["n_pools"] == 1 else f"{W['n_pools']} rotating KV pools (> 3x L2)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks, "graph": use_graph, "speculation": spec, "accept_logits": logits_mode,
-            "sampling": sampling,
+            "sampling": sampling, "mss": mss,
             **({"emulated_shard_of_world": emu} if (emu > 1 and world == 1) else {}), **({"ablation_skip": os.environ["AS_BENCH_SKIP"]}
                                                        if os.environ.get("AS_BENCH_SKIP") else {}),
             "breakdown_ms": {"select": round(t_sel, 4), "attention": round(t_attn_b, 4), "accept_commit": round(t_acc, 4),
@@ -715,6 +717,88 @@ def measure_sampling(W, steps):
             "alu": {"achieved_warp_inst_per_s": round(achieved, 1), "peak_warp_inst_per_s": issue_peak,
                     "frac": round(achieved / issue_peak, 4), "warp_inst_per_token": round(winst, 4)},
             "algorithmic_bytes": nbytes, "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4), "launches": 1}
+
+
+def measure_mss(W, steps):
+    """NEXT-3(b): SpecInfer multi-step speculative sampling (as_mss_verify, R25)
+    on this config's selected trees with |V| = 128 256 fp32 target/draft rows
+    per node (q = softmax(z), z ~ N(0, sigma^2), sigma ~ U(1, 4) per node;
+    p = softmax(z + 0.5 N(0, 1)); every child's token DRAWN from its parent's q).
+    WALK mode reads the rows of the visited nodes only (algorithmic bytes =
+    p row of every visited node + q row of every visited node with children);
+    ALL_NODES reads every node's rows (HBM-bound, for context)."""
+    ada = W["ada"]
+    if W["dtype"] != torch.bfloat16:
+        return None
+    R, V, n = W["R"], synth.LLAMA3_VOCAB, W["n"]
+    dv = W["device"]
+    gen = torch.Generator(device=dv).manual_seed(synth.SEED_BASE + 11)
+    offs = W["sel"]["tree_offsets"]
+    par = W["sel"]["tree_parent"]
+    sigma = torch.empty((R, 1), device=dv).uniform_(1.0, 4.0, generator=gen)
+    z = torch.randn((R, V), generator=gen, device=dv) * sigma
+    q = torch.softmax(z, dim=-1)
+    z.add_(0.5 * torch.randn((R, V), generator=gen, device=dv))
+    p = torch.softmax(z, dim=-1)
+    del z
+    offs_h = offs.cpu().numpy().astype(np.int64)
+    U = int(offs_h[-1])  # rows in use
+    par_h = par[:U].cpu().numpy().astype(np.int64)
+    req = np.repeat(np.arange(n), np.diff(offs_h))
+    prow = torch.from_numpy(offs_h[req] + par_h).to(dv)  # parent row of every node
+    tok = torch.zeros(R, dtype=torch.int32, device=dv)
+    tok[:U] = torch.multinomial(q[prow], 1, generator=gen).squeeze(1).to(torch.int32)
+    uni = torch.rand(R, generator=gen, device=dv).clamp_(min=2.0 ** -24)
+    bon = torch.rand(R, generator=gen, device=dv).clamp_(min=2.0 ** -24)
+    mp = W["max_path"]
+    rec = torch.empty((n, mp + 2), dtype=torch.int32, device=dv)
+    em = torch.empty(R, dtype=torch.int32, device=dv)
+    ws = W.get("mss_ws") or ada.Workspace(256, dv)  # (scripts/mss_trace.py passes a traced one)
+    res = {}
+    modes = ((ada.AS_MSS_WALK, "walk"), (ada.AS_MSS_ALL_NODES, "all_nodes"))
+    if "mss_ws" in W:
+        modes = modes[:1]
+    for mode, name in modes:
+        def call():
+            ada.mss_verify(offs, par, tok, p, q, uni, bon, max_path=mp, mode=mode, records=rec, emitted=em,
+                           workspace=ws)
+        for _ in range(3):
+            call()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(steps):
+                call()
+        g.replay()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        g.replay()
+        e.record()
+        torch.cuda.synchronize()
+        res[name] = s.elapsed_time(e) * 1e3 / steps
+        if mode == ada.AS_MSS_WALK:
+            rec_h = rec.cpu().numpy()
+    assert ada.check_device_error(ws)[0] == 0
+    has_kids = np.zeros(U, bool)
+    nonroot = np.ones(U, bool)
+    nonroot[offs_h[:-1][np.diff(offs_h) > 0]] = False
+    has_kids[(offs_h[req] + par_h)[nonroot]] = True
+    visited = [int(offs_h[i] + rec_h[i, 2 + k]) for i in range(n) for k in range(int(rec_h[i, 0]))]
+    walk_bytes = sum(V * 4 * (2 if has_kids[r] else 1) for r in visited)
+    all_bytes = int(U * V * 4 + has_kids.sum() * V * 4)
+    peak = float(_peaks()[0]["hbm_gbs"])
+    acc = rec_h[:, 0].astype(np.float64)
+    res.setdefault("all_nodes", float("nan"))
+    return {"step": "SpecInfer multi-step speculative sampling (as_mss_verify)", "rows": R, "vocab": V,
+            "walk_us": round(res["walk"], 2), "all_nodes_us": round(res["all_nodes"], 2),
+            "mean_accept_len": round(float(acc.mean()), 3), "visited_rows": len(visited),
+            "walk_algorithmic_bytes": walk_bytes, "walk_hbm_gbs": round(walk_bytes / (res["walk"] * 1e-6) / 1e9, 1),
+            "walk_hbm_frac": round(walk_bytes / (res["walk"] * 1e-6) / 1e9 / peak, 4),
+            "all_nodes_algorithmic_bytes": all_bytes,
+            "all_nodes_hbm_frac": round(all_bytes / (res["all_nodes"] * 1e-6) / 1e9 / peak, 4),
+            "inputs": "q = softmax(N(0, sigma^2)), sigma ~ U(1,4); p = softmax(z + 0.5 N(0,1)); children drawn from q",
+            "launches": 1}
 
 
 def measure_e2e(W, step, steps, world):

@@ -345,7 +345,7 @@ as_status as_sample_tokens(int32_t n_rows, int32_t vocab, const void* logits, as
  *   bonus_uniforms [n_tree_rows] (uniforms in (0, 1]); target_probs,
  *   draft_probs [n_tree_rows, vocab] f32 (rows of leaves of draft_probs are
  *   not read); records int32 [n_req, max_path + 2]; emitted int32 [n_tree_rows].
- * Supported: vocab <= 360448, trees <= AS_MAX_TREE nodes, max_path >= 1.
+ * Supported: vocab <= 294912, trees <= AS_MAX_TREE nodes, max_path >= 1.
  * Device preconditions: AS_DEV_TREE_TOO_BIG, AS_DEV_ROWS_OVERFLOW,
  *   AS_DEV_BAD_TOKEN, AS_DEV_PATH_TOO_LONG.
  * Workspace: >= 256 bytes (device error word), 256-byte aligned.

@@ -155,7 +155,8 @@ as_status as_mss_verify(as_mss_mode mode, int32_t n_req, int32_t req_begin, int3
     if (!workspace || !al256(workspace) || workspace_bytes < kWsHeaderBytes) return AS_ERR_WORKSPACE;
     return launch_mss(req_begin, req_end, n_tree_rows, vocab, tree_offsets, tree_parent, tree_tokens, target_probs,
                       draft_probs, uniforms, bonus_uniforms, emitted, mode == AS_MSS_WALK ? records : nullptr,
-                      max_path, mode == AS_MSS_WALK ? 1 : 0, workspace, S(stream)) == 0 ? AS_OK : AS_ERR_CUDA;
+                      max_path, mode == AS_MSS_WALK ? 1 : 0, workspace, workspace_bytes, S(stream)) == 0 ? AS_OK
+                                                                                                    : AS_ERR_CUDA;
 }
 
 // ----------------------------------------------------------------- select

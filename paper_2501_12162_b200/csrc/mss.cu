@@ -11,34 +11,39 @@
 //               N <- sum p~ (N == 0: keep the previous p~, stop trying)
 //   no child accepted: bonus = first v with cum(v) >= r_b N and p~(v) > 0
 //                      (else the last v with p~(v) > 0).
-// p~ after h rejections is never stored: residual() replays the h updates on
-// the (p, q) pair -- the same sequence of fp64 operations the oracle performs
-// (one __dmul_rn, one __dsub_rn, one max per rejection; no FMA), so every
-// element value is bit-identical to oracle/mss.py's; only the sums' association
-// differs (last bits -- the oracle reports each decision's margin).
+// Every residual element is the same sequence of fp64 operations the oracle
+// performs (one __dmul_rn, one __dsub_rn, one max per rejection; no FMA), so
+// element values are bit-identical to oracle/mss.py's; only the sums'
+// association differs (last bits -- the oracle reports each decision's margin).
 //
-// One thread-block cluster of C CTAs (C = 8, or 16 for vocabularies past 180k)
-// per task.  CTA c holds the slice [c S, (c+1) S) of the node's p and q rows in
-// shared memory (S = E * 512 floats, E a multiple of 4 with E/4 odd so the
-// per-thread float4 chunks are bank-conflict free): the rows are read from HBM
-// ONCE per node, every later pass (the residual mass after each rejection, the
-// bonus inverse CDF) runs from shared memory, and the cluster combines per-CTA
-// fp64 partials through DSMEM (each CTA writes its partial into every peer,
-// one cluster barrier, all CTAs sum them in rank order -> identical N
-// everywhere).  A decision reads p(x), q(x) straight from the owning CTA's
-// shared memory (ld.shared::cluster).
+// One thread-block cluster of C CTAs (C = 8, or 16 for vocabularies past 147k)
+// per task.  CTA c owns the slice [c S, (c+1) S) of the vocabulary (S = E * 512,
+// E a multiple of 4 with E/4 odd so per-thread float4 chunks are bank-conflict
+// free): the node's p slice lands in shared memory by bulk copy (TMA engine)
+// once per node; a node with children widens p into an fp64 residual R in
+// shared memory while summing it, then bulk-copies its q slice over p (from
+// L2: prefetched when the node starts), so every rejection updates R in place
+// from shared memory (O(1) work per entry per rejection); the children's
+// q(x_j) are loaded when the node starts, and the CTA owning the next child's
+// token pushes p~(x) to its peers with each mass exchange, so a decision is
+// local arithmetic.  The cluster combines per-CTA fp64 partials
+// through DSMEM (each CTA pushes its partial into every peer, one cluster
+// barrier, all CTAs sum them in rank order -> identical N everywhere).
+// Measured (c2): ~2 us per node to load + sum, ~4.3 us per
+// rejection (an fp64 pass over the slice + one cluster barrier).
 //   walk = 1: task = request; the cluster walks from the root, visiting only the
 //             nodes on the accepted path (HBM traffic = path rows, not tree rows),
 //             and writes the accept record {len, bonus, path} (the layout of
 //             as_accept_tokens' *_RECORDS phases: AS_ACCEPT_COMMIT_RECORDS then
 //             commits the path's K/V).
 //   walk = 0: task = node; every node's emitted token (all-nodes mode).
-// Persistent grid: as many clusters as fit (one 150 KB CTA per SM), tasks strided.
+// Persistent grid: as many clusters as fit (one 225 KB CTA per SM), tasks strided.
 #include <cooperative_groups.h>
 #include <mutex>
 #include <map>
 
 #include "params.cuh"
+#include "tc_ptx.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -66,13 +71,34 @@ struct MssParams {
     int S;      // floats per CTA slice (E * kMssThreads)
     int vec4;   // rows 16-byte aligned (vocab % 4 == 0 and aligned bases)
     void* ws;
+    unsigned long long* trace;  // debug build: cluster-0 per-node timeline [64][8] (globaltimer ns) or NULL
 };
 
+#ifdef AS_DEBUG
+#define MSS_TRACE(k, e, v)                                                                                   \
+    do {                                                                                                     \
+        if (p.trace && blockIdx.x == 0 && t == 0 && (k) < 64 && (k) >= 0) p.trace[(k) * 8 + (e)] = (v);                  \
+    } while (0)
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long x;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(x));
+    return x;
+}
+#else
+#define MSS_TRACE(k, e, v) \
+    do {                   \
+    } while (0)
+__device__ __forceinline__ unsigned long long gtime() { return 0; }
+#endif
+
 struct MssShared {
+    // (p slice P [S] f32 and residual R [S] f64 follow this struct in shared memory)
     double hN[kMssMaxKids];      // history: mass N_k before rejection k
     int hx[kMssMaxKids];         // history: rejected token x_k
     int kid[kMssMaxKids];        // children of the current node (local index)
     double part[2][kMssMaxC];    // cluster exchange of CTA partial sums (double-buffered)
+    double nrx[2];               // p~(x) of the next child to try, pushed by the owning CTA
+    float kid_q[kMssMaxKids];    // q(x_j) of the children's tokens (loaded when the node starts)
     int ipart[2][kMssMaxC][2];   // cluster exchange of (first crossing, last with mass)
     double wsum[kMssWarps];
     double wscan[kMssWarps];
@@ -80,17 +106,17 @@ struct MssShared {
     int t_par[AS_MAX_TREE];      // the task's request: parents, draft tokens, uniforms
     int t_tok[AS_MAX_TREE];
     float t_uni[AS_MAX_TREE];
-    int n_kids, hlen, node, K, o, flag;
-    double N;
+    int n_kids, node, K, o, flag;
     int path[AS_MAX_TREE];
-    int plen;
+    int plen, acc;
+    uint64_t bar;                // row loads (bulk copies, complete_tx)
 };
 
-__device__ __forceinline__ double residual(float pf, float qf, int v, const MssShared& sh, int hlen) {
-    double t = (double)pf;
-    const double qd = (double)qf;
-    for (int k = 0; k < hlen; ++k) t = (v == sh.hx[k]) ? 0.0 : fmax(0.0, __dsub_rn(t, __dmul_rn(sh.hN[k], qd)));
-    return t;
+__device__ __forceinline__ double f2d(float f) { return (double)f; }
+
+// p~ at entry i of this CTA's slice: mat == 0 -> p (P holds p), else R[i].
+__device__ __forceinline__ double res_at(const float* P, const double* R, int mat, int i) {
+    return mat ? R[i] : f2d(P[i]);
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -99,54 +125,123 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     return v;
 }
 
-// Cluster-wide sum of one fp64 value per CTA: written into every peer's slot,
-// one cluster barrier, summed in rank order (identical result on every CTA).
-__device__ double cluster_sum(cg::cluster_group& cl, MssShared& sh, double mine, int& xbuf, int C, int rank) {
+// Cluster mass from the per-thread chunk sums tau: warp xor trees, warp 0
+// reduces the 16 warp sums and pushes the CTA total into every peer, one
+// cluster barrier, every thread sums the C totals in rank order.  The CTA
+// owning entry `x_off` (x_owner >= 0: the next child's token) also pushes
+// p~ there, so the next decision reads it locally (*nrx).
+__device__ double cluster_mass(cg::cluster_group& cl, MssShared& sh, double tau, int& xbuf, int C, int rank,
+                               int x_owner, int x_off, const float* P, const double* R, int mat, double* nrx) {
+    const int t = threadIdx.x;
+    const double ws = warp_sum_d(tau);
+    if ((t & 31) == 0) sh.wsum[t >> 5] = ws;
+    __syncthreads();
     const int b = xbuf;
     xbuf ^= 1;
-    if (threadIdx.x < (unsigned)C) cl.map_shared_rank(&sh.part[b][0], (int)threadIdx.x)[rank] = mine;
+    if (t < 32) {
+        const double cta = warp_sum_d(t < kMssWarps ? sh.wsum[t] : 0.0);
+        if (t < C) {
+            cl.map_shared_rank(&sh.part[b][0], t)[rank] = cta;
+            if (x_owner == rank) cl.map_shared_rank(&sh.nrx[0], t)[b] = res_at(P, R, mat, x_off);
+        }
+    }
     cl.sync();
+    if (nrx) *nrx = sh.nrx[b];
     double s = 0.0;
     for (int c = 0; c < C; ++c) s = __dadd_rn(s, sh.part[b][c]);
     return s;
 }
 
-// One pass over the CTA's slice: tau = this thread's sequential residual sum
-// over its chunk; the CTA total (warp xor trees, warps in order); the cluster
-// mass.  Returns N (every thread); *tau_out = tau; *cta_out = the CTA total.
-__device__ double mass_pass(cg::cluster_group& cl, MssShared& sh, const float* P, const float* Q, int base_v,
-                            int E, int hlen, int& xbuf, int C, int rank, double* tau_out, double* cta_out) {
+// Chunk sums use four independent chains (element j of each float4 -> chain j),
+// combined (c0 + c1) + (c2 + c3): a fixed order, short dependency chains.
+__device__ __forceinline__ double comb4(const double c[4]) {
+    return __dadd_rn(__dadd_rn(c[0], c[1]), __dadd_rn(c[2], c[3]));
+}
+
+// Sum of this thread's chunk of p, widened into R on the way (R = p in fp64).
+__device__ __forceinline__ double widen_sum(const float* P, double* R, int E) {
     const int t = threadIdx.x;
+    double c[4] = {0.0, 0.0, 0.0, 0.0};
     const float4* P4 = reinterpret_cast<const float4*>(P + t * E);
-    const float4* Q4 = reinterpret_cast<const float4*>(Q + t * E);
-    double tau = 0.0;
-    const int v0 = base_v + t * E;
-    if (hlen == 0) {
+    double2* R2 = reinterpret_cast<double2*>(R + t * E);
+    for (int k = 0; k < E / 4; ++k) {
+        const float4 a = P4[k];
+        const double d0 = f2d(a.x), d1 = f2d(a.y), d2 = f2d(a.z), d3 = f2d(a.w);
+        R2[2 * k] = make_double2(d0, d1);
+        R2[2 * k + 1] = make_double2(d2, d3);
+        c[0] = __dadd_rn(c[0], d0);
+        c[1] = __dadd_rn(c[1], d1);
+        c[2] = __dadd_rn(c[2], d2);
+        c[3] = __dadd_rn(c[3], d3);
+    }
+    return comb4(c);
+}
+
+// sum of this thread's chunk of p (mat == 0) or R
+__device__ __forceinline__ double chunk_sum(const float* P, const double* R, int mat, int E) {
+    const int t = threadIdx.x;
+    double c[4] = {0.0, 0.0, 0.0, 0.0};
+    if (!mat) {
+        const float4* P4 = reinterpret_cast<const float4*>(P + t * E);
         for (int k = 0; k < E / 4; ++k) {
             const float4 a = P4[k];
-            tau = __dadd_rn(tau, (double)a.x);
-            tau = __dadd_rn(tau, (double)a.y);
-            tau = __dadd_rn(tau, (double)a.z);
-            tau = __dadd_rn(tau, (double)a.w);
+            c[0] = __dadd_rn(c[0], f2d(a.x));
+            c[1] = __dadd_rn(c[1], f2d(a.y));
+            c[2] = __dadd_rn(c[2], f2d(a.z));
+            c[3] = __dadd_rn(c[3], f2d(a.w));
         }
     } else {
+        const double2* R2 = reinterpret_cast<const double2*>(R + t * E);
         for (int k = 0; k < E / 4; ++k) {
-            const float4 a = P4[k], b = Q4[k];
-            const int v = v0 + 4 * k;
-            tau = __dadd_rn(tau, residual(a.x, b.x, v, sh, hlen));
-            tau = __dadd_rn(tau, residual(a.y, b.y, v + 1, sh, hlen));
-            tau = __dadd_rn(tau, residual(a.z, b.z, v + 2, sh, hlen));
-            tau = __dadd_rn(tau, residual(a.w, b.w, v + 3, sh, hlen));
+            const double2 a = R2[2 * k], b = R2[2 * k + 1];
+            c[0] = __dadd_rn(c[0], a.x);
+            c[1] = __dadd_rn(c[1], a.y);
+            c[2] = __dadd_rn(c[2], b.x);
+            c[3] = __dadd_rn(c[3], b.y);
         }
     }
-    *tau_out = tau;
-    const double ws = warp_sum_d(tau);
-    if ((t & 31) == 0) sh.wsum[t >> 5] = ws;
-    __syncthreads();
-    double cta = 0.0;
-    for (int w = 0; w < kMssWarps; ++w) cta = __dadd_rn(cta, sh.wsum[w]);
-    *cta_out = cta;
-    return cluster_sum(cl, sh, cta, xbuf, C, rank);
+    return comb4(c);
+}
+
+__device__ __forceinline__ double rej1(double old, double Nx, float q, bool is_x) {
+    return is_x ? 0.0 : fmax(0.0, __dsub_rn(old, __dmul_rn(Nx, f2d(q))));
+}
+
+// One rejection: R (p~) and q (in P's place) from shared memory.
+__device__ __forceinline__ double reject_next(const float* Qs, double* R, int base_v, int E, double Nx, int x) {
+    const int t = threadIdx.x;
+    const int i0 = t * E;
+    double c[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < E; k += 4) {
+        const int i = i0 + k;
+        const float4 q4 = *reinterpret_cast<const float4*>(Qs + i);
+        const double2 a = *reinterpret_cast<const double2*>(R + i), b = *reinterpret_cast<const double2*>(R + i + 2);
+        const double n0 = rej1(a.x, Nx, q4.x, base_v + i == x), n1 = rej1(a.y, Nx, q4.y, base_v + i + 1 == x);
+        const double n2 = rej1(b.x, Nx, q4.z, base_v + i + 2 == x), n3 = rej1(b.y, Nx, q4.w, base_v + i + 3 == x);
+        *reinterpret_cast<double2*>(R + i) = make_double2(n0, n1);
+        *reinterpret_cast<double2*>(R + i + 2) = make_double2(n2, n3);
+        c[0] = __dadd_rn(c[0], n0);
+        c[1] = __dadd_rn(c[1], n1);
+        c[2] = __dadd_rn(c[2], n2);
+        c[3] = __dadd_rn(c[3], n3);
+    }
+    return comb4(c);
+}
+
+// Rebuild p~ after `h` rejections from p and q in global memory (the rare
+// empty-residual case: the walk keeps the previous residual).
+__device__ void rebuild(float* P, double* R, const float* pg, const float* qg, int base_v, int lim, int E,
+                        const MssShared& sh, int h) {
+    const int i0 = threadIdx.x * E;
+    for (int k = 0; k < E; ++k) {
+        const int i = i0 + k;
+        const float pf = i < lim ? pg[base_v + i] : 0.f;
+        const float qf = i < lim ? qg[base_v + i] : 0.f;
+        double v = f2d(pf);
+        for (int j = 0; j < h; ++j) v = rej1(v, sh.hN[j], qf, base_v + i == sh.hx[j]);
+        R[i] = v;
+        P[i] = pf;
+    }
 }
 
 __global__ void __launch_bounds__(kMssThreads, 1) mss_kernel(const MssParams p) {
@@ -156,11 +251,21 @@ __global__ void __launch_bounds__(kMssThreads, 1) mss_kernel(const MssParams p) 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MssShared& sh = *reinterpret_cast<MssShared*>(smem_raw);
     float* P = reinterpret_cast<float*>(smem_raw + align_up(sizeof(MssShared), 128));
-    float* Q = P + p.S;
+    double* R = reinterpret_cast<double*>(P + p.S);  // S is a multiple of 4: 16-B aligned
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int S = p.S, E = p.E, V = p.vocab;
     const int base_v = rank * S;
+    const int lim = min(S, max(0, V - base_v));  // valid entries of this slice
     int xbuf = 0;
+    int trace_k = 0;
+    uint32_t phase = 0;
+    if (t == 0) {
+        ptx::mbar_init(&sh.bar, 1);
+        ptx::fence_mbar_init();
+    }
+    // the padding past the row end is zero for every node (bulk copies never write it)
+    for (int i = lim + t; i < S; i += kMssThreads) P[i] = 0.f;
+    __syncthreads();
 
     pdl_wait();
     const int row_begin = p.tree_offsets[p.req_begin];
@@ -211,80 +316,113 @@ __global__ void __launch_bounds__(kMssThreads, 1) mss_kernel(const MssParams p) 
         int bonus = -1;
         for (;;) {  // one node per iteration (all-nodes mode: exactly one)
             const int u = sh.node;
-            cl.sync();  // peers are done reading the previous node's rows from this CTA
-            // ---- children of u (warp 0, in local index order), then the rows ----
+            const int tk = trace_k++;
+            cl.sync();  // peers are done reading the previous node's slice from this CTA
+            MSS_TRACE(tk, 0, gtime());
+            MSS_TRACE(tk, 6, (unsigned long long)u);
+            // ---- children of u (warp 0, in local index order) ----
             if (warp == 0) {
                 int cnt = 0;
                 for (int c0 = u + 1; c0 < K; c0 += 32) {
                     const int c = c0 + lane;
                     const bool is_kid = c < K && sh.t_par[c] == u;
-                    const unsigned m = __ballot_sync(0xffffffffu, is_kid);
-                    if (is_kid) sh.kid[cnt + __popc(m & ((1u << lane) - 1u))] = c;
-                    cnt += __popc(m);
+                    const unsigned msk = __ballot_sync(0xffffffffu, is_kid);
+                    if (is_kid) sh.kid[cnt + __popc(msk & ((1u << lane) - 1u))] = c;
+                    cnt += __popc(msk);
                 }
                 if (lane == 0) sh.n_kids = cnt;
+                __syncwarp();
+                const float* qrow = p.q + (size_t)(o + u) * (size_t)V;
+                for (int j = lane; j < cnt; j += 32) {  // q(x_j): the decisions read it locally
+                    const int x = sh.t_tok[sh.kid[j]];
+                    sh.kid_q[j] = (x >= 0 && x < V) ? __ldg(qrow + x) : 0.f;
+                }
             }
             __syncthreads();
             const int n_kids = sh.n_kids;
-            const bool need_q = n_kids > 0;  // a leaf only samples its bonus from p
             const size_t row = (size_t)(o + u) * (size_t)V;
             const float* pr = p.p + row;
             const float* qr = p.q + row;
-            const int lim = min(S, max(0, V - base_v));  // valid floats of this slice
+            // ---- the p slice -> shared memory; q slice and the likely next rows -> L2 ----
             if (p.vec4) {
-                const float4* pr4 = reinterpret_cast<const float4*>(pr + base_v);
-                const float4* qr4 = reinterpret_cast<const float4*>(qr + base_v);
-                float4* P4 = reinterpret_cast<float4*>(P);
-                float4* Q4 = reinterpret_cast<float4*>(Q);
-                const int n4 = lim >> 2;
-                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-                int i = t;
-                for (; i + 3 * kMssThreads < n4; i += 4 * kMssThreads) {
-                    float4 a[4], b[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) a[k] = __ldcs(pr4 + i + k * kMssThreads);
-                    if (need_q) {
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) b[k] = __ldcs(qr4 + i + k * kMssThreads);
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) b[k] = z;
+                const uint32_t bytes = (uint32_t)lim * 4u;
+                constexpr uint32_t kPiece = 16384;
+                const uint32_t pieces = (bytes + kPiece - 1) / kPiece;
+                if (warp == 0) {
+                    if (lane == 0) {
+                        if (bytes) ptx::mbar_arrive_expect_tx(&sh.bar, bytes);
+                        else ptx::mbar_arrive(&sh.bar);
                     }
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        P4[i + k * kMssThreads] = a[k];
-                        Q4[i + k * kMssThreads] = b[k];
+                    __syncwarp();
+                    for (uint32_t k = lane; k < pieces; k += 32) {
+                        const uint32_t off = k * kPiece;
+                        ptx::bulk_g2s(reinterpret_cast<unsigned char*>(P) + off,
+                                      reinterpret_cast<const unsigned char*>(pr + base_v) + off,
+                                      min(kPiece, bytes - off), &sh.bar);
+                    }
+                    if (bytes && n_kids > 0 && lane == 31) ptx::bulk_prefetch_l2(qr + base_v, bytes);
+                    // walk: the first two children's rows (the likely next node)
+                    if (p.walk && bytes && lane < 4 && lane / 2 < n_kids) {
+                        const size_t crow = (size_t)(o + sh.kid[lane / 2]) * (size_t)V + base_v;
+                        ptx::bulk_prefetch_l2((lane & 1) ? p.q + crow : p.p + crow, bytes);
                     }
                 }
-                for (; i < n4; i += kMssThreads) {
-                    P4[i] = __ldcs(pr4 + i);
-                    Q4[i] = need_q ? __ldcs(qr4 + i) : z;
-                }
-                for (int j = n4 + t; j < (S >> 2); j += kMssThreads) {
-                    P4[j] = z;
-                    Q4[j] = z;
-                }
+                ptx::mbar_wait(&sh.bar, phase);
+                phase ^= 1;
             } else {
-                for (int i = t; i < S; i += kMssThreads) {
-                    P[i] = i < lim ? __ldcs(pr + base_v + i) : 0.f;
-                    Q[i] = (i < lim && need_q) ? __ldcs(qr + base_v + i) : 0.f;
-                }
+                for (int i = t; i < lim; i += kMssThreads) P[i] = __ldcs(pr + base_v + i);
             }
             __syncthreads();
-            double tau = 0.0, cta = 0.0, N = 0.0;
+            MSS_TRACE(tk, 1, gtime());
+            MSS_TRACE(tk, 7, (unsigned long long)n_kids);
+            int mat = 0;   // history entries materialised in R (0: p~ = p)
+            int hlen = 0;  // rejections so far
+            double N = 0.0, tau = 0.0;
             int accepted = -1;
-            int hlen = 0;
             if (n_kids > 0) {
-                N = mass_pass(cl, sh, P, Q, base_v, E, 0, xbuf, C, rank, &tau, &cta);
+                // owner / offset of a child's token (owner -1: out of range)
+                auto own = [&](int j, int* off) {
+                    const int x = sh.t_tok[sh.kid[j]];
+                    if (x < 0 || x >= V) {
+                        *off = 0;
+                        return -1;
+                    }
+                    *off = x - (x / S) * S;
+                    return x / S;
+                };
+                int xo, xoff;
+                xo = own(0, &xoff);
+                double rx;  // p~(x_j) under the current residual (pushed by its owner)
+                // p -> R (fp64) while summing; then the q slice replaces p in P by bulk
+                // copy (from L2: prefetched at the node start), overlapping the mass
+                // exchange and the first decision -- every rejection pass then runs
+                // from shared memory
+                tau = widen_sum(P, R, E);
+                mat = 1;
+                __syncthreads();  // P is read: the q copy may overwrite it
+                const bool q_tma = p.vec4 && lim > 0;
+                if (q_tma && warp == 0) {
+                    ptx::fence_proxy_async_smem();
+                    const uint32_t bytes = (uint32_t)lim * 4u;
+                    constexpr uint32_t kPiece = 16384;
+                    if (lane == 0) ptx::mbar_arrive_expect_tx(&sh.bar, bytes);
+                    __syncwarp();
+                    for (uint32_t k = lane; k < (bytes + kPiece - 1) / kPiece; k += 32)
+                        ptx::bulk_g2s(reinterpret_cast<unsigned char*>(P) + k * kPiece,
+                                      reinterpret_cast<const unsigned char*>(qr + base_v) + k * kPiece,
+                                      min(kPiece, bytes - k * kPiece), &sh.bar);
+                } else if (!q_tma) {
+                    for (int i = t; i < lim; i += kMssThreads) P[i] = __ldg(qr + base_v + i);
+                }
+                bool q_ready = !q_tma;
+                N = cluster_mass(cl, sh, tau, xbuf, C, rank, xo, xoff, P, R, 1, &rx);
+                MSS_TRACE(tk, 2, gtime());
                 for (int j = 0; j < n_kids; ++j) {
                     const int x = sh.t_tok[sh.kid[j]];
+                    // the decision (every thread, identically): p~(x) and q(x) are local
                     bool acc = false;
                     if (x >= 0 && x < V) {
-                        const int owner = x / S, off = x - owner * S;
-                        const float px = *cl.map_shared_rank(P + off, owner);
-                        const float qx = *cl.map_shared_rank(Q + off, owner);
-                        const double rx = residual(px, qx, x, sh, hlen);
-                        const double lhs = __dmul_rn(__dmul_rn((double)sh.t_uni[sh.kid[j]], N), (double)qx);
+                        const double lhs = __dmul_rn(__dmul_rn((double)sh.t_uni[sh.kid[j]], N), f2d(sh.kid_q[j]));
                         acc = rx > 0.0 && lhs <= rx;
                     } else if (t == 0 && rank == 0) {
                         set_dev_error(p.ws, AS_DEV_BAD_TOKEN, req);
@@ -293,25 +431,49 @@ __global__ void __launch_bounds__(kMssThreads, 1) mss_kernel(const MssParams p) 
                         accepted = j;
                         break;
                     }
-                    // rejected: the residual after this rejection and its mass (entry
-                    // hlen is read by nobody before the barrier below)
-                    if (t == 0) {
+                    // rejected: p~ <- max(0, p~ - N q), p~(x) <- 0, in place; its mass
+                    if (t == 0) {  // history: read only by the rare rebuild below
                         sh.hN[hlen] = N;
                         sh.hx[hlen] = x;
                     }
-                    __syncthreads();
-                    const double N2 = mass_pass(cl, sh, P, Q, base_v, E, hlen + 1, xbuf, C, rank, &tau, &cta);
-                    if (N2 == 0.0) break;  // empty residual: keep the previous p~
+                    if (!q_ready) {
+                        ptx::mbar_wait(&sh.bar, phase);
+                        phase ^= 1;
+                        q_ready = true;
+                    }
+                    if (j < 8) MSS_TRACE(32 + tk, j, gtime());
+                    tau = reject_next(P, R, base_v, E, N, x);  // R: p~, P: q
+                    if (j < 8) MSS_TRACE(48 + tk, j, gtime());
+                    if (j + 1 < n_kids) xo = own(j + 1, &xoff);
+                    else xo = -1;
+                    const double N2 = cluster_mass(cl, sh, tau, xbuf, C, rank, xo, xoff, P, R, 1, &rx);
+                    if (N2 == 0.0) {
+                        // empty residual: keep the previous p~ -- rebuilt from p and q in
+                        // global memory by replaying the hlen earlier rejections (P <- p)
+                        rebuild(P, R, pr, qr, base_v, lim, E, sh, hlen);
+                        __syncthreads();
+                        tau = chunk_sum(P, R, 1, E);
+                        break;
+                    }
                     ++hlen;
                     N = N2;
                 }
+                if (!q_ready) {  // accepted before any rejection: retire the q copy
+                    ptx::mbar_wait(&sh.bar, phase);
+                    phase ^= 1;
+                }
             }
+            MSS_TRACE(tk, 3, gtime());
+            MSS_TRACE(tk, 4, (unsigned long long)hlen);
             int emit;
             if (accepted >= 0) {
                 emit = sh.t_tok[sh.kid[accepted]];
             } else {
                 // ---- bonus: inverse CDF of the current residual ----
-                N = mass_pass(cl, sh, P, Q, base_v, E, hlen, xbuf, C, rank, &tau, &cta);
+                // (tau / N of the current p~: a leaf computes them now; a node whose
+                // children were all rejected has them from its last pass)
+                if (n_kids == 0) tau = chunk_sum(P, R, 0, E);
+                N = cluster_mass(cl, sh, tau, xbuf, C, rank, -1, 0, P, R, mat, nullptr);
                 const double thr = __dmul_rn((double)p.bonus_uni[o + u], N);
                 // exclusive prefix of the per-thread chunk sums inside the CTA
                 double inc = tau;
@@ -321,65 +483,68 @@ __global__ void __launch_bounds__(kMssThreads, 1) mss_kernel(const MssParams p) 
                     if (lane >= d) inc = __dadd_rn(inc, y);
                 }
                 if (lane == 31) sh.wscan[warp] = inc;
-                // prefix of the CTA totals before this CTA, in rank order
-                const int b = xbuf ^ 1;  // the buffer mass_pass just used
-                double pc = 0.0;
+                const int b = xbuf ^ 1;  // the buffer cluster_mass just used
+                double pc = 0.0;  // CTA totals before this CTA, in rank order
                 for (int c = 0; c < rank; ++c) pc = __dadd_rn(pc, sh.part[b][c]);
                 __syncthreads();
                 double wpre = 0.0;
                 for (int w = 0; w < warp; ++w) wpre = __dadd_rn(wpre, sh.wscan[w]);
                 const double base = __dadd_rn(pc, __dadd_rn(wpre, __dsub_rn(inc, tau)));
-                int first = INT_MAX, last = -1;
-                double s = 0.0;
-                const int v0 = base_v + t * E;
-                for (int k = 0; k < E; ++k) {
-                    const int v = v0 + k;
-                    const double val = hlen ? residual(P[t * E + k], Q[t * E + k], v, sh, hlen) : (double)P[t * E + k];
-                    if (val > 0.0) {
-                        last = v;
-                        s = __dadd_rn(s, val);
-                        if (__dadd_rn(base, s) >= thr) {
-                            first = v;
-                            break;
-                        }
+                // cum(v) = fl(base + s_k), s_k = the sequential prefix of this thread's
+                // chunk.  s_k <= s_E <= tau (1 + 2^-40) (tau sums the same non-negative
+                // values in another order, E < 2^12 terms) and fl addition is monotone, so
+                // a chunk whose fl(base + tau (1 + 2^-40)) < thr holds no crossing.
+                int first = INT_MAX;
+                if (__dadd_rn(base, __dmul_rn(tau, 1.0 + 0x1p-40)) >= thr) {
+                    double s = 0.0;
+                    for (int k = 0; k < E && first == INT_MAX; k += 2) {
+                        const int i = t * E + k;
+                        const double r0 = res_at(P, R, mat, i), r1 = res_at(P, R, mat, i + 1);
+                        const double s0 = __dadd_rn(s, r0), s1 = __dadd_rn(s0, r1);
+                        if (r0 > 0.0 && __dadd_rn(base, s0) >= thr) first = base_v + i;
+                        else if (r1 > 0.0 && __dadd_rn(base, s1) >= thr) first = base_v + i + 1;
+                        s = s1;
                     }
                 }
-                int wm = first, wl = last;
+                int wm = first;
 #pragma unroll
-                for (int d = 16; d > 0; d >>= 1) {
-                    wm = min(wm, __shfl_xor_sync(0xffffffffu, wm, d));
-                    wl = max(wl, __shfl_xor_sync(0xffffffffu, wl, d));
-                }
-                if (lane == 0) {
-                    sh.wmin[warp] = wm;
-                    sh.wmax[warp] = wl;
-                }
-                __syncthreads();
-                if (t == 0) {
-                    int bm = INT_MAX, bl = -1;
-                    for (int w = 0; w < kMssWarps; ++w) {
-                        bm = min(bm, sh.wmin[w]);
-                        bl = max(bl, sh.wmax[w]);
-                    }
-                    sh.wmin[0] = bm;
-                    sh.wmax[0] = bl;
-                }
+                for (int d = 16; d > 0; d >>= 1) wm = min(wm, __shfl_xor_sync(0xffffffffu, wm, d));
+                if (lane == 0) sh.wmin[warp] = wm;
                 __syncthreads();
                 const int ib = xbuf;
                 xbuf ^= 1;
-                if (t < C) {
-                    int* dst = cl.map_shared_rank(&sh.ipart[ib][0][0], t);
-                    dst[2 * rank] = sh.wmin[0];
-                    dst[2 * rank + 1] = sh.wmax[0];
+                if (t < 32) {
+                    int bm = t < kMssWarps ? sh.wmin[t] : INT_MAX;
+#pragma unroll
+                    for (int d = 16; d > 0; d >>= 1) bm = min(bm, __shfl_xor_sync(0xffffffffu, bm, d));
+                    if (t < C) cl.map_shared_rank(&sh.ipart[ib][0][0], t)[2 * rank] = bm;
                 }
                 cl.sync();
                 int gm = INT_MAX, gl = -1;
-                for (int c = 0; c < C; ++c) {
-                    gm = min(gm, sh.ipart[ib][c][0]);
-                    gl = max(gl, sh.ipart[ib][c][1]);
+                for (int c = 0; c < C; ++c) gm = min(gm, sh.ipart[ib][c][0]);
+                if (gm == INT_MAX) {
+                    // rounding left the threshold unreached: the last token with mass (rare)
+                    int last = -1;
+                    for (int k = 0; k < E; ++k)
+                        if (res_at(P, R, mat, t * E + k) > 0.0) last = base_v + t * E + k;
+#pragma unroll
+                    for (int d = 16; d > 0; d >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, d));
+                    if (lane == 0) sh.wmax[warp] = last;
+                    __syncthreads();
+                    const int ib2 = xbuf;
+                    xbuf ^= 1;
+                    if (t < 32) {
+                        int bl = t < kMssWarps ? sh.wmax[t] : -1;
+#pragma unroll
+                        for (int d = 16; d > 0; d >>= 1) bl = max(bl, __shfl_xor_sync(0xffffffffu, bl, d));
+                        if (t < C) cl.map_shared_rank(&sh.ipart[ib2][0][0], t)[2 * rank + 1] = bl;
+                    }
+                    cl.sync();
+                    for (int c = 0; c < C; ++c) gl = max(gl, sh.ipart[ib2][c][1]);
                 }
                 emit = gm != INT_MAX ? gm : (gl >= 0 ? gl : 0);
                 bonus = emit;
+                MSS_TRACE(tk, 5, gtime());
             }
             if (t == 0 && rank == 0) {
                 if (p.emitted) p.emitted[o + u] = emit;
@@ -408,7 +573,7 @@ __global__ void __launch_bounds__(kMssThreads, 1) mss_kernel(const MssParams p) 
                 __syncthreads();
                 for (int k = t; k < K; k += kMssThreads) {
                     bool on = false;
-                    for (int m = 0; m < len; ++m) on |= sh.path[m] == k;
+                    for (int m2 = 0; m2 < len; ++m2) on |= sh.path[m2] == k;
                     if (!on) p.emitted[o + k] = -1;
                 }
             }
@@ -421,12 +586,15 @@ __global__ void __launch_bounds__(kMssThreads, 1) mss_kernel(const MssParams p) 
 // ---------------------------------------------------------------------------
 // Host side.
 // ---------------------------------------------------------------------------
+constexpr size_t kMssSmemMax = 227 * 1024;
+
 static void mss_geometry(int vocab, int* C, int* E) {
-    // smallest E (multiple of 4, E/4 odd) with C * 512 * E >= vocab, C = 8 first
+    // smallest E (multiple of 4, E/4 odd) with C * 512 * E >= vocab, C = 8 first;
+    // shared memory: p slice (4 B) + materialised residual (8 B) per entry
     for (int c : {8, 16}) {
         int e = 4;
         while ((long long)c * kMssThreads * e < vocab) e += 8;  // 4, 12, 20, ... keep E/4 odd
-        if (2LL * e * kMssThreads * 4 + (long long)align_up(sizeof(MssShared), 128) <= 200 * 1024) {
+        if (12LL * e * kMssThreads + (long long)align_up(sizeof(MssShared), 128) <= (long long)kMssSmemMax) {
             *C = c;
             *E = e;
             return;
@@ -440,13 +608,13 @@ size_t mss_smem_bytes(int vocab) {
     int C, E;
     mss_geometry(vocab, &C, &E);
     if (!C) return 0;
-    return align_up(sizeof(MssShared), 128) + 2 * (size_t)E * kMssThreads * 4;
+    return align_up(sizeof(MssShared), 128) + 12 * (size_t)E * kMssThreads;
 }
 
 int launch_mss(int req_begin, int req_end, int n_tree_rows, int vocab, const int32_t* tree_offsets,
                const int32_t* tree_parent, const int32_t* tree_tokens, const float* p_rows, const float* q_rows,
                const float* uni, const float* bonus_uni, int32_t* emitted, int32_t* records, int max_path, int walk,
-               void* ws, cudaStream_t stream) {
+               void* ws, size_t ws_bytes, cudaStream_t stream) {
     int C, E;
     mss_geometry(vocab, &C, &E);
     if (!C) return 1;
@@ -460,7 +628,7 @@ int launch_mss(int req_begin, int req_end, int n_tree_rows, int vocab, const int
         static std::map<std::pair<int, size_t>, int> fit;  // (device, smem) -> active clusters
         std::lock_guard<std::mutex> lk(mu);
         if (!attrs_set[dev]) {
-            if (cudaFuncSetAttribute(mss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+            if (cudaFuncSetAttribute(mss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMssSmemMax) !=
                     cudaSuccess ||
                 cudaFuncSetAttribute(mss_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
                 return -1;
@@ -513,6 +681,13 @@ int launch_mss(int req_begin, int req_end, int n_tree_rows, int vocab, const int
     p.S = E * kMssThreads;
     p.vec4 = (vocab % 4 == 0) && ((reinterpret_cast<uintptr_t>(p_rows) | reinterpret_cast<uintptr_t>(q_rows)) % 16 == 0);
     p.ws = ws;
+    p.trace = nullptr;
+#ifdef AS_DEBUG
+    if (ws_bytes >= kWsHeaderBytes + 64 * 8 * 8)
+        p.trace = reinterpret_cast<unsigned long long*>(reinterpret_cast<unsigned char*>(ws) + kWsHeaderBytes);
+#else
+    (void)ws_bytes;
+#endif
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(n_clusters * C);
     cfg.blockDim = dim3(kMssThreads);

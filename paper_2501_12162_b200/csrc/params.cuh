@@ -91,7 +91,7 @@ size_t mss_smem_bytes(int vocab);
 int launch_mss(int req_begin, int req_end, int n_tree_rows, int vocab, const int32_t* tree_offsets,
                const int32_t* tree_parent, const int32_t* tree_tokens, const float* p_rows, const float* q_rows,
                const float* uni, const float* bonus_uni, int32_t* emitted, int32_t* records, int max_path, int walk,
-               void* ws, cudaStream_t stream);
+               void* ws, size_t ws_bytes, cudaStream_t stream);
 int launch_attn_tc(const CUtensorMap* maps, const TcParams& p, int head_dim, int n_sms, cudaStream_t stream);
 int tc_ctas_per_sm();
 size_t beam_ws_bytes(int n_req, int width, int vocab);
