@@ -52,8 +52,16 @@ CONFIGS = {
     "c5": dict(desc="long-context stress: 32 requests, 32k-token KV prefixes, 64-node trees, Llama-3-8B shapes",
                n_req=32, d=8, w=8, sigma=(1.0, 4.0), A=9.0, n_max=63, budget=2048, L=32768, n_q=32, n_kv=8,
                head_dim=128, page_size=64, dtype="bf16"),
+    # the c3 batch verify-only -- sizes K_i = 4 + floor(61 u^4) trimmed to sum <= 4096,
+    # random recursive trees of depth <= 8, given (no select in the step)
+    "c3b": dict(desc="c3 verify-only: 256 requests, fixed sizes K = 4 + floor(61 u^4) (sum <= 4096), random "
+                     "recursive trees of depth <= 8, Llama-3-8B shapes, 2k KV; step = attention + accept",
+                n_req=256, d=8, w=8, sigma=(1.0, 8.0), A="mix", n_max=63, budget=4096, L=2048, n_q=32, n_kv=8,
+                head_dim=128, page_size=64, dtype="bf16", verify_only=True),
 }
-CONFIG_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}
+CONFIG_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4, "c3b": 2}
+# requests of the bounded CPU-oracle sample (cpu_baseline and the --impl reference arm alike)
+ORACLE_SAMPLE_REQ = {"c1": 1, "c2": 64, "c3": 64, "c3b": 64, "c4": 16, "c5": 2}
 METRIC = "verified tree tokens/sec and attn HBM GB/s (% roofline) at 1/2/4/8 B200"
 L2_BYTES = 126 * 1024 * 1024
 
@@ -130,6 +138,8 @@ def make_workload(cfg_name, device="cuda", seed_salt=0, rank=0, world=1, engine=
         sel = oracle.select_literal(F["cand_offsets"], F["cand_parent"], F["cand_prob"], A, c["d"], c["n_max"],
                                     c["budget"])
         _set_targets(W, sel["tree_offsets"], sel["tree_src"])
+        if c.get("verify_only"):
+            _set_given_trees(W, synth.rng_for(CONFIG_INDEX[cfg_name], 77 + seed_salt))
         return W
     import paper_2501_12162_b200 as ada
     W["ada"] = ada
@@ -152,7 +162,42 @@ def make_workload(cfg_name, device="cuda", seed_salt=0, rank=0, world=1, engine=
     # the first (GPU) selection and gathered on the host (synthetic target model).
     run_select(W)
     _set_targets(W, W["sel"]["tree_offsets"].cpu().numpy(), W["sel"]["tree_src"].cpu().numpy())
+    if c.get("verify_only"):
+        _set_given_trees(W, synth.rng_for(CONFIG_INDEX[cfg_name], 77 + seed_salt))
     return W
+
+
+def _set_given_trees(W, rng):
+    """c3b: trees given, not selected: K_i = 4 + floor(61 u^4), the
+    batch trimmed (last requests first) until sum K <= budget, random recursive
+    trees of depth <= 8; draft tokens random; each node's target token is one of
+    its children's tokens with probability 0.6 (else random), so walks go deep."""
+    n, R = W["n"], W["R"]
+    sizes = 4 + np.floor(61 * rng.random(n) ** 4).astype(np.int64)
+    while sizes.sum() > W["c"]["budget"]:
+        sizes[np.argmax(sizes)] -= 1
+    to = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    par = np.concatenate([synth.random_tree_parents(rng, int(k), max_depth=8) for k in sizes]).astype(np.int32)
+    used = int(to[-1])
+    tok = rng.integers(0, synth.LLAMA3_VOCAB, used).astype(np.int32)
+    tgt = rng.integers(0, synth.LLAMA3_VOCAB, used).astype(np.int32)
+    for i in range(n):
+        o = int(to[i])
+        for v in range(int(sizes[i])):
+            kids = [c for c in range(v + 1, int(sizes[i])) if par[o + c] == v]
+            if kids and rng.random() < 0.6:
+                tgt[o + v] = tok[o + kids[int(rng.integers(0, len(kids)))]]
+    dev = W["device"]
+    if "sel" in W:  # the CUDA path's tree buffers (the oracle engine has none)
+        W["sel"]["tree_offsets"].copy_(torch.from_numpy(to))
+        W["sel"]["tree_parent"][:used].copy_(torch.from_numpy(par))
+        W["sel"]["tree_token"][:used].copy_(torch.from_numpy(tok))
+    t = np.zeros(R, np.int32)
+    t[:used] = tgt
+    W["target_tokens"] = torch.from_numpy(t).to(dev)
+    W["given"] = dict(tree_offsets=to, tree_parent=par, tree_token=tok, target=tgt)
+    W["tree_sizes"] = sizes.astype(np.int64)
+    W["tree_tokens_total"] = used
 
 
 def _set_targets(W, to, src):
@@ -178,7 +223,7 @@ def run_attention(W):
     kc, vc = W["pools"][W["pool_idx"]]
     out, _ = ada.tree_verify_attn(W["q"], W["k_tree"], W["v_tree"], kc, vc, W["page_table"], W["kv_len"],
                                   W["sel"]["tree_offsets"], W["sel"]["tree_parent"], W["sm_scale"], out=W["out"],
-                                  workspace=W["ws_attn"])
+                                  workspace=W["ws_attn"], schedule=W.get("schedule"))
     return out
 
 
@@ -268,7 +313,7 @@ class Step:
         skip = os.environ.get("AS_BENCH_SKIP", "")  # ablation only (never for reported numbers)
         if eb:
             _record(eb[0], external)
-        if "select" not in skip:
+        if "select" not in skip and not W["c"].get("verify_only"):
             run_select(W)
         if eb:
             _record(eb[1], external)
@@ -342,6 +387,26 @@ def _traffic_from_profiles(cfg):
 
 
 # --------------------------------------------------------------------------- CPU oracle legs
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def _tree_size_summary(sizes):
+    s = np.asarray(sizes, np.int64)
+    edges = [1, 2, 4, 8, 16, 32, 64, 128, 257]
+    hist = {f"{edges[k]}-{edges[k + 1] - 1}": int(((s >= edges[k]) & (s < edges[k + 1])).sum())
+            for k in range(len(edges) - 1)}
+    return {"min": int(s.min()), "p10": float(np.percentile(s, 10)), "median": float(np.median(s)),
+            "p90": float(np.percentile(s, 90)), "max": int(s.max()), "mean": round(float(s.mean()), 2),
+            "hist": {k: v for k, v in hist.items() if v}}
+
+
 def cpu_oracle_sample(W, n_sample_req, threads):
     """Time the CPU oracle (as it stands) on a bounded sample of the workload:
     full select (Alg. 2 literal), attention for `n_sample_req` requests, and the
@@ -350,8 +415,12 @@ def cpu_oracle_sample(W, n_sample_req, threads):
     F = W["host"]
     c = W["c"]
     t0 = time.perf_counter()
-    sel = oracle.select_literal(F["cand_offsets"], F["cand_parent"], F["cand_prob"], W["A"], c["d"], c["n_max"],
-                                c["budget"])
+    if c.get("verify_only"):  # c3b: the trees are given (no select in the step)
+        gv = W["given"]
+        sel = dict(tree_offsets=gv["tree_offsets"], tree_parent=gv["tree_parent"])
+    else:
+        sel = oracle.select_literal(F["cand_offsets"], F["cand_parent"], F["cand_prob"], W["A"], c["d"],
+                                    c["n_max"], c["budget"])
     t_sel = time.perf_counter() - t0
     n = W["n"]
     reqs = list(range(min(n_sample_req, n)))
@@ -377,9 +446,12 @@ def cpu_oracle_sample(W, n_sample_req, threads):
     oracle.tree_attn(q, kt, vt, hk, hv, pt2, kl, offs, sel["tree_parent"][rows], np.float32(W["sm_scale"]),
                      n_threads=threads, want_lse=False)
     t_attn = time.perf_counter() - t0
-    toks = np.asarray(F["cand_token"])
-    req_of = np.repeat(np.arange(len(reqs)), sizes)
-    tt = toks[F["cand_offsets"][np.array(reqs)][req_of] + sel["tree_src"][rows]]
+    if c.get("verify_only"):
+        tt = W["given"]["tree_token"][rows]
+    else:
+        toks = np.asarray(F["cand_token"])
+        req_of = np.repeat(np.arange(len(reqs)), sizes)
+        tt = toks[F["cand_offsets"][np.array(reqs)][req_of] + sel["tree_src"][rows]]
     tg = W["target_tokens"].cpu().numpy()[rows]
     t0 = time.perf_counter()
     acc = oracle.accept_walk(offs, sel["tree_parent"][rows], tt, target_tokens=tg, max_path=W["max_path"])
@@ -388,7 +460,9 @@ def cpu_oracle_sample(W, n_sample_req, threads):
     frac = len(reqs) / n
     secs = t_sel * frac + t_attn + t_acc
     desc = (f"oracle (C, fp64) on {len(reqs)}/{n} requests of {W['cfg']}: attention + walk/commit for those "
-            f"requests, Alg. 2 select on the full batch pro-rated ({t_sel:.3f}s x {frac:.3f}); {threads} threads")
+            f"requests, " + ("trees given (verify-only)" if c.get("verify_only") else
+                             f"Alg. 2 select on the full batch pro-rated ({t_sel:.3f}s x {frac:.3f})") +
+            f"; {threads} threads")
     return int(sizes.sum()), secs, desc
 
 
@@ -396,7 +470,7 @@ def cpu_oracle_sample(W, n_sample_req, threads):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -405,6 +479,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-spec", action="store_true", help="skip the NEXT-1 speculation-layer measurement")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e / cpu legs)")
+    ap.add_argument("--schedule", default="", help="attention schedule override, e.g. nq=2,cs=1,split=0 (A/B only)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -428,6 +503,8 @@ def main():
         dist_ctx = ShardedAccept()  # default process group
     emu = int(os.environ.get("AS_BENCH_EMULATE_WORLD", "0"))  # analysis only: one rank's shard of an N-GPU run
     W = make_workload(args.config, "cuda", rank=rank, world=emu if (emu > 1 and world == 1) else world)
+    if args.schedule:
+        W["schedule"] = W["ada"].parse_schedule(args.schedule)
     step = Step(W, dist_ctx)
     use_graph = not args.no_graph
     for _ in range(2):  # eager warm-up (attribute setup, NCCL communicator)
@@ -491,10 +568,17 @@ def main():
     t_sel = float(np.mean([e[0].elapsed_time(e[1]) for e in brk_ev]))
     t_attn_b = float(np.mean([e[1].elapsed_time(e[2]) for e in brk_ev]))
     t_acc = float(np.mean([e[2].elapsed_time(e[3]) for e in brk_ev]))
+    # per-step distributions: attention launches of the timed graph, whole steps of the
+    # instrumented replay (select start -> accept end)
+    attn_each = np.array([e[0].elapsed_time(e[1]) for e in attn_ev])
+    step_each = np.array([e[0].elapsed_time(e[3]) for e in brk_ev])
+    dist_stats = lambda a: {"median": round(float(np.median(a)), 4), "p10": round(float(np.percentile(a, 10)), 4),
+                            "p90": round(float(np.percentile(a, 90)), 4), "n": int(len(a))}
     if world > 1:
+        # max over ranks: the step and the attention launch (the roofline uses the slowest rank)
         t = torch.tensor([total_ms, t_attn], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms, t_attn_max = float(t[0]), float(t[1])
+        total_ms, t_attn = float(t[0]), float(t[1])
     ms_per_step = total_ms / args.steps
     tokens = int(W["tree_tokens_total"])
     value = tokens / (ms_per_step / 1e3)
@@ -541,14 +625,20 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         threads = os.cpu_count() or 1
-        n_s = {"c1": 1, "c2": 64, "c3": 64, "c4": 16, "c5": 2}[args.config]
-        toks_t, secs_t, reps = 0, 0.0, 0
-        while secs_t < 10.0 and reps < 50:
-            toks, secs, desc = cpu_oracle_sample(W, n_s, threads)
-            toks_t, secs_t, reps = toks_t + toks, secs_t + secs, reps + 1
-        cpu = {"value": round(toks_t / secs_t, 2), "unit": "verified tree tokens/s", "cores": threads,
-               "kind": "oracle", "sample": f"{desc}; repeated {reps}x", "seconds": round(secs_t, 3)}
-    launches_per_step = 3 if world == 1 else 4  # select, attention, walk, commit (+ the NCCL all-gather)
+        n_s = ORACLE_SAMPLE_REQ[args.config]
+        timed = {}
+        for nth, budget_s in ((threads, 10.0), (1, 8.0)):  # all cores, then one thread
+            toks_t, secs_t, reps = 0, 0.0, 0
+            while (secs_t < budget_s and reps < 50) or reps == 0:
+                toks, secs, desc = cpu_oracle_sample(W, n_s, nth)
+                toks_t, secs_t, reps = toks_t + toks, secs_t + secs, reps + 1
+            timed[nth] = (toks_t / secs_t, desc, reps, secs_t)
+        v, desc, reps, secs_t = timed[threads]
+        cpu = {"value": round(v, 2), "unit": "verified tree tokens/s", "cores": threads, "kind": "oracle",
+               "sample": f"{desc}; repeated {reps}x", "seconds": round(secs_t, 3), "cpu_model": _cpu_model(),
+               "single_thread_value": round(timed[1][0], 2), "single_thread_seconds": round(timed[1][3], 3)}
+    # select, attention, accept (walk + commit at N>1, plus the NCCL all-gather); no select in c3b
+    launches_per_step = (3 if world == 1 else 4) - (1 if W["c"].get("verify_only") else 0)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "verified tree tokens/s", "n_gpus": world,
@@ -558,7 +648,8 @@ def main():
             "config": {"workload": f"{args.config}: {W['c']['desc']}", "n_req": W["n"],
                        "tree_tokens": tokens, "kv_len": W["c"]["L"], "q_heads": W["c"]["n_q"],
                        "kv_heads": W["c"]["n_kv"], "head_dim": W["D"], "page_size": W["page_size"],
-                       "budget": W["c"]["budget"], "parallelism": f"kv-head sharding x{world}" if world > 1
+                       "budget": W["c"]["budget"], "tree_sizes": _tree_size_summary(W["tree_sizes"]),
+                       "verify_only": bool(W["c"].get("verify_only", False)), "parallelism": f"kv-head sharding x{world}" if world > 1
                        else "1 GPU", "l2": ("inputs larger than L2: KV %.0f MiB/GPU" % (W["kv_bytes"] / 2**20))
                        if W["n_pools"] == 1 else f"{W['n_pools']} rotating KV pools (> 3x L2)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
@@ -568,6 +659,10 @@ def main():
                                                        if os.environ.get("AS_BENCH_SKIP") else {}),
             "breakdown_ms": {"select": round(t_sel, 4), "attention": round(t_attn_b, 4), "accept_commit": round(t_acc, 4),
                              "note": "separate instrumented replay (events around every call)"},
+            "attention_tokens_per_s": round(tokens / (t_attn / 1e3), 1),
+            "distribution_ms": {"attention": dist_stats(attn_each), "step": dist_stats(step_each),
+                                "note": "attention: CUDA events around each launch of the timed graph; step: "
+                                        "select start -> accept end in the instrumented replay"},
         }
         print(json.dumps(line), flush=True)
     if dist_ctx is not None:
@@ -873,7 +968,9 @@ def main_reference(args, rank, world):
         return
     W = make_workload(args.config, "cpu", engine="oracle")
     threads = os.cpu_count() or 1
-    n_s = {"c1": 1, "c2": 2, "c3": 8, "c4": 1, "c5": 1}[args.config]
+    # the cpu_baseline sample, shrunk for long runs so that K + W steps stay within a few minutes
+    n_s = max(1, min(ORACLE_SAMPLE_REQ[args.config],
+                     ORACLE_SAMPLE_REQ[args.config] * 40 // max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         cpu_oracle_sample(W, n_s, threads)
     tot_tok, tot_s = 0, 0.0
@@ -889,7 +986,7 @@ def main_reference(args, rank, world):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; no datasets)",
             "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}"},
             "cpu_baseline": {"value": round(value, 2), "unit": "verified tree tokens/s", "cores": threads,
-                             "kind": "oracle", "sample": desc},
+                             "kind": "oracle", "sample": desc, "cpu_model": _cpu_model()},
             "e2e": {"value": round(value, 2), "unit": "verified tree tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -223,6 +223,34 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
                               float sm_scale, void* out, float* lse, void* workspace,
                               size_t workspace_bytes, void* stream);
 
+/*
+ * Schedule override of the bf16 path (A/B tests and tuning; every choice gives
+ * bit-identical results).  NULL or zero fields = the library's choice.
+ *   q_tiles_per_cta  1: one 128-row q-tile per CTA (2 CTAs / SM); 2: the two
+ *                    q-tiles of a (request, kv head) in one CTA sharing every
+ *                    K/V tile (1 CTA / SM); 0: auto (2 when trees span > 1 q-tile)
+ *   cluster_ctas     2 or 4: clusters of one-q-tile CTAs, each K/V tile fetched
+ *                    once and multicast (measured slower); 0/1: none
+ *   split            0: whole units only; 1 or -1/auto: split-KV / tail pieces allowed
+ * Unknown values return AS_ERR_INVALID_ARG.
+ */
+typedef struct {
+    int32_t q_tiles_per_cta;
+    int32_t cluster_ctas;
+    int32_t split;
+} as_attn_schedule;
+
+as_status as_tree_verify_attn_sched(as_dtype dtype, int32_t n_req, int32_t n_tree_rows,
+                                    int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
+                                    const void* q, const void* k_tree, const void* v_tree,
+                                    const void* k_cache, const void* v_cache, int32_t num_pages,
+                                    int32_t page_size, const int32_t* page_table,
+                                    int32_t max_pages_per_req, const int32_t* kv_len,
+                                    const int32_t* tree_offsets, const int32_t* tree_parent,
+                                    float sm_scale, void* out, float* lse, void* workspace,
+                                    size_t workspace_bytes, void* stream,
+                                    const as_attn_schedule* schedule);
+
 /* ------------------------------------------------------------------------- */
 /* Accept: acceptance walk + KV commit                               */
 /* ------------------------------------------------------------------------- */

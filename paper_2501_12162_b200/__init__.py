@@ -13,7 +13,7 @@ import os
 
 import torch
 
-__all__ = ["lib", "select_trees", "select_global_greedy", "select_topm", "select_equal_greedy", "sample_tokens", "mss_verify", "AS_MSS_WALK", "AS_MSS_ALL_NODES", "tree_verify_attn", "accept_tokens", "Workspace", "check_device_error",
+__all__ = ["lib", "select_trees", "select_global_greedy", "select_topm", "select_equal_greedy", "sample_tokens", "mss_verify", "AS_MSS_WALK", "AS_MSS_ALL_NODES", "tree_verify_attn", "AttnSchedule", "parse_schedule", "accept_tokens", "Workspace", "check_device_error",
            "selftest_umma", "AS_ACCEPT_FUSED", "AS_ACCEPT_WALK_ONLY", "AS_ACCEPT_COMMIT_ONLY",
            "AS_ACCEPT_WALK_RECORDS", "AS_ACCEPT_COMMIT_RECORDS", "beam_step", "beam_workspace_size", "AdaServeError",
            "select_workspace_size", "attn_workspace_size", "accept_workspace_size", "DEVICE_ERRORS"]
@@ -67,6 +67,7 @@ def lib():
         L.as_tree_verify_attn.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp,
                                           _c_i32, _c_i32, _vp, _c_i32, _vp, _vp, _vp, _f32, _vp, _vp, _vp, _c_sz,
                                           _vp]
+        L.as_tree_verify_attn_sched.argtypes = L.as_tree_verify_attn.argtypes + [_vp]
         L.as_accept_tokens.argtypes = [_c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_i32,
                                        _c_i32, _c_i32, _vp, _vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_i32, _vp, _vp,
                                        _c_i32, _c_i32, _vp, _c_i32, _vp, _vp, _vp, _c_sz, _vp]
@@ -308,11 +309,31 @@ def select_equal_greedy(cand_offsets, cand_parent, cand_prob, budget, cand_token
     return select_topm(cand_offsets, cand_parent, cand_prob, budget // n - 1, budget % n, cand_token, out, workspace)
 
 
+class AttnSchedule(ctypes.Structure):
+    """as_attn_schedule: q_tiles_per_cta (0 auto, 1, 2), cluster_ctas (0/1, 2, 4),
+    split (-1 auto, 0 whole units only, 1 allowed) -- A/B overrides, results identical."""
+    _fields_ = [("q_tiles_per_cta", ctypes.c_int32), ("cluster_ctas", ctypes.c_int32), ("split", ctypes.c_int32)]
+
+
+def parse_schedule(spec):
+    """'nq=2,cs=1,split=0' (any subset) -> AttnSchedule; None/'' -> None."""
+    if not spec:
+        return None
+    s = AttnSchedule(0, 0, -1)
+    for kv in str(spec).split(","):
+        k, v = kv.split("=")
+        setattr(s, {"nq": "q_tiles_per_cta", "cs": "cluster_ctas", "split": "split"}[k.strip()], int(v))
+    return s
+
+
 def tree_verify_attn(q, k_tree, v_tree, k_cache, v_cache, page_table, kv_len, tree_offsets, tree_parent, sm_scale,
-                     want_lse=False, out=None, lse=None, workspace=None):
+                     want_lse=False, out=None, lse=None, workspace=None, schedule=None):
     """as_tree_verify_attn.  q [R, n_q, d], k_tree/v_tree [R, n_kv, d],
     caches [pages, n_kv, page_size, d] (bf16 -> tcgen05 path, fp32 -> SIMT path),
-    page_table [n, max_pages] int32, kv_len [n] int32.  Returns (out, lse)."""
+    page_table [n, max_pages] int32, kv_len [n] int32.  Returns (out, lse).
+    schedule: None, an AttnSchedule, or a parse_schedule string (A/B only)."""
+    if isinstance(schedule, str):
+        schedule = parse_schedule(schedule)
     R, n_q, d = q.shape
     n_kv = k_tree.shape[1]
     n = tree_offsets.numel() - 1
@@ -326,11 +347,12 @@ def tree_verify_attn(q, k_tree, v_tree, k_cache, v_cache, page_table, kv_len, tr
     if want_lse and lse is None:
         lse = torch.empty((R, n_q), dtype=torch.float32, device=q.device)
     ws = workspace if workspace is not None else Workspace(attn_workspace_size(dt, n, R, n_q, d, 0), q.device)
-    st = lib().as_tree_verify_attn(dt, n, R, n_q, n_kv, d, _ptr(q), _ptr(k_tree), _ptr(v_tree), _ptr(k_cache),
-                                   _ptr(v_cache), k_cache.shape[0], k_cache.shape[2], _ptr(page_table),
-                                   page_table.shape[1] if page_table.dim() == 2 else 0, _ptr(kv_len),
-                                   _ptr(tree_offsets), _ptr(tree_parent), float(sm_scale), _ptr(out),
-                                   _ptr(lse if want_lse else None), ws.ptr, ws.nbytes, _stream())
+    st = lib().as_tree_verify_attn_sched(dt, n, R, n_q, n_kv, d, _ptr(q), _ptr(k_tree), _ptr(v_tree),
+                                         _ptr(k_cache), _ptr(v_cache), k_cache.shape[0], k_cache.shape[2],
+                                         _ptr(page_table), page_table.shape[1] if page_table.dim() == 2 else 0,
+                                         _ptr(kv_len), _ptr(tree_offsets), _ptr(tree_parent), float(sm_scale),
+                                         _ptr(out), _ptr(lse if want_lse else None), ws.ptr, ws.nbytes, _stream(),
+                                         ctypes.byref(schedule) if schedule is not None else None)
     _check(st, "as_tree_verify_attn")
     return out, (lse if want_lse else None)
 

@@ -228,6 +228,24 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
                               const int32_t* kv_len, const int32_t* tree_offsets, const int32_t* tree_parent,
                               float sm_scale, void* out, float* lse, void* workspace, size_t workspace_bytes,
                               void* stream) {
+    return as_tree_verify_attn_sched(dtype, n_req, n_tree_rows, n_q_heads, n_kv_heads, head_dim, q, k_tree, v_tree,
+                                     k_cache, v_cache, num_pages, page_size, page_table, max_pages_per_req, kv_len,
+                                     tree_offsets, tree_parent, sm_scale, out, lse, workspace, workspace_bytes, stream,
+                                     nullptr);
+}
+
+as_status as_tree_verify_attn_sched(as_dtype dtype, int32_t n_req, int32_t n_tree_rows, int32_t n_q_heads,
+                                    int32_t n_kv_heads, int32_t head_dim, const void* q, const void* k_tree,
+                                    const void* v_tree, const void* k_cache, const void* v_cache, int32_t num_pages,
+                                    int32_t page_size, const int32_t* page_table, int32_t max_pages_per_req,
+                                    const int32_t* kv_len, const int32_t* tree_offsets, const int32_t* tree_parent,
+                                    float sm_scale, void* out, float* lse, void* workspace, size_t workspace_bytes,
+                                    void* stream, const as_attn_schedule* schedule) {
+    if (schedule && (schedule->q_tiles_per_cta < 0 || schedule->q_tiles_per_cta > 2 ||
+                     !(schedule->cluster_ctas == 0 || schedule->cluster_ctas == 1 || schedule->cluster_ctas == 2 ||
+                       schedule->cluster_ctas == 4) ||
+                     schedule->split < -1 || schedule->split > 1))
+        return AS_ERR_INVALID_ARG;
     if (n_req < 0 || n_tree_rows < 0 || n_q_heads <= 0 || n_kv_heads <= 0 || num_pages < 0 || max_pages_per_req < 0)
         return AS_ERR_INVALID_ARG;
     if (n_q_heads % n_kv_heads != 0) return AS_ERR_UNSUPPORTED;
@@ -307,18 +325,16 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
     // is the caller's row allocation per request: one q-tile -> one-q-tile CTAs, two
     // per SM; more -> the q-tiles of a head share every K/V tile fetch (NQ = 2: two
     // q-tiles in one CTA; cs: a cluster of one-q-tile CTAs with multicast).
-    // AS_ATTN_NQ / AS_ATTN_CS override the choice (schedule A/B; results identical).
+    // as_tree_verify_attn_sched overrides the choice (A/B; results identical).
     {
         const long long rows_per_req = n_req > 0 ? (long long)n_tree_rows / n_req : 0;
         const long long qt = (G * rows_per_req + 127) / 128;
         p.nq = qt > 1 ? 2 : 1;
         p.cs = 1;
-        const char* nqe = getenv("AS_ATTN_NQ");
-        if (nqe && (atoi(nqe) == 1 || atoi(nqe) == 2)) p.nq = atoi(nqe);
-        const char* cse = getenv("AS_ATTN_CS");
-        if (cse && (atoi(cse) == 1 || atoi(cse) == 2 || atoi(cse) == 4)) {
-            p.cs = atoi(cse);
-            if (p.cs > 1) p.nq = 1;
+        if (schedule && schedule->q_tiles_per_cta > 0) p.nq = schedule->q_tiles_per_cta;
+        if (schedule && schedule->cluster_ctas > 1) {
+            p.cs = schedule->cluster_ctas;
+            p.nq = 1;
         }
     }
     {
@@ -327,9 +343,8 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
         const size_t cnt_bytes = align_up((size_t)p.n_units * 8, 256);  // tile counters + merge counters
         const size_t need = kWsHeaderBytes + kAttnTraceBytes + cnt_bytes + 2 * (size_t)nsm * tc_ctas_per_sm() * slot;
         unsigned char* base = reinterpret_cast<unsigned char*>(workspace) + kWsHeaderBytes + kAttnTraceBytes;
-        const char* skenv = getenv("AS_ATTN_STREAMK");  // A/B switch (debug)
-        // A/B: AS_ATTN_STREAMK=0 whole units only (no split-KV)
-        p.stream_k = (workspace_bytes >= need && !(skenv && atoi(skenv) == 0)) ? ((skenv && atoi(skenv) == 2) ? 2 : 1) : 0;
+        // split-KV / tail pieces need the counters and partial slots in the workspace
+        p.stream_k = (workspace_bytes >= need && !(schedule && schedule->split == 0)) ? 1 : 0;
         p.cnt = reinterpret_cast<int*>(base);
         p.cnt2 = p.cnt + p.n_units;
         p.partial = reinterpret_cast<float*>(base + cnt_bytes);

@@ -764,11 +764,15 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
 // Host side.
 // ---------------------------------------------------------------------------
 int pdl_enabled() {
+#ifdef AS_DEBUG
     static const int v = [] {
-        const char* e = getenv("AS_PDL");  // A/B switch: 0 = plain stream ordering
+        const char* e = getenv("AS_PDL");  // A/B switch (debug build): 0 = plain stream ordering
         return (e && e[0] == '0') ? 0 : 1;
     }();
     return v;
+#else
+    return 1;
+#endif
 }
 
 static int cluster_size_for(int n) {

@@ -28,7 +28,7 @@ s.record(); [b.copy_(a) for _ in range(5)]; e.record(); torch.cuda.synchronize()
 print(f"calib copy: {5*2*a.numel()*2/(s.elapsed_time(e)/1e3)/1e9:.0f} GB/s")
 PY
 one() {
-  timeout 200 python bench.py --config ${CFG:-c2} --steps 20 --warmup 5 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python -c "
+  timeout 200 python bench.py --config ${CFG:-c2} --schedule "$SCHED" --steps 20 --warmup 5 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); r=d['roofline']
 print('${CFG:-c2} $TAG', 'attn_ms', r['attn_ms'], 'GB/s', r['achieved'], 'frac', r['frac'], 'step_ms', d['ms_per_step'], 'bd', d['breakdown_ms'])"
@@ -38,5 +38,5 @@ for KL in 1 2 3; do
 TAG="klead$KL" AS_ATTN_KLEAD=$KL one
 done
 TAG="mode2" AS_ATTN_DEBUG_MODE=2 one
-TAG="streamk0" AS_ATTN_STREAMK=0 one
+TAG="streamk0" SCHED="split=0" one
 done

@@ -1,7 +1,7 @@
 """Randomised stress of the bf16 attention path against the oracle (GPU; not
 part of the test suite): random batch sizes, tree sizes/shapes, prefix lengths
 (incl. 0 and page-boundary values), head layouts and head dims, under every
-schedule switch (AS_ATTN_NQ 1/2, AS_ATTN_STREAMK 0/1).  Usage:
+schedule switch (nq 1/2, split 0/1 via as_tree_verify_attn_sched).  Usage:
     python scripts/stress_attn.py [cases] [seed]
 Prints one line per failing case and a summary."""
 import os
@@ -43,12 +43,10 @@ for c in range(cases):
     g = workload_to_device(w, torch.bfloat16)
     for nq in ("1", "2"):
         for sk in ("0", "1"):
-            os.environ["AS_ATTN_NQ"] = nq
-            os.environ["AS_ATTN_STREAMK"] = sk
             ws = ada.Workspace(256)
             out, lse = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"],
                                             g["page_table"], g["kv_len"], g["tree_offsets"], g["tree_parent"],
-                                            scale, want_lse=True, workspace=ws)
+                                            scale, want_lse=True, workspace=ws, schedule=f"nq={nq},split={sk}")
             code = ada.check_device_error(ws)[0]
             err = float(np.abs(out.float().cpu().numpy() - ref).max())
             lerr = float(np.abs(lse.cpu().numpy() - ref_lse).max())

@@ -474,23 +474,27 @@ def test_attn_fp32(ada, ci):
     assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-4
 
 
-def _shape_env(monkeypatch, shape):
-    """Schedule overrides: "1"/"2" = AS_ATTN_NQ (q-tiles per CTA), "cs2"/"cs4" =
-    AS_ATTN_CS (clusters of one-q-tile CTAs sharing K/V by multicast)."""
+def _sched(shape, split=None):
+    """as_tree_verify_attn_sched overrides: "1"/"2" = q-tiles per CTA, "cs2"/"cs4" =
+    clusters of one-q-tile CTAs sharing K/V by multicast; split "0" = whole units."""
+    parts = []
     if shape.startswith("cs"):
-        monkeypatch.setenv("AS_ATTN_CS", shape[2:])
+        parts.append(f"cs={shape[2:]}")
     elif shape != "auto":
-        monkeypatch.setenv("AS_ATTN_NQ", shape)
+        parts.append(f"nq={shape}")
+    if split is not None:
+        parts.append(f"split={0 if split == '0' else 1}")
+    return ",".join(parts) or None
 
 
 @pytest.mark.parametrize("ci", range(1, len(ATTN_CASES)))
 @pytest.mark.parametrize("nq", ["auto", "1", "2", "cs2", "cs4"])
-def test_attn_bf16(ada, ci, nq, monkeypatch):
+def test_attn_bf16(ada, ci, nq):
     """Every CTA shape: one q-tile per CTA (NQ=1), paired q-tiles sharing every
     K/V tile (NQ=2; odd q-tile counts leave the second group idle), and clusters
     of 2 / 4 one-q-tile CTAs fetching each K/V tile once and multicasting it
     (CTAs past a head's last q-tile only stream and release)."""
-    _shape_env(monkeypatch, nq)
+    sched = _sched(nq)
     w = _attn_case(ATTN_CASES[ci], True, 400 + ci)
     scale = np.float32(1.0 / np.sqrt(w["q"].shape[2]))
     ref, ref_lse = oracle_attn(w, scale)
@@ -498,7 +502,7 @@ def test_attn_bf16(ada, ci, nq, monkeypatch):
     ws = ada.Workspace(256)
     out, lse = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"], g["page_table"],
                                     g["kv_len"], g["tree_offsets"], g["tree_parent"], scale, want_lse=True,
-                                    workspace=ws)
+                                    workspace=ws, schedule=sched)
     assert ada.check_device_error(ws)[0] == 0
     err = np.abs(out.float().cpu().numpy() - ref).max()
     assert err <= BF16_TOL, err
@@ -506,8 +510,8 @@ def test_attn_bf16(ada, ci, nq, monkeypatch):
 
 
 @pytest.mark.parametrize("nq", ["1", "2", "cs2"])
-def test_attn_bf16_request_chunks(ada, nq, monkeypatch):
-    _shape_env(monkeypatch, nq)
+def test_attn_bf16_request_chunks(ada, nq):
+    sched = _sched(nq)
     """More units than the kernel's per-CTA piece lists hold (n_kv * q-tiles *
     n_req > 64 * 2 * SMs): the library verifies the batch in request chunks;
     every request, including those at chunk edges, must match the oracle."""
@@ -522,7 +526,7 @@ def test_attn_bf16_request_chunks(ada, nq, monkeypatch):
     g = workload_to_device(w, torch.bfloat16)
     ws = ada.Workspace(256)
     out, _ = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"], g["page_table"],
-                                  g["kv_len"], g["tree_offsets"], g["tree_parent"], scale, workspace=ws)
+                                  g["kv_len"], g["tree_offsets"], g["tree_parent"], scale, workspace=ws, schedule=sched)
     assert ada.check_device_error(ws)[0] == 0
     assert np.abs(out.float().cpu().numpy() - ref).max() <= BF16_TOL
 
@@ -549,14 +553,13 @@ def test_attn_bf16_plan_capacity_chunks(ada):
 
 @pytest.mark.parametrize("sk", ["0", "1", "2"])
 @pytest.mark.parametrize("shape", ["1", "cs2"])
-def test_attn_bf16_many_units(ada, sk, shape, monkeypatch):
+def test_attn_bf16_many_units(ada, sk, shape):
     """More units than CTAs (64 requests x 8 kv heads = 512 > 296 one-q-tile
-    CTAs), ragged kv lengths, under every AS_ATTN_STREAMK setting (0: never
+    CTAs), ragged kv lengths, under every split setting (0: never
     split; 1/2: split-KV allowed -- not taken here, units outnumber CTAs), two
     launches on one workspace.  (A tail stream-K schedule for this regime was
     tried in commit 2530b31 and measured slower.)"""
-    monkeypatch.setenv("AS_ATTN_STREAMK", sk)
-    _shape_env(monkeypatch, shape)
+    sched = _sched(shape, sk)
     rng = np.random.default_rng(57)
     n = 64
     sizes = rng.integers(20, 33, n)
@@ -570,7 +573,7 @@ def test_attn_bf16_many_units(ada, sk, shape, monkeypatch):
     for rep in range(2):  # the second launch reuses the (self-resetting) counters
         out, lse = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"],
                                         g["page_table"], g["kv_len"], g["tree_offsets"], g["tree_parent"], scale,
-                                        want_lse=True, workspace=ws)
+                                        want_lse=True, workspace=ws, schedule=sched)
         assert ada.check_device_error(ws)[0] == 0
         err = np.abs(out.float().cpu().numpy() - ref).max()
         assert err <= BF16_TOL, (rep, err)
@@ -616,13 +619,13 @@ def test_attn_bf16_nan_in_unused_cache_slots(ada):
 
 @pytest.mark.parametrize("nq", ["1", "2", "cs2", "cs4"])
 @pytest.mark.parametrize("pad", ["nan", "inf"])
-def test_attn_bf16_nan_in_tree_padding(ada, nq, pad, monkeypatch):
+def test_attn_bf16_nan_in_tree_padding(ada, nq, pad):
     """Tree tiles are loaded 64 rows at a time from the request's first row: the
     rows past K_i belong to the next request or to the caller's padding past
     tree_offsets[n] (e.g. a budget-sized torch.empty buffer).  NaN/Inf there
     must not reach any output (P is 0 there, but 0 * NaN = NaN in the PV MMA).
     K_i around the 64-row tile edges: 63, 64, 65, 127, 128."""
-    _shape_env(monkeypatch, nq)
+    sched = _sched(nq)
     sizes = [63, 64, 65, 127, 128, 1, 191, 256]
     w = _attn_case((sizes, [70, 0, 129, 64, 5, 33, 64, 1], 8, 2, 128, 64, "random", 1.0), True, 91)
     scale = np.float32(1.0 / np.sqrt(128))
@@ -640,7 +643,7 @@ def test_attn_bf16_nan_in_tree_padding(ada, nq, pad, monkeypatch):
     par[:R] = g["tree_parent"]
     ws = ada.Workspace(256)
     out, lse = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"], g["page_table"],
-                                    g["kv_len"], g["tree_offsets"], par, scale, want_lse=True, workspace=ws)
+                                    g["kv_len"], g["tree_offsets"], par, scale, want_lse=True, workspace=ws, schedule=sched)
     assert ada.check_device_error(ws)[0] == 0
     o = out[:R].float().cpu().numpy()
     assert np.isfinite(o).all()
@@ -735,12 +738,13 @@ def test_dist_accept_and_commit_single_rank_nccl(ada):
 
 @pytest.mark.parametrize("cfg,shape", [("c2", "auto"), ("c3", "auto"), ("c4", "auto"), ("c5", "auto"),
                                        ("c4", "cs4"), ("c4", "2"), ("c5", "cs2"), ("c3", "cs2")])
-def test_attn_bf16_full_size_sampled(ada, cfg, shape, monkeypatch):
+def test_attn_bf16_full_size_sampled(ada, cfg, shape):
     """BASELINE full sizes in the launch bench.py times; the oracle checks sampled
     requests (all their heads).  The oracle's trees come from the oracle's own
     select on the same forest (asserted bit-identical to the GPU's)."""
     import bench
     W = bench.make_workload(cfg, device="cuda", seed_salt=5)
+    W["schedule"] = ada.parse_schedule(_sched(shape))  # the CTA shape under test (None: the library's choice)
     bench.run_select(W)
     out = bench.run_attention(W)
     torch.cuda.synchronize()
