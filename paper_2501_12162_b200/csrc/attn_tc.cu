@@ -280,34 +280,38 @@ __device__ __noinline__ void split_merge(const float* __restrict__ slot0, size_t
 }
 
 // Tail stream-K merge (DESIGN.md §5 "Schedule"): the last of a unit's pieces to
-// finish combines its own unnormalised (O in TMEM, m, l) with the n_oth other
-// pieces' fp32 partials (slots s0..s2) for row r:
+// finish combines its own unnormalised (O in TMEM, m, l) with the other pieces'
+// fp32 partials for row r.  The n_pc <= 3 pieces are combined in the unit's
+// piece order (own_pos = this piece's position, slot[k] = piece k's partial
+// slot), whichever piece merges, so the result is deterministic:
 // out_row[c] = sum_k 2^(m_k - M) O_k[c] / sum_k 2^(m_k - M) l_k, M = max_k m_k.
 template <int D>
 __device__ __noinline__ void tail_merge(uint32_t o_addr, float m_own, float l_own, const float* __restrict__ part0,
-                                        size_t slot_floats, int n_oth, int s0, int s1, int s2, int r,
+                                        size_t slot_floats, int n_pc, int own_pos, int s0, int s1, int s2, int r,
                                         __nv_bfloat16* out_row, float* lse_out) {
     const int sl[3] = {s0, s1, s2};
     const float* src[3];
     float mo[3], wo[3], lo[3];
-    float M = m_own;
+    float M = -INFINITY;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         src[k] = part0 + (size_t)sl[k] * slot_floats;
         mo[k] = -INFINITY;
         lo[k] = 0.f;
-        if (k < n_oth) {
+        if (k == own_pos) {
+            mo[k] = m_own;
+            lo[k] = l_own;
+        } else if (k < n_pc) {
             mo[k] = __ldcg(src[k] + 128 * D + r);
             lo[k] = __ldcg(src[k] + 128 * D + 128 + r);
         }
         M = fmaxf(M, mo[k]);
     }
-    const float w_own = m_own == -INFINITY ? 0.f : ptx::ex2(m_own - M);
-    float Ltot = l_own * w_own;
+    float Ltot = 0.f;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         wo[k] = mo[k] == -INFINITY ? 0.f : ptx::ex2(mo[k] - M);
-        Ltot += lo[k] * wo[k];
+        Ltot = fmaf(lo[k], wo[k], Ltot);
     }
     const float inv = 1.f / Ltot;
 #pragma unroll 1
@@ -319,20 +323,23 @@ __device__ __noinline__ void tail_merge(uint32_t o_addr, float m_own, float l_ow
         for (int k = 0; k < 3; ++k)
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-                q[k][j] = (k < n_oth) ? __ldcg(reinterpret_cast<const float4*>(src[k]) + (c0 / 4 + j) * 128 + r)
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                q[k][j] = (k < n_pc && k != own_pos)
+                              ? __ldcg(reinterpret_cast<const float4*>(src[k]) + (c0 / 4 + j) * 128 + r)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
         ptx::tmem_ld_wait();
         uint32_t pk[16];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            float a[4] = {__uint_as_float(oa[4 * j]) * w_own, __uint_as_float(oa[4 * j + 1]) * w_own,
-                          __uint_as_float(oa[4 * j + 2]) * w_own, __uint_as_float(oa[4 * j + 3]) * w_own};
+            const float4 own = make_float4(__uint_as_float(oa[4 * j]), __uint_as_float(oa[4 * j + 1]),
+                                           __uint_as_float(oa[4 * j + 2]), __uint_as_float(oa[4 * j + 3]));
+            float a[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                a[0] = fmaf(q[k][j].x, wo[k], a[0]);
-                a[1] = fmaf(q[k][j].y, wo[k], a[1]);
-                a[2] = fmaf(q[k][j].z, wo[k], a[2]);
-                a[3] = fmaf(q[k][j].w, wo[k], a[3]);
+                const float4 v = k == own_pos ? own : q[k][j];
+                a[0] = fmaf(v.x, wo[k], a[0]);
+                a[1] = fmaf(v.y, wo[k], a[1]);
+                a[2] = fmaf(v.z, wo[k], a[2]);
+                a[3] = fmaf(v.w, wo[k], a[3]);
             }
             __nv_bfloat162 h0 = __floats2bfloat162_rn(a[0] * inv, a[1] * inv);
             __nv_bfloat162 h1 = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
@@ -1116,14 +1123,15 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     return c;
                 };
                 const long long cA = cta_of(pc.x0), cB = cta_of((long long)pc.x0 + u.nt - 1);
-                int oth[3] = {0, 0, 0}, n_oth = 0;
-                for (long long c = cA; c <= cB && n_oth < 3; ++c) {
-                    if (c == (long long)cl) continue;
+                int slots[3] = {0, 0, 0}, n_pc = 0, own_pos = 0;  // the unit's pieces in stream order
+                for (long long c = cA; c <= cB && n_pc < 3; ++c) {
                     const int e = (c > cA || start(cA) == pc.x0) ? 0 : 1;
-                    oth[n_oth++] = tail_slot<NQ>((int)c * CS + crank, e, grp);  // same rank in cluster c
+                    if (c == (long long)cl) own_pos = n_pc;
+                    slots[n_pc++] = tail_slot<NQ>((int)c * CS + crank, e, grp);  // same rank in cluster c
                 }
-                tail_merge<D>(o_addr, m_ref, l_sum, p.partial, p.slot_floats, n_oth, oth[0], oth[1], oth[2], r,
-                              row_ok ? p.out + orow * D : nullptr, (row_ok && p.lse != nullptr) ? p.lse + orow : nullptr);
+                tail_merge<D>(o_addr, m_ref, l_sum, p.partial, p.slot_floats, n_pc, own_pos, slots[0], slots[1],
+                              slots[2], r, row_ok ? p.out + orow * D : nullptr,
+                              (row_ok && p.lse != nullptr) ? p.lse + orow : nullptr);
                 if (warp == lead_warp && lane == 0) p.cnt[wq] = 0;  // last user of the counter this launch
                 if (kDebug && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
                     unsigned long long tn;

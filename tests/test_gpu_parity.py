@@ -580,6 +580,23 @@ def test_attn_bf16_many_units(ada, sk, shape):
         assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-2
 
 
+def test_attn_bf16_deterministic_under_tail_pieces(ada):
+    """c2's batch (512 one-q-tile units on 296 CTAs) runs the tail stream-K
+    schedule, where the LAST piece of a cut unit to finish merges it: the merge
+    combines the pieces in stream order whoever merges, so two launches (and a
+    graph replay) give bit-identical outputs."""
+    import bench
+    W = bench.make_workload("c2", "cuda", seed_salt=3)
+    bench.run_select(W)
+    a = bench.run_attention(W).clone()
+    for _ in range(3):
+        W["ws_attn"] = ada.Workspace(W["ws_attn"].nbytes)
+        b = bench.run_attention(W)
+        torch.cuda.synchronize()
+        used = int(W["sel"]["tree_offsets"][-1])
+        assert torch.equal(a[:used], b[:used])
+
+
 def test_attn_tree_too_big_is_flagged(ada):
     """K_i > AS_MAX_TREE (256): the request is skipped and AS_DEV_TREE_TOO_BIG
     reported with its index; the other requests are still verified."""
