@@ -163,6 +163,65 @@ __device__ __forceinline__ uint64_t cand_key(float f, int j) {
     return ((uint64_t)fb << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)j);
 }
 
+// desired_i (SLO stage length with unlimited budget) from request i's sorted
+// keys ks[0..nr), one warp.  The result is the sequential fp64 loop's (R9):
+//   * warp fp64 scans over 32-key chunks while every f-hat so far is >= 2^-24
+//     and the sums stay < 64 -- all partial sums are then exact, so the scan's
+//     values ARE the loop's (f-hat = m 2^(e-23), e >= -24: multiples of 2^-47);
+//   * at the first f-hat < 2^-24 (pi is sorted, so every later one is smaller
+//     too) the exact state n_acc after the prefix is known; the loop cannot
+//     cross a_cap in the remaining rem entries when n_acc + rem (f + 2^-40) <
+//     a_cap (each remaining add contributes at most f plus half an ulp <= 2^-48
+//     of a sum < 64; the slack also covers the bound's own rounding), so
+//     desired = lim without running it;
+//   * otherwise the lane-uniform sequential loop resumes from that exact state
+//     (identical to the oracle).
+__device__ int slo_prefix_len(const SelectParams& p, double A_i, const uint64_t* ks, int nr) {
+    const int lane = lane_id();
+    const double a_cap = fmin(A_i, (double)p.depth_d + 1.0);
+    const int lim = min(p.n_max, nr);
+    if (!(1.0 < a_cap) || lim == 0) return 0;
+    double run = 1.0;  // the loop's n_acc after t0 entries (exact)
+    int t0 = 0;
+    for (int c0 = 0; c0 < lim; c0 += 32) {
+        const int s = c0 + lane;
+        const float f = s < lim ? __uint_as_float((uint32_t)(ks[s] >> 32)) : 0.f;
+        const unsigned tiny = __ballot_sync(0xffffffffu, s < lim && !(f >= 5.9604644775390625e-08f));
+        const int nv = tiny ? __ffs(tiny) - 1 : 32;  // exact entries of this chunk
+        double incl = (lane < nv) ? (double)f : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        incl += run;
+        const double tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (!(tot < 64.0)) {  // partial sums may round: the sequential loop from the start
+            run = 1.0;
+            t0 = 0;
+            break;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, lane < nv && s < lim && incl >= a_cap);
+        if (hit) return c0 + __ffs(hit);  // count includes the crossing element
+        run = tot;
+        t0 = min(lim, c0 + nv);
+        if (tiny) {
+            const int rem = lim - t0;
+            const double fmax_rem = (double)__uint_as_float((uint32_t)(ks[t0] >> 32));
+            if (run + (double)rem * (fmax_rem + 0x1p-40) < a_cap) return lim;  // cannot cross
+            break;
+        }
+        if (t0 >= lim) return lim;
+    }
+    double nacc = run;  // the lane-uniform sequential loop from the exact state at t0
+    int t = t0;
+    while (t < lim && nacc < a_cap) {
+        nacc += (double)__uint_as_float((uint32_t)(ks[t] >> 32));
+        ++t;
+    }
+    return t;
+}
+
 template <int E>
 __device__ __forceinline__ int sort_request(const SelectParams& p, int i, const float* prob, const int* par,
                                             int nr, uint64_t* key_out) {
@@ -209,54 +268,8 @@ __device__ __forceinline__ int sort_request(const SelectParams& p, int i, const 
     for (int e = 0; e < E; ++e)
         if (e * 32 + lane < nr) key_out[cnt[e]] = key[e];
     __syncwarp();
-    float fv[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const int s = e * 32 + lane;
-        fv[e] = (s < nr) ? __uint_as_float((uint32_t)(key_out[s] >> 32)) : 0.f;
-    }
     if (p.topm) return min(p.n_max + (i < p.n_max_extra ? 1 : 0), nr);  // per-request greedy cap
-    // SLO stage threshold with unlimited budget: the loop adds
-    // f-hat in pi order in fp64 starting from n_acc = 1.0 (R9) and stops at the
-    // first k with n_acc >= A_cap, or at lim = min(n_max, nr).
-    const double a_cap = fmin(p.A[i], (double)p.depth_d + 1.0);
-    const int lim = min(p.n_max, nr);
-    if (!(1.0 < a_cap) || lim == 0) return 0;
-    // Fast path (R9): if every f-hat >= 2^-24 each one is a multiple of 2^-47;
-    // while 1 + sum < 2^6 every partial sum is then exact in fp64, so a warp
-    // scan gives exactly the sequential loop's partial sums.
-    bool small = false;
-#pragma unroll
-    for (int e = 0; e < E; ++e) small |= (e * 32 + lane < nr) && !(fv[e] >= 5.9604644775390625e-08f);
-    if (!__any_sync(0xffffffffu, small)) {
-        double run = 1.0;  // n_acc before chunk e
-        int kst = -1;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-            double incl = (double)fv[e];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            incl += run;  // n_acc after position e*32 + lane
-            const int s = e * 32 + lane;
-            const unsigned hit = __ballot_sync(0xffffffffu, s < lim && incl >= a_cap);
-            const double tot = __shfl_sync(0xffffffffu, incl, 31);
-            if (kst < 0 && hit) kst = e * 32 + __ffs(hit);  // count includes the crossing element
-            run = tot;
-        }
-        // exactness guard: every partial sum < 64 (checked on the final, monotone total)
-        if (run < 64.0) return kst < 0 ? lim : min(kst, lim);
-    }
-    // General case: the lane-uniform sequential loop (identical to the oracle).
-    double nacc = 1.0;
-    int t = 0;
-    while (t < lim && nacc < a_cap) {
-        nacc += (double)__uint_as_float((uint32_t)(key_out[t] >> 32));
-        ++t;
-    }
-    return t;
+    return slo_prefix_len(p, p.A[i], key_out, nr);
 }
 
 // Exclusive scan of data[0..n) (shared) into out[0..n); returns the total.
@@ -313,42 +326,6 @@ __device__ int block_sum(int v, int* red) {
     const int r = red[32];
     __syncthreads();
     return r;
-}
-
-// desired_i (SLO stage length with unlimited budget) from request i's sorted
-// keys ks[0..nr), one warp.  Same arithmetic as the tail of sort_request: the
-// warp fp64 scan when it is provably exact (R9), else the sequential loop.
-__device__ int slo_prefix_len(const SelectParams& p, int i, const uint64_t* ks, int nr) {
-    const int lane = lane_id();
-    const double a_cap = fmin(p.A[i], (double)p.depth_d + 1.0);
-    const int lim = min(p.n_max, nr);
-    if (!(1.0 < a_cap) || lim == 0) return 0;
-    double run = 1.0;
-    bool exact = true;
-    for (int c0 = 0; c0 < lim; c0 += 32) {
-        const int s = c0 + lane;
-        const float f = s < lim ? __uint_as_float((uint32_t)(ks[s] >> 32)) : 0.f;
-        if (__any_sync(0xffffffffu, s < lim && !(f >= 5.9604644775390625e-08f))) { exact = false; break; }
-        double incl = (double)f;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        incl += run;
-        const unsigned hit = __ballot_sync(0xffffffffu, s < lim && incl >= a_cap);
-        run = __shfl_sync(0xffffffffu, incl, 31);
-        if (!(run < 64.0)) { exact = false; break; }  // partial sums so far must be < 2^6
-        if (hit) return c0 + __ffs(hit);              // count includes the crossing element
-    }
-    if (exact) return lim;
-    double nacc = 1.0;  // the lane-uniform sequential loop (identical to the oracle)
-    int t = 0;
-    while (t < lim && nacc < a_cap) {
-        nacc += (double)__uint_as_float((uint32_t)(ks[t] >> 32));
-        ++t;
-    }
-    return t;
 }
 
 // ---------------------------------------------------------------------------
@@ -469,6 +446,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
                 rank_s[lo - k + s] = 0;
             }
             __syncthreads();
+            if (p.dbg_stop == 11) return;
             // (1b) rank counting: warp wg compares every element with its slice of keys
             if (active) {
                 const int per = (nr + W - 1) / W;
@@ -486,13 +464,15 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
                 }
             }
             __syncthreads();
+            if (p.dbg_stop == 12) return;
             // (1c) scatter into pi order
             for (int s = wg * 32 + lane; s < nr; s += W * 32) keyc[off - i + rank_s[lo - k + s]] = ukey_s[lo - k + s];
             __syncthreads();
+            if (p.dbg_stop == 13) return;
             // (1d) desired_i (warp 0 of the group) and the A-order rank (warp 1, or 0)
             if (active && wg == 0) {
                 const int des = p.topm ? min(p.n_max + (i < p.n_max_extra ? 1 : 0), nr)
-                                       : slo_prefix_len(p, i, keyc + (off - i), nr);
+                                       : slo_prefix_len(p, A_s[i], keyc + (off - i), nr);
                 if (lane == 0) desired_s[k] = des;
             }
             if (active && p.topm) {
@@ -618,7 +598,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_trees_kernel(SelectPara
             }
             __syncthreads();
             for (int x = tid; x < 256; x += kSelThreads) hist[x] = 0;
+            if (p.dbg_stop == 40 + 2 * pass) return;
             cl_sync();  // every CTA's contribution to hs has landed
+            if (p.dbg_stop == 41 + 2 * pass) return;
             if (warp == 0) {
                 int loc[8];
                 int lsum = 0;

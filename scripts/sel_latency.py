@@ -34,8 +34,8 @@ if len(sys.argv) > 2:  # child: one stop value
         best = min(best, s.elapsed_time(e) * 1e3 / reps)
     print(f"{sys.argv[1]} stop={sys.argv[2]} pdl={os.environ.get('AS_PDL', '1')}: {best:.2f} us/launch")
 else:
-    for pdl in ("1", "0"):
-        for stop in ["0", "1", "2", "3", "4", "5", "6", "99"]:
+    for pdl in os.environ.get("SEL_PDL", "1 0").split():
+        for stop in os.environ.get("SEL_STOPS", "0 1 2 3 4 5 6 99").split():
             env = dict(os.environ, AS_SEL_STOP=stop, AS_PDL=pdl)
             r = subprocess.run([sys.executable, __file__, sys.argv[1], stop], env=env, capture_output=True, text=True)
             print(r.stdout.strip() or r.stderr[-500:])

@@ -284,6 +284,22 @@ def test_select_exact_sum_guards(ada):
         B = int(rng.integers(40, 1500))
         got = _gpu_select(ada, F, A, 8, n_max, B)
         _assert_select_equal(F, A, 8, n_max, B, got)
+    # (c) the SLO threshold inside a tail of tiny f-hat: chains 0.5, 0.25, 0.125, then
+    # 40 entries of 2^-26 (decreasing by ulps); A puts the crossing inside the tiny tail,
+    # exactly on a partial sum, or just out of reach (the kernel's bound must not cut it)
+    K = 44
+    big = [0.5, 0.25, 0.125]
+    tiny = [np.float32(2.0 ** -26) * np.float32(1 - 2.0 ** -20 * j) for j in range(K - 4)]
+    chain = np.array([1.0] + big + tiny, np.float32)
+    run = 1.0 + sum(big)
+    As = [run + 1.5 * 2.0 ** -26, run + 7 * 2.0 ** -26, run + float(np.sum(np.array(tiny[:20], np.float64))),
+          run + 39.9 * 2.0 ** -26, run + 40.5 * 2.0 ** -26, run + 2.0 ** -30, run - 2.0 ** -40, run + 1e-3]
+    n = len(As)
+    F = dict(cand_offsets=np.arange(0, (n + 1) * K, K, dtype=np.int32),
+             cand_parent=np.concatenate([[0] + list(range(K - 1))] * n).astype(np.int32),
+             cand_prob=np.tile(chain, n))
+    got = _gpu_select(ada, F, np.array(As), 100, 60, n * K)
+    _assert_select_equal(F, np.array(As), 100, 60, n * K, got)
 
 
 @pytest.mark.parametrize("n,maxn", [(4096, 5), (2500, 100)])
