@@ -372,7 +372,6 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kt,
                         const __grid_constant__ CUtensorMap tm_vt, const TcParams p) {
     static_assert(CS == 1 || CS == 2 || CS == 4, "cluster size");
-    static_assert(NQ == 1 || CS == 1, "clusters pair one-q-tile CTAs");
     using S = TcSmem<D, NQ>;
     constexpr int NCH = S::NCH;
     constexpr int kKStages = S::KST, kVStages = S::VST;
@@ -1249,9 +1248,9 @@ static int launch_shape(const CUtensorMap* maps, const TcParams& p, int grid, cu
 
 // CTAs of a cluster shape that can be resident at once (the persistent grid and the
 // co-resident split-KV pieces need every CTA resident): per device, cached.
-template <int D, int CS>
+template <int D, int NQ, int CS>
 static int resident_ctas(int n_sms) {
-    const int want = n_sms * TcCfg<1>::CTAS;
+    const int want = n_sms * TcCfg<NQ>::CTAS;
     if (CS == 1) return want;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
@@ -1259,13 +1258,13 @@ static int resident_ctas(int n_sms) {
     static int cache[64] = {0};
     std::lock_guard<std::mutex> lk(mu);
     if (cache[dev] == 0) {
-        const int smem = TcSmem<D, 1>::ALLOC;
-        if (cudaFuncSetAttribute(tree_attn_tc_kernel<D, 1, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        const int smem = TcSmem<D, NQ>::ALLOC;
+        if (cudaFuncSetAttribute(tree_attn_tc_kernel<D, NQ, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
             cudaSuccess)
             return 0;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(want);
-        cfg.blockDim = dim3(TcCfg<1>::THREADS);
+        cfg.blockDim = dim3(TcCfg<NQ>::THREADS);
         cfg.dynamicSmemBytes = smem;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1275,7 +1274,7 @@ static int resident_ctas(int n_sms) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, tree_attn_tc_kernel<D, 1, CS>, &cfg) != cudaSuccess) {
+        if (cudaOccupancyMaxActiveClusters(&nc, tree_attn_tc_kernel<D, NQ, CS>, &cfg) != cudaSuccess) {
             cudaGetLastError();
             return 0;
         }
@@ -1293,13 +1292,14 @@ int tc_ctas_per_sm() { return kCtasPerSm; }
 // are verified in request chunks.
 int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, int n_sms, cudaStream_t stream) {
     const int nq = p0.nq == 2 ? 2 : 1;
-    const int cs = (nq == 1 && (p0.cs == 2 || p0.cs == 4)) ? p0.cs : 1;
+    int cs = ((nq == 1 && (p0.cs == 2 || p0.cs == 4)) || (nq == 2 && p0.cs == 2)) ? p0.cs : 1;
     int grid_full = n_sms * (nq == 2 ? TcCfg<2>::CTAS : TcCfg<1>::CTAS);
     if (cs > 1) {
-        const int res = head_dim == 128 ? (cs == 2 ? resident_ctas<128, 2>(n_sms) : resident_ctas<128, 4>(n_sms))
-                                        : (cs == 2 ? resident_ctas<64, 2>(n_sms) : resident_ctas<64, 4>(n_sms));
-        if (res < cs) return -1;
-        grid_full = res / cs * cs;
+        const int res = nq == 2 ? (head_dim == 128 ? resident_ctas<128, 2, 2>(n_sms) : resident_ctas<64, 2, 2>(n_sms))
+                      : head_dim == 128 ? (cs == 2 ? resident_ctas<128, 1, 2>(n_sms) : resident_ctas<128, 1, 4>(n_sms))
+                                        : (cs == 2 ? resident_ctas<64, 1, 2>(n_sms) : resident_ctas<64, 1, 4>(n_sms));
+        if (res >= cs) grid_full = res / cs * cs;
+        else cs = 1;  // the device cannot co-schedule the cluster shape: same result without it
     }
     const int qpu = nq * cs;  // q-tiles per unit
     const int units_per_req = p0.n_kv * ((p0.mt_max + qpu - 1) / qpu);
@@ -1323,12 +1323,14 @@ int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, in
         if (grid <= 0) continue;
         int rc;
         if (head_dim == 128) {
-            rc = nq == 2 ? launch_shape<128, 2, 1>(maps, p, grid, stream)
+            rc = nq == 2 ? (cs == 2 ? launch_shape<128, 2, 2>(maps, p, grid, stream)
+                                    : launch_shape<128, 2, 1>(maps, p, grid, stream))
                  : cs == 2 ? launch_shape<128, 1, 2>(maps, p, grid, stream)
                  : cs == 4 ? launch_shape<128, 1, 4>(maps, p, grid, stream)
                            : launch_shape<128, 1, 1>(maps, p, grid, stream);
         } else {
-            rc = nq == 2 ? launch_shape<64, 2, 1>(maps, p, grid, stream)
+            rc = nq == 2 ? (cs == 2 ? launch_shape<64, 2, 2>(maps, p, grid, stream)
+                                    : launch_shape<64, 2, 1>(maps, p, grid, stream))
                  : cs == 2 ? launch_shape<64, 1, 2>(maps, p, grid, stream)
                  : cs == 4 ? launch_shape<64, 1, 4>(maps, p, grid, stream)
                            : launch_shape<64, 1, 1>(maps, p, grid, stream);

@@ -494,7 +494,9 @@ def _sched(shape, split=None):
     """as_tree_verify_attn_sched overrides: "1"/"2" = q-tiles per CTA, "cs2"/"cs4" =
     clusters of one-q-tile CTAs sharing K/V by multicast; split "0" = whole units."""
     parts = []
-    if shape.startswith("cs"):
+    if shape == "2cs2":  # two NQ=2 CTAs of a cluster: four q-tiles share each K/V fetch
+        parts.append("nq=2,cs=2")
+    elif shape.startswith("cs"):
         parts.append(f"cs={shape[2:]}")
     elif shape != "auto":
         parts.append(f"nq={shape}")
@@ -504,7 +506,7 @@ def _sched(shape, split=None):
 
 
 @pytest.mark.parametrize("ci", range(1, len(ATTN_CASES)))
-@pytest.mark.parametrize("nq", ["auto", "1", "2", "cs2", "cs4"])
+@pytest.mark.parametrize("nq", ["auto", "1", "2", "cs2", "cs4", "2cs2"])
 def test_attn_bf16(ada, ci, nq):
     """Every CTA shape: one q-tile per CTA (NQ=1), paired q-tiles sharing every
     K/V tile (NQ=2; odd q-tile counts leave the second group idle), and clusters
@@ -525,7 +527,7 @@ def test_attn_bf16(ada, ci, nq):
     assert np.abs(lse.cpu().numpy() - ref_lse).max() <= BF16_TOL
 
 
-@pytest.mark.parametrize("nq", ["1", "2", "cs2"])
+@pytest.mark.parametrize("nq", ["1", "2", "cs2", "2cs2"])
 def test_attn_bf16_request_chunks(ada, nq):
     sched = _sched(nq)
     """More units than the kernel's per-CTA piece lists hold (n_kv * q-tiles *
@@ -568,7 +570,7 @@ def test_attn_bf16_plan_capacity_chunks(ada):
 
 
 @pytest.mark.parametrize("sk", ["0", "1", "2"])
-@pytest.mark.parametrize("shape", ["1", "cs2"])
+@pytest.mark.parametrize("shape", ["1", "cs2", "2cs2"])
 def test_attn_bf16_many_units(ada, sk, shape):
     """More units than CTAs (64 requests x 8 kv heads = 512 > 296 one-q-tile
     CTAs), ragged kv lengths, under every split setting (0: never
@@ -650,7 +652,7 @@ def test_attn_bf16_nan_in_unused_cache_slots(ada):
     assert np.abs(o - ref).max() <= BF16_TOL
 
 
-@pytest.mark.parametrize("nq", ["1", "2", "cs2", "cs4"])
+@pytest.mark.parametrize("nq", ["1", "2", "cs2", "cs4", "2cs2"])
 @pytest.mark.parametrize("pad", ["nan", "inf"])
 def test_attn_bf16_nan_in_tree_padding(ada, nq, pad):
     """Tree tiles are loaded 64 rows at a time from the request's first row: the
@@ -770,7 +772,8 @@ def test_dist_accept_and_commit_single_rank_nccl(ada):
 
 
 @pytest.mark.parametrize("cfg,shape", [("c2", "auto"), ("c3", "auto"), ("c4", "auto"), ("c5", "auto"),
-                                       ("c4", "cs4"), ("c4", "2"), ("c5", "cs2"), ("c3", "cs2")])
+                                       ("c4", "cs4"), ("c4", "2"), ("c5", "cs2"), ("c3", "cs2"), ("c4", "2cs2"),
+                                       ("c5", "2cs2")])
 def test_attn_bf16_full_size_sampled(ada, cfg, shape):
     """BASELINE full sizes in the launch bench.py times; the oracle checks sampled
     requests (all their heads).  The oracle's trees come from the oracle's own
