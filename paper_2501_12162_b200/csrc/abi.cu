@@ -359,6 +359,7 @@ as_status as_tree_verify_attn_sched(as_dtype dtype, int32_t n_req, int32_t n_tre
         p.slot_floats = 128 * head_dim + 256;
     }
     p.req_base = 0;
+    p.tail_mode = 1;
     p.debug_mode = 0;
     p.evict_first = 1;
     p.k_lead = 1;
@@ -368,6 +369,7 @@ as_status as_tree_verify_attn_sched(as_dtype dtype, int32_t n_req, int32_t n_tre
     // Experiment switches, compiled only into the debug build (AS_DEBUG=1 build.py):
     // the product library reads no environment variable on this path.
     if (const char* dbg = getenv("AS_ATTN_DEBUG_MODE")) p.debug_mode = atoi(dbg);  // timing only (wrong outputs)
+    if (const char* tm = getenv("AS_ATTN_TAIL")) p.tail_mode = atoi(tm);           // schedule A/B
     if (const char* ef = getenv("AS_ATTN_EVICT_FIRST")) p.evict_first = atoi(ef);  // L2 evict-first hint A/B
     if (const char* kl = getenv("AS_ATTN_KLEAD")) p.k_lead = atoi(kl);             // K stream lead over V
     if (p.k_lead < 0) p.k_lead = 0;

@@ -112,6 +112,16 @@ struct TcSmem {
             p.trace[(size_t)(idx) * 8 + (e)] = clock64();                                      \
     } while (0)
 
+// CTA-0 epilogue trace (debug): event e of the CTA's piece k (rows 3000.. of the tile trace).
+#define AS_EPI_TRACE(e, k)                                                                        \
+    do {                                                                                          \
+        if (kDebug && p.trace != nullptr && blockIdx.x == 0 && gtid == 0 && grp == 0 && (k) < 64) { \
+            unsigned long long tn_;                                                               \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn_));                               \
+            p.trace[(size_t)(3000 + (k)) * 8 + (e)] = tn_;                                        \
+        }                                                                                         \
+    } while (0)
+
 // Named barrier of one softmax warp group (128 threads; ids 1 and 2, constant
 // operands so the kernel claims only the barriers it uses).
 __device__ __forceinline__ void group_bar(int grp) {
@@ -563,6 +573,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         }
         __syncthreads();
         __shared__ int s_ntail;
+        __shared__ int s_geff;  // whole-unit schedule slots (balanced waves)
         if (!sk_split) {
             // Whole units, unit k on CTA k mod G.  Tail stream-K (units > CTAs and the
             // last partial wave more than half full): the W1 = U / G full waves stay
@@ -574,7 +585,17 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             const int W1 = U / G, R = U - W1 * G;
             if (threadIdx.x == 0) {
                 int nt_rec = 0;
-                bool tail = p.stream_k && can_plan && W1 >= 1 && 2 * R > G && W1 + 2 <= kMaxRec;
+                // Balanced whole-unit waves (below) for few waves, when they keep every SM busy:
+                // W = ceil(U/G) <= 3 units per slot on Geff = ceil(U/W) slots; idle slots are
+                // second CTAs of some SMs (c2: 512 units on 256 of 296 slots, 2 each -- no
+                // pieces, no merges; measured 105 vs 111 us).  Otherwise tail stream-K: with
+                // many waves its piece/merge overhead is amortised (c3, c4: 1-2 % faster), and
+                // balanced waves would leave SMs empty (c5: 256 units, 148 one-CTA SMs).
+                const int Wv0 = U > 0 ? (U + G - 1) / G : 1;
+                const int Geff0 = U > 0 ? (U + Wv0 - 1) / Wv0 : G;
+                const bool balanced_ok = Wv0 <= 3 && Geff0 * TcCfg<NQ>::CTAS >= G;
+                bool tail = p.stream_k && can_plan && W1 >= 1 && 2 * R > G && W1 + 2 <= kMaxRec && p.tail_mode &&
+                            !balanced_ok;
                 bool ok = can_plan;
                 if (tail) {
                     const long long k0 = (long long)W1 * G;  // first remainder unit
@@ -609,7 +630,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         pos = ustart + te;
                     }
                 }
-                const int n_whole = tail ? W1 : (U > cl ? (U - 1 - cl) / G + 1 : 0);
+                // whole units in balanced waves (the first Geff slots; the rest idle)
+                const int Geff = (tail || !balanced_ok) ? G : Geff0;
+                s_geff = Geff;
+                const int n_whole = tail ? W1 : ((U > cl && cl < Geff) ? (U - 1 - cl) / Geff + 1 : 0);
                 ok = ok && n_whole <= kMaxRec;
                 if (!ok) set_dev_error(p.ws, AS_DEV_TREE_TOO_BIG, -2);
                 s_ntail = ok ? nt_rec : 0;
@@ -620,7 +644,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         const int nrec_static = (!sk_split && s_nrec > 0) ? s_nrec - s_ntail : 0;
         const int rec_base = (!sk_split && s_nrec > 0) ? s_ntail : 0;
         for (int q = threadIdx.x; q < nrec_static; q += blockDim.x) {
-            const long long k = (long long)cl + (long long)q * G;
+            const long long k = (long long)cl + (long long)q * s_geff;
             int lo_b = 0, hi_b = n - 1;  // last i with preu[i] <= k
             while (lo_b < hi_b) {
                 const int mid = (lo_b + hi_b + 1) >> 1;
@@ -1036,8 +1060,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 if (lane == 0 && quad == 0 && grp == 0) AS_TRACE(6, tbase + t - pc.tb);
             }
             // ---- epilogue ----
+            AS_EPI_TRACE(0, unit_it);  // last P written
             ptx::mbar_wait(of, unit_it & 1);
             ptx::tc_fence_after();
+            AS_EPI_TRACE(1, unit_it);  // O complete
             if (kDebug && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
                 unsigned long long tn;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
@@ -1097,9 +1123,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     part[128 * D + r] = m_ref;
                     part[128 * D + 128 + r] = l_sum;
                 }
+                AS_EPI_TRACE(2, unit_it);  // O stored (partial or output)
                 if (tailp) {
                     // publish, then count this piece's tiles in; the piece completing the count merges
                     __threadfence();
+                    AS_EPI_TRACE(3, unit_it);  // partial visible
                     group_bar(grp);
                     if (warp == lead_warp && lane == 0)
                         s_merge[grp] = atomicAdd(p.cnt + wq, pc.te - pc.tb) + (pc.te - pc.tb) == u.nt;
@@ -1108,6 +1136,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     group_bar(grp);
                 }
             }
+            AS_EPI_TRACE(4, unit_it);  // published / merge decided
             if (merge_now) {
                 __threadfence();  // the other pieces' partials, published before their counts
                 // the unit's pieces: the CTAs whose remainder-stream ranges [tr*c/G, tr*(c+1)/G)
@@ -1138,6 +1167,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 4] = tn;  // tail merge done
                 }
             }
+            AS_EPI_TRACE(5, unit_it);  // merge done (or nothing)
+            AS_EPI_TRACE(6, unit_it + (merge_now ? 1000 : 0) * 0);
+            if (kDebug && p.trace != nullptr && blockIdx.x == 0 && gtid == 0 && grp == 0 && unit_it < 64)
+                p.trace[(size_t)(3000 + unit_it) * 8 + 7] = (unsigned long long)((merge_now ? 2 : 0) + (tailp ? 1 : 0) + (full ? 4 : 0));
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(oe);
@@ -1211,6 +1244,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         unsigned long long* rec = p.trace + (size_t)(p.trace_cap + blockIdx.x) * 8;
         rec[0] = t_start;
         rec[1] = t_end;
+        if (!sk_split) {  // (split-KV uses slot 3 for "all pieces published")
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            rec[3] = (1ull << 40) | ((unsigned long long)cur0.nrec << 16) | smid;
+        }
     }
 }
 

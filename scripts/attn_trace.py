@@ -63,6 +63,26 @@ if len(cta):
           f"p90 {np.percentile(en, 90):.2f}  max {en.max():.2f}")
     print(f"  busy fraction (sum of CTA spans / (CTAs x makespan)) {((en - st).sum() / (len(cta) * en.max())):.3f}")
     print("  end-time histogram (us):", np.histogram(en, bins=10)[0].tolist(), np.round(np.histogram(en, bins=10)[1], 1).tolist())
+    tagged = cta[(cta[:, 3] >> 40) == 1]
+    if len(tagged):
+        smid = tagged[:, 3] & 0xFFFF
+        nrec = (tagged[:, 3] >> 16) & 0xFFFF
+        en_t = (tagged[:, 1] - t0c) / 1e3
+        merged = tagged[:, 4] != 0
+        print(f"  end: CTAs that merged a tail unit {en_t[merged].mean():.2f} us (n={merged.sum()}), "
+              f"others {en_t[~merged].mean():.2f} (n={(~merged).sum()})")
+        for nr in sorted(set(nrec.tolist())):
+            m = nrec == nr
+            print(f"  end with {nr} pieces: mean {en_t[m].mean():.2f} (n={m.sum()})")
+        order = np.argsort(smid)
+        # SM halves (die proxy): smid < 74 vs >= 74
+        lo = smid < 74
+        print(f"  end by smid half: <74 {en_t[lo].mean():.2f}  >=74 {en_t[~lo].mean():.2f}")
+        per_sm = {}
+        for s_, e_ in zip(smid.tolist(), en_t.tolist()):
+            per_sm.setdefault(s_, []).append(e_)
+        early = sorted(per_sm.items(), key=lambda kv: min(kv[1]))[:12]
+        print("  earliest-finishing SMs (smid: ends):", [(k, [round(x, 1) for x in v]) for k, v in early])
     for col, nm in ((5, "partial written"), (4, "merge done")):
         sel = cta[cta[:, col] != 0]
         if len(sel):
@@ -79,6 +99,14 @@ if len(cta):
         if (sp[:, 5] != 0).any():
             print(f"  split pieces: partial written median {np.median(pw):.2f} max {pw.max():.2f}; all published median "
               f"{np.median(pub):.2f}; merge done median {np.median(mg):.2f} max {mg.max():.2f} (us)")
+ep = tr[3000:3064].copy()
+ep = ep[ep[:, 0] != 0]
+if len(ep):
+    print("CTA-0 epilogues (us rel. to last P written): O complete, O stored, partial visible, decided, done; flags(1 tail,2 merged,4 full)")
+    for r_ in ep:
+        rel_ = lambda e: round((r_[e] - r_[0]) / 1e3, 2) if r_[e] else None
+        print("  ", rel_(1), rel_(2), rel_(3), rel_(4), rel_(5), int(r_[7]))
+tr = tr[:3000]
 n = int((tr[:, 0] != 0).sum())
 tr = tr[:n].astype(np.float64)
 t0 = tr[0, 0]
