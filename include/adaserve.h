@@ -402,7 +402,10 @@ as_status as_reset_workspace(void* workspace, size_t workspace_bytes, void* stre
  * D[M=128, N] = A[128, K] . B[N, K]^T with bf16 A/B (device, K-major rows) and
  * fp32 D (device), N in {64,128}, K in {64,128}; bit 0 of b_mn_major treats B
  * as [K, N] (N contiguous), as the PV product does with V; bit 1 stages A in
- * tensor memory (the A-from-TMEM form used for P).  Debug/tests only. */
+ * tensor memory (the A-from-TMEM form used for P); bit 2 runs the CTA-pair form
+ * (a 2-CTA cluster, tcgen05.mma.cta_group::2 with M = 256: A and D have 256
+ * rows, each CTA holds 128 A rows and half of B along N; MN-major needs N =
+ * 128).  Debug/tests only. */
 as_status as_selftest_umma(const void* a, const void* b, float* d, int32_t n, int32_t k,
                            int32_t b_mn_major, void* stream);
 

@@ -406,6 +406,6 @@ def accept_tokens(phase, tree_offsets, tree_parent=None, tree_tokens=None, targe
 
 def selftest_umma(a, b, n, k, b_mn_major):
     """Debug: D = A . B^T (or A . B for MN-major B) through tcgen05 (see adaserve.h)."""
-    d = torch.empty((128, n), dtype=torch.float32, device=a.device)
+    d = torch.empty((256 if b_mn_major & 4 else 128, n), dtype=torch.float32, device=a.device)
     _check(lib().as_selftest_umma(_ptr(a), _ptr(b), _ptr(d), n, k, int(b_mn_major), _stream()), "selftest")
     return d

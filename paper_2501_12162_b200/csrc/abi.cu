@@ -468,9 +468,12 @@ as_status as_selftest_umma(const void* a, const void* b, float* d, int32_t n, in
                            void* stream) {
     if (!a || !b || !d) return AS_ERR_INVALID_ARG;
     if ((n != 64 && n != 128) || (k != 64 && k != 128)) return AS_ERR_UNSUPPORTED;
+    const bool pair = (b_mn_major & 4) != 0;  // bit 2: CTA pair, M = 256 (cta_group::2)
+    if (pair && (b_mn_major & 1) && n != 128) return AS_ERR_UNSUPPORTED;  // MN-major halves are 64-wide chunks
+    const int m = pair ? 256 : 128;
     CUtensorMap ma, mb;
     {
-        uint64_t dims[2] = {(uint64_t)k, 128};
+        uint64_t dims[2] = {(uint64_t)k, (uint64_t)m};
         uint64_t str[1] = {(uint64_t)k * 2};
         uint32_t box[2] = {64, 128};
         if (!make_map(&ma, a, 2, dims, str, box)) return AS_ERR_CUDA;
@@ -478,7 +481,7 @@ as_status as_selftest_umma(const void* a, const void* b, float* d, int32_t n, in
     if (!(b_mn_major & 1)) {  // bit 0: B MN-major; bit 1: A staged in TMEM
         uint64_t dims[2] = {(uint64_t)k, (uint64_t)n};
         uint64_t str[1] = {(uint64_t)k * 2};
-        uint32_t box[2] = {64, (uint32_t)n};
+        uint32_t box[2] = {64, (uint32_t)(pair ? n / 2 : n)};
         if (!make_map(&mb, b, 2, dims, str, box)) return AS_ERR_CUDA;
     } else {
         uint64_t dims[2] = {(uint64_t)n, (uint64_t)k};
@@ -486,9 +489,10 @@ as_status as_selftest_umma(const void* a, const void* b, float* d, int32_t n, in
         uint32_t box[2] = {64, (uint32_t)k};
         if (!make_map(&mb, b, 2, dims, str, box)) return AS_ERR_CUDA;
     }
-    return launch_umma_selftest(&ma, &mb, d, n, k, (b_mn_major & 1) ? 1 : 0, a, (b_mn_major & 2) ? 1 : 0, S(stream)) == 0
-               ? AS_OK
-               : AS_ERR_CUDA;
+    const int rc = pair ? launch_umma2_selftest(&ma, &mb, d, n, k, b_mn_major & 1, a, (b_mn_major & 2) ? 1 : 0, S(stream))
+                        : launch_umma_selftest(&ma, &mb, d, n, k, (b_mn_major & 1) ? 1 : 0, a, (b_mn_major & 2) ? 1 : 0,
+                                               S(stream));
+    return rc == 0 ? AS_OK : AS_ERR_CUDA;
 }
 
 }  // extern "C"

@@ -102,6 +102,8 @@ int launch_beam(int n_req, int layer, int width, int vocab, const float* probs, 
 int launch_stream_bw(const void* src, const int* order, int n_chunks, int chunk_bytes, int stages, int mode,
                      unsigned long long* sink, int grid, const CUtensorMap* tmap, cudaStream_t stream);
 #endif
+int launch_umma2_selftest(const CUtensorMap* ma, const CUtensorMap* mb, float* d, int N, int K, int b_mn,
+                          const void* a_g, int a_tmem, cudaStream_t stream);
 int launch_umma_selftest(const CUtensorMap* ma, const CUtensorMap* mb, float* d, int N, int K, int b_mn,
                          const void* a_g, int a_tmem, cudaStream_t stream);
 

@@ -28,11 +28,14 @@ def ada():
 
 # --------------------------------------------------------------------------- tcgen05 building blocks
 @pytest.mark.parametrize("n,k,mn", [(64, 128, 0), (128, 128, 0), (64, 64, 0), (128, 64, 1), (64, 64, 1),
-                                    (128, 128, 1), (128, 128, 3), (64, 64, 3), (128, 64, 2)])
+                                    (128, 128, 1), (128, 128, 3), (64, 64, 3), (128, 64, 2),
+                                    (64, 128, 4), (128, 128, 4), (64, 64, 4), (128, 128, 5), (128, 64, 5),
+                                    (128, 128, 7), (128, 64, 7), (64, 128, 6)])
 def test_umma_selftest(ada, n, k, mn):
-    """bit 0: B MN-major (the PV/V form); bit 1: A staged in TMEM (the P form)."""
+    """bit 0: B MN-major (the PV/V form); bit 1: A staged in TMEM (the P form);
+    bit 2: the CTA pair (tcgen05.mma.cta_group::2, M = 256, B split along N)."""
     g = torch.Generator(device="cpu").manual_seed(n * 7 + k + mn)
-    a = torch.randn(128, k, generator=g).to(torch.bfloat16)
+    a = torch.randn(256 if mn & 4 else 128, k, generator=g).to(torch.bfloat16)
     b = torch.randn((k, n) if mn & 1 else (n, k), generator=g).to(torch.bfloat16)
     d = ada.selftest_umma(a.cuda(), b.cuda(), n, k, mn).cpu()
     ref = a.double() @ (b.double() if mn & 1 else b.double().T)
