@@ -232,12 +232,17 @@ as_status as_tree_verify_attn(as_dtype dtype, int32_t n_req, int32_t n_tree_rows
  *   cluster_ctas     2 or 4: clusters of one-q-tile CTAs, each K/V tile fetched
  *                    once and multicast (measured slower); 0/1: none
  *   split            0: whole units only; 1 or -1/auto: split-KV / tail pieces allowed
+ *   cta_pair         1: CTA pairs -- one tcgen05.mma.cta_group::2 (M = 256) per q-tile
+ *                    pair of a 2-CTA cluster, each CTA loading half of every K/V tile
+ *                    (head_dim 128, page_size >= 64, >= 2 q-tiles per (request, kv
+ *                    head), else AS_ERR_UNSUPPORTED); 0 / -1: not used
  * Unknown values return AS_ERR_INVALID_ARG.
  */
 typedef struct {
     int32_t q_tiles_per_cta;
     int32_t cluster_ctas;
     int32_t split;
+    int32_t cta_pair;
 } as_attn_schedule;
 
 as_status as_tree_verify_attn_sched(as_dtype dtype, int32_t n_req, int32_t n_tree_rows,

@@ -311,18 +311,21 @@ def select_equal_greedy(cand_offsets, cand_parent, cand_prob, budget, cand_token
 
 class AttnSchedule(ctypes.Structure):
     """as_attn_schedule: q_tiles_per_cta (0 auto, 1, 2), cluster_ctas (0/1, 2, 4),
-    split (-1 auto, 0 whole units only, 1 allowed) -- A/B overrides, results identical."""
-    _fields_ = [("q_tiles_per_cta", ctypes.c_int32), ("cluster_ctas", ctypes.c_int32), ("split", ctypes.c_int32)]
+    split (-1 auto, 0 whole units only, 1 allowed), cta_pair (1: cta_group::2 pairs)
+    -- A/B overrides, results identical."""
+    _fields_ = [("q_tiles_per_cta", ctypes.c_int32), ("cluster_ctas", ctypes.c_int32), ("split", ctypes.c_int32),
+                ("cta_pair", ctypes.c_int32)]
 
 
 def parse_schedule(spec):
     """'nq=2,cs=1,split=0' (any subset) -> AttnSchedule; None/'' -> None."""
     if not spec:
         return None
-    s = AttnSchedule(0, 0, -1)
+    s = AttnSchedule(0, 0, -1, 0)
     for kv in str(spec).split(","):
         k, v = kv.split("=")
-        setattr(s, {"nq": "q_tiles_per_cta", "cs": "cluster_ctas", "split": "split"}[k.strip()], int(v))
+        setattr(s, {"nq": "q_tiles_per_cta", "cs": "cluster_ctas", "split": "split", "pair": "cta_pair"}[k.strip()],
+                int(v))
     return s
 
 

@@ -244,7 +244,7 @@ as_status as_tree_verify_attn_sched(as_dtype dtype, int32_t n_req, int32_t n_tre
     if (schedule && (schedule->q_tiles_per_cta < 0 || schedule->q_tiles_per_cta > 2 ||
                      !(schedule->cluster_ctas == 0 || schedule->cluster_ctas == 1 || schedule->cluster_ctas == 2 ||
                        schedule->cluster_ctas == 4) ||
-                     schedule->split < -1 || schedule->split > 1))
+                     schedule->split < -1 || schedule->split > 1 || schedule->cta_pair < -1 || schedule->cta_pair > 1))
         return AS_ERR_INVALID_ARG;
     if (n_req < 0 || n_tree_rows < 0 || n_q_heads <= 0 || n_kv_heads <= 0 || num_pages < 0 || max_pages_per_req < 0)
         return AS_ERR_INVALID_ARG;
@@ -287,6 +287,12 @@ as_status as_tree_verify_attn_sched(as_dtype dtype, int32_t n_req, int32_t n_tre
     }
     const int box_rows = page_size < 64 ? page_size : 64;
     const int kv_split_d = page_size >= 64 ? 1 : 0;  // one box covers a whole 64-key tile
+    // CTA pair (cta_group::2): trees spanning >= 2 q-tiles per (request, kv head),
+    // head_dim 128, whole-tile boxes; each CTA loads half of every K/V tile
+    const long long qt_req = n_req > 0 ? ((long long)G * (n_tree_rows / n_req) + 127) / 128 : 0;
+    int pair = 0;
+    if (schedule && schedule->cta_pair == 1) pair = 1;
+    if (pair && !(head_dim == 128 && kv_split_d && qt_req >= 2)) return AS_ERR_UNSUPPORTED;
     {
         const uint64_t np = (uint64_t)(num_pages > 0 ? num_pages : 1);
         const void* kc = k_cache ? k_cache : k_tree;  // never dereferenced when there are no pages
@@ -295,8 +301,10 @@ as_status as_tree_verify_attn_sched(as_dtype dtype, int32_t n_req, int32_t n_tre
             uint64_t dims[5] = {64, (uint64_t)page_size, NCH, (uint64_t)n_kv_heads, np};
             uint64_t str[4] = {D * 2, 128, (uint64_t)page_size * D * 2, (uint64_t)n_kv_heads * page_size * D * 2};
             uint32_t box[5] = {64, (uint32_t)box_rows, (uint32_t)NCH, 1, 1};
-            if (!make_map(&maps[1], kc, 5, dims, str, box)) return AS_ERR_CUDA;
-            if (!make_map(&maps[2], vc, 5, dims, str, box)) return AS_ERR_CUDA;
+            uint32_t kbox[5] = {64, 32, (uint32_t)NCH, 1, 1};  // pair: 32 of the tile's keys
+            uint32_t vbox[5] = {64, 64, 1, 1, 1};              // pair: one d-chunk of all 64 keys
+            if (!make_map(&maps[1], kc, 5, dims, str, pair ? kbox : box)) return AS_ERR_CUDA;
+            if (!make_map(&maps[2], vc, 5, dims, str, pair ? vbox : box)) return AS_ERR_CUDA;
         } else {
             uint64_t dims[4] = {D, (uint64_t)page_size, (uint64_t)n_kv_heads, np};
             uint64_t str[3] = {D * 2, (uint64_t)page_size * D * 2, (uint64_t)n_kv_heads * page_size * D * 2};
@@ -309,8 +317,10 @@ as_status as_tree_verify_attn_sched(as_dtype dtype, int32_t n_req, int32_t n_tre
         uint64_t dims[4] = {64, (uint64_t)n_tree_rows, NCH, (uint64_t)n_kv_heads};
         uint64_t str[3] = {(uint64_t)n_kv_heads * D * 2, 128, D * 2};
         uint32_t box[4] = {64, 64, (uint32_t)NCH, 1};
-        if (!make_map(&maps[3], k_tree, 4, dims, str, box)) return AS_ERR_CUDA;
-        if (!make_map(&maps[4], v_tree, 4, dims, str, box)) return AS_ERR_CUDA;
+        uint32_t kbox[4] = {64, 32, (uint32_t)NCH, 1};
+        uint32_t vbox[4] = {64, 64, 1, 1};
+        if (!make_map(&maps[3], k_tree, 4, dims, str, pair ? kbox : box)) return AS_ERR_CUDA;
+        if (!make_map(&maps[4], v_tree, 4, dims, str, pair ? vbox : box)) return AS_ERR_CUDA;
     }
     TcParams p;
     p.n_req = n_req; p.n_tree_rows = n_tree_rows; p.n_q = n_q_heads; p.n_kv = n_kv_heads; p.G = G;
@@ -343,6 +353,11 @@ as_status as_tree_verify_attn_sched(as_dtype dtype, int32_t n_req, int32_t n_tre
         if (schedule && schedule->cluster_ctas > 1) {
             p.cs = schedule->cluster_ctas;
             if (!(schedule->q_tiles_per_cta == 2 && p.cs == 2)) p.nq = 1;  // (2, 2): two NQ=2 CTAs
+        }
+        p.pair = pair;
+        if (pair) {  // q-tiles per CTA: 2 when the head spans > 2 q-tiles, else 1 (the pair covers 2)
+            p.nq = (schedule && schedule->q_tiles_per_cta > 0) ? schedule->q_tiles_per_cta : (qt > 2 ? 2 : 1);
+            p.cs = 2;
         }
     }
     {

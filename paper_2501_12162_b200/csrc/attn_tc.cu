@@ -78,12 +78,16 @@ struct PieceRec {
     int x0, tr;        // tail pieces only (Piece::x0, Piece::tr)
 };
 
-template <int D, int NQ>
+// PR (CTA pair, cta_group::2): each CTA holds HALF of every K/V tile (K: 32 of
+// the 64 keys; V: its 64-column d-chunk), so a stage is 8 KB and the rings are
+// twice as deep in the same shared memory.
+template <int D, int NQ, bool PR = false>
 struct TcSmem {
-    static constexpr int KST = TcCfg<NQ>::KST, VST = TcCfg<NQ>::VST;
+    static constexpr int KST = TcCfg<NQ>::KST * (PR ? 2 : 1), VST = TcCfg<NQ>::VST * (PR ? 2 : 1);
     static constexpr int NCH = D / 64;                        // 128-byte swizzle chunks along d
     static constexpr int Q_BYTES = NCH * kBM * 128;           // 16 KB per chunk (one q-tile)
-    static constexpr int KV_BYTES = NCH * kBN * 128;          // 8 KB per chunk
+    static constexpr int KV_BYTES = NCH * kBN * 128 / (PR ? 2 : 1);  // 8 KB per chunk (PR: per half tile)
+    static constexpr int KH_ROWS = PR ? kBN / 2 : kBN;        // K rows held per CTA
     static constexpr int OFF_Q = 0;                           // [NQ] q-tiles
     static constexpr int OFF_K = OFF_Q + NQ * Q_BYTES;
     static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
@@ -376,13 +380,23 @@ __device__ __forceinline__ int tail_slot(int cta, int e, int grp) {
 // V tile is fetched by ONE of them (round robin over the tile's two operands) and
 // multicast into all CS shared memories; every CTA releases a ring slot in all
 // CS CTAs (DESIGN.md §5 "Clusters").
-template <int D, int NQ, int CS>
+//
+// PR = CTA pair (CS = 2, D = 128): the pair's q-tile j of CTA 0 and q-tile j of
+// CTA 1 form ONE M = 256 tcgen05.mma.cta_group::2 issued by the leader (rank 0);
+// each CTA loads only its half of every K tile (32 keys) and V tile (its d-chunk)
+// -- half the TMA work and shared-memory traffic per CTA.  The peer's loads land
+// on its own barriers; its warp 1 forwards each landing to the leader (after
+// zeroing V rows past the valid keys of its half); the leader's MMA commits are
+// multicast to both CTAs, and both CTAs' softmax warps arrive on the leader's
+// p_full / o_empty barriers (DESIGN.md §5 "CTA pairs").
+template <int D, int NQ, int CS, bool PR = false>
 __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kc,
                         const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ CUtensorMap tm_kt,
                         const __grid_constant__ CUtensorMap tm_vt, const TcParams p) {
     static_assert(CS == 1 || CS == 2 || CS == 4, "cluster size");
-    using S = TcSmem<D, NQ>;
+    static_assert(!PR || (CS == 2 && D == 128), "CTA pairs: clusters of 2, head_dim 128");
+    using S = TcSmem<D, NQ, PR>;
     constexpr int NCH = S::NCH;
     constexpr int kKStages = S::KST, kVStages = S::VST;
     constexpr uint16_t kMask = (uint16_t)((1u << CS) - 1);  // every CTA of the cluster
@@ -411,26 +425,30 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     const int lane = lane_id();
     pdl_launch_dependents();
 
+    const bool leader = !PR || crank == 0;  // PR: the CTA that issues the pair's MMAs
     if (threadIdx.x == 0) {
-        ptx::mbar_init(q_full, 1);
+        // PR: the leader's full barriers also wait for the peer's forwarded landing
+        const int fw = (PR && leader) ? 2 : 1;
+        ptx::mbar_init(q_full, fw);
         ptx::mbar_init(q_empty, NQ);  // one commit per MMA warp
         // a ring slot is free once every MMA warp of every CTA of the cluster released it
+        // (PR: the leader's MMA warps release both CTAs' slots with multicast commits)
         for (int s = 0; s < kKStages; ++s) {
-            ptx::mbar_init(k_full + s, 1);
-            ptx::mbar_init(k_empty + s, NQ * CS);
+            ptx::mbar_init(k_full + s, fw);
+            ptx::mbar_init(k_empty + s, PR ? NQ : NQ * CS);
         }
         for (int s = 0; s < kVStages; ++s) {
-            ptx::mbar_init(v_full + s, 1);
-            ptx::mbar_init(v_empty + s, NQ * CS);
+            ptx::mbar_init(v_full + s, fw);
+            ptx::mbar_init(v_empty + s, PR ? NQ : NQ * CS);
         }
         for (int q = 0; q < NQ; ++q) {
             for (int b = 0; b < 2; ++b) {
                 ptx::mbar_init(s_full(q, b), 1);
-                ptx::mbar_init(p_full(q, b), 4);  // the q-tile's 4 softmax warps
+                ptx::mbar_init(p_full(q, b), PR ? 8 : 4);  // the q-tile's 4 softmax warps (PR: of both CTAs)
                 ptx::mbar_init(pv_done(q, b), 1);
             }
             ptx::mbar_init(o_full(q), 1);
-            ptx::mbar_init(o_empty(q), 4);
+            ptx::mbar_init(o_empty(q), PR ? 8 : 4);
         }
         ptx::fence_mbar_init();
         ptx::tma_prefetch(&tm_q);
@@ -439,7 +457,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         ptx::tma_prefetch(&tm_kt);
         ptx::tma_prefetch(&tm_vt);
     }
-    if (warp == 1) ptx::tmem_alloc(tmem_holder, TcCfg<NQ>::TMEM);
+    if (warp == 1) {
+        if (PR) ptx::tmem_alloc_pair(tmem_holder, TcCfg<NQ>::TMEM);
+        else ptx::tmem_alloc(tmem_holder, TcCfg<NQ>::TMEM);
+    }
     ptx::tc_fence_before();
     __syncthreads();
     if (CS > 1) ptx::cluster_sync();  // peers' barriers initialised before any multicast or remote arrive
@@ -721,8 +742,29 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     unsigned char* dst = smem + (is_k ? S::OFF_K : S::OFF_V) + st * S::KV_BYTES;
                     // cluster: operand 2t (K) / 2t+1 (V) is fetched by CTA (2t + !is_k) % CS and
                     // multicast; every CTA posts the bytes it will receive on its own barrier
-                    const bool owner = CS == 1 || (2 * t + (is_k ? 0 : 1)) % CS == crank;
-                    if (t < u.n_prefix) {
+                    const bool owner = CS == 1 || PR || (2 * t + (is_k ? 0 : 1)) % CS == crank;
+                    if (PR && t < u.n_prefix) {
+                        // this CTA's half: K keys [32 rank, 32 rank + 32) of the tile (box {64,
+                        // 32, 2 chunks}); V d-chunk rank of all 64 keys (box {64, 64, 1 chunk})
+                        const CUtensorMap* tm_c = is_k ? &tm_kc : &tm_vc;
+                        const int key0 = t * kBN;
+                        const int page = pt_s[key0 / p.page_size - chunk0];
+                        const int slot = key0 % p.page_size;
+                        if (page < 0 || page >= p.num_pages) set_dev_error(p.ws, AS_DEV_BAD_PAGE, p.req_base + u.i);
+                        ptx::mbar_wait(empty, ph ^ 1);
+                        AS_TRACE(is_k ? 0 : 1, myit);
+                        ptx::mbar_arrive_expect_tx(full, (uint32_t)S::KV_BYTES);
+                        if (is_k) ptx::tma_load_5d_hint(dst, tm_c, full, 0, slot + crank * (kBN / 2), 0, u.g, page, pol);
+                        else ptx::tma_load_5d_hint(dst, tm_c, full, 0, slot, crank, u.g, page, pol);
+                    } else if (PR) {
+                        const CUtensorMap* tm_t = is_k ? &tm_kt : &tm_vt;
+                        const int row0 = u.off + (t - u.n_prefix) * kBN;
+                        ptx::mbar_wait(empty, ph ^ 1);
+                        AS_TRACE(is_k ? 0 : 1, myit);
+                        ptx::mbar_arrive_expect_tx(full, (uint32_t)S::KV_BYTES);
+                        if (is_k) ptx::tma_load_4d(dst, tm_t, full, 0, row0 + crank * (kBN / 2), 0, u.g);
+                        else ptx::tma_load_4d(dst, tm_t, full, 0, row0, crank, u.g);
+                    } else if (t < u.n_prefix) {
                         const CUtensorMap* tm_c = is_k ? &tm_kc : &tm_vc;
                         const int key0 = t * kBN;
                         const int valid = min(kBN, u.L - key0);
@@ -787,8 +829,9 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         // unit never wait on each other; a K/V slot is free once every MMA warp
         // has released it (a warp whose q-tile the unit lacks releases it at once).
         const int q = warp - 1;
-        constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(kBM, kBN, 0);
-        constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(kBM, D, 1);
+        // PR: M = 256 (this q-tile of both CTAs)
+        constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(PR ? 2 * kBM : kBM, kBN, 0);
+        constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(PR ? 2 * kBM : kBM, D, 1);
         const uint32_t q_base = ptx::smem_u32(smem + S::OFF_Q) + q * S::Q_BYTES;
         const uint32_t k_base = ptx::smem_u32(smem + S::OFF_K);
         const uint32_t v_base = ptx::smem_u32(smem + S::OFF_V);
@@ -803,13 +846,68 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 if (after_mma) ptx::mma_commit(bar);
                 else ptx::mbar_arrive(bar);
             } else if (after_mma) {
-                ptx::mma_commit_mc(bar, kMask);
+                if (PR) ptx::mma_commit_pair(bar, kMask);
+                else ptx::mma_commit_mc(bar, kMask);
             } else {
 #pragma unroll
                 for (int r2 = 0; r2 < CS; ++r2) ptx::mbar_arrive_remote(bar, (uint32_t)r2);
             }
         };
-        while (rec_next(p, sc, pc)) {
+        // completion signal of the MMAs issued so far: the local barrier (PR: both CTAs')
+        auto signal = [&](uint64_t* bar) {
+            if (PR) ptx::mma_commit_pair(bar, kMask);
+            else ptx::mma_commit(bar);
+        };
+        auto arrive_all = [&](uint64_t* bar) {  // non-MMA arrival (debug / idle paths)
+            if (PR) {
+                ptx::mbar_arrive_remote(bar, 0);
+                ptx::mbar_arrive_remote(bar, 1);
+            } else {
+                ptx::mbar_arrive(bar);
+            }
+        };
+        if (PR && !leader) {
+            // ---- CTA-pair peer: warp 1 forwards each landing of this CTA's halves to
+            // the leader's barrier, in the leader's consumption order (Q; K_tb; K_t+1,
+            // V_t ...), zeroing V rows past the valid keys first (see do_pv) ----
+            if (q == 0) {
+                uint32_t fk = 0, fv = 0, fu = 0;
+                auto fwd_k = [&]() {
+                    const int st = fk % kKStages;
+                    ptx::mbar_wait(k_full + st, (fk / kKStages) & 1);
+                    if (lane == 0) ptx::mbar_arrive_remote(k_full + st, 0);
+                    __syncwarp();
+                    ++fk;
+                };
+                auto fwd_v = [&](const Unit& u, int t) {
+                    const int st = fv % kVStages;
+                    ptx::mbar_wait(v_full + st, (fv / kVStages) & 1);
+                    const int valid = t < u.n_prefix ? min(kBN, u.L - t * kBN) : min(kBN, u.K - (t - u.n_prefix) * kBN);
+                    if (valid < kBN) {
+                        unsigned char* vs = smem + S::OFF_V + st * S::KV_BYTES;
+                        for (int x = lane; x < (kBN - valid) * 8; x += 32)
+                            reinterpret_cast<uint4*>(vs + valid * 128)[x] = make_uint4(0, 0, 0, 0);
+                        ptx::fence_proxy_async_smem();
+                    }
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_remote(v_full + st, 0);
+                    __syncwarp();
+                    ++fv;
+                };
+                while (rec_next(p, sc, pc)) {
+                    const Unit& u = pc.u;
+                    ptx::mbar_wait(q_full, fu & 1);
+                    if (lane == 0) ptx::mbar_arrive_remote(q_full, 0);
+                    __syncwarp();
+                    fwd_k();
+                    for (int t = pc.tb; t < pc.te; ++t) {
+                        if (t + 1 < pc.te) fwd_k();
+                        fwd_v(u, t);
+                    }
+                    ++fu;
+                }
+            }
+        } else while (rec_next(p, sc, pc)) {
             const Unit& u = pc.u;
             const bool mine = crank * NQ + q < u.nq;
             ptx::mbar_wait(q_full, unit_it & 1);
@@ -820,9 +918,12 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 ptx::tc_fence_after();
                 if (lane == 0) {
                     if (!mine || (kDebug && p.debug_mode >= 2)) {
-                        if (mine) ptx::mbar_arrive(s_full(q, s_it & 1));
+                        if (mine) arrive_all(s_full(q, s_it & 1));
                         release(k_empty + st, false);
-                        if (t == pc.te - 1) ptx::mbar_arrive(q_empty);
+                        if (t == pc.te - 1) {
+                            if (PR) arrive_all(q_empty);
+                            else ptx::mbar_arrive(q_empty);
+                        }
                     } else {
                         const uint32_t s_col = tq + (s_it & 1) * 64;
                         if (q == 0) AS_TRACE(7, k_it);
@@ -830,12 +931,14 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         for (int ks = 0; ks < D / 16; ++ks) {
                             const int c = ks >> 2, kk = ks & 3;
                             const uint64_t a = ptx::sw128_desc(q_base + c * kBM * 128 + kk * 32, 0, 1024);
-                            const uint64_t b = ptx::sw128_desc(k_base + st * S::KV_BYTES + c * kBN * 128 + kk * 32, 0, 1024);
-                            ptx::mma_bf16_ss(s_col, a, b, idesc_qk, ks > 0 ? 1u : 0u);
+                            const uint64_t b =
+                                ptx::sw128_desc(k_base + st * S::KV_BYTES + c * S::KH_ROWS * 128 + kk * 32, 0, 1024);
+                            if (PR) ptx::mma_bf16_ss_pair(s_col, a, b, idesc_qk, ks > 0 ? 1u : 0u);
+                            else ptx::mma_bf16_ss(s_col, a, b, idesc_qk, ks > 0 ? 1u : 0u);
                         }
-                        ptx::mma_commit(s_full(q, s_it & 1));
+                        signal(s_full(q, s_it & 1));
                         release(k_empty + st, true);
-                        if (t == pc.te - 1) ptx::mma_commit(q_empty);
+                        if (t == pc.te - 1) signal(q_empty);
                     }
                 }
                 __syncwarp();
@@ -863,7 +966,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     if (valid < kBN) {
                         unsigned char* vs = smem + S::OFF_V + st * S::KV_BYTES;
                         const int nvec = (kBN - valid) * 8;  // 16-byte vectors per chunk
-                        for (int c = 0; c < NCH; ++c)
+                        for (int c = 0; c < (PR ? 1 : NCH); ++c)  // PR: this CTA's d-chunk only
                             for (int x = lane; x < nvec; x += 32)
                                 reinterpret_cast<uint4*>(vs + c * kBN * 128 + valid * 128)[x] = make_uint4(0, 0, 0, 0);
                         ptx::fence_proxy_async_smem();
@@ -878,17 +981,18 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 if (kDebug && p.debug_mode >= 2) {
                     if (lane == 0) {
                         release(v_empty + st, false);
-                        ptx::mbar_arrive(pv_done(q, pbuf));
+                        arrive_all(pv_done(q, pbuf));
                     }
                 } else if (lane == 0) {
 #pragma unroll
                     for (int kk = 0; kk < kBN / 16; ++kk) {
                         // A = P_t: bf16 pairs over the first 32 columns of S buffer pbuf
                         const uint64_t b = ptx::sw128_desc(v_base + st * S::KV_BYTES + kk * 16 * 128, kBN * 128, 1024);
-                        ptx::mma_bf16_ts(o_col, tq + pbuf * 64 + kk * 8, b, idesc_pv, (t > pc.tb || kk > 0) ? 1u : 0u);
+                        if (PR) ptx::mma_bf16_ts_pair(o_col, tq + pbuf * 64 + kk * 8, b, idesc_pv, (t > pc.tb || kk > 0) ? 1u : 0u);
+                        else ptx::mma_bf16_ts(o_col, tq + pbuf * 64 + kk * 8, b, idesc_pv, (t > pc.tb || kk > 0) ? 1u : 0u);
                     }
                     release(v_empty + st, true);
-                    ptx::mma_commit(pv_done(q, pbuf));
+                    signal(pv_done(q, pbuf));
                 }
                 __syncwarp();
                 ++v_it;
@@ -901,8 +1005,8 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             do_pv(pc.te - 1);
             if (mine) {
                 if (lane == 0) {
-                    if (kDebug && p.debug_mode >= 2) ptx::mbar_arrive(o_full(q));
-                    else ptx::mma_commit(o_full(q));
+                    if (kDebug && p.debug_mode >= 2) arrive_all(o_full(q));
+                    else signal(o_full(q));
                 }
                 ++o_it;
             }
@@ -930,7 +1034,27 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         while (rec_next(p, sc, pc)) {
             const Unit& u = pc.u;
             const int qi = crank * NQ + grp;  // this group's q-tile within the unit
-            if (qi >= u.nq) continue;          // the unit has no q-tile for this group
+            if (PR ? grp >= u.nq : qi >= u.nq) continue;  // the unit has no q-tile (PR: pair) for this group
+            if (PR && qi >= u.nq) {
+                // CTA pair: the leader's half of this pair exists, ours does not -- keep the
+                // barrier protocol (our TMEM rows are computed and ignored), no math, no output
+                for (int t = pc.tb; t < pc.te; ++t, ++s_cnt) {
+                    const uint32_t b = s_cnt & 1;
+                    ptx::mbar_wait(s_full(grp, b), (s_cnt >> 1) & 1);
+                    ptx::tc_fence_after();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_remote(p_full(grp, b), 0);
+                }
+                ptx::mbar_wait(of, unit_it & 1);
+                ptx::tc_fence_after();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_remote(oe, 0);
+                ++unit_it;
+                tbase += pc.te - pc.tb;
+                continue;
+            }
             const int G = p.G;
             const int rr = (u.mt + qi) * kBM + r;
             const bool row_ok = rr < u.K * G;
@@ -985,7 +1109,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 if (kDebug && p.debug_mode >= 1) {  // timing experiment: no softmax math
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(p_full(grp, b));
+                    if (lane == 0) {
+                        if (leader) ptx::mbar_arrive(p_full(grp, b));
+                        else ptx::mbar_arrive_remote(p_full(grp, b), 0);
+                    }
                     continue;
                 }
                 float* x = reinterpret_cast<float*>(sr);
@@ -1056,7 +1183,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(p_full(grp, b));
+                if (lane == 0) {  // PR: the leader's barrier counts both CTAs' warps
+                    if (leader) ptx::mbar_arrive(p_full(grp, b));
+                    else ptx::mbar_arrive_remote(p_full(grp, b), 0);
+                }
                 if (lane == 0 && quad == 0 && grp == 0) AS_TRACE(6, tbase + t - pc.tb);
             }
             // ---- epilogue ----
@@ -1173,7 +1303,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 p.trace[(size_t)(3000 + unit_it) * 8 + 7] = (unsigned long long)((merge_now ? 2 : 0) + (tailp ? 1 : 0) + (full ? 4 : 0));
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(oe);
+            if (lane == 0) {
+                if (leader) ptx::mbar_arrive(oe);
+                else ptx::mbar_arrive_remote(oe, 0);
+            }
             if (kDebug && !full && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
                 unsigned long long tn;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
@@ -1235,7 +1368,8 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     if (CS > 1) ptx::cluster_sync();  // no peer still multicasts into, or arrives on, this CTA
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem, TcCfg<NQ>::TMEM);
+        if (PR) ptx::tmem_dealloc_pair(tmem, TcCfg<NQ>::TMEM);
+        else ptx::tmem_dealloc(tmem, TcCfg<NQ>::TMEM);
     }
     if (kDebug && p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceCtas) {
         // per-CTA timeline (debug): start/end globaltimer, after the CTA-0 tile trace
@@ -1255,10 +1389,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
-template <int D, int NQ, int CS>
+template <int D, int NQ, int CS, bool PR = false>
 static int launch_shape(const CUtensorMap* maps, const TcParams& p, int grid, cudaStream_t stream) {
-    const int smem = TcSmem<D, NQ>::ALLOC;
-    if (cudaFuncSetAttribute(tree_attn_tc_kernel<D, NQ, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+    const int smem = TcSmem<D, NQ, PR>::ALLOC;
+    if (cudaFuncSetAttribute(tree_attn_tc_kernel<D, NQ, CS, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
         cudaSuccess)
         return -1;
     cudaLaunchConfig_t cfg = {};
@@ -1278,7 +1412,7 @@ static int launch_shape(const CUtensorMap* maps, const TcParams& p, int grid, cu
     }
     na += fill_launch_attrs(attr + na);
     cfg.numAttrs = na;
-    if (cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<D, NQ, CS>, maps[0], maps[1], maps[2], maps[3], maps[4], p) !=
+    if (cudaLaunchKernelEx(&cfg, tree_attn_tc_kernel<D, NQ, CS, PR>, maps[0], maps[1], maps[2], maps[3], maps[4], p) !=
         cudaSuccess)
         return -1;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
@@ -1286,7 +1420,7 @@ static int launch_shape(const CUtensorMap* maps, const TcParams& p, int grid, cu
 
 // CTAs of a cluster shape that can be resident at once (the persistent grid and the
 // co-resident split-KV pieces need every CTA resident): per device, cached.
-template <int D, int NQ, int CS>
+template <int D, int NQ, int CS, bool PR = false>
 static int resident_ctas(int n_sms) {
     const int want = n_sms * TcCfg<NQ>::CTAS;
     if (CS == 1) return want;
@@ -1296,9 +1430,9 @@ static int resident_ctas(int n_sms) {
     static int cache[64] = {0};
     std::lock_guard<std::mutex> lk(mu);
     if (cache[dev] == 0) {
-        const int smem = TcSmem<D, NQ>::ALLOC;
-        if (cudaFuncSetAttribute(tree_attn_tc_kernel<D, NQ, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
+        const int smem = TcSmem<D, NQ, PR>::ALLOC;
+        if (cudaFuncSetAttribute(tree_attn_tc_kernel<D, NQ, CS, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem) != cudaSuccess)
             return 0;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(want);
@@ -1312,7 +1446,7 @@ static int resident_ctas(int n_sms) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, tree_attn_tc_kernel<D, NQ, CS>, &cfg) != cudaSuccess) {
+        if (cudaOccupancyMaxActiveClusters(&nc, tree_attn_tc_kernel<D, NQ, CS, PR>, &cfg) != cudaSuccess) {
             cudaGetLastError();
             return 0;
         }
@@ -1330,9 +1464,14 @@ int tc_ctas_per_sm() { return kCtasPerSm; }
 // are verified in request chunks.
 int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, int n_sms, cudaStream_t stream) {
     const int nq = p0.nq == 2 ? 2 : 1;
-    int cs = ((nq == 1 && (p0.cs == 2 || p0.cs == 4)) || (nq == 2 && p0.cs == 2)) ? p0.cs : 1;
+    const bool pair = p0.pair != 0 && head_dim == 128;  // CTA pairs (cta_group::2); the host checked the shape
+    int cs = pair ? 2 : ((nq == 1 && (p0.cs == 2 || p0.cs == 4)) || (nq == 2 && p0.cs == 2)) ? p0.cs : 1;
     int grid_full = n_sms * (nq == 2 ? TcCfg<2>::CTAS : TcCfg<1>::CTAS);
-    if (cs > 1) {
+    if (pair) {
+        const int res = nq == 2 ? resident_ctas<128, 2, 2, true>(n_sms) : resident_ctas<128, 1, 2, true>(n_sms);
+        if (res < 2) return -1;  // (the maps were built for half tiles: no fallback here)
+        grid_full = res / 2 * 2;
+    } else if (cs > 1) {
         const int res = nq == 2 ? (head_dim == 128 ? resident_ctas<128, 2, 2>(n_sms) : resident_ctas<64, 2, 2>(n_sms))
                       : head_dim == 128 ? (cs == 2 ? resident_ctas<128, 1, 2>(n_sms) : resident_ctas<128, 1, 4>(n_sms))
                                         : (cs == 2 ? resident_ctas<64, 1, 2>(n_sms) : resident_ctas<64, 1, 4>(n_sms));
@@ -1343,8 +1482,9 @@ int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, in
     const int units_per_req = p0.n_kv * ((p0.mt_max + qpu - 1) / qpu);
     int chunk = units_per_req > 0 ? max(1, kMaxRec * (grid_full / cs) / units_per_req) : p0.n_req;
     // the prologue's schedule plan holds at most PLAN_N requests (prefix sums, geometry)
-    const int plan_half = head_dim == 128 ? (nq == 2 ? TcSmem<128, 2>::PLAN_N : TcSmem<128, 1>::PLAN_N)
-                                          : (nq == 2 ? TcSmem<64, 2>::PLAN_N : TcSmem<64, 1>::PLAN_N);
+    const int plan_half = pair ? (nq == 2 ? TcSmem<128, 2, true>::PLAN_N : TcSmem<128, 1, true>::PLAN_N)
+                          : head_dim == 128 ? (nq == 2 ? TcSmem<128, 2>::PLAN_N : TcSmem<128, 1>::PLAN_N)
+                                            : (nq == 2 ? TcSmem<64, 2>::PLAN_N : TcSmem<64, 1>::PLAN_N);
     chunk = min(chunk, plan_half);
     for (int r0 = 0; r0 < p0.n_req; r0 += chunk) {
         TcParams p = p0;
@@ -1360,7 +1500,10 @@ int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, in
         if (!p.stream_k && p.n_units * cs < grid) grid = p.n_units * cs;
         if (grid <= 0) continue;
         int rc;
-        if (head_dim == 128) {
+        if (pair) {
+            rc = nq == 2 ? launch_shape<128, 2, 2, true>(maps, p, grid, stream)
+                         : launch_shape<128, 1, 2, true>(maps, p, grid, stream);
+        } else if (head_dim == 128) {
             rc = nq == 2 ? (cs == 2 ? launch_shape<128, 2, 2>(maps, p, grid, stream)
                                     : launch_shape<128, 2, 1>(maps, p, grid, stream))
                  : cs == 2 ? launch_shape<128, 1, 2>(maps, p, grid, stream)

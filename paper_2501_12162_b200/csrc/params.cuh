@@ -65,6 +65,7 @@ struct TcParams {
     int req_base;         // caller's index of request 0 of this launch (device-error reports)
     int nq;               // host in: CTA shape (1 or 2 q-tiles per CTA); kernel: q-tiles per unit (nq * cs)
     int cs;               // thread-block cluster size (1, 2, 4; one-q-tile CTAs sharing K/V by multicast)
+    int pair;             // 1: CTA pairs (cs = 2, tcgen05.mma.cta_group::2, half K/V tiles per CTA)
     int mt_max;           // q-tiles per (request, kv head) upper bound (unit id stride)
     int stream_k;         // 1: split-KV allowed (needs cnt/cnt2/partial in the workspace), 0: whole units only
     int tail_mode;        // 1: tail stream-K for a partial last wave; 0: balanced whole-unit waves

@@ -38,6 +38,8 @@ torch.cuda.synchronize()
 print(f"calibration: torch copy {2 * _a.numel() * 2 * 5 / (_s.elapsed_time(_e) / 1e3) / 1e9:.0f} GB/s")
 del _a, _b
 W = bench.make_workload(args.config, "cuda", world=int(os.environ.get("AS_BENCH_EMULATE_WORLD", "1")))
+if os.environ.get("AS_TRACE_SCHEDULE"):
+    W["schedule"] = W["ada"].parse_schedule(os.environ["AS_TRACE_SCHEDULE"])
 for _ in range(3):
     bench.run_attention(W)
 torch.cuda.synchronize()

@@ -618,6 +618,28 @@ def test_attn_bf16_deterministic_under_tail_pieces(ada):
         assert torch.equal(a[:used], b[:used])
 
 
+@pytest.mark.parametrize("ci", [4, 5, 8, 10])
+@pytest.mark.parametrize("nq", ["1", "2"])
+def test_attn_bf16_cta_pair(ada, ci, nq):
+    """CTA pairs (as_attn_schedule.cta_pair): one tcgen05.mma.cta_group::2 (M = 256)
+    per q-tile pair of a 2-CTA cluster, each CTA loading half of every K/V tile;
+    1 or 2 q-tiles per CTA; odd q-tile counts leave the peer's half idle; trees
+    up to 256 nodes, page sizes 64 / 128."""
+    w = _attn_case(ATTN_CASES[ci], True, 900 + ci)
+    scale = np.float32(1.0 / np.sqrt(w["q"].shape[2]))
+    ref, ref_lse = oracle_attn(w, scale)
+    g = workload_to_device(w, torch.bfloat16)
+    ws = ada.Workspace(256)
+    for rep in range(2):
+        out, lse = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"],
+                                        g["page_table"], g["kv_len"], g["tree_offsets"], g["tree_parent"], scale,
+                                        want_lse=True, workspace=ws, schedule=f"pair=1,nq={nq}")
+        assert ada.check_device_error(ws)[0] == 0
+        err = np.abs(out.float().cpu().numpy() - ref).max()
+        assert err <= BF16_TOL, (rep, err)
+        assert np.abs(lse.cpu().numpy() - ref_lse).max() <= 1e-2
+
+
 def test_attn_tree_too_big_is_flagged(ada):
     """K_i > AS_MAX_TREE (256): the request is skipped and AS_DEV_TREE_TOO_BIG
     reported with its index; the other requests are still verified."""
