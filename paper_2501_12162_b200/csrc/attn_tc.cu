@@ -114,6 +114,8 @@ struct TcSmem {
     do {                                                                                       \
         if (kDebug && p.trace != nullptr && blockIdx.x == 0 && (int)(idx) < p.trace_cap)      \
             p.trace[(size_t)(idx) * 8 + (e)] = clock64();                                      \
+        else if (kDebug && PR && p.trace != nullptr && blockIdx.x == 1 && (int)(idx) < 500)    \
+            p.trace[(size_t)(2500 + (idx)) * 8 + (e)] = clock64();                             \
     } while (0)
 
 // CTA-0 epilogue trace (debug): event e of the CTA's piece k (rows 3000.. of the tile trace).
@@ -875,6 +877,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 auto fwd_k = [&]() {
                     const int st = fk % kKStages;
                     ptx::mbar_wait(k_full + st, (fk / kKStages) & 1);
+                    if (lane == 0) AS_TRACE(0, fk);
                     if (lane == 0) ptx::mbar_arrive_remote(k_full + st, 0);
                     __syncwarp();
                     ++fk;
@@ -890,6 +893,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         ptx::fence_proxy_async_smem();
                     }
                     __syncwarp();
+                    if (lane == 0) AS_TRACE(1, fv);
                     if (lane == 0) ptx::mbar_arrive_remote(v_full + st, 0);
                     __syncwarp();
                     ++fv;

@@ -108,7 +108,8 @@ if len(ep):
     for r_ in ep:
         rel_ = lambda e: round((r_[e] - r_[0]) / 1e3, 2) if r_[e] else None
         print("  ", rel_(1), rel_(2), rel_(3), rel_(4), rel_(5), int(r_[7]))
-tr = tr[:3000]
+peer = tr[2500:3000].copy()
+tr = tr[:2500]
 n = int((tr[:, 0] != 0).sum())
 tr = tr[:n].astype(np.float64)
 t0 = tr[0, 0]
@@ -130,3 +131,12 @@ print("QK issue interval             ", ns(np.diff(tr[:, 7])))
 print("cols: Kiss Viss Kland Vland PViss Sstart Send QKiss ; rows = tiles 20..36 (ns rel. to tile 20 K issue)")
 if n > 20:
     print(np.round(tr[20:37, :8] - tr[20, 0]))
+pn = int((peer[:, 5] != 0).sum())
+if pn > 40:
+    # peer CTA (pair mode): forward K / V times, softmax start / end, same clock base as CTA 0's tile 20 K issue
+    pr = (peer[:pn].astype(np.float64) - t0) / args.ghz
+    print("peer CTA 1 (pair): softmax start - leader softmax start", ns(pr[20:pn, 5] - tr[20:pn, 5]))
+    print("peer CTA 1 (pair): softmax duration                    ", ns(pr[20:pn, 6] - pr[20:pn, 5]))
+    print("peer CTA 1 (pair): softmax end - leader softmax end    ", ns(pr[20:pn, 6] - tr[20:pn, 6]))
+    print("peer rows 20..30: Kfwd Vfwd Sstart Send (rel. leader tile 20 K issue)")
+    print(np.round(pr[20:31][:, [0, 1, 5, 6]] - tr[20, 0]))
