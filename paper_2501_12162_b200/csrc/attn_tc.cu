@@ -128,6 +128,19 @@ struct TcSmem {
         }                                                                                         \
     } while (0)
 
+// CTA pair, peer side: the 4 warps of a softmax group count themselves on a
+// shared counter (acq_rel: the last one sees the others' TMEM writes) and the
+// last forwards ONE cluster-scope arrive to the leader's barrier -- one remote
+// release per group and tile instead of four.
+__device__ __forceinline__ void peer_group_arrive(int* cnt, uint64_t* bar) {
+    int old;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(ptx::smem_u32(cnt)) : "memory");
+    if (old == 3) {
+        *reinterpret_cast<volatile int*>(cnt) = 0;  // next use of this counter is two tiles later
+        ptx::mbar_arrive_remote(bar, 0);
+    }
+}
+
 // Named barrier of one softmax warp group (128 threads; ids 1 and 2, constant
 // operands so the kernel claims only the barriers it uses).
 __device__ __forceinline__ void group_bar(int grp) {
@@ -428,6 +441,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     pdl_launch_dependents();
 
     const bool leader = !PR || crank == 0;  // PR: the CTA that issues the pair's MMAs
+    __shared__ int pcnt_s[NQ][2], ocnt_s[NQ];  // CTA pair, peer: softmax group arrival counters
+    if (threadIdx.x < NQ) {
+        pcnt_s[threadIdx.x][0] = pcnt_s[threadIdx.x][1] = 0;
+        ocnt_s[threadIdx.x] = 0;
+    }
     if (threadIdx.x == 0) {
         // PR: the leader's full barriers also wait for the peer's forwarded landing
         const int fw = (PR && leader) ? 2 : 1;
@@ -446,11 +464,12 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         for (int q = 0; q < NQ; ++q) {
             for (int b = 0; b < 2; ++b) {
                 ptx::mbar_init(s_full(q, b), 1);
-                ptx::mbar_init(p_full(q, b), PR ? 8 : 4);  // the q-tile's 4 softmax warps (PR: of both CTAs)
+                // the q-tile's 4 softmax warps (PR: + one forwarded arrival for the peer's 4)
+                ptx::mbar_init(p_full(q, b), PR ? 5 : 4);
                 ptx::mbar_init(pv_done(q, b), 1);
             }
             ptx::mbar_init(o_full(q), 1);
-            ptx::mbar_init(o_empty(q), PR ? 8 : 4);
+            ptx::mbar_init(o_empty(q), PR ? 5 : 4);
         }
         ptx::fence_mbar_init();
         ptx::tma_prefetch(&tm_q);
@@ -1048,13 +1067,13 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     ptx::tc_fence_after();
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive_remote(p_full(grp, b), 0);
+                    if (lane == 0) peer_group_arrive(&pcnt_s[grp][b], p_full(grp, b));
                 }
                 ptx::mbar_wait(of, unit_it & 1);
                 ptx::tc_fence_after();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive_remote(oe, 0);
+                if (lane == 0) peer_group_arrive(&ocnt_s[grp], oe);
                 ++unit_it;
                 tbase += pc.te - pc.tb;
                 continue;
@@ -1115,7 +1134,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     __syncwarp();
                     if (lane == 0) {
                         if (leader) ptx::mbar_arrive(p_full(grp, b));
-                        else ptx::mbar_arrive_remote(p_full(grp, b), 0);
+                        else peer_group_arrive(&pcnt_s[grp][b], p_full(grp, b));
                     }
                     continue;
                 }
@@ -1189,7 +1208,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 __syncwarp();
                 if (lane == 0) {  // PR: the leader's barrier counts both CTAs' warps
                     if (leader) ptx::mbar_arrive(p_full(grp, b));
-                    else ptx::mbar_arrive_remote(p_full(grp, b), 0);
+                    else peer_group_arrive(&pcnt_s[grp][b], p_full(grp, b));
                 }
                 if (lane == 0 && quad == 0 && grp == 0) AS_TRACE(6, tbase + t - pc.tb);
             }
@@ -1309,7 +1328,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             __syncwarp();
             if (lane == 0) {
                 if (leader) ptx::mbar_arrive(oe);
-                else ptx::mbar_arrive_remote(oe, 0);
+                else peer_group_arrive(&ocnt_s[grp], oe);
             }
             if (kDebug && !full && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {
                 unsigned long long tn;

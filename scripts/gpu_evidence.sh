@@ -30,6 +30,19 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:"sel
    -o gpurun_out/prof_small_${TAG}_c2 -f python bench.py --profile --steps 2 --warmup 3 --no-graph > gpurun_out/ncu_small_${TAG}.log 2>&1
 echo "ncu small rc=$?"
 fi
+if [ -z "$SKIP_SHARDS" ]; then
+for W in 2 4 8; do for C in c2 c4 c5; do
+  AS_BENCH_EMULATE_WORLD=$W timeout 300 python bench.py --config $C --no-cpu-baseline --no-spec --no-e2e > gpurun_out/bench_${TAG}_${C}_w$W.json 2>/dev/null
+  tail -1 gpurun_out/bench_${TAG}_${C}_w$W.json | python -c "
+import json,sys
+d=json.loads(sys.stdin.read()); r=d['roofline']
+print('$C w$W attn_us', round(r['attn_ms']*1e3,1), 'step_us', round(d['ms_per_step']*1e3,1))" 2>&1 | tail -1
+done; done
+fi
+if [ -z "$SKIP_SEL" ]; then
+python -m paper_2501_12162_b200.build --debug > /dev/null 2>&1
+for C in c2 c3 c4; do AS_DEBUG_LIB=1 SEL_PDL=1 SEL_STOPS="99" timeout 300 python scripts/sel_latency.py $C 2>&1 | tail -1; done
+fi
 if [ -z "$SKIP_SAN" ]; then
 for TOOL in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $TOOL --error-exitcode 9 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/sanitizer_${TOOL}_${TAG}.log 2>&1
