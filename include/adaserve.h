@@ -69,7 +69,8 @@ enum {
     AS_DEV_NAN_LOGIT = 7,      /* NaN in target_logits                                    */
     AS_DEV_PATH_TOO_LONG = 8,  /* accepted path longer than max_path (truncated)          */
     AS_DEV_BAD_PAGE = 9,       /* page id outside [0, num_pages)                          */
-    AS_DEV_BAD_TOKEN = 10      /* draft token outside [0, vocab) (as_mss_verify)          */
+    AS_DEV_BAD_TOKEN = 10,     /* draft token outside [0, vocab) (as_mss_verify)          */
+    AS_DEV_NOT_RESIDENT = 11   /* split-KV pieces not co-resident (SMs held elsewhere): gave up */
 };
 
 #define AS_MAX_TREE 256 /* nodes per tree (incl. root) accepted by as_tree_verify_attn */
@@ -209,7 +210,9 @@ as_status as_select_topm(int32_t n_req, int32_t n_cand_total, const int32_t* can
  *   n_q_heads % n_kv_heads == 0; for AS_BF16 the group size n_q/n_kv must be
  *   a power of two <= 16.  Heads are the caller's LOCAL heads (KV-head sharding).
  * Device preconditions: AS_DEV_TREE_TOO_BIG, AS_DEV_BAD_PARENT,
- *   AS_DEV_ROWS_OVERFLOW, AS_DEV_BAD_PAGE.
+ *   AS_DEV_ROWS_OVERFLOW, AS_DEV_BAD_PAGE; AS_DEV_NOT_RESIDENT if the split-KV
+ *   pieces of a unit cannot all be resident (the device shared with another
+ *   tenant): the call returns after 0.5 s with that unit's output unspecified.
  */
 size_t as_attn_workspace_size(as_dtype dtype, int32_t n_req, int32_t n_tree_rows,
                               int32_t n_q_heads, int32_t head_dim, int32_t max_kv_len);

@@ -29,7 +29,7 @@ AS_ACCEPT_WALK_RECORDS, AS_ACCEPT_COMMIT_RECORDS = 3, 4
 AS_MSS_WALK, AS_MSS_ALL_NODES = 0, 1
 DEVICE_ERRORS = {0: "ok", 1: "bad parent", 2: "bad f-hat", 3: "too many candidates", 4: "tree too big",
                  5: "rows overflow", 6: "page overflow", 7: "NaN logit", 8: "path too long", 9: "bad page",
-                 10: "bad token"}
+                 10: "bad token", 11: "split-KV pieces not co-resident"}
 
 _c_i32, _c_sz, _vp, _f32 = ctypes.c_int32, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_float
 _lib = None

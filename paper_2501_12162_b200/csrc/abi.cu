@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include "params.cuh"
@@ -55,11 +56,14 @@ constexpr int kMaxKLead = 1;  // must stay < the K ring depth (2)
 int sm_count() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-    static int cache[64] = {0};
-    if (dev < 64 && cache[dev]) return cache[dev];
+    static std::atomic<int> cache[64];  // per device (zero-initialised statics; re-entrant)
+    if (dev < 64) {
+        const int c = cache[dev].load(std::memory_order_relaxed);
+        if (c) return c;
+    }
     int n = 148;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (dev < 64) cache[dev] = n;
+    if (dev < 64) cache[dev].store(n, std::memory_order_relaxed);
     return n;
 }
 

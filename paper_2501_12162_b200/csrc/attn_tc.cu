@@ -1354,7 +1354,20 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 group_bar(grp);
                 if (warp == lead_warp && lane == 0) {
                     atomicAdd(p.cnt + wq, pc.te - pc.tb);
-                    while (*reinterpret_cast<volatile int*>(p.cnt + wq) < u.nt) __nanosleep(64);
+                    // the unit's pieces are co-resident by construction (one per CTA of a grid
+                    // sized to the device); if another tenant (MPS, a concurrent kernel) holds
+                    // SMs they may not be -- give up after 0.5 s with a device error instead
+                    // of hanging (a cooperative launch is not capturable with PDL edges)
+                    unsigned long long t0w, tw;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0w));
+                    while (*reinterpret_cast<volatile int*>(p.cnt + wq) < u.nt) {
+                        __nanosleep(64);
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw));
+                        if (tw - t0w > 500000000ull) {
+                            set_dev_error(p.ws, AS_DEV_NOT_RESIDENT, p.req_base + u.i);
+                            break;
+                        }
+                    }
                 }
                 group_bar(grp);
                 __threadfence();

@@ -760,7 +760,15 @@ int pdl_enabled() {
 static int cluster_size_for(int n) {
     int cs = n;  // as many CTAs as possible: more warps per request (latency-bound)
     if (cs < 1) cs = 1;
-    if (cs > kSelMaxCluster) cs = kSelMaxCluster;
+    int cap = kSelMaxCluster;
+#ifdef AS_DEBUG
+    static const int dbg_cap = [] {  // A/B: cluster size cap (debug build)
+        const char* e = getenv("AS_SEL_CS");
+        return e ? atoi(e) : 0;
+    }();
+    if (dbg_cap > 0) cap = dbg_cap;
+#endif
+    if (cs > cap) cs = cap;
     return cs;
 }
 
