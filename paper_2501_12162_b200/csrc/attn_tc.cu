@@ -464,12 +464,12 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         for (int q = 0; q < NQ; ++q) {
             for (int b = 0; b < 2; ++b) {
                 ptx::mbar_init(s_full(q, b), 1);
-                // the q-tile's 4 softmax warps (PR: + one forwarded arrival for the peer's 4)
-                ptx::mbar_init(p_full(q, b), PR ? 5 : 4);
+                // the q-tile's 4 softmax warps (PR leader: + one arrival forwarded for the peer's 4)
+                ptx::mbar_init(p_full(q, b), (PR && leader) ? 5 : 4);
                 ptx::mbar_init(pv_done(q, b), 1);
             }
             ptx::mbar_init(o_full(q), 1);
-            ptx::mbar_init(o_empty(q), PR ? 5 : 4);
+            ptx::mbar_init(o_empty(q), (PR && leader) ? 5 : 4);
         }
         ptx::fence_mbar_init();
         ptx::tma_prefetch(&tm_q);
@@ -890,7 +890,35 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         if (PR && !leader) {
             // ---- CTA-pair peer: warp 1 forwards each landing of this CTA's halves to
             // the leader's barrier, in the leader's consumption order (Q; K_tb; K_t+1,
-            // V_t ...), zeroing V rows past the valid keys first (see do_pv) ----
+            // V_t ...), zeroing V rows past the valid keys first (see do_pv); warp 2
+            // (NQ = 2) forwards the softmax groups' P / O-drained signals: the softmax
+            // warps arrive locally (a cluster-scope release costs their issuing thread
+            // ~0.5 us per tile, measured) ----
+            if (NQ == 2 && q == 1) {
+                uint32_t gs[NQ], gu[NQ];
+                for (int j = 0; j < NQ; ++j) gs[j] = gu[j] = 0;
+                RecCursor sc2 = cur0;
+                Piece pc2;
+                while (rec_next(p, sc2, pc2)) {
+                    const Unit& u = pc2.u;
+                    for (int t = pc2.tb; t < pc2.te; ++t)
+                        for (int j = 0; j < NQ; ++j) {
+                            if (j >= u.nq) continue;  // the pair is inactive (the leader skips it too)
+                            const uint32_t b = gs[j] & 1;
+                            ptx::mbar_wait(p_full(j, b), (gs[j] >> 1) & 1);
+                            if (lane == 0) ptx::mbar_arrive_remote(p_full(j, b), 0);
+                            __syncwarp();
+                            ++gs[j];
+                        }
+                    for (int j = 0; j < NQ; ++j) {
+                        if (j >= u.nq) continue;
+                        ptx::mbar_wait(o_empty(j), gu[j] & 1);
+                        if (lane == 0) ptx::mbar_arrive_remote(o_empty(j), 0);
+                        __syncwarp();
+                        ++gu[j];
+                    }
+                }
+            }
             if (q == 0) {
                 uint32_t fk = 0, fv = 0, fu = 0;
                 auto fwd_k = [&]() {
@@ -937,10 +965,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             auto do_qk = [&](int t) {
                 const int st = k_it % kKStages;
                 ptx::mbar_wait(k_full + st, (k_it / kKStages) & 1);
-                if (lane == 0 && q == 0) AS_TRACE(2, k_it);
+                if (lane == 0 && q == 0 && !(kDebug && p.debug_mode == 5)) AS_TRACE(2, k_it);
                 ptx::tc_fence_after();
                 if (lane == 0) {
-                    if (!mine || (kDebug && p.debug_mode >= 2)) {
+                    if (!mine || (kDebug && p.debug_mode >= 2 && p.debug_mode < 5)) {
                         if (mine) arrive_all(s_full(q, s_it & 1));
                         release(k_empty + st, false);
                         if (t == pc.te - 1) {
@@ -949,7 +977,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                         }
                     } else {
                         const uint32_t s_col = tq + (s_it & 1) * 64;
-                        if (q == 0) AS_TRACE(7, k_it);
+                        if (q == 0 && !(kDebug && p.debug_mode == 5)) AS_TRACE(7, k_it);
 #pragma unroll
                         for (int ks = 0; ks < D / 16; ++ks) {
                             const int c = ks >> 2, kk = ks & 3;
@@ -971,7 +999,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             auto do_pv = [&](int t) {
                 const int st = v_it % kVStages;
                 ptx::mbar_wait(v_full + st, (v_it / kVStages) & 1);
-                if (lane == 0 && q == 0) AS_TRACE(3, v_it);
+                if (lane == 0 && q == 0 && !(kDebug && p.debug_mode == 5)) AS_TRACE(3, v_it);
                 if (!mine) {
                     if (lane == 0) release(v_empty + st, false);
                     __syncwarp();
@@ -997,11 +1025,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 }
                 const uint32_t pbuf = p_it & 1;
                 ptx::mbar_wait(p_full(q, pbuf), (p_it >> 1) & 1);
-                if (lane == 0 && q == 0) AS_TRACE(4, v_it);
+                if (lane == 0 && q == 0 && !(kDebug && p.debug_mode == 5)) AS_TRACE(4, v_it);
                 if (t == pc.tb) ptx::mbar_wait(o_empty(q), (o_it & 1) ^ 1);  // O drained by the last epilogue
                 ptx::tc_fence_after();
                 __syncwarp();
-                if (kDebug && p.debug_mode >= 2) {
+                if (kDebug && p.debug_mode >= 2 && p.debug_mode < 5) {
                     if (lane == 0) {
                         release(v_empty + st, false);
                         arrive_all(pv_done(q, pbuf));
@@ -1028,7 +1056,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             do_pv(pc.te - 1);
             if (mine) {
                 if (lane == 0) {
-                    if (kDebug && p.debug_mode >= 2) arrive_all(o_full(q));
+                    if (kDebug && p.debug_mode >= 2 && p.debug_mode < 5) arrive_all(o_full(q));
                     else signal(o_full(q));
                 }
                 ++o_it;
@@ -1067,13 +1095,19 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     ptx::tc_fence_after();
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) peer_group_arrive(&pcnt_s[grp][b], p_full(grp, b));
+                    if (lane == 0) {  // NQ = 2: forwarded by the peer's warp 2; NQ = 1: last warp forwards
+                        if (NQ == 2) ptx::mbar_arrive(p_full(grp, b));
+                        else peer_group_arrive(&pcnt_s[grp][b], p_full(grp, b));
+                    }
                 }
                 ptx::mbar_wait(of, unit_it & 1);
                 ptx::tc_fence_after();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) peer_group_arrive(&ocnt_s[grp], oe);
+                if (lane == 0) {
+                    if (NQ == 2) ptx::mbar_arrive(oe);
+                    else peer_group_arrive(&ocnt_s[grp], oe);
+                }
                 ++unit_it;
                 tbase += pc.te - pc.tb;
                 continue;
@@ -1129,11 +1163,13 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 ptx::tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
                 ptx::tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
                 ptx::tmem_ld_wait();
-                if (kDebug && p.debug_mode >= 1) {  // timing experiment: no softmax math
+                if (kDebug && p.debug_mode == 5 && lane == 0 && quad == 0 && grp == 0) AS_TRACE(2, tbase + t - pc.tb);
+                if (kDebug && p.debug_mode >= 1 && p.debug_mode < 5) {  // timing experiment: no softmax math
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) {
                         if (leader) ptx::mbar_arrive(p_full(grp, b));
+                        else if (NQ == 2) ptx::mbar_arrive(p_full(grp, b));
                         else peer_group_arrive(&pcnt_s[grp][b], p_full(grp, b));
                     }
                     continue;
@@ -1164,6 +1200,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 const float tmax = ptx::max3(ptx::max3(mx[0], mx[1], mx[2]), ptx::max3(mx[3], mx[4], mx[5]),
                                              fmaxf(mx[6], mx[7])) * sl2;
                 const float m_new = fmaxf(m_ref, tmax);
+                if (kDebug && p.debug_mode == 5 && lane == 0 && quad == 0 && grp == 0) AS_TRACE(3, tbase + t - pc.tb);
                 if (t > pc.tb) {
                     const bool need = m_new > m_ref + kRescaleThresh;
                     if (__any_sync(0xffffffffu, need)) {
@@ -1201,13 +1238,16 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     pk[c >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                 }
                 l_sum += (rs[0] + rs[1]) + (rs[2] + rs[3]);
+                if (kDebug && p.debug_mode == 5 && lane == 0 && quad == 0 && grp == 0) AS_TRACE(4, tbase + t - pc.tb);
                 // P_t over the first 32 columns of S_t's buffer (S_t already in registers)
                 ptx::tmem_st32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
                 ptx::tmem_st_wait();
+                if (kDebug && p.debug_mode == 5 && lane == 0 && quad == 0 && grp == 0) AS_TRACE(7, tbase + t - pc.tb);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {  // PR: the leader's barrier counts both CTAs' warps
                     if (leader) ptx::mbar_arrive(p_full(grp, b));
+                    else if (NQ == 2) ptx::mbar_arrive(p_full(grp, b));
                     else peer_group_arrive(&pcnt_s[grp][b], p_full(grp, b));
                 }
                 if (lane == 0 && quad == 0 && grp == 0) AS_TRACE(6, tbase + t - pc.tb);
@@ -1328,6 +1368,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             __syncwarp();
             if (lane == 0) {
                 if (leader) ptx::mbar_arrive(oe);
+                else if (NQ == 2) ptx::mbar_arrive(oe);
                 else peer_group_arrive(&ocnt_s[grp], oe);
             }
             if (kDebug && !full && p.trace != nullptr && gtid == 0 && grp == 0 && blockIdx.x < kTraceCtas) {

@@ -126,6 +126,15 @@ print("P ready -> MMA sees P         ", ns(tr[:, 4] - tr[:, 6]))
 print("V landed -> PV issue (wait P) ", ns(tr[:, 4] - tr[:, 3]))
 print("producer waits for K slot: K issue minus PV of tile-4 issue", ns(tr[4:, 0] - tr[:-4, 4]))
 np.set_printoptions(linewidth=200, suppress=True)
+if os.environ.get("AS_ATTN_DEBUG_MODE") == "5":
+    # softmax sub-stamps: 2 S loaded, 3 max done, 4 exp done, 7 P stored
+    print("softmax: start->S loaded", ns(tr[:, 2] - tr[:, 5]), " ->max", ns(tr[:, 3] - tr[:, 2]),
+          " ->exp", ns(tr[:, 4] - tr[:, 3]), " ->P stored", ns(tr[:, 7] - tr[:, 4]), " ->arrived", ns(tr[:, 6] - tr[:, 7]))
+    pn2 = int((peer[:, 5] != 0).sum())
+    if pn2 > 40:
+        pr2 = peer[:pn2].astype(np.float64) / args.ghz
+        print("peer:    start->S loaded", ns(pr2[:, 2] - pr2[:, 5]), " ->max", ns(pr2[:, 3] - pr2[:, 2]),
+              " ->exp", ns(pr2[:, 4] - pr2[:, 3]), " ->P stored", ns(pr2[:, 7] - pr2[:, 4]), " ->arrived", ns(pr2[:, 6] - pr2[:, 7]))
 print("QK issue -> softmax start      ", ns(tr[:, 5] - tr[:, 7]))
 print("QK issue interval             ", ns(np.diff(tr[:, 7])))
 print("cols: Kiss Viss Kland Vland PViss Sstart Send QKiss ; rows = tiles 20..36 (ns rel. to tile 20 K issue)")
