@@ -31,6 +31,8 @@
 //               tcgen05.ld O, * 1/l, bf16 store, optional natural-log LSE; or,
 //               for a unit split across CTAs (split-KV), the fp32 partial
 //               (O, m, l), then a share of the unit's cooperative merge.
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "params.cuh"
@@ -1548,6 +1550,10 @@ int launch_attn_tc(const CUtensorMap* maps, const TcParams& p0, int head_dim, in
         const int res = nq == 2 ? resident_ctas<128, 2, 2, true>(n_sms) : resident_ctas<128, 1, 2, true>(n_sms);
         if (res < 2) return -1;  // (the maps were built for half tiles: no fallback here)
         grid_full = res / 2 * 2;
+#ifdef AS_DEBUG
+        if (getenv("AS_ATTN_PAIR_GRID")) grid_full = atoi(getenv("AS_ATTN_PAIR_GRID"));  // A/B: force the grid
+        if (getenv("AS_ATTN_VERBOSE")) fprintf(stderr, "pair nq=%d resident=%d grid=%d\n", nq, res, grid_full);
+#endif
     } else if (cs > 1) {
         const int res = nq == 2 ? (head_dim == 128 ? resident_ctas<128, 2, 2>(n_sms) : resident_ctas<64, 2, 2>(n_sms))
                       : head_dim == 128 ? (cs == 2 ? resident_ctas<128, 1, 2>(n_sms) : resident_ctas<128, 1, 4>(n_sms))
