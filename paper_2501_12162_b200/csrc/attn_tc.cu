@@ -315,7 +315,68 @@ __device__ __noinline__ void split_merge(const float* __restrict__ slot0, size_t
 // fp32 partials for row r.  The n_pc <= 3 pieces are combined in the unit's
 // piece order (own_pos = this piece's position, slot[k] = piece k's partial
 // slot), whichever piece merges, so the result is deterministic:
-// out_row[c] = sum_k 2^(m_k - M) O_k[c] / sum_k 2^(m_k - M) l_k, M = max_k m_k.
+// out_row[c] = sum_k 2^(m_k - M) O_k[c] / sum_k 2^(m_k - M) l_k, M = max_k m_k,
+// the sum evaluated as a = w_0 O_0; a = fma(O_k, w_k, a) for k = 1, 2.
+// One L2 round trip per remote piece: a round issues the loads of all its
+// columns at once (the partial was written moments ago by another SM) and the
+// running sum is kept in this piece's O columns of TMEM between rounds.
+template <int D, int NC, int NR>
+__device__ __forceinline__ void tail_round(uint32_t o_addr, int cb, const float* r0p, const float* r1p, float w0,
+                                           float w1, bool own_after, bool fresh, float w_own, bool fin, float inv,
+                                           int r, __nv_bfloat16* out_row) {
+    float4 q[NR][NC / 4];
+#pragma unroll
+    for (int j = 0; j < NC / 4; ++j) {  // every load of the round in flight before the first use
+        q[0][j] = __ldcg(reinterpret_cast<const float4*>(r0p) + (cb / 4 + j) * 128 + r);
+        if (NR > 1) q[NR - 1][j] = __ldcg(reinterpret_cast<const float4*>(r1p) + (cb / 4 + j) * 128 + r);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; c += 32) {
+        uint32_t oa[32];
+        ptx::tmem_ld32(o_addr + cb + c, oa);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            const float t = __uint_as_float(oa[e]);
+            const float4 v0 = q[0][(c + e) >> 2];
+            const float x0 = (e & 3) == 0 ? v0.x : (e & 3) == 1 ? v0.y : (e & 3) == 2 ? v0.z : v0.w;
+            float x1 = 0.f;
+            if (NR > 1) {
+                const float4 v1 = q[NR - 1][(c + e) >> 2];
+                x1 = (e & 3) == 0 ? v1.x : (e & 3) == 1 ? v1.y : (e & 3) == 2 ? v1.z : v1.w;
+            }
+            float a;
+            if (own_after) {  // remotes precede this piece in the unit's order
+                a = fmaf(x0, w0, 0.f);
+                if (NR > 1) a = fmaf(x1, w1, a);
+                a = fmaf(t, w_own, a);
+            } else {          // TMEM holds the running sum (or this piece's own O, fresh)
+                a = fresh ? fmaf(t, w_own, 0.f) : t;
+                a = fmaf(x0, w0, a);
+                if (NR > 1) a = fmaf(x1, w1, a);
+            }
+            oa[e] = __float_as_uint(a);
+        }
+        if (fin) {
+            if (out_row != nullptr) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(oa[2 * j]) * inv,
+                                                             __uint_as_float(oa[2 * j + 1]) * inv);
+                    pk[j] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(out_row + cb + c);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            }
+        } else {
+            ptx::tmem_st32(o_addr + cb + c, oa);
+        }
+    }
+    if (!fin) ptx::tmem_st_wait();
+}
+
 template <int D>
 __device__ __noinline__ void tail_merge(uint32_t o_addr, float m_own, float l_own, const float* __restrict__ part0,
                                         size_t slot_floats, int n_pc, int own_pos, int s0, int s1, int s2, int r,
@@ -345,43 +406,40 @@ __device__ __noinline__ void tail_merge(uint32_t o_addr, float m_own, float l_ow
         Ltot = fmaf(lo[k], wo[k], Ltot);
     }
     const float inv = 1.f / Ltot;
+    const float wown = own_pos == 0 ? wo[0] : own_pos == 1 ? wo[1] : wo[2];
+    if (n_pc <= 1) {  // (a merger has >= 2 pieces; kept defined)
 #pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 32) {
-        uint32_t oa[32];
-        ptx::tmem_ld32(o_addr + c0, oa);
-        float4 q[3][8];
+        for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t oa[32];
+            ptx::tmem_ld32(o_addr + c0, oa);
+            ptx::tmem_ld_wait();
+            if (out_row != nullptr) {
+                uint32_t pk[16];
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
+                for (int j = 0; j < 16; ++j) {
+                    __nv_bfloat162 h = __floats2bfloat162_rn(fmaf(__uint_as_float(oa[2 * j]), wown, 0.f) * inv,
+                                                             fmaf(__uint_as_float(oa[2 * j + 1]), wown, 0.f) * inv);
+                    pk[j] = *reinterpret_cast<uint32_t*>(&h);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(out_row + c0);
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-                q[k][j] = (k < n_pc && k != own_pos)
-                              ? __ldcg(reinterpret_cast<const float4*>(src[k]) + (c0 / 4 + j) * 128 + r)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-        ptx::tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const float4 own = make_float4(__uint_as_float(oa[4 * j]), __uint_as_float(oa[4 * j + 1]),
-                                           __uint_as_float(oa[4 * j + 2]), __uint_as_float(oa[4 * j + 3]));
-            float a[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const float4 v = k == own_pos ? own : q[k][j];
-                a[0] = fmaf(v.x, wo[k], a[0]);
-                a[1] = fmaf(v.y, wo[k], a[1]);
-                a[2] = fmaf(v.z, wo[k], a[2]);
-                a[3] = fmaf(v.w, wo[k], a[3]);
+                for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
             }
-            __nv_bfloat162 h0 = __floats2bfloat162_rn(a[0] * inv, a[1] * inv);
-            __nv_bfloat162 h1 = __floats2bfloat162_rn(a[2] * inv, a[3] * inv);
-            pk[2 * j] = *reinterpret_cast<uint32_t*>(&h0);
-            pk[2 * j + 1] = *reinterpret_cast<uint32_t*>(&h1);
         }
-        if (out_row != nullptr) {
-            uint4* dst = reinterpret_cast<uint4*>(out_row + c0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-        }
+    } else if (own_pos == 0) {
+        // a = own w0, then each later piece in order: one round per remote piece
+        tail_round<D, D, 1>(o_addr, 0, src[1], nullptr, wo[1], 0.f, false, true, wown, n_pc == 2, inv, r, out_row);
+        if (n_pc == 3)
+            tail_round<D, D, 1>(o_addr, 0, src[2], nullptr, wo[2], 0.f, false, false, wown, true, inv, r, out_row);
+    } else if (own_pos == 1) {
+        tail_round<D, D, 1>(o_addr, 0, src[0], nullptr, wo[0], 0.f, true, false, wown, n_pc == 2, inv, r, out_row);
+        if (n_pc == 3)
+            tail_round<D, D, 1>(o_addr, 0, src[2], nullptr, wo[2], 0.f, false, false, wown, true, inv, r, out_row);
+    } else {  // own last of three: both remotes first, half the columns per round
+#pragma unroll 1
+        for (int cb = 0; cb < D; cb += D / 2)
+            tail_round<D, D / 2, 2>(o_addr, cb, src[0], src[1], wo[0], wo[1], true, false, wown, true, inv, r,
+                                    out_row);
     }
     if (lse_out != nullptr) *lse_out = (M + __log2f(Ltot)) * 0.6931471805599453f;
 }
@@ -637,7 +695,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 // balanced waves would leave SMs empty (c5: 256 units, 148 one-CTA SMs).
                 const int Wv0 = U > 0 ? (U + G - 1) / G : 1;
                 const int Geff0 = U > 0 ? (U + Wv0 - 1) / Wv0 : G;
-                const bool balanced_ok = Wv0 <= 3 && Geff0 * TcCfg<NQ>::CTAS >= G;
+                const bool balanced_ok = Wv0 <= 3 && Geff0 * TcCfg<NQ>::CTAS >= G && p.tail_mode != 2;
                 bool tail = p.stream_k && can_plan && W1 >= 1 && 2 * R > G && W1 + 2 <= kMaxRec && p.tail_mode &&
                             !balanced_ok;
                 bool ok = can_plan;

@@ -68,7 +68,7 @@ struct TcParams {
     int pair;             // 1: CTA pairs (cs = 2, tcgen05.mma.cta_group::2, half K/V tiles per CTA)
     int mt_max;           // q-tiles per (request, kv head) upper bound (unit id stride)
     int stream_k;         // 1: split-KV allowed (needs cnt/cnt2/partial in the workspace), 0: whole units only
-    int tail_mode;        // 1: tail stream-K for a partial last wave; 0: balanced whole-unit waves
+    int tail_mode;        // 1: tail stream-K for a partial last wave; 0: balanced whole-unit waves; 2: tail even when balanced waves fit (debug A/B)
     int* cnt;             // [n_units] tiles completed per split unit (zeroed, self-resetting)
     int* cnt2;            // [n_units] pieces that finished merging (zeroed, self-resetting)
     float* partial;       // [2 * gridDim.x][slot_floats] partial (O, m, l) of split units
