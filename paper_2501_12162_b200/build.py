@@ -42,7 +42,7 @@ def _stale(lib: str) -> bool:
 def _build_one(lib: str, sources, defines, tag: str):
     def compile_one(src):
         obj = os.path.join(CSRC, f"{src[:-3]}{tag}.o")
-        cmd = [NVCC, *FLAGS, *defines, "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o",
+        cmd = [NVCC, *FLAGS, *defines, *os.environ.get("AS_NVCC_DEFINES", "").split(), "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o",
                obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

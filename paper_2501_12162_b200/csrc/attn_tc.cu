@@ -1287,17 +1287,24 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                     m_ref = m_new;
                 }
                 const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
-                float rs[4] = {0.f, 0.f, 0.f, 0.f};
+                // the softmax warps are issue-bound (two groups per SM): scale/shift and the
+                // row sum run as packed f32x2 FFMA2 / FADD2, two columns per instruction
+                // (moving a quarter of the ex2 off MUFU onto a polynomial measured 15 % slower)
+                const uint64_t s2 = ptx::f2pack(sl2, sl2), nm2 = ptx::f2pack(neg_m, neg_m);
+                uint64_t rsa = 0ull, rsb = 0ull;  // packed (even, odd) column partial sums
                 uint32_t pk[kBN / 2];
 #pragma unroll
                 for (int c = 0; c < kBN; c += 2) {
-                    const float p0 = ptx::ex2(fmaf(x[c], sl2, neg_m));
-                    const float p1 = ptx::ex2(fmaf(x[c + 1], sl2, neg_m));
-                    rs[(c >> 1) & 3] += p0 + p1;
+                    const uint64_t y = ptx::ffma2(ptx::f2pack(x[c], x[c + 1]), s2, nm2);
+                    const float p0 = ptx::ex2(ptx::f2lo(y));
+                    const float p1 = ptx::ex2(ptx::f2hi(y));
+                    if ((c >> 1) & 1) rsb = ptx::fadd2(rsb, ptx::f2pack(p0, p1));
+                    else rsa = ptx::fadd2(rsa, ptx::f2pack(p0, p1));
                     __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                     pk[c >> 1] = *reinterpret_cast<uint32_t*>(&h2);
                 }
-                l_sum += (rs[0] + rs[1]) + (rs[2] + rs[3]);
+                rsa = ptx::fadd2(rsa, rsb);
+                l_sum += ptx::f2lo(rsa) + ptx::f2hi(rsa);
                 if (kDebug && p.debug_mode == 5 && lane == 0 && quad == 0 && grp == 0) AS_TRACE(4, tbase + t - pc.tb);
                 // P_t over the first 32 columns of S_t's buffer (S_t already in registers)
                 ptx::tmem_st32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
