@@ -530,6 +530,29 @@ def test_attn_bf16(ada, ci, nq):
     assert np.abs(lse.cpu().numpy() - ref_lse).max() <= BF16_TOL
 
 
+@pytest.mark.parametrize("nq,q_scale", [("auto", 4.0), ("auto", 8.0), ("1", 4.0), ("2", 4.0), ("2cs2", 4.0)])
+def test_attn_bf16_long_context_peaky(ada, nq, q_scale):
+    """c5-length prefixes (32k and 20k keys plus a short one) with peaky queries
+    (q scaled 4x / 8x: a few keys dominate each row, so bf16 rounding of P and
+    the lazy rescale matter most), Llama-3-8B heads, 64-node trees: every CTA
+    shape against the fp64 oracle within the 2e-2 bound."""
+    rng = np.random.default_rng(77 if q_scale == 4.0 else 78)
+    w = synth.tree_workload(rng, [64, 33, 8], [32768, 20000, 4097], 32, 8, 128, 64, shape="random", bf16=True,
+                            q_scale=q_scale)
+    scale = np.float32(1.0 / np.sqrt(128))
+    ref, ref_lse = oracle_attn(w, scale)
+    g = workload_to_device(w, torch.bfloat16)
+    ws = ada.Workspace(256)
+    out, lse = ada.tree_verify_attn(g["q"], g["k_tree"], g["v_tree"], g["k_cache"], g["v_cache"], g["page_table"],
+                                    g["kv_len"], g["tree_offsets"], g["tree_parent"], scale, want_lse=True,
+                                    workspace=ws, schedule=_sched(nq))
+    assert ada.check_device_error(ws)[0] == 0
+    err = np.abs(out.float().cpu().numpy() - ref).max()
+    print(f"long-context peaky q_scale={q_scale} shape={nq}: max abs err {err:.5f} (bound {BF16_TOL})")
+    assert err <= BF16_TOL, err
+    assert np.abs(lse.cpu().numpy() - ref_lse).max() <= BF16_TOL
+
+
 @pytest.mark.parametrize("nq", ["1", "2", "cs2", "2cs2"])
 def test_attn_bf16_request_chunks(ada, nq):
     sched = _sched(nq)
