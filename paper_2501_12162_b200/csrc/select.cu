@@ -47,7 +47,10 @@ namespace cg = cooperative_groups;
 
 namespace as {
 
-constexpr int kSelThreads = 1024;
+#ifndef AS_SEL_THREADS
+#define AS_SEL_THREADS 512
+#endif
+constexpr int kSelThreads = AS_SEL_THREADS;
 constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kSelMaxReq = 4096;                // requests handled by one call
 constexpr int kSelMaxCluster = 16;
