@@ -366,9 +366,9 @@ __device__ __forceinline__ void tail_round(uint32_t o_addr, int cb, const float*
                                                              __uint_as_float(oa[2 * j + 1]) * inv);
                     pk[j] = *reinterpret_cast<uint32_t*>(&h);
                 }
-                uint4* dst = reinterpret_cast<uint4*>(out_row + cb + c);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+                unsigned char* dst = reinterpret_cast<unsigned char*>(out_row + cb + c);
+                ptx::st_global_v8(dst, &pk[0]);  // 32-byte stores: full L2 sectors
+                ptx::st_global_v8(dst + 32, &pk[8]);
             }
         } else {
             ptx::tmem_st32(o_addr + cb + c, oa);
@@ -1350,26 +1350,34 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 // co-resident split-KV: one piece per CTA, one slot per q-tile; tail: tail_slot()
                 const int slot = tailp ? tail_slot<NQ>((int)blockIdx.x, -2 - pc.x, grp) : 2 * (int)blockIdx.x + grp;
                 float* part = p.partial + (size_t)slot * p.slot_floats;  // O as [D/4][128] float4, then m[128], l[128]
+                if (full) {
+                    // output row: 64 columns per TMEM round trip (two loads, one wait), bf16,
+                    // 32-byte stores (full L2 sectors; the row is contiguous, 2*D bytes)
 #pragma unroll
-                for (int c0 = 0; c0 < D; c0 += 32) {
-                    uint32_t oa[32];
-                    ptx::tmem_ld32(o_addr + c0, oa);
-                    ptx::tmem_ld_wait();
-                    if (full) {
+                    for (int c0 = 0; c0 < D; c0 += 64) {
+                        uint32_t oa[64];
+                        ptx::tmem_ld32(o_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(&oa[0]));
+                        ptx::tmem_ld32(o_addr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&oa[32]));
+                        ptx::tmem_ld_wait();
                         if (row_ok) {
-                            uint32_t pkk[16];
+                            uint32_t pkk[32];
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) {
+                            for (int j = 0; j < 32; ++j) {
                                 __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(oa[2 * j]) * inv,
                                                                           __uint_as_float(oa[2 * j + 1]) * inv);
                                 pkk[j] = *reinterpret_cast<uint32_t*>(&h2);
                             }
-                            uint4* dst = reinterpret_cast<uint4*>(p.out + orow * D + c0);
+                            unsigned char* dst = reinterpret_cast<unsigned char*>(p.out + orow * D + c0);
 #pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                dst[j] = make_uint4(pkk[4 * j], pkk[4 * j + 1], pkk[4 * j + 2], pkk[4 * j + 3]);
+                            for (int j = 0; j < 4; ++j) ptx::st_global_v8(dst + 32 * j, &pkk[8 * j]);
                         }
-                    } else {
+                    }
+                } else {
+#pragma unroll
+                    for (int c0 = 0; c0 < D; c0 += 32) {
+                        uint32_t oa[32];
+                        ptx::tmem_ld32(o_addr + c0, oa);
+                        ptx::tmem_ld_wait();
                         // column-quad-major [D/4][128] float4: a warp's store is 512 contiguous bytes
                         float4* dst = reinterpret_cast<float4*>(part) + (c0 / 4) * 128 + r;
 #pragma unroll
