@@ -1351,28 +1351,25 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 const int slot = tailp ? tail_slot<NQ>((int)blockIdx.x, -2 - pc.x, grp) : 2 * (int)blockIdx.x + grp;
                 float* part = p.partial + (size_t)slot * p.slot_floats;  // O as [D/4][128] float4, then m[128], l[128]
                 if (full) {
-                    // output row: all D columns in one TMEM round trip (D/32 loads, one wait), bf16,
+                    // output row: 64 columns per TMEM round trip (two loads, one wait), bf16,
                     // 32-byte stores (full L2 sectors; the row is contiguous, 2*D bytes)
-                    constexpr int EC = D;  // one TMEM round trip for the whole row (64 columns per trip: 1 % slower)
 #pragma unroll
-                    for (int c0 = 0; c0 < D; c0 += EC) {
-                        uint32_t oa[EC];
-#pragma unroll
-                        for (int q = 0; q < EC; q += 32)
-                            ptx::tmem_ld32(o_addr + c0 + q, *reinterpret_cast<uint32_t(*)[32]>(&oa[q]));
+                    for (int c0 = 0; c0 < D; c0 += 64) {
+                        uint32_t oa[64];
+                        ptx::tmem_ld32(o_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(&oa[0]));
+                        ptx::tmem_ld32(o_addr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&oa[32]));
                         ptx::tmem_ld_wait();
                         if (row_ok) {
+                            uint32_t pkk[32];
 #pragma unroll
-                            for (int q = 0; q < EC; q += 16) {
-                                uint32_t pkk[8];
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) {
-                                    __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(oa[q + 2 * j]) * inv,
-                                                                              __uint_as_float(oa[q + 2 * j + 1]) * inv);
-                                    pkk[j] = *reinterpret_cast<uint32_t*>(&h2);
-                                }
-                                ptx::st_global_v8(reinterpret_cast<unsigned char*>(p.out + orow * D + c0 + q), pkk);
+                            for (int j = 0; j < 32; ++j) {
+                                __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(oa[2 * j]) * inv,
+                                                                          __uint_as_float(oa[2 * j + 1]) * inv);
+                                pkk[j] = *reinterpret_cast<uint32_t*>(&h2);
                             }
+                            unsigned char* dst = reinterpret_cast<unsigned char*>(p.out + orow * D + c0);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) ptx::st_global_v8(dst + 32 * j, &pkk[8 * j]);
                         }
                     }
                 } else {
