@@ -366,9 +366,9 @@ __device__ __forceinline__ void tail_round(uint32_t o_addr, int cb, const float*
                                                              __uint_as_float(oa[2 * j + 1]) * inv);
                     pk[j] = *reinterpret_cast<uint32_t*>(&h);
                 }
-                unsigned char* dst = reinterpret_cast<unsigned char*>(out_row + cb + c);
-                ptx::st_global_v8(dst, &pk[0]);  // 32-byte stores: full L2 sectors
-                ptx::st_global_v8(dst + 32, &pk[8]);
+                uint4* dst = reinterpret_cast<uint4*>(out_row + cb + c);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
             }
         } else {
             ptx::tmem_st32(o_addr + cb + c, oa);

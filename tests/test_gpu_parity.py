@@ -196,6 +196,27 @@ def test_select_fuzz(ada, seed):
 
 
 @pytest.mark.parametrize("seed", range(4))
+def test_select_radix_shared_key_bits(ada, seed):
+    """The throughput stage's radix select starts below the key bits all tails
+    share (AND / OR over the cluster): f-hat squeezed into [0.5, 0.5 + 2^-s] by a
+    monotone map (parent >= child and exact ties preserved) leaves only the low
+    mantissa bits and the request/index word to decide -- bit-exact vs Alg. 2."""
+    rng = np.random.default_rng(900 + seed)
+    for it in range(12):
+        n = int(rng.integers(2, [40, 300, 700, 2][seed] + 1))
+        F = synth.random_forest(rng, n, int(rng.integers(8, 80)), tie_prob=float(rng.choice([0.0, 0.5])))
+        sq = [4, 10, 18, 23][int(rng.integers(0, 4))]
+        F["cand_prob"] = (np.float32(0.5) + F["cand_prob"] * np.float32(2.0 ** -sq)).astype(np.float32)
+        N = int(F["cand_offsets"][-1])
+        A = rng.uniform(-1, 3, n)
+        d = int(rng.integers(1, 9))
+        n_max = int(rng.integers(0, 20))
+        B = int(rng.integers(n, N + 5))
+        got = _gpu_select(ada, F, A, d, n_max, B)
+        _assert_select_equal(F, A, d, n_max, B, got)
+
+
+@pytest.mark.parametrize("seed", range(4))
 def test_select_global_greedy_is_lexsort_topk(ada, seed):
     """NEXT-4 GlobalGreedy through select_global_greedy: every root,
     then the global top-(B - n) non-root candidates by (f-hat desc, request asc,
