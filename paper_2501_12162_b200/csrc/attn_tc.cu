@@ -45,7 +45,7 @@ constexpr int kBN = 64;           // keys per tile
 // Two CTA shapes (template NQ = q-tiles processed per CTA):
 //  NQ = 1: 192 threads (TMA producer, MMA, 4 softmax warps), 2 CTAs per SM,
 //          256 TMEM columns, 2+2-stage K/V rings -- every unit its own K/V stream;
-//  NQ = 2: 352 threads (producer, 2 MMA warps, 2 x 4 softmax warps), 1 CTA/SM, all
+//  NQ = 2: 384 threads (producer, 2 MMA warps, 1 idle, 2 x 4 softmax warps), 1 CTA/SM, all
 //          512 TMEM columns, 4+5-stage rings -- the two q-tiles of a (request,
 //          kv head) share every K/V tile (loaded once for both), chosen when the
 //          trees span more than one 128-row q-tile (c4/c5 shapes).
@@ -56,9 +56,13 @@ template <int NQ> struct TcCfg;
 template <> struct TcCfg<1> {
     static constexpr int THREADS = 192, CTAS = 2, TMEM = 256, KST = 2, VST = 2;
 };
+// NQ = 2: warps 0-3 = producer, 2 MMA issuers, one idle warp (warpgroup 0);
+// softmax groups = warps 4-7 and 8-11 (warpgroups 1, 2), so setmaxnreg moves
+// registers from warpgroup 0 to the softmax warpgroups.
 template <> struct TcCfg<2> {
-    static constexpr int THREADS = 352, CTAS = 1, TMEM = 512, KST = 4, VST = 5;
+    static constexpr int THREADS = 384, CTAS = 1, TMEM = 512, KST = 4, VST = 5;
 };
+constexpr int kRegLow = 56, kRegHigh = 224;  // 128 * 56 + 256 * 224 = 384 * 168 (the launch allocation)
 constexpr int kCtasPerSm = 2;     // max over the shapes (workspace sizing)
 constexpr int kPtChunk = 256;     // page-table entries staged per refill
 constexpr float kRescaleThresh = 8.0f;  // log2 units
@@ -554,7 +558,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
     // ---------------- schedule plan (all threads; K/V rings used as scratch) ----------------
     __shared__ int sk_split;  // split-KV pieces per unit (0: whole units)
     __shared__ long long scan_tmp[33];
-    __shared__ int red_tmp[3][16];  // per warp (<= 10 warps)
+    __shared__ int red_tmp[3][16];  // per warp (<= 12 warps)
     RecCursor cur0;
     {
         const int n = p.n_req;
@@ -768,6 +772,12 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 2] = tn;  // plan done
     }
 
+    constexpr int SM0 = NQ == 2 ? 4 : 1 + NQ;  // first softmax warp
+    // setmaxnreg inside the role branches (warpgroup-uniform): in code common to all
+    // roles ptxas compiled the whole kernel under the decreased budget
+    if constexpr (NQ == 2) {
+        if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegLow));
+    }
     if (warp == 0) {
         // ===================== TMA producer (whole warp) =====================
         // K_{t+lead} (lane 0) and V_t (lane 1) are issued by the same
@@ -1124,9 +1134,10 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             __syncwarp();
             ++unit_it;
         }
-    } else {
-        // ============ softmax + epilogue (warps 1+NQ .. : 4 per q-tile) ============
-        const int grp = (warp - 1 - NQ) >> 2;  // q-tile of the unit this warp group handles
+    } else if (warp >= SM0) {
+        // ============ softmax + epilogue (warps SM0 .. : 4 per q-tile) ============
+        if constexpr (NQ == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegHigh));
+        const int grp = (warp - SM0) >> 2;  // q-tile of the unit this warp group handles
         const int quad = warp & 3;        // TMEM lane quadrant this warp may access
         const int r = quad * 32 + lane;   // Q row in the tile == TMEM lane
         const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
@@ -1134,7 +1145,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         const uint32_t o_addr = sp_addr + 128;
         uint64_t* const of = o_full(grp);
         uint64_t* const oe = o_empty(grp);
-        const int gtid = (int)threadIdx.x - 32 * (1 + NQ) - 128 * grp;  // 0..127 within the group
+        const int gtid = (int)threadIdx.x - 32 * SM0 - 128 * grp;  // 0..127 within the group
         const float sl2 = p.scale_log2;
         // this row's ancestor-or-self bit words, one per 64-node tree tile ([word][row]: conflict-free)
         uint64_t* const anc_s = reinterpret_cast<uint64_t*>(smem + S::OFF_ANC) + grp * kAncWords * kBM + r;
@@ -1331,7 +1342,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             }
             const bool full = (pc.tb == 0 && pc.te == u.nt);
             const bool tailp = !full && pc.x <= -2;  // tail stream-K piece (else co-resident split-KV)
-            const int lead_warp = 1 + NQ + 4 * grp;  // first softmax warp of this group
+            const int lead_warp = SM0 + 4 * grp;  // first softmax warp of this group
             const int wq = pc.w + qi;                // counters of this q-tile
             const size_t orow = (size_t)(u.off + node) * p.n_q + (size_t)u.g * G + hh;
             __shared__ int s_merge[NQ];
