@@ -502,6 +502,9 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
 
     const int warp = warp_id();
     const int lane = lane_id();
+    unsigned long long t_entry = 0;  // debug mode 6: the per-CTA timeline starts at kernel entry
+    if (kDebug && p.trace != nullptr && threadIdx.x == 0 && p.debug_mode == 6)
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
     pdl_launch_dependents();
 
     const bool leader = !PR || crank == 0;  // PR: the CTA that issues the pair's MMAs
@@ -604,6 +607,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
             red_tmp[2][warp] = wn;
         }
         __syncthreads();
+        if (kDebug && p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceCtas && p.debug_mode == 6) {
+            unsigned long long tn;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+            p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 5] = tn;  // plan: loads + reductions done
+        }
         int U = 0, maxnt = 0, minnt = 0x7fffffff;
         for (int k = 0; k < (int)(blockDim.x / 32); ++k) {
             U += red_tmp[0][k];
@@ -647,6 +655,11 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
                 if (pass == 0) T = scan_tmp[32];
                 __syncthreads();
             }
+        }
+        if (kDebug && p.trace != nullptr && threadIdx.x == 0 && blockIdx.x < kTraceCtas && p.debug_mode == 6) {
+            unsigned long long tn;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+            p.trace[(size_t)(p.trace_cap + blockIdx.x) * 8 + 4] = tn;  // plan: scans done
         }
         PieceRec* recs = reinterpret_cast<PieceRec*>(smem + S::OFF_REC);
         __shared__ int s_nrec;
@@ -1539,7 +1552,7 @@ __global__ void __launch_bounds__(TcCfg<NQ>::THREADS, TcCfg<NQ>::CTAS)
         unsigned long long t_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         unsigned long long* rec = p.trace + (size_t)(p.trace_cap + blockIdx.x) * 8;
-        rec[0] = t_start;
+        rec[0] = p.debug_mode == 6 ? t_entry : t_start;
         rec[1] = t_end;
         if (!sk_split) {  // (split-KV uses slot 3 for "all pieces published")
             unsigned smid;

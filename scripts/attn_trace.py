@@ -65,6 +65,10 @@ if len(cta):
           f"p90 {np.percentile(en, 90):.2f}  max {en.max():.2f}")
     print(f"  busy fraction (sum of CTA spans / (CTAs x makespan)) {((en - st).sum() / (len(cta) * en.max())):.3f}")
     print("  end-time histogram (us):", np.histogram(en, bins=10)[0].tolist(), np.round(np.histogram(en, bins=10)[1], 1).tolist())
+    if os.environ.get("AS_ATTN_DEBUG_MODE") == "6":  # prologue / plan sub-phases, per CTA from its own entry
+        rel = lambda c: np.median((cta[:, c] - cta[:, 0]) / 1e3)
+        print(f"  per CTA from entry (median us): loads+reductions {rel(5):.2f}, scans {rel(4):.2f}, "
+              f"plan done {rel(2):.2f}, first S tile {rel(6):.2f}, O ready {rel(7):.2f}")
     tagged = cta[(cta[:, 3] >> 40) == 1]
     if len(tagged):
         smid = tagged[:, 3] & 0xFFFF
