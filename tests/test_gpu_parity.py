@@ -55,7 +55,9 @@ def _rand_probs(rng, shape, sigma, ties):
 
 @pytest.mark.parametrize("V,width,n,d,ties", [(1000, 8, 6, 4, False), (1000, 8, 5, 3, True),
                                               (8195, 2, 3, 3, False), (20, 16, 4, 3, False),
-                                              (5, 1, 3, 4, True), (128256, 8, 3, 2, False)])
+                                              (5, 1, 3, 4, True), (128256, 8, 3, 2, False),
+                                              # > 4 CTAs per SM of rows (layer 2: 640 / 608 rows): the LDGSTS-ring scan
+                                              (3000, 8, 80, 3, False), (4096, 8, 76, 2, True)])
 def test_beam_layers_bit_exact(ada, V, width, n, d, ties):
     """d speculation layers on the GPU (as_beam_step) == the oracle's beam step
     applied layer by layer: parents, tokens and f-hat bit-exact."""
